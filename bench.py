@@ -1,0 +1,316 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 NTT hot path (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json metric "fwd/inv NTT Mcoeff/s (N=16384, batched
+limbs)", config 3): N = 16384, 32 RNS limbs of distinct 50-bit NTT primes
+(largest < 2^50, == 1 mod 32768), 64 polynomials -> 2048 rows = 33,554,432
+coefficients, uniform in [0, q) from std::mt19937_64 (bench.hpp:126-131).
+A step = forward NTT (fin 1, fout 1) + inverse NTT (fin 1, fout 1) over the
+whole batch; `value` = coefficient transforms per second (2 x 33.5 M per step)
+across all ranks, in Mcoeff/s. Inputs (256 MiB) exceed the 126 MB L2.
+
+Multi-GPU: one process per GPU, each rank transforms its own cfg3 batch
+(independent ciphertext polynomials; no collective): weak scaling.
+
+--impl reference: the reference's own CPU code (oracle/_ref/libnttref.so, built
+from the unmodified nttkit headers) on all host threads, same config/metric, on
+a bounded sample of rows per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+METRIC = "fwd/inv NTT Mcoeff/s (N=16384, batched limbs)"
+N = 16384
+NLIMBS = 32
+NPOLYS = 64
+SEED = 3 ^ 20260809
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), float(p.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+def cfg3_moduli():
+    from primes import largest_ntt_primes
+
+    return largest_ntt_primes(50, N, NLIMBS)
+
+
+def make_inputs(moduli, npolys, seed):
+    """[npolys][nlimbs][N] uniform in [0, q_l); the generator runs in parallel
+    per row (row r seeded seed + r) with numpy for speed."""
+    from oracle_lib import Oracle
+
+    o = Oracle()
+    L = len(moduli)
+    x = np.empty((npolys * L, N), np.uint64)
+    for r in range(npolys * L):
+        x[r] = o.mt19937_64(seed + r, N, moduli[r % L])
+    return x.reshape(-1)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                          f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout
+                    self.samples.append([s.strip() for s in out.strip().split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(s[0]) for s in self.samples if len(s) >= 8 and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) >= 8 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            if len(s) >= 8:
+                for k, name in enumerate(names):
+                    if s[4 + k].lower().startswith("active"):
+                        reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
+
+
+def cpu_reference(moduli, rows, reps, threads):
+    """The reference's NttTables::forward/inverse on `rows` rows, all threads."""
+    from oracle_lib import Ref
+
+    ref = Ref()
+    x = make_inputs(moduli, rows // len(moduli) or 1, SEED)[: rows * N]
+    out = np.empty_like(x)
+    import ctypes as C
+
+    mods = np.asarray(moduli, np.uint64)
+    p = ref.lib.ref_plan_create(N, mods.ctypes.data_as(C.POINTER(C.c_uint64)), mods.size)
+    ptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint64))  # noqa: E731
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        ref.lib.ref_plan_ntt(p, 0, ptr(out), ptr(x), rows, 1, 1, threads)
+        ref.lib.ref_plan_ntt(p, 1, ptr(out), ptr(out), rows, 1, 1, threads)
+        times.append(time.perf_counter() - t0)
+    ref.lib.ref_plan_destroy(p)
+    assert np.array_equal(out, x), "reference round trip failed"
+    return times
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    moduli = cfg3_moduli()
+    threads = os.cpu_count() or 1
+    rows = max(len(moduli), min(2048, 64 * threads))  # bounded sample per step
+    rows -= rows % len(moduli)
+    cpu_reference(moduli, rows, max(1, args.warmup), threads)  # warm-up
+    times = cpu_reference(moduli, rows, args.steps, threads)
+    t = statistics.median(times)
+    v = 2 * rows * N / t / 1e6
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "Mcoeff/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic (mt19937_64, uniform [0,q))",
+        "config": {"workload": "cfg3: N=16384, 32 limbs x 64 polys, fwd(1,1)+inv(1,1)",
+                   "sample_rows_per_step": rows},
+        "cpu_baseline": {"value": v, "unit": "Mcoeff/s", "cores": threads, "kind": "reference",
+                         "sample": f"{rows} rows of N=16384 (of 2048), fwd+inv per step"},
+        "e2e": {"value": v, "unit": "Mcoeff/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2103_16400_b200 as nk
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    moduli = cfg3_moduli()
+    plan = nk.RnsNtt(N, moduli, device=local)
+    words = NPOLYS * NLIMBS * N
+    x = make_inputs(moduli, NPOLYS, SEED + rank * 100003)
+    d_in = torch.from_numpy(x.view(np.int64)).cuda()
+    d_f = torch.empty_like(d_in)
+    d_b = torch.empty_like(d_in)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        plan.forward(d_f, d_in, 1, 1)
+        plan.inverse(d_b, d_f, 1, 1)
+
+    # correctness gate before timing (bench.hpp:346-356 convention)
+    step()
+    torch.cuda.synchronize()
+    assert torch.equal(d_b, d_in), "round trip mismatch"
+    from oracle_lib import Oracle
+
+    o = Oracle()
+    rows_chk = NLIMBS
+    want = o.forward(N, moduli, x[: rows_chk * N], 1, 1, threads=os.cpu_count() or 1)
+    assert np.array_equal(d_f[: rows_chk * N].cpu().numpy().view(np.uint64), want), \
+        "forward mismatch vs oracle"
+
+    for _ in range(args.warmup):
+        step()
+    # per-kernel events on the launching stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    l0 = nk.launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        plan.forward(d_f, d_in, 1, 1)
+        ev[i][1].record(stream)
+        plan.inverse(d_b, d_f, 1, 1)
+        ev[i][2].record(stream)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    launches = nk.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    total_ms = t_start.elapsed_time(t_end)
+    fwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
+    inv_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    coeffs_step = 2 * words * world
+    value = coeffs_step / (ms_step * 1e-3) / 1e6
+
+    # ---- end to end through the C-ABI host-buffer calls (pinned memory) ----
+    hx = torch.from_numpy(x.view(np.int64)).pin_memory().numpy().view(np.uint64)
+    hf = torch.empty(words, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    hb = torch.empty(words, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    e2e_steps = max(2, min(args.steps, 5))
+    plan.forward(hf, hx, 1, 1)
+    plan.inverse(hb, hf, 1, 1)
+    assert np.array_equal(hb, x)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        plan.forward(hf, hx, 1, 1)
+        plan.inverse(hb, hf, 1, 1)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = coeffs_step / e2e_s / 1e6
+
+    hbm, smmax, peak_kind = peaks()
+    # dominant kernel: the forward block kernel (one launch per forward)
+    fwd_bytes = 16 * words  # read + write each coefficient once
+    achieved = fwd_bytes / (fwd_ms * 1e-3) / 1e9
+    butterflies = (N // 2) * 14 * NPOLYS * NLIMBS
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            threads = os.cpu_count() or 1
+            rows = 2 * NLIMBS
+            times = cpu_reference(moduli, rows, 3, threads)
+            tt = statistics.median(times)
+            cpu = {"value": 2 * rows * N / tt / 1e6, "unit": "Mcoeff/s", "cores": threads,
+                   "kind": "reference",
+                   "sample": f"{rows} rows of N=16384 fwd+inv (reference NttTables, -O3 -DNDEBUG)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mcoeff/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (mt19937_64, uniform [0,q))",
+            "config": {"workload": "cfg3: N=16384, 32 limbs x 64 polys per GPU, fwd(1,1)+inv(1,1)",
+                       "rows_per_gpu": NPOLYS * NLIMBS, "l2": "inputs 256 MiB > 126 MB L2",
+                       "parallelism": f"limb/poly sharding x{world}, no collective"},
+            "fwd_ms": fwd_ms, "inv_ms": inv_ms,
+            "fwd_mcoeff_s": words / fwd_ms / 1e3, "inv_mcoeff_s": words / inv_ms / 1e3,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None, "kernel": "ntt_block<14,5,52,fwd>",
+                         "peak_kind": peak_kind, "algorithmic_bytes_per_launch": fwd_bytes},
+            "int_pipe": {"butterflies_per_launch": butterflies,
+                         "gbfly_s": butterflies / (fwd_ms * 1e-3) / 1e9},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "Mcoeff/s", "h2d_bytes_per_step": 2 * 8 * words,
+                    "d2h_bytes_per_step": 2 * 8 * words,
+                    "path": "nk_ntt_forward_host + nk_ntt_inverse_host (pinned host buffers)"},
+            "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,162 @@
+/*
+ * nttkit_b200 — C-ABI drop-in for the polynomial-arithmetic hot path of Intel
+ * HEXL (arXiv 2103.16400) as restated by nttkit (/root/reference/proj/), run on
+ * B200 (sm_100a) kernels.
+ *
+ * Plain C types only: pointers, sizes, a CUDA stream as `void*` (a
+ * cudaStream_t; NULL = the legacy default stream). Every entry point returns 0
+ * on success and a negative NK_ERR_* code otherwise; nk_last_error() gives the
+ * message (thread-local), which is the reference's std::invalid_argument text
+ * for argument errors.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj/):
+ *   nk_plan_create          NttTables(n, Modulus)                 include/nttkit/ntt.hpp:210
+ *                           NttTables(n, Modulus, root)           include/nttkit/ntt.hpp:212-213
+ *                           NttTables(n, m, optional root, bs)    include/nttkit/ntt.hpp:217-247
+ *                           (HEXL: NTT(degree, q[, root])         PAPER.md:468,476)
+ *                           — one plan holds the tables of `nlimbs` RNS moduli.
+ *   nk_ntt_forward[_host]   NttTables::forward(result, operand, in, out)  ntt.hpp:268-285
+ *                           (HEXL: NTT::ComputeForward            PAPER.md:485-486)
+ *   nk_ntt_inverse[_host]   NttTables::inverse(result, operand, in, out)  ntt.hpp:289-306
+ *                           (HEXL: NTT::ComputeInverse            PAPER.md:495-496)
+ *   nk_eltwise_mult_mod[_host]  eltwise_mult_mod(r, a, b, Modulus, f)     eltwise.hpp:180-188
+ *                           (HEXL: EltwiseMultMod                 PAPER.md:542-544)
+ *   nk_eltwise_fma_mod[_host]   eltwise_fma_mod(r, a, y, z?, Modulus, f)  eltwise.hpp:263-271
+ *                           and eltwise_fma_mod<B>                eltwise.hpp:231-259
+ *                           (HEXL: EltwiseFMAMod, z == NULL is the vector-scalar
+ *                            multiply                             PAPER.md:521,527-529)
+ *   nk_eltwise_add_mod      eltwise_add_mod                       eltwise.hpp:47-57
+ *   nk_eltwise_neg_mod      eltwise_neg_mod                       eltwise.hpp:60-70
+ *   nk_poly_mult_mod[_host] poly_mult_mod(result, f, g, tables)   ring.hpp:28-43
+ *   nk_modulus              Modulus(q)                            modarith.hpp:106-129
+ *   nk_minimal_primitive_root  minimal_primitive_root             ntt.hpp:172-197
+ *   nk_tables_host          NttTables table accessors             ntt.hpp:249-261
+ *
+ * Batched layout (device entry points): `npolys * nlimbs` contiguous rows of n
+ * uint64 words, polynomial-major: row r = poly * nlimbs + l holds limb
+ * (limb0 + l) of the plan. A single-polynomial reference call is
+ * npolys = nlimbs = 1. result and operand must be identical (in place) or
+ * disjoint (ntt.hpp:267-268); partial overlap is NK_ERR_OVERLAP.
+ *
+ * Device entry points are asynchronous on `stream`. *_host entry points take
+ * host buffers and block until the result is back in host memory, like the
+ * reference calls.
+ */
+#ifndef NTTKIT_B200_H
+#define NTTKIT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  NK_OK = 0,
+  NK_ERR_MODULUS = -1,          /* "Modulus: value must be a prime in [3, 2^62)"            modarith.hpp:109-111 */
+  NK_ERR_N = -2,                /* "NttTables: n must be a power of two in [2, 2^20]"         ntt.hpp:219-221 */
+  NK_ERR_Q_MOD_2N = -3,         /* "NttTables: q must satisfy q == 1 (mod 2n)"                ntt.hpp:223-225 */
+  NK_ERR_BIT_SHIFT = -4,        /* "NttTables: accumulator width must be 52 or 64"            ntt.hpp:226-228 */
+  NK_ERR_BIT_SHIFT_52 = -5,     /* "NttTables: 52-bit accumulator requires 4q < 2^52"         ntt.hpp:229-231 */
+  NK_ERR_ROOT = -6,             /* "NttTables: root is not a primitive 2n'th root of unity"   ntt.hpp:232-236 */
+  NK_ERR_FWD_IN_FACTOR = -7,    /* "forward: input_mod_factor must be 1, 2 or 4"              ntt.hpp:270-272 */
+  NK_ERR_FWD_OUT_FACTOR = -8,   /* "forward: output_mod_factor must be 1 or 4"                ntt.hpp:273-275 */
+  NK_ERR_INV_IN_FACTOR = -9,    /* "inverse: input_mod_factor must be 1 or 2"                 ntt.hpp:291-293 */
+  NK_ERR_INV_OUT_FACTOR = -10,  /* "inverse: output_mod_factor must be 1 or 2"                ntt.hpp:294-296 */
+  NK_ERR_LENGTH = -11,          /* "transform: buffer length must equal n" / "eltwise: operand lengths must match"
+                                   ntt.hpp:329-331, eltwise.hpp:26-30, ring.hpp:31-33 */
+  NK_ERR_MULT_FACTOR = -12,     /* "eltwise_mult_mod: input_mod_factor must be 1, 2 or 4"     eltwise.hpp:141-143,162-164 */
+  NK_ERR_MULT_INT_RANGE = -13,  /* "eltwise_mult_mod_int: requires input_mod_factor*q < 2^63" eltwise.hpp:144-146 */
+  NK_ERR_MULT_FLOAT_RANGE = -14,/* "eltwise_mult_mod_float: requires q < 2^50"                eltwise.hpp:165-167 */
+  NK_ERR_FMA_FACTOR = -15,      /* "eltwise_fma_mod: input_mod_factor must be 1, 2, 4 or 8"   eltwise.hpp:239-242 */
+  NK_ERR_FMA_MODULUS = -16,     /* "eltwise_fma_mod: requires q < 2^61"                       eltwise.hpp:243-245 */
+  NK_ERR_FMA_SCALAR = -17,      /* "eltwise_fma_mod: scalar must be < q"                      eltwise.hpp:246-248 */
+  NK_ERR_FMA_WIDTH = -18,       /* "eltwise_fma_mod: requires input_mod_factor*q < 2^BitShift" eltwise.hpp:249-251 */
+  NK_ERR_POLY_MODULUS = -19,    /* "poly_mult_mod: requires q < 2^61"                         ring.hpp:34-36 */
+  NK_ERR_OVERLAP = -20,         /* result/operand partially overlap (ntt.hpp:267-268 contract) */
+  NK_ERR_LIMB = -21,            /* limb range outside the plan */
+  NK_ERR_NULL = -22,            /* NULL pointer where a buffer is required */
+  NK_ERR_CUDA = -100            /* CUDA runtime error; message has the CUDA error string */
+};
+
+typedef struct nk_plan nk_plan;
+
+/* ---------------- host-only (no GPU needed) ---------------- */
+const char* nk_last_error(void);
+const char* nk_version(void);
+/* Modulus(q): bits = bit_width(q), barrett = floor(2^(63+bits)/q). */
+int nk_modulus(uint64_t q, uint32_t* bits, uint64_t* barrett_factor);
+/* Smallest primitive `order`-th root of unity mod q (order a power of two dividing q-1). */
+int nk_minimal_primitive_root(uint64_t order, uint64_t q, uint64_t* root);
+/* Host precompute exactly as NttTables: root = NULL selects the minimal root (an explicit
+ * *root is validated like std::optional<uint64_t> root, ntt.hpp:232-237), bit_shift = 0 selects
+ * 52 iff 4q < 2^52. Any output pointer may be NULL; arrays hold n words. */
+int nk_tables_host(uint64_t n, uint64_t q, const uint64_t* root, int bit_shift, uint64_t* psi,
+                   uint64_t* root_powers_rev, uint64_t* root_precons_rev,
+                   uint64_t* inv_root_powers_rev, uint64_t* inv_root_precons_rev,
+                   uint64_t* inv_n, uint64_t* inv_n_precon, int* bit_shift_out);
+
+/* ---------------- plans (device tables) ---------------- */
+/* roots: NULL selects each limb's minimal root; otherwise nlimbs explicit roots, each
+ * validated as NttTables(n, m, root) does (0 is rejected, ntt.hpp:234).
+ * bit_shift: 0 = automatic per limb, else 52 or 64 for every limb. */
+int nk_plan_create(nk_plan** plan, int device, uint64_t n, const uint64_t* moduli,
+                   const uint64_t* roots, uint32_t nlimbs, int bit_shift);
+void nk_plan_destroy(nk_plan* plan);
+int nk_plan_info(const nk_plan* plan, uint32_t limb, uint64_t* n, uint64_t* q, uint64_t* psi,
+                 int* bit_shift, uint32_t* nlimbs);
+
+/* ---------------- device-pointer entry points (async on stream) ---------------- */
+int nk_ntt_forward(const nk_plan* plan, uint64_t* d_result, const uint64_t* d_operand,
+                   uint32_t limb0, uint32_t nlimbs, uint32_t npolys,
+                   uint64_t input_mod_factor, uint64_t output_mod_factor, void* stream);
+int nk_ntt_inverse(const nk_plan* plan, uint64_t* d_result, const uint64_t* d_operand,
+                   uint32_t limb0, uint32_t nlimbs, uint32_t npolys,
+                   uint64_t input_mod_factor, uint64_t output_mod_factor, void* stream);
+/* Dyadic product of rows under each row's limb modulus (eltwise_mult_mod per row). */
+int nk_plan_eltwise_mult_mod(const nk_plan* plan, uint64_t* d_result, const uint64_t* d_a,
+                             const uint64_t* d_b, uint32_t limb0, uint32_t nlimbs,
+                             uint32_t npolys, uint64_t input_mod_factor, void* stream);
+/* poly_mult_mod over npolys*nlimbs row pairs: fwd(1,4) x2, mult(4), inv(1,1). */
+int nk_poly_mult_mod(const nk_plan* plan, uint64_t* d_result, const uint64_t* d_f,
+                     const uint64_t* d_g, uint32_t limb0, uint32_t nlimbs, uint32_t npolys,
+                     void* stream);
+
+int nk_eltwise_mult_mod(uint64_t* d_result, const uint64_t* d_a, const uint64_t* d_b,
+                        uint64_t n, uint64_t q, uint64_t input_mod_factor, void* stream);
+/* d_z may be NULL (vector-scalar multiply). bit_shift: 0 = automatic, 52 or 64. */
+int nk_eltwise_fma_mod(uint64_t* d_result, const uint64_t* d_a, uint64_t y, const uint64_t* d_z,
+                       uint64_t n, uint64_t q, uint64_t input_mod_factor, int bit_shift,
+                       void* stream);
+int nk_eltwise_add_mod(uint64_t* d_result, const uint64_t* d_a, const uint64_t* d_b, uint64_t n,
+                       uint64_t q, void* stream);
+int nk_eltwise_neg_mod(uint64_t* d_result, const uint64_t* d_a, uint64_t n, uint64_t q,
+                       void* stream);
+
+/* ---------------- host-buffer entry points (blocking, reference semantics) ----------------
+ * Copy host -> device, run, copy device -> host on the plan's device. Pinned host
+ * memory gives full PCIe bandwidth; pageable memory works too. `length` is the
+ * number of words in each buffer and must equal npolys*nlimbs*n (NK_ERR_LENGTH). */
+int nk_ntt_forward_host(const nk_plan* plan, uint64_t* result, const uint64_t* operand,
+                        uint64_t length, uint32_t limb0, uint32_t nlimbs, uint32_t npolys,
+                        uint64_t input_mod_factor, uint64_t output_mod_factor, void* stream);
+int nk_ntt_inverse_host(const nk_plan* plan, uint64_t* result, const uint64_t* operand,
+                        uint64_t length, uint32_t limb0, uint32_t nlimbs, uint32_t npolys,
+                        uint64_t input_mod_factor, uint64_t output_mod_factor, void* stream);
+int nk_poly_mult_mod_host(const nk_plan* plan, uint64_t* result, const uint64_t* f,
+                          const uint64_t* g, uint64_t length, uint32_t limb0, uint32_t nlimbs,
+                          uint32_t npolys, void* stream);
+int nk_eltwise_mult_mod_host(uint64_t* result, const uint64_t* a, const uint64_t* b, uint64_t n,
+                             uint64_t q, uint64_t input_mod_factor, int device, void* stream);
+int nk_eltwise_fma_mod_host(uint64_t* result, const uint64_t* a, uint64_t y, const uint64_t* z,
+                            uint64_t n, uint64_t q, uint64_t input_mod_factor, int bit_shift,
+                            int device, void* stream);
+
+/* Number of kernels the library has launched in this process (for the bench's
+ * gpu_launches claim). */
+uint64_t nk_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

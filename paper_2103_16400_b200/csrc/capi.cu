@@ -1,0 +1,636 @@
+// C-ABI of nttkit_b200 (include/nttkit_b200.h): argument validation that
+// mirrors the reference's std::invalid_argument checks, plan (device table)
+// management, and kernel launches. No CPU compute fallback exists: every
+// transform and element-wise product runs in the sm_100a kernels below, and a
+// missing/failed CUDA device is reported as NK_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/nttkit_b200.h"
+#include "eltwise_kernels.cuh"
+#include "host_math.hpp"
+#include "ntt_kernels.cuh"
+
+using nk::host::u128;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(NK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define NK_CUDA(call)                                   \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+  } while (0)
+
+// Small per-thread cache of validated moduli: Modulus(q) runs Miller-Rabin
+// (modarith.hpp:108-115); element-wise calls re-validate the same q repeatedly.
+bool valid_modulus(uint64_t q, nk::host::Modulus* m) {
+  thread_local nk::host::Modulus cache[4];
+  thread_local int next = 0;
+  for (auto& c : cache)
+    if (c.q == q && q != 0) { *m = c; return true; }
+  if (!nk::host::make_modulus(q, m)) return false;
+  cache[next] = *m;
+  next = (next + 1) & 3;
+  return true;
+}
+
+bool overlap_bad(const void* a, const void* b, uint64_t bytes) {
+  if (a == b) return false;
+  const uintptr_t x = reinterpret_cast<uintptr_t>(a), y = reinterpret_cast<uintptr_t>(b);
+  return x < y + bytes && y < x + bytes;
+}
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+int ensure_device(int dev) {
+  int cur = -1;
+  NK_CUDA(cudaGetDevice(&cur));
+  if (cur != dev) NK_CUDA(cudaSetDevice(dev));
+  return 0;
+}
+
+}  // namespace
+
+struct nk_plan {
+  int device = 0;
+  uint64_t n = 0;
+  uint32_t logn = 0, nlimbs = 0;
+  std::vector<uint64_t> q, psi;
+  std::vector<int> bs;
+  ulonglong2* tw_fwd = nullptr;  // [limb][n]
+  ulonglong2* tw_inv = nullptr;  // [limb][n]
+  nk::LimbConst* lc = nullptr;   // [limb]
+  nk::MultConst* mc[3] = {nullptr, nullptr, nullptr};  // fin = 1, 2, 4
+};
+
+// ---------------------------------------------------------------------------
+// kernel dispatch
+// ---------------------------------------------------------------------------
+namespace {
+
+template <int LOGB, int BS, bool FWD>
+int launch_block_t(const nk::NttArgs& a, uint64_t grid, cudaStream_t st) {
+  constexpr int LOGV = 5;
+  constexpr size_t smem = nk::block_smem_bytes<LOGB, LOGV>();
+  static std::once_flag once[64];
+  static cudaError_t attr_err[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::call_once(once[dev & 63], [&] {
+    attr_err[dev & 63] = cudaFuncSetAttribute(nk::ntt_block<LOGB, LOGV, BS, FWD>,
+                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(smem));
+  });
+  if (attr_err[dev & 63] != cudaSuccess) return cuda_fail(attr_err[dev & 63], "cudaFuncSetAttribute");
+  nk::ntt_block<LOGB, LOGV, BS, FWD><<<static_cast<unsigned>(grid), 1 << (LOGB - LOGV), smem, st>>>(a);
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+template <int BS, bool FWD>
+int launch_block(uint32_t logb, const nk::NttArgs& a, uint64_t grid, cudaStream_t st) {
+  switch (logb) {
+    case 11: return launch_block_t<11, BS, FWD>(a, grid, st);
+    case 12: return launch_block_t<12, BS, FWD>(a, grid, st);
+    case 13: return launch_block_t<13, BS, FWD>(a, grid, st);
+    default: return launch_block_t<14, BS, FWD>(a, grid, st);
+  }
+}
+
+template <int BS, bool FWD>
+int launch_global(uint32_t k, uint32_t lo, bool first_iltm, bool last, const nk::NttArgs& a,
+                  cudaStream_t st) {
+  const uint64_t threads = a.rows << (a.logn - k);
+  const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
+  switch (k) {
+    case 1: nk::ntt_global_pass<1, BS, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
+    case 2: nk::ntt_global_pass<2, BS, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
+    default: nk::ntt_global_pass<3, BS, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
+  }
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+template <int BS, bool FWD>
+int launch_small(const nk::NttArgs& a, cudaStream_t st) {
+  const size_t smem = a.n * sizeof(uint64_t);
+  if (smem > 48 * 1024) {
+    NK_CUDA(cudaFuncSetAttribute(nk::ntt_small<BS, FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  }
+  const unsigned threads = static_cast<unsigned>(a.n / 2 < 256 ? a.n / 2 : 256);
+  nk::ntt_small<BS, FWD><<<static_cast<unsigned>(a.rows), threads, smem, st>>>(a);
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+constexpr uint32_t kLogBlock = 14;
+
+// Full transform of a.rows rows, all with accumulator width BS.
+template <int BS, bool FWD>
+int run_ntt(nk::NttArgs a, cudaStream_t st) {
+  const uint32_t logn = a.logn;
+  if (logn <= 10) return launch_small<BS, FWD>(a, st);
+  if (logn <= kLogBlock) return launch_block<BS, FWD>(logn, a, a.rows, st);
+  // long rows: high bits in global passes of <= 3 stages, low 14 bits per block
+  const uint32_t gbits = logn - kLogBlock;
+  uint32_t ks[2] = {gbits, 0};
+  if (gbits > 3) { ks[0] = (gbits + 1) / 2; ks[1] = gbits - ks[0]; }
+  const int np = ks[1] ? 2 : 1;
+  const uint64_t grid = a.rows << gbits;
+  if (FWD) {
+    uint32_t top = logn;
+    for (int p = 0; p < np; ++p) {
+      const uint32_t lo = top - ks[p];
+      if (int rc = launch_global<BS, true>(ks[p], lo, p == 0 && a.fin == 1, false, a, st)) return rc;
+      a.in = a.out;  // later passes run in place on the result
+      top = lo;
+    }
+    a.fin = 2;  // block stages never see the first stage
+    return launch_block<BS, true>(kLogBlock, a, grid, st);
+  } else {
+    const int fout = a.fout;
+    if (int rc = launch_block<BS, false>(kLogBlock, a, grid, st)) return rc;
+    a.in = a.out;
+    a.fout = fout;
+    uint32_t lo = kLogBlock;
+    for (int p = 0; p < np; ++p) {
+      if (int rc = launch_global<BS, false>(ks[p], lo, false, p == np - 1, a, st)) return rc;
+      lo += ks[p];
+    }
+    return 0;
+  }
+}
+
+int check_limbs(const nk_plan* p, uint32_t limb0, uint32_t nlimbs) {
+  if (!p) return fail(NK_ERR_NULL, "plan is NULL");
+  if (nlimbs == 0 || static_cast<uint64_t>(limb0) + nlimbs > p->nlimbs)
+    return fail(NK_ERR_LIMB, "limb range outside the plan");
+  return 0;
+}
+
+int ntt_dispatch(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, uint32_t limb0,
+                 uint32_t nlimbs, uint32_t npolys, uint64_t fin, uint64_t fout, cudaStream_t st) {
+  nk::NttArgs a{};
+  a.out = res;
+  a.in = op;
+  a.tw = fwd ? p->tw_fwd : p->tw_inv;
+  a.lc = p->lc;
+  a.n = p->n;
+  a.logn = p->logn;
+  a.limb0 = limb0;
+  a.nlimbs = nlimbs;
+  a.fin = static_cast<int>(fin);
+  a.fout = static_cast<int>(fout);
+  if (npolys == 0) return 0;
+  // one launch when the limb range shares an accumulator width, else one per limb
+  bool uniform = true;
+  for (uint32_t l = 1; l < nlimbs; ++l) uniform &= p->bs[limb0 + l] == p->bs[limb0];
+  const uint32_t runs = uniform ? 1 : nlimbs;
+  for (uint32_t l = 0; l < runs; ++l) {
+    nk::NttArgs b = a;
+    if (uniform) {
+      b.rows = static_cast<uint64_t>(npolys) * nlimbs;
+      b.row_mul = 1;
+      b.row_add = 0;
+    } else {
+      b.rows = npolys;
+      b.row_mul = nlimbs;
+      b.row_add = l;
+    }
+    const int bs = p->bs[limb0 + (uniform ? 0 : l)];
+    int rc;
+    if (bs == 52) rc = fwd ? run_ntt<52, true>(b, st) : run_ntt<52, false>(b, st);
+    else rc = fwd ? run_ntt<64, true>(b, st) : run_ntt<64, false>(b, st);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+unsigned eltwise_grid(uint64_t work) {
+  // enough CTAs for every SM to stream; grid-stride covers the rest
+  uint64_t g = (work + 255) / 256;
+  const uint64_t cap = 148ull * 16;
+  return static_cast<unsigned>(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host-only entry points
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* nk_last_error(void) { return g_err.c_str(); }
+const char* nk_version(void) { return "nttkit_b200 0.1 (sm_100a)"; }
+uint64_t nk_launch_count(void) { return g_launches.load(); }
+
+int nk_modulus(uint64_t q, uint32_t* bits, uint64_t* barrett_factor) {
+  nk::host::Modulus m;
+  if (!nk::host::make_modulus(q, &m))
+    return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
+  if (bits) *bits = m.bits;
+  if (barrett_factor) *barrett_factor = m.barrett;
+  return 0;
+}
+
+int nk_minimal_primitive_root(uint64_t order, uint64_t q, uint64_t* root) {
+  nk::host::Modulus m;
+  if (!nk::host::make_modulus(q, &m))
+    return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
+  const uint64_t r = nk::host::minimal_primitive_root(order, q);
+  if (!r)
+    return fail(NK_ERR_Q_MOD_2N,
+                "minimal_primitive_root: order must be a power of two dividing q-1");
+  if (root) *root = r;
+  return 0;
+}
+
+int nk_tables_host(uint64_t n, uint64_t q, const uint64_t* root, int bit_shift, uint64_t* psi,
+                   uint64_t* w, uint64_t* wp, uint64_t* wi, uint64_t* wip, uint64_t* ninv,
+                   uint64_t* ninvp, int* bs_out) {
+  nk::host::Tables t;
+  std::string msg;
+  if (int rc = nk::host::build_tables(n, q, root, bit_shift, &t, &msg)) return fail(rc, msg);
+  if (psi) *psi = t.psi;
+  if (w) std::memcpy(w, t.w.data(), n * 8);
+  if (wp) std::memcpy(wp, t.wp.data(), n * 8);
+  if (wi) std::memcpy(wi, t.wi.data(), n * 8);
+  if (wip) std::memcpy(wip, t.wip.data(), n * 8);
+  if (ninv) *ninv = t.ninv;
+  if (ninvp) *ninvp = t.ninvp;
+  if (bs_out) *bs_out = t.bs;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// plans
+// ---------------------------------------------------------------------------
+void nk_plan_destroy(nk_plan* p) {
+  if (!p) return;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(p->device);
+  cudaFree(p->tw_fwd);
+  cudaFree(p->tw_inv);
+  cudaFree(p->lc);
+  for (auto* m : p->mc) cudaFree(m);
+  cudaSetDevice(cur);
+  delete p;
+}
+
+int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli,
+                   const uint64_t* roots, uint32_t nlimbs, int bit_shift) {
+  if (!out || !moduli) return fail(NK_ERR_NULL, "nk_plan_create: NULL argument");
+  *out = nullptr;
+  if (nlimbs == 0) return fail(NK_ERR_LIMB, "nk_plan_create: at least one modulus is required");
+  // host tables first: argument errors are reported before any device work
+  std::vector<nk::host::Tables> tabs(nlimbs);
+  std::string msg;
+  for (uint32_t l = 0; l < nlimbs; ++l)
+    if (int rc = nk::host::build_tables(n, moduli[l], roots ? &roots[l] : nullptr, bit_shift,
+                                        &tabs[l], &msg))
+      return fail(rc, msg);
+  if (int rc = ensure_device(device)) return rc;
+  nk_plan* p = new nk_plan();
+  p->device = device;
+  p->n = n;
+  p->logn = tabs[0].logn;
+  p->nlimbs = nlimbs;
+  std::vector<ulonglong2> hf(n * nlimbs), hi(n * nlimbs);
+  std::vector<nk::LimbConst> hl(nlimbs);
+  std::vector<nk::MultConst> hm[3];
+  for (auto& v : hm) v.resize(nlimbs);
+  for (uint32_t l = 0; l < nlimbs; ++l) {
+    const auto& t = tabs[l];
+    p->q.push_back(t.q);
+    p->psi.push_back(t.psi);
+    p->bs.push_back(t.bs);
+    for (uint64_t i = 0; i < n; ++i) {
+      hf[l * n + i] = make_ulonglong2(t.w[i], t.wp[i]);
+      hi[l * n + i] = make_ulonglong2(t.wi[i], t.wip[i]);
+    }
+    // -q modulo 2^64 (the 52-bit negated modulus of ntt.hpp:85-92 agrees modulo 2^52,
+    // see modmath.cuh)
+    hl[l] = nk::LimbConst{t.q, 2 * t.q, ~t.q + 1, t.ninv, t.ninvp, t.bs, 0};
+    nk::host::Modulus m;
+    nk::host::make_modulus(t.q, &m);
+    const int fins[3] = {1, 2, 4};
+    for (int f = 0; f < 3; ++f) hm[f][l] = nk::MultConst{t.q, 2 * t.q, m.barrett, m.bits - 1, fins[f]};
+  }
+  auto cleanup = [&](int rc) { nk_plan_destroy(p); return rc; };
+  cudaError_t e;
+  if ((e = cudaMalloc(&p->tw_fwd, hf.size() * sizeof(ulonglong2))) ||
+      (e = cudaMalloc(&p->tw_inv, hi.size() * sizeof(ulonglong2))) ||
+      (e = cudaMalloc(&p->lc, hl.size() * sizeof(nk::LimbConst))))
+    return cleanup(cuda_fail(e, "cudaMalloc(plan tables)"));
+  for (int f = 0; f < 3; ++f)
+    if ((e = cudaMalloc(&p->mc[f], nlimbs * sizeof(nk::MultConst))))
+      return cleanup(cuda_fail(e, "cudaMalloc(plan consts)"));
+  if ((e = cudaMemcpy(p->tw_fwd, hf.data(), hf.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(p->tw_inv, hi.data(), hi.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(p->lc, hl.data(), hl.size() * sizeof(nk::LimbConst), cudaMemcpyHostToDevice)))
+    return cleanup(cuda_fail(e, "cudaMemcpy(plan tables)"));
+  for (int f = 0; f < 3; ++f)
+    if ((e = cudaMemcpy(p->mc[f], hm[f].data(), nlimbs * sizeof(nk::MultConst), cudaMemcpyHostToDevice)))
+      return cleanup(cuda_fail(e, "cudaMemcpy(plan consts)"));
+  *out = p;
+  return 0;
+}
+
+int nk_plan_info(const nk_plan* p, uint32_t limb, uint64_t* n, uint64_t* q, uint64_t* psi,
+                 int* bit_shift, uint32_t* nlimbs) {
+  if (!p) return fail(NK_ERR_NULL, "plan is NULL");
+  if (limb >= p->nlimbs) return fail(NK_ERR_LIMB, "limb outside the plan");
+  if (n) *n = p->n;
+  if (q) *q = p->q[limb];
+  if (psi) *psi = p->psi[limb];
+  if (bit_shift) *bit_shift = p->bs[limb];
+  if (nlimbs) *nlimbs = p->nlimbs;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// transforms
+// ---------------------------------------------------------------------------
+int nk_ntt_forward(const nk_plan* p, uint64_t* res, const uint64_t* op, uint32_t limb0,
+                   uint32_t nlimbs, uint32_t npolys, uint64_t fin, uint64_t fout, void* stream) {
+  if (fin != 1 && fin != 2 && fin != 4)
+    return fail(NK_ERR_FWD_IN_FACTOR, "forward: input_mod_factor must be 1, 2 or 4");
+  if (fout != 1 && fout != 4)
+    return fail(NK_ERR_FWD_OUT_FACTOR, "forward: output_mod_factor must be 1 or 4");
+  if (int rc = check_limbs(p, limb0, nlimbs)) return rc;
+  if (!res || !op) return fail(NK_ERR_NULL, "forward: NULL buffer");
+  if (overlap_bad(res, op, static_cast<uint64_t>(npolys) * nlimbs * p->n * 8))
+    return fail(NK_ERR_OVERLAP, "forward: result and operand must alias fully or not overlap");
+  if (int rc = ensure_device(p->device)) return rc;
+  return ntt_dispatch(p, true, res, op, limb0, nlimbs, npolys, fin, fout, S(stream));
+}
+
+int nk_ntt_inverse(const nk_plan* p, uint64_t* res, const uint64_t* op, uint32_t limb0,
+                   uint32_t nlimbs, uint32_t npolys, uint64_t fin, uint64_t fout, void* stream) {
+  if (fin != 1 && fin != 2)
+    return fail(NK_ERR_INV_IN_FACTOR, "inverse: input_mod_factor must be 1 or 2");
+  if (fout != 1 && fout != 2)
+    return fail(NK_ERR_INV_OUT_FACTOR, "inverse: output_mod_factor must be 1 or 2");
+  if (int rc = check_limbs(p, limb0, nlimbs)) return rc;
+  if (!res || !op) return fail(NK_ERR_NULL, "inverse: NULL buffer");
+  if (overlap_bad(res, op, static_cast<uint64_t>(npolys) * nlimbs * p->n * 8))
+    return fail(NK_ERR_OVERLAP, "inverse: result and operand must alias fully or not overlap");
+  if (int rc = ensure_device(p->device)) return rc;
+  return ntt_dispatch(p, false, res, op, limb0, nlimbs, npolys, fin, fout, S(stream));
+}
+
+int nk_plan_eltwise_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* a, const uint64_t* b,
+                             uint32_t limb0, uint32_t nlimbs, uint32_t npolys, uint64_t fin,
+                             void* stream) {
+  if (int rc = check_limbs(p, limb0, nlimbs)) return rc;
+  if (fin != 1 && fin != 2 && fin != 4)
+    return fail(NK_ERR_MULT_FACTOR, "eltwise_mult_mod: input_mod_factor must be 1, 2 or 4");
+  for (uint32_t l = 0; l < nlimbs; ++l)
+    if (p->q[limb0 + l] >= (uint64_t{1} << 50) && u128{fin} * p->q[limb0 + l] >= (u128{1} << 63))
+      return fail(NK_ERR_MULT_INT_RANGE, "eltwise_mult_mod_int: requires input_mod_factor*q < 2^63");
+  if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_mult_mod: NULL buffer");
+  if (npolys == 0) return 0;
+  if (int rc = ensure_device(p->device)) return rc;
+  const int fi = fin == 1 ? 0 : (fin == 2 ? 1 : 2);
+  const uint64_t rows = static_cast<uint64_t>(npolys) * nlimbs;
+  nk::eltwise_mult_kernel<<<eltwise_grid(rows * p->n / 2), 256, 0, S(stream)>>>(
+      res, a, b, p->n, rows, nk::MultConst{}, p->mc[fi] + limb0, nlimbs);
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const uint64_t* g,
+                     uint32_t limb0, uint32_t nlimbs, uint32_t npolys, void* stream) {
+  if (int rc = check_limbs(p, limb0, nlimbs)) return rc;
+  for (uint32_t l = 0; l < nlimbs; ++l)
+    if (p->q[limb0 + l] >= (uint64_t{1} << 61))
+      return fail(NK_ERR_POLY_MODULUS, "poly_mult_mod: requires q < 2^61");
+  if (!res || !f || !g) return fail(NK_ERR_NULL, "poly_mult_mod: NULL buffer");
+  const uint64_t bytes = static_cast<uint64_t>(npolys) * nlimbs * p->n * 8;
+  if (overlap_bad(res, f, bytes) || overlap_bad(res, g, bytes))
+    return fail(NK_ERR_OVERLAP, "poly_mult_mod: result must alias an operand fully or not overlap");
+  if (npolys == 0) return 0;
+  if (int rc = ensure_device(p->device)) return rc;
+  cudaStream_t st = S(stream);
+  uint64_t* gh = nullptr;
+  NK_CUDA(cudaMallocAsync(&gh, bytes, st));
+  // ring.hpp:39-42: g^ = fwd(g,1,4) first so that result may alias g
+  int rc = ntt_dispatch(p, true, gh, g, limb0, nlimbs, npolys, 1, 4, st);
+  if (!rc) rc = ntt_dispatch(p, true, res, f, limb0, nlimbs, npolys, 1, 4, st);
+  if (!rc) rc = nk_plan_eltwise_mult_mod(p, res, res, gh, limb0, nlimbs, npolys, 4, stream);
+  if (!rc) rc = ntt_dispatch(p, false, res, res, limb0, nlimbs, npolys, 1, 1, st);
+  cudaError_t e = cudaFreeAsync(gh, st);
+  if (rc) return rc;
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// element-wise (single modulus)
+// ---------------------------------------------------------------------------
+int nk_eltwise_mult_mod(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
+                        uint64_t fin, void* stream) {
+  nk::host::Modulus m;
+  if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
+  // dispatch of eltwise.hpp:180-188 and the checks of the path it picks
+  if (fin != 1 && fin != 2 && fin != 4)
+    return fail(NK_ERR_MULT_FACTOR, "eltwise_mult_mod: input_mod_factor must be 1, 2 or 4");
+  if (q >= (uint64_t{1} << 50) && u128{fin} * q >= (u128{1} << 63))
+    return fail(NK_ERR_MULT_INT_RANGE, "eltwise_mult_mod_int: requires input_mod_factor*q < 2^63");
+  if (n == 0) return 0;
+  if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_mult_mod: NULL buffer");
+  const nk::MultConst c{q, 2 * q, m.barrett, m.bits - 1, static_cast<int>(fin)};
+  cudaStream_t st = S(stream);
+  nk::eltwise_mult_kernel<<<eltwise_grid(n / 2 + 1), 256, 0, st>>>(res, a, b, n, 1, c, nullptr, 1);
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int nk_eltwise_fma_mod(uint64_t* res, const uint64_t* a, uint64_t y, const uint64_t* z, uint64_t n,
+                       uint64_t q, uint64_t fin, int bit_shift, void* stream) {
+  nk::host::Modulus m;
+  if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
+  int bs = bit_shift;
+  if (bs == 0) bs = (u128{fin} * q < (u128{1} << 52)) ? 52 : 64;  // eltwise.hpp:266
+  if (bs != 52 && bs != 64) return fail(NK_ERR_BIT_SHIFT, "eltwise_fma_mod: accumulator width must be 52 or 64");
+  if (fin != 1 && fin != 2 && fin != 4 && fin != 8)
+    return fail(NK_ERR_FMA_FACTOR, "eltwise_fma_mod: input_mod_factor must be 1, 2, 4 or 8");
+  if (q >= (uint64_t{1} << 61)) return fail(NK_ERR_FMA_MODULUS, "eltwise_fma_mod: requires q < 2^61");
+  if (y >= q) return fail(NK_ERR_FMA_SCALAR, "eltwise_fma_mod: scalar must be < q");
+  if (u128{fin} * q >= (u128{1} << bs))
+    return fail(NK_ERR_FMA_WIDTH, "eltwise_fma_mod: requires input_mod_factor*q < 2^BitShift");
+  if (n == 0) return 0;
+  if (!res || !a) return fail(NK_ERR_NULL, "eltwise_fma_mod: NULL buffer");
+  const nk::FmaConst c{q, y, static_cast<uint64_t>((static_cast<u128>(y) << bs) / q),
+                       static_cast<int>(fin), bs};
+  cudaStream_t st = S(stream);
+  const unsigned grid = eltwise_grid(n / 2 + 1);
+  if (bs == 52) {
+    if (z) nk::eltwise_fma_kernel<52, true><<<grid, 256, 0, st>>>(res, a, z, n, c);
+    else nk::eltwise_fma_kernel<52, false><<<grid, 256, 0, st>>>(res, a, z, n, c);
+  } else {
+    if (z) nk::eltwise_fma_kernel<64, true><<<grid, 256, 0, st>>>(res, a, z, n, c);
+    else nk::eltwise_fma_kernel<64, false><<<grid, 256, 0, st>>>(res, a, z, n, c);
+  }
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int nk_eltwise_add_mod(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
+                       void* stream) {
+  nk::host::Modulus m;
+  if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
+  if (n == 0) return 0;
+  if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_add_mod: NULL buffer");
+  nk::eltwise_add_kernel<<<eltwise_grid(n), 256, 0, S(stream)>>>(res, a, b, n, q);
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int nk_eltwise_neg_mod(uint64_t* res, const uint64_t* a, uint64_t n, uint64_t q, void* stream) {
+  nk::host::Modulus m;
+  if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
+  if (n == 0) return 0;
+  if (!res || !a) return fail(NK_ERR_NULL, "eltwise_neg_mod: NULL buffer");
+  nk::eltwise_neg_kernel<<<eltwise_grid(n), 256, 0, S(stream)>>>(res, a, n, q);
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// host-buffer wrappers: H2D, kernels, D2H on `stream`, then wait.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct DevBuf {
+  uint64_t* p = nullptr;
+  cudaStream_t st = nullptr;
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+};
+
+int h2d(DevBuf& d, const uint64_t* h, uint64_t words, cudaStream_t st) {
+  d.st = st;
+  NK_CUDA(cudaMallocAsync(&d.p, words * 8, st));
+  if (h) NK_CUDA(cudaMemcpyAsync(d.p, h, words * 8, cudaMemcpyHostToDevice, st));
+  return 0;
+}
+
+int finish(uint64_t* h, const DevBuf& d, uint64_t words, cudaStream_t st) {
+  NK_CUDA(cudaMemcpyAsync(h, d.p, words * 8, cudaMemcpyDeviceToHost, st));
+  NK_CUDA(cudaStreamSynchronize(st));
+  return 0;
+}
+
+int ntt_host(bool fwd, const nk_plan* p, uint64_t* res, const uint64_t* op, uint64_t length,
+             uint32_t limb0, uint32_t nlimbs, uint32_t npolys, uint64_t fin, uint64_t fout,
+             void* stream) {
+  if (!p) return fail(NK_ERR_NULL, "plan is NULL");
+  const uint64_t words = static_cast<uint64_t>(npolys) * nlimbs * p->n;
+  if (length != words) return fail(NK_ERR_LENGTH, "transform: buffer length must equal n");
+  if (!res || !op) return fail(NK_ERR_NULL, "transform: NULL buffer");
+  if (int rc = ensure_device(p->device)) return rc;
+  cudaStream_t st = S(stream);
+  DevBuf d;
+  if (int rc = h2d(d, op, words, st)) return rc;
+  int rc = fwd ? nk_ntt_forward(p, d.p, d.p, limb0, nlimbs, npolys, fin, fout, stream)
+               : nk_ntt_inverse(p, d.p, d.p, limb0, nlimbs, npolys, fin, fout, stream);
+  if (rc) return rc;
+  return finish(res, d, words, st);
+}
+
+}  // namespace
+
+int nk_ntt_forward_host(const nk_plan* p, uint64_t* res, const uint64_t* op, uint64_t length,
+                        uint32_t limb0, uint32_t nlimbs, uint32_t npolys, uint64_t fin,
+                        uint64_t fout, void* stream) {
+  if (fin != 1 && fin != 2 && fin != 4)
+    return fail(NK_ERR_FWD_IN_FACTOR, "forward: input_mod_factor must be 1, 2 or 4");
+  if (fout != 1 && fout != 4)
+    return fail(NK_ERR_FWD_OUT_FACTOR, "forward: output_mod_factor must be 1 or 4");
+  return ntt_host(true, p, res, op, length, limb0, nlimbs, npolys, fin, fout, stream);
+}
+
+int nk_ntt_inverse_host(const nk_plan* p, uint64_t* res, const uint64_t* op, uint64_t length,
+                        uint32_t limb0, uint32_t nlimbs, uint32_t npolys, uint64_t fin,
+                        uint64_t fout, void* stream) {
+  if (fin != 1 && fin != 2)
+    return fail(NK_ERR_INV_IN_FACTOR, "inverse: input_mod_factor must be 1 or 2");
+  if (fout != 1 && fout != 2)
+    return fail(NK_ERR_INV_OUT_FACTOR, "inverse: output_mod_factor must be 1 or 2");
+  return ntt_host(false, p, res, op, length, limb0, nlimbs, npolys, fin, fout, stream);
+}
+
+int nk_poly_mult_mod_host(const nk_plan* p, uint64_t* res, const uint64_t* f, const uint64_t* g,
+                          uint64_t length, uint32_t limb0, uint32_t nlimbs, uint32_t npolys,
+                          void* stream) {
+  if (!p) return fail(NK_ERR_NULL, "plan is NULL");
+  const uint64_t words = static_cast<uint64_t>(npolys) * nlimbs * p->n;
+  if (length != words) return fail(NK_ERR_LENGTH, "poly_mult_mod: operand lengths must equal n");
+  if (!res || !f || !g) return fail(NK_ERR_NULL, "poly_mult_mod: NULL buffer");
+  if (int rc = ensure_device(p->device)) return rc;
+  cudaStream_t st = S(stream);
+  DevBuf df, dg;
+  if (int rc = h2d(df, f, words, st)) return rc;
+  if (int rc = h2d(dg, g, words, st)) return rc;
+  if (int rc = nk_poly_mult_mod(p, df.p, df.p, dg.p, limb0, nlimbs, npolys, stream)) return rc;
+  return finish(res, df, words, st);
+}
+
+int nk_eltwise_mult_mod_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n,
+                             uint64_t q, uint64_t fin, int device, void* stream) {
+  if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_mult_mod: NULL buffer");
+  if (int rc = ensure_device(device)) return rc;
+  cudaStream_t st = S(stream);
+  DevBuf da, db;
+  if (int rc = h2d(da, a, n, st)) return rc;
+  if (int rc = h2d(db, b, n, st)) return rc;
+  if (int rc = nk_eltwise_mult_mod(da.p, da.p, db.p, n, q, fin, stream)) return rc;
+  return finish(res, da, n, st);
+}
+
+int nk_eltwise_fma_mod_host(uint64_t* res, const uint64_t* a, uint64_t y, const uint64_t* z,
+                            uint64_t n, uint64_t q, uint64_t fin, int bit_shift, int device,
+                            void* stream) {
+  if (!res || !a) return fail(NK_ERR_NULL, "eltwise_fma_mod: NULL buffer");
+  if (int rc = ensure_device(device)) return rc;
+  cudaStream_t st = S(stream);
+  DevBuf da, dz;
+  if (int rc = h2d(da, a, n, st)) return rc;
+  if (z)
+    if (int rc = h2d(dz, z, n, st)) return rc;
+  if (int rc = nk_eltwise_fma_mod(da.p, da.p, y, z ? dz.p : nullptr, n, q, fin, bit_shift, stream))
+    return rc;
+  return finish(res, da, n, st);
+}
+
+}  // extern "C"

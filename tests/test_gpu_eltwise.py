@@ -1,0 +1,223 @@
+"""GPU parity: element-wise kernels and poly multiply against the oracle.
+
+Mirrors tests/test_eltwise.cpp and tests/test_ring.cpp of the reference
+(boundary-heavy samplers, float-path correction triples, factor-8 boundary,
+FMA known answer, schoolbook and monomial-sign known answers) plus the
+BASELINE cfg2 / cfg5 shapes.
+"""
+import numpy as np
+import pytest
+import torch
+
+from primes import (cfg2_modulus, cfg5, config_seed, largest_ntt_primes, primes_with_bits,
+                    smallest_ntt_primes)
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint64).view(np.int64)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy().view(np.uint64)
+
+
+def sample_inputs(oracle, q, factor, n, seed):
+    """Boundary-heavy values in [0, factor*q) (test_eltwise.cpp:22-27)."""
+    v = oracle.mt19937_64(seed, n, factor * q)
+    edges = [0, 1, q - 1, q % (factor * q), factor * q - 1]
+    for i, e in enumerate(edges[:n]):
+        v[i] = e
+    return v
+
+
+MULT_QS = [17, 97] + [primes_with_bits(b, 1)[0] for b in (20, 30, 49, 50, 58, 60, 61, 62)]
+
+
+@pytest.mark.parametrize("q", MULT_QS)
+@pytest.mark.parametrize("fin", [1, 2, 4])
+@pytest.mark.parametrize("n", [1, 2, 7, 2048, 4097])
+def test_mult_matches_oracle(nk, oracle, q, fin, n):
+    if fin * q >= (1 << 63):
+        with pytest.raises(ValueError, match="input_mod_factor\\*q < 2\\^63"):
+            nk.eltwise_mult_mod(torch.empty(n, dtype=torch.int64, device="cuda"),
+                                dev(np.zeros(n)), dev(np.zeros(n)), q, fin)
+        return
+    a = sample_inputs(oracle, q, fin, n, 11 + n)
+    b = sample_inputs(oracle, q, fin, n, 12 + n)
+    r = torch.empty(n, dtype=torch.int64, device="cuda")
+    nk.eltwise_mult_mod(r, dev(a), dev(b), q, fin)
+    want = oracle.eltwise_mult_mod(a, b, q, fin)
+    assert np.array_equal(host(r), want)
+    # int and float reference paths agree where both apply
+    if q < (1 << 50):
+        assert np.array_equal(want, oracle.eltwise_mult_mod(a, b, q, fin, path=1))
+
+
+def test_float_path_correction_cases(nk, oracle):
+    """test_eltwise.cpp:117-133: quotient estimate overshoot triples."""
+    cases = [(1125899906842597, 1006683697935267, 1120468225943409),
+             (1125899906842201, 549202230126986, 905685617713605),
+             (562949953421381, 526777231650305, 71630581939326),
+             (1099511627689, 611973561147, 954725405533)]
+    for q, x, y in cases:
+        got = nk.eltwise_mult_mod(None, np.array([x], np.uint64), np.array([y], np.uint64), q, 1)
+        assert int(got[0]) == (x * y) % q
+
+
+def test_mult_identities(nk, oracle):
+    """test_eltwise.cpp:80-93."""
+    q = primes_with_bits(50, 1)[0]
+    a = oracle.mt19937_64(35, 256, 4 * q)
+    ones = np.ones(256, np.uint64)
+    got = nk.eltwise_mult_mod(None, a, ones, q, 4)
+    assert np.array_equal(got, a % np.uint64(q))
+    top = np.full(256, q - 1, np.uint64)
+    assert np.all(nk.eltwise_mult_mod(None, top, top, q, 1) == 1)
+
+
+FMA_QS = [17] + [primes_with_bits(b, 1)[0] for b in (20, 30, 48, 50, 60)]
+
+
+@pytest.mark.parametrize("q", FMA_QS)
+@pytest.mark.parametrize("fin", [1, 2, 4, 8])
+@pytest.mark.parametrize("bs", [0, 52, 64])
+@pytest.mark.parametrize("with_z", [True, False])
+def test_fma_matches_oracle(nk, oracle, q, fin, bs, with_z):
+    n = 1027
+    width = bs or (52 if fin * q < (1 << 52) else 64)
+    a = sample_inputs(oracle, q, fin, n, 45 + fin)
+    z = sample_inputs(oracle, q, fin, n, 46 + fin) if with_z else None
+    y = int(oracle.mt19937_64(47 + fin, 1, q)[0])
+    r = torch.empty(n, dtype=torch.int64, device="cuda")
+    if fin * q >= (1 << width):
+        with pytest.raises(ValueError, match="BitShift"):
+            nk.eltwise_fma_mod(r, dev(a), y, None if z is None else dev(z), q, fin, bs)
+        return
+    nk.eltwise_fma_mod(r, dev(a), y, None if z is None else dev(z), q, fin, bs)
+    want = oracle.eltwise_fma_mod(a, y, z, q, fin, bs)
+    assert np.array_equal(host(r), want)
+    exact = [(int(x) * y + (0 if z is None else int(zz))) % q
+             for x, zz in zip(a[:64], (z if z is not None else np.zeros(64, np.uint64))[:64])]
+    assert [int(v) for v in want[:64]] == exact
+
+
+def test_fma_known_answers(nk):
+    """test_eltwise.cpp:180-208: 2*3+4 mod 17 = 10; factor-8 boundary."""
+    out = nk.eltwise_fma_mod(None, np.array([2], np.uint64), 3, np.array([4], np.uint64), 17, 1)
+    assert int(out[0]) == 10
+    for bits in (20, 50, 60):
+        q = primes_with_bits(bits, 1)[0]
+        a = np.full(4, 8 * q - 1, np.uint64)
+        got = nk.eltwise_fma_mod(None, a, q - 1, a, q, 8)
+        assert all(int(v) == ((8 * q - 1) * (q - 1) + 8 * q - 1) % q for v in got)
+
+
+def test_add_neg(nk, oracle):
+    q = primes_with_bits(61, 1)[0]
+    a = oracle.mt19937_64(31, 4096, q)
+    b = oracle.mt19937_64(32, 4096, q)
+    r = torch.empty(4096, dtype=torch.int64, device="cuda")
+    nk.eltwise_add_mod(r, dev(a), dev(b), q)
+    assert np.array_equal(host(r), oracle.eltwise_add_mod(a, b, q))
+    a[0] = 0
+    nk.eltwise_neg_mod(r, dev(a), q)
+    assert np.array_equal(host(r), oracle.eltwise_neg_mod(a, q))
+
+
+def test_cfg2_full(nk, oracle):
+    """BASELINE cfg2: 2^20 words, q = largest prime < 2^60, fin 1: vector-vector,
+    vector-scalar (FMA without addend) and FMA."""
+    q = cfg2_modulus()
+    assert q == 1152921504606846883
+    n = 1 << 20
+    s = config_seed(2)
+    a = oracle.mt19937_64(s, n, q)
+    b = oracle.mt19937_64(s + 1, n, q)
+    z = oracle.mt19937_64(s + 2, n, q)
+    y = int(oracle.mt19937_64(s + 3, 1, q)[0])
+    r = torch.empty(n, dtype=torch.int64, device="cuda")
+    nk.eltwise_mult_mod(r, dev(a), dev(b), q, 1)
+    assert np.array_equal(host(r), oracle.eltwise_mult_mod(a, b, q, 1))
+    nk.eltwise_fma_mod(r, dev(a), y, None, q, 1)
+    assert np.array_equal(host(r), oracle.eltwise_fma_mod(a, y, None, q, 1))
+    nk.eltwise_fma_mod(r, dev(a), y, dev(z), q, 1)
+    assert np.array_equal(host(r), oracle.eltwise_fma_mod(a, y, z, q, 1))
+
+
+# ---------------------------------------------------------------------------
+# ring
+# ---------------------------------------------------------------------------
+def test_poly_known_answers(nk):
+    """test_ring.cpp: X * X^(n-1) = -1, monomial sign table, ring identity."""
+    t = nk.NttTables(8, nk.Modulus(97))
+    for i in range(8):
+        for j in range(8):
+            xi = np.zeros(8, np.uint64)
+            xj = np.zeros(8, np.uint64)
+            xi[i] = 1
+            xj[j] = 1
+            want = np.zeros(8, np.uint64)
+            if i + j < 8:
+                want[i + j] = 1
+            else:
+                want[i + j - 8] = 96
+            assert np.array_equal(nk.poly_mult_mod(None, xi, xj, t), want), (i, j)
+
+
+@pytest.mark.parametrize("logn", [1, 2, 4, 6, 8])
+@pytest.mark.parametrize("bits", [20, 30, 50, 61])
+def test_poly_matches_naive(nk, oracle, logn, bits):
+    """test_ring.cpp:80-98."""
+    n = 1 << logn
+    q = smallest_ntt_primes(bits, n, 1)[0]
+    t = nk.NttTables(n, nk.Modulus(q))
+    for rep in range(3):
+        f = oracle.mt19937_64(53 + rep, n, q)
+        g = oracle.mt19937_64(54 + rep, n, q)
+        f[0] = q - 1
+        assert np.array_equal(nk.poly_mult_mod(None, f, g, t), oracle.naive_negacyclic(f, g, q))
+
+
+def test_poly_alias_and_errors(nk, oracle):
+    n = 16
+    t = nk.NttTables(n, nk.Modulus(97))
+    f = oracle.mt19937_64(57, n, 97)
+    g = oracle.mt19937_64(58, n, 97)
+    df, dg = dev(f), dev(g)
+    want = oracle.poly_mult_mod(n, [97], f, g)
+    t.poly_mult_mod(df, df, dg)
+    assert np.array_equal(host(df), want)
+    df = dev(f)
+    t.poly_mult_mod(dg, df, dg)  # result aliases g
+    assert np.array_equal(host(dg), want)
+    q62 = smallest_ntt_primes(62, 16, 1)[0]
+    t62 = nk.NttTables(16, nk.Modulus(q62))
+    with pytest.raises(ValueError, match="q < 2\\^61"):
+        nk.poly_mult_mod(None, f, g, t62)
+
+
+def test_cfg5_sample(nk, oracle):
+    """BASELINE cfg5 layout (N=16384, 16 limbs x 128 pairs): full GPU run, oracle
+    on a deterministic sample of 64 row pairs."""
+    c = cfg5()
+    n, moduli, npolys = c["n"], c["moduli"], c["npolys"]
+    plan = nk.RnsNtt(n, moduli)
+    L = len(moduli)
+    rows = npolys * L
+    s = config_seed(5)
+    f = np.empty((rows, n), np.uint64)
+    g = np.empty((rows, n), np.uint64)
+    for r in range(rows):
+        f[r] = oracle.mt19937_64(s + 2 * r, n, moduli[r % L])
+        g[r] = oracle.mt19937_64(s + 2 * r + 1, n, moduli[r % L])
+    df, dg = dev(f.reshape(-1)), dev(g.reshape(-1))
+    out = torch.empty_like(df)
+    plan.poly_mult_mod(out, df, dg)
+    got = host(out).reshape(rows, n)
+    sample = list(range(0, rows, rows // 64))[:64]
+    for r in sample:
+        want = oracle.poly_mult_mod(n, [moduli[r % L]], f[r], g[r])
+        assert np.array_equal(got[r], want), r

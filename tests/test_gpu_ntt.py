@@ -1,0 +1,199 @@
+"""GPU parity: the sm_100a NTT kernels (through the C-ABI) against the CPU
+oracle, bit for bit, canonical AND lazy outputs.
+
+Mirrors the reference's tests/test_ntt.cpp cases (known answers, lifted inputs
+across (fin, fout), round trips, accumulator widths, maximum size) and adds the
+batched RNS shapes of the BASELINE configs.
+"""
+import numpy as np
+import pytest
+import torch
+
+from primes import largest_ntt_primes, smallest_ntt_primes, config_seed, cfg3, cfg4
+
+pytestmark = pytest.mark.gpu
+
+FWD_FACTORS = [(1, 1), (1, 4), (2, 1), (2, 4), (4, 1), (4, 4)]
+INV_FACTORS = [(1, 1), (1, 2), (2, 1), (2, 2)]
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x).view(np.int64)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy().view(np.uint64)
+
+
+def lifted(oracle, x, moduli, n, fin, seed):
+    """x + q*r with r < fin, per row modulus (test_ntt.cpp:164-166)."""
+    if fin == 1:
+        return x.copy()
+    r = oracle.mt19937_64(seed, x.size, fin)
+    q = np.repeat(np.asarray(moduli, dtype=np.uint64), n)
+    q = np.tile(q, x.size // q.size)
+    return x + q * r
+
+
+def rows_of(oracle, moduli, n, npolys, seed):
+    """[npolys][nlimbs][n], row limb l uniform in [0, q_l)."""
+    out = np.empty((npolys, len(moduli), n), np.uint64)
+    k = 0
+    for p in range(npolys):
+        for l, q in enumerate(moduli):
+            out[p, l] = oracle.mt19937_64(seed + 1000 * k, n, q)
+            k += 1
+    return out.reshape(-1)
+
+
+def check_dir(nk, oracle, n, moduli, npolys, seed, fwd_factors=FWD_FACTORS,
+              inv_factors=INV_FACTORS, bit_shift=0):
+    plan = nk.RnsNtt(n, moduli, bit_shift=bit_shift)
+    x = rows_of(oracle, moduli, n, npolys, seed)
+    for fin, fout in fwd_factors:
+        xi = lifted(oracle, x, moduli, n, fin, seed + fin)
+        d = dev(xi)
+        out = torch.empty_like(d)
+        plan.forward(out, d, fin, fout)
+        want = oracle.forward(n, moduli, xi, fin, fout, bit_shift=bit_shift, threads=8)
+        got = host(out)
+        assert np.array_equal(got, want), f"fwd n={n} fin={fin} fout={fout} mism={np.sum(got != want)}"
+        # in place
+        plan.forward(d, d, fin, fout)
+        assert np.array_equal(host(d), want)
+    for fin, fout in inv_factors:
+        xi = lifted(oracle, x, moduli, n, fin, seed + 7 * fin)
+        d = dev(xi)
+        out = torch.empty_like(d)
+        plan.inverse(out, d, fin, fout)
+        want = oracle.inverse(n, moduli, xi, fin, fout, bit_shift=bit_shift, threads=8)
+        got = host(out)
+        assert np.array_equal(got, want), f"inv n={n} fin={fin} fout={fout} mism={np.sum(got != want)}"
+
+
+@pytest.mark.parametrize("logn", list(range(1, 11)))
+@pytest.mark.parametrize("bits", [20, 30, 50, 61])
+def test_small_sizes_match_oracle(nk, oracle, logn, bits):
+    n = 1 << logn
+    moduli = smallest_ntt_primes(bits, n, 2)
+    check_dir(nk, oracle, n, moduli, 3, 100 + logn * 7 + bits)
+
+
+@pytest.mark.parametrize("logn", [11, 12, 13, 14])
+@pytest.mark.parametrize("bits", [30, 50, 60, 61])
+def test_block_sizes_match_oracle(nk, oracle, logn, bits):
+    n = 1 << logn
+    moduli = largest_ntt_primes(bits, n, 3)
+    check_dir(nk, oracle, n, moduli, 2, 300 + logn * 7 + bits)
+
+
+@pytest.mark.parametrize("logn", [15, 16, 17, 18])
+@pytest.mark.parametrize("bits", [50, 60])
+def test_long_rows_match_oracle(nk, oracle, logn, bits):
+    n = 1 << logn
+    moduli = largest_ntt_primes(bits, n, 2)
+    check_dir(nk, oracle, n, moduli, 1, 500 + logn + bits,
+              fwd_factors=[(1, 1), (1, 4), (4, 1), (2, 4)], inv_factors=[(1, 1), (2, 1), (1, 2)])
+
+
+def test_maximum_size_round_trip(nk, oracle):
+    """test_ntt.cpp:335-347: N = 2^20 forward then inverse is the identity; plus
+    one direction against the oracle."""
+    n = 1 << 20
+    q = smallest_ntt_primes(50, n, 1)[0]
+    plan = nk.RnsNtt(n, [q])
+    x = oracle.mt19937_64(21, n, q)
+    d = dev(x)
+    f = plan.forward(torch.empty_like(d), d, 1, 1)
+    assert np.array_equal(host(f), oracle.forward(n, [q], x, 1, 1))
+    b = plan.inverse(torch.empty_like(d), f, 1, 1)
+    assert np.array_equal(host(b), x)
+
+
+@pytest.mark.parametrize("n", [64, 4096, 16384])
+def test_accumulator_widths(nk, oracle, n):
+    """Forced beta = 2^64 tables on a 50-bit prime agree with the oracle using the
+    same width; canonical outputs agree across widths (test_ntt.cpp:228-248)."""
+    moduli = largest_ntt_primes(49, n, 2)
+    check_dir(nk, oracle, n, moduli, 2, 77, bit_shift=64)
+    check_dir(nk, oracle, n, moduli, 2, 78, bit_shift=52)
+
+
+def test_mixed_width_limbs(nk, oracle):
+    """One plan with 50-bit (beta 2^52) and 60-bit (beta 2^64) limbs."""
+    n = 4096
+    moduli = [largest_ntt_primes(50, n, 1)[0], largest_ntt_primes(60, n, 1)[0],
+              largest_ntt_primes(40, n, 1)[0]]
+    check_dir(nk, oracle, n, moduli, 3, 91)
+
+
+def test_known_answers(nk):
+    """test_ntt.cpp:80-114: zero, delta and the n=2, q=5 by-hand vectors."""
+    t = nk.NttTables(2, nk.Modulus(5))
+    assert t.root() == 2
+    assert list(t.forward(None, np.array([1, 1], np.uint64), 1, 1)) == [3, 4]
+    assert list(t.inverse(None, np.array([3, 4], np.uint64), 1, 1)) == [1, 1]
+    assert list(t.inverse(None, np.zeros(2, np.uint64), 1, 1)) == [0, 0]
+    t8 = nk.NttTables(8, nk.Modulus(97))
+    assert list(t8.forward(None, np.zeros(8, np.uint64), 1, 1)) == [0] * 8
+    delta = np.zeros(8, np.uint64)
+    delta[0] = 42
+    assert list(t8.forward(None, delta, 1, 1)) == [42] * 8
+
+
+def test_custom_root(nk, oracle):
+    """NttTables(n, m, root) with a non-minimal primitive root (ntt.hpp:212-213)."""
+    n = 1024
+    q = largest_ntt_primes(50, n, 1)[0]
+    psi = oracle.minimal_primitive_root(2 * n, q)
+    root = oracle.lib.oc_pow_mod(psi, 3, q)  # odd power: still primitive
+    t = nk.NttTables(n, nk.Modulus(q), root)
+    assert t.root() == root
+    x = oracle.mt19937_64(3, n, q)
+    got = t.forward(None, x, 1, 4)
+    assert np.array_equal(got, oracle.forward(n, [q], x, 1, 4, root=root))
+    got = t.forward(None, x, 1, 1)
+    ref = oracle.reference_ntt(q, root, x, "forward")
+    assert np.array_equal(got, ref)
+
+
+def test_definitional_transform(nk, oracle):
+    """Against the O(N^2) definition (ntt.hpp:457-508) at cfg1 size."""
+    n = 4096
+    q = largest_ntt_primes(50, n, 1)[0]
+    t = nk.NttTables(n, nk.Modulus(q))
+    x = oracle.mt19937_64(config_seed(1), n, q)
+    f = t.forward(None, x, 1, 1)
+    assert np.array_equal(f, oracle.reference_ntt(q, t.root(), x, "forward"))
+    assert np.array_equal(t.inverse(None, f, 1, 1), x)
+
+
+def test_cfg3_full(nk, oracle):
+    """BASELINE cfg3: N=16384, 32 limbs x 64 polys, forward(1,1) and inverse(1,1)."""
+    c = cfg3()
+    n, moduli, npolys = c["n"], c["moduli"], c["npolys"]
+    plan = nk.RnsNtt(n, moduli)
+    x = rows_of(oracle, moduli, n, npolys, config_seed(3))
+    d = dev(x)
+    f = plan.forward(torch.empty_like(d), d, 1, 1)
+    fh = host(f)
+    assert np.array_equal(fh, oracle.forward(n, moduli, x, 1, 1, threads=16))
+    b = plan.inverse(torch.empty_like(d), f, 1, 1)
+    assert np.array_equal(host(b), x)
+
+
+def test_cfg4_full(nk, oracle):
+    """BASELINE cfg4: N=65536, 24 60-bit limbs x 16 polys, fwd(4,1) and inv(2,1)."""
+    c = cfg4()
+    n, moduli, npolys = c["n"], c["moduli"], c["npolys"]
+    plan = nk.RnsNtt(n, moduli)
+    x = rows_of(oracle, moduli, n, npolys, config_seed(4))
+    x4 = lifted(oracle, x, moduli, n, 4, 44)
+    d = dev(x4)
+    f = plan.forward(torch.empty_like(d), d, 4, 1)
+    fh = host(f)
+    assert np.array_equal(fh, oracle.forward(n, moduli, x4, 4, 1, threads=16))
+    x2 = lifted(oracle, fh, moduli, n, 2, 45)
+    b = plan.inverse(torch.empty_like(d), dev(x2), 2, 1)
+    assert np.array_equal(host(b), x)
