@@ -394,6 +394,32 @@ int oc_ntt_root(uint64_t n, uint64_t q, uint64_t root, int bit_shift, int dir, u
   return 0;
 }
 
+/* First `nstages` stages of forward_impl / inverse_impl (debug aid for kernel bring-up) */
+int oc_ntt_stages(uint64_t n, uint64_t q, int dir, uint64_t* a, uint64_t fin, int nstages) {
+  tables_t t;
+  int rc = tables_build(&t, n, q, 0, 0);
+  if (rc) return rc;
+  if (dir == 0) {
+    uint64_t tt = n >> 1, m = 1;
+    for (int s = 0; m < n && s < nstages; m <<= 1, tt >>= 1, ++s)
+      for (uint64_t i = 0; i < m; ++i)
+        for (uint64_t j = 0; j < tt; ++j)
+          fwd_bfly(&a[2 * i * tt + j], &a[2 * i * tt + j + tt], t.w[m + i], t.wp[m + i], &t,
+                   s == 0 && fin == 1);
+  } else {
+    uint64_t tt = 1, m = n;
+    for (int s = 0; m > 1 && s < nstages; m >>= 1, tt <<= 1, ++s) {
+      const uint64_t h = m >> 1;
+      for (uint64_t i = 0; i < h; ++i)
+        for (uint64_t j = 0; j < tt; ++j)
+          inv_bfly(&a[2 * i * tt + j], &a[2 * i * tt + j + tt], t.wi[h + i], t.wip[h + i], &t,
+                   s == 0 && fin == 1);
+    }
+  }
+  tables_free(&t);
+  return 0;
+}
+
 /* reference_ntt, ntt.hpp:457-508 (independent: only full-width % arithmetic) */
 int oc_reference_ntt(uint64_t n, uint64_t q, uint64_t psi, int dir, const uint64_t* a, uint64_t* out) {
   if (n < 2 || (n & (n - 1))) return -1;

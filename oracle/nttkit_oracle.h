@@ -61,6 +61,7 @@ int oc_ntt_inverse(uint64_t n, const uint64_t* moduli, uint32_t nmod, int bit_sh
                    uint64_t fin, uint64_t fout, int threads);
 int oc_ntt_root(uint64_t n, uint64_t q, uint64_t root, int bit_shift, int dir, uint64_t* result,
                 const uint64_t* operand, uint64_t fin, uint64_t fout);
+int oc_ntt_stages(uint64_t n, uint64_t q, int dir, uint64_t* a, uint64_t fin, int nstages);
 /* O(n^2) definitional transform (ntt.hpp:457-508); dir 0 = forward, 1 = inverse */
 int oc_reference_ntt(uint64_t n, uint64_t q, uint64_t psi, int dir,
                      const uint64_t* a, uint64_t* out);

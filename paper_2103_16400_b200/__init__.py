@@ -38,7 +38,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnttkit_b200.so")
+LIB_PATH = os.environ.get("NK_LIB_PATH") or os.path.join(_HERE, "libnttkit_b200.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "nttkit_b200.h")
 
 u64 = C.c_uint64
@@ -51,6 +51,7 @@ _SIGS = {
     "nk_last_error": (C.c_char_p, []),
     "nk_version": (C.c_char_p, []),
     "nk_launch_count": (u64, []),
+    "nk_debug_dump_to": (None, [vp]),
     "nk_modulus": (C.c_int, [u64, C.POINTER(C.c_uint32), u64p]),
     "nk_minimal_primitive_root": (C.c_int, [u64, u64, u64p]),
     "nk_tables_host": (C.c_int, [u64, u64, u64p, C.c_int, u64p, u64p, u64p, u64p, u64p, u64p,

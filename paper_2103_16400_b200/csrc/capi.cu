@@ -3,9 +3,11 @@
 // management, and kernel launches. No CPU compute fallback exists: every
 // transform and element-wise product runs in the sm_100a kernels below, and a
 // missing/failed CUDA device is reported as NK_ERR_CUDA.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -22,6 +24,7 @@ using nk::host::u128;
 namespace {
 
 thread_local std::string g_err;
+uint64_t* g_dbg = nullptr;  // nk_debug_dump_to()
 std::atomic<uint64_t> g_launches{0};
 
 int fail(int code, const std::string& msg) {
@@ -60,6 +63,12 @@ bool overlap_bad(const void* a, const void* b, uint64_t bytes) {
 
 cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
+uint64_t dbits(double d) {
+  uint64_t u;
+  std::memcpy(&u, &d, 8);
+  return u;
+}
+
 int ensure_device(int dev) {
   int cur = -1;
   NK_CUDA(cudaGetDevice(&cur));
@@ -86,60 +95,122 @@ struct nk_plan {
 // ---------------------------------------------------------------------------
 namespace {
 
-template <int LOGB, int BS, bool FWD>
-int launch_block_t(const nk::NttArgs& a, uint64_t grid, cudaStream_t st) {
-  constexpr int LOGV = 5;
-  constexpr size_t smem = nk::block_smem_bytes<LOGB, LOGV>();
-  static std::once_flag once[64];
-  static cudaError_t attr_err[64];
+// ---- TMA tensor maps (driver entry point fetched through the runtime) ----
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int encode_fn(EncodeTiledFn* out) {
+  static EncodeTiledFn fn = nullptr;
+  static cudaError_t err = cudaSuccess;
+  static std::once_flag once;
+  std::call_once(once, [&] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    if (err == cudaSuccess && q != cudaDriverEntryPointSuccess) err = cudaErrorNotSupported;
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  if (err != cudaSuccess) return cuda_fail(err, "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+  *out = fn;
+  return 0;
+}
+
+// 2D view [words/16][16] of a row buffer, 128B swizzle, boxes of 256 x 128 B.
+int make_row_map(CUtensorMap* map, const uint64_t* base, uint64_t words) {
+  EncodeTiledFn fn;
+  if (int rc = encode_fn(&fn)) return rc;
+  const cuuint64_t dims[2] = {16, words / 16};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {16, 256};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint64_t*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  return 0;
+}
+
+int sm_count() {
+  static int n[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  std::call_once(once[dev & 63], [&] {
-    attr_err[dev & 63] = cudaFuncSetAttribute(nk::ntt_block<LOGB, LOGV, BS, FWD>,
-                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(smem));
-  });
-  if (attr_err[dev & 63] != cudaSuccess) return cuda_fail(attr_err[dev & 63], "cudaFuncSetAttribute");
-  nk::ntt_block<LOGB, LOGV, BS, FWD><<<static_cast<unsigned>(grid), 1 << (LOGB - LOGV), smem, st>>>(a);
+  if (!n[dev & 63]) cudaDeviceGetAttribute(&n[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev & 63] ? n[dev & 63] : 148;
+}
+
+template <class K>
+int set_smem(K kernel, size_t bytes) {
+  // idempotent and cheap; done per launch so every device of the process is covered
+  NK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+  return 0;
+}
+
+template <class A, bool FWD, bool IL>
+int launch_tma_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
+  CUtensorMap map;
+  if (int rc = make_row_map(&map, a.in, buf_words)) return rc;
+  auto kern = nk::ntt_block14_tma<A, FWD, IL>;
+  if (int rc = set_smem(kern, nk::kTmaSmemBytes)) return rc;
+  const uint64_t g = nitems < static_cast<uint64_t>(sm_count()) ? nitems : sm_count();
+  kern<<<static_cast<unsigned>(g), 512, nk::kTmaSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));
   g_launches++;
   NK_CUDA(cudaGetLastError());
   return 0;
 }
 
-template <int BS, bool FWD>
-int launch_block(uint32_t logb, const nk::NttArgs& a, uint64_t grid, cudaStream_t st) {
-  switch (logb) {
-    case 11: return launch_block_t<11, BS, FWD>(a, grid, st);
-    case 12: return launch_block_t<12, BS, FWD>(a, grid, st);
-    case 13: return launch_block_t<13, BS, FWD>(a, grid, st);
-    default: return launch_block_t<14, BS, FWD>(a, grid, st);
-  }
+template <class A, bool FWD>
+int launch_tma(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm, cudaStream_t st) {
+  return iltm ? launch_tma_t<A, FWD, true>(a, nitems, buf_words, st)
+              : launch_tma_t<A, FWD, false>(a, nitems, buf_words, st);
 }
 
-template <int BS, bool FWD>
+template <int LOGB, class A, bool FWD, bool IL>
+int launch_block_t(const nk::NttArgs& a, uint64_t grid, cudaStream_t st) {
+  constexpr int LOGV = 5;
+  constexpr size_t smem = nk::block_smem_bytes<LOGB, LOGV>();
+  auto kern = nk::ntt_block<LOGB, LOGV, A, FWD, IL>;
+  if (smem > 48 * 1024)
+    if (int rc = set_smem(kern, smem)) return rc;
+  kern<<<static_cast<unsigned>(grid), 1 << (LOGB - LOGV), smem, st>>>(a);
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+template <class A, bool FWD>
+int launch_block(uint32_t logb, const nk::NttArgs& a, uint64_t grid, bool iltm, cudaStream_t st) {
+#define NK_LB(L) \
+  return iltm ? launch_block_t<L, A, FWD, true>(a, grid, st) : launch_block_t<L, A, FWD, false>(a, grid, st)
+  switch (logb) {
+    case 11: NK_LB(11);
+    case 12: NK_LB(12);
+    default: NK_LB(13);
+  }
+#undef NK_LB
+}
+
+template <class A, bool FWD>
 int launch_global(uint32_t k, uint32_t lo, bool first_iltm, bool last, const nk::NttArgs& a,
                   cudaStream_t st) {
   const uint64_t threads = a.rows << (a.logn - k);
   const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
   switch (k) {
-    case 1: nk::ntt_global_pass<1, BS, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
-    case 2: nk::ntt_global_pass<2, BS, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
-    default: nk::ntt_global_pass<3, BS, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
+    case 1: nk::ntt_global_pass<1, A, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
+    case 2: nk::ntt_global_pass<2, A, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
+    default: nk::ntt_global_pass<3, A, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
   }
   g_launches++;
   NK_CUDA(cudaGetLastError());
   return 0;
 }
 
-template <int BS, bool FWD>
+template <class A, bool FWD>
 int launch_small(const nk::NttArgs& a, cudaStream_t st) {
   const size_t smem = a.n * sizeof(uint64_t);
-  if (smem > 48 * 1024) {
-    NK_CUDA(cudaFuncSetAttribute(nk::ntt_small<BS, FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-  }
   const unsigned threads = static_cast<unsigned>(a.n / 2 < 256 ? a.n / 2 : 256);
-  nk::ntt_small<BS, FWD><<<static_cast<unsigned>(a.rows), threads, smem, st>>>(a);
+  nk::ntt_small<A, FWD><<<static_cast<unsigned>(a.rows), threads, smem, st>>>(a);
   g_launches++;
   NK_CUDA(cudaGetLastError());
   return 0;
@@ -147,36 +218,35 @@ int launch_small(const nk::NttArgs& a, cudaStream_t st) {
 
 constexpr uint32_t kLogBlock = 14;
 
-// Full transform of a.rows rows, all with accumulator width BS.
-template <int BS, bool FWD>
-int run_ntt(nk::NttArgs a, cudaStream_t st) {
+// Full transform of a.rows rows with arithmetic policy A. buf_words: words in
+// the input buffer (for the tensor map of the TMA kernel).
+template <class A, bool FWD>
+int run_ntt(nk::NttArgs a, uint64_t buf_words, cudaStream_t st) {
   const uint32_t logn = a.logn;
-  if (logn <= 10) return launch_small<BS, FWD>(a, st);
-  if (logn <= kLogBlock) return launch_block<BS, FWD>(logn, a, a.rows, st);
+  if (logn <= 10) return launch_small<A, FWD>(a, st);
+  if (logn < kLogBlock) return launch_block<A, FWD>(logn, a, a.rows, a.fin == 1, st);
+  if (logn == kLogBlock) return launch_tma<A, FWD>(a, a.rows, buf_words, a.fin == 1, st);
   // long rows: high bits in global passes of <= 3 stages, low 14 bits per block
   const uint32_t gbits = logn - kLogBlock;
   uint32_t ks[2] = {gbits, 0};
   if (gbits > 3) { ks[0] = (gbits + 1) / 2; ks[1] = gbits - ks[0]; }
   const int np = ks[1] ? 2 : 1;
-  const uint64_t grid = a.rows << gbits;
+  const uint64_t nitems = a.rows << gbits;
   if (FWD) {
     uint32_t top = logn;
     for (int p = 0; p < np; ++p) {
       const uint32_t lo = top - ks[p];
-      if (int rc = launch_global<BS, true>(ks[p], lo, p == 0 && a.fin == 1, false, a, st)) return rc;
+      if (int rc = launch_global<A, true>(ks[p], lo, p == 0 && a.fin == 1, false, a, st)) return rc;
       a.in = a.out;  // later passes run in place on the result
       top = lo;
     }
-    a.fin = 2;  // block stages never see the first stage
-    return launch_block<BS, true>(kLogBlock, a, grid, st);
+    return launch_tma<A, true>(a, nitems, buf_words, false, st);
   } else {
-    const int fout = a.fout;
-    if (int rc = launch_block<BS, false>(kLogBlock, a, grid, st)) return rc;
+    if (int rc = launch_tma<A, false>(a, nitems, buf_words, a.fin == 1, st)) return rc;
     a.in = a.out;
-    a.fout = fout;
     uint32_t lo = kLogBlock;
     for (int p = 0; p < np; ++p) {
-      if (int rc = launch_global<BS, false>(ks[p], lo, false, p == np - 1, a, st)) return rc;
+      if (int rc = launch_global<A, false>(ks[p], lo, false, p == np - 1, a, st)) return rc;
       lo += ks[p];
     }
     return 0;
@@ -203,6 +273,7 @@ int ntt_dispatch(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, 
   a.nlimbs = nlimbs;
   a.fin = static_cast<int>(fin);
   a.fout = static_cast<int>(fout);
+  a.dbg = g_dbg;
   if (npolys == 0) return 0;
   // one launch when the limb range shares an accumulator width, else one per limb
   bool uniform = true;
@@ -220,9 +291,13 @@ int ntt_dispatch(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, 
       b.row_add = l;
     }
     const int bs = p->bs[limb0 + (uniform ? 0 : l)];
+    const uint64_t words = static_cast<uint64_t>(npolys) * nlimbs * p->n;
     int rc;
-    if (bs == 52) rc = fwd ? run_ntt<52, true>(b, st) : run_ntt<52, false>(b, st);
-    else rc = fwd ? run_ntt<64, true>(b, st) : run_ntt<64, false>(b, st);
+    if (bs == 52)
+      rc = fwd ? run_ntt<nk::Arith52F, true>(b, words, st) : run_ntt<nk::Arith52F, false>(b, words, st);
+    else
+      rc = fwd ? run_ntt<nk::ArithInt<64>, true>(b, words, st)
+               : run_ntt<nk::ArithInt<64>, false>(b, words, st);
     if (rc) return rc;
   }
   return 0;
@@ -245,6 +320,7 @@ extern "C" {
 const char* nk_last_error(void) { return g_err.c_str(); }
 const char* nk_version(void) { return "nttkit_b200 0.1 (sm_100a)"; }
 uint64_t nk_launch_count(void) { return g_launches.load(); }
+void nk_debug_dump_to(uint64_t* d_buf) { g_dbg = d_buf; }
 
 int nk_modulus(uint64_t q, uint32_t* bits, uint64_t* barrett_factor) {
   nk::host::Modulus m;
@@ -327,13 +403,18 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
     p->q.push_back(t.q);
     p->psi.push_back(t.psi);
     p->bs.push_back(t.bs);
+    // beta = 2^52 limbs run on the FP64 pipe (nk::Arith52F): table words hold the
+    // doubles' bit patterns (exact: every value is below 2^52)
+    const bool fp = (t.bs == 52);
+    auto enc = [fp](uint64_t x) { return fp ? dbits(static_cast<double>(x)) : x; };
     for (uint64_t i = 0; i < n; ++i) {
-      hf[l * n + i] = make_ulonglong2(t.w[i], t.wp[i]);
-      hi[l * n + i] = make_ulonglong2(t.wi[i], t.wip[i]);
+      hf[l * n + i] = make_ulonglong2(enc(t.w[i]), enc(t.wp[i]));
+      hi[l * n + i] = make_ulonglong2(enc(t.wi[i]), enc(t.wip[i]));
     }
     // -q modulo 2^64 (the 52-bit negated modulus of ntt.hpp:85-92 agrees modulo 2^52,
     // see modmath.cuh)
-    hl[l] = nk::LimbConst{t.q, 2 * t.q, ~t.q + 1, t.ninv, t.ninvp, t.bs, 0};
+    hl[l] = nk::LimbConst{t.q, 2 * t.q, ~t.q + 1, enc(t.ninv), enc(t.ninvp), 2 * t.q + nk::kDBias,
+                          std::ldexp(static_cast<double>(t.q), -52), t.bs, 0};
     nk::host::Modulus m;
     nk::host::make_modulus(t.q, &m);
     const int fins[3] = {1, 2, 4};

@@ -102,4 +102,124 @@ __device__ __forceinline__ void inv_bfly(uint64_t& x0, uint64_t& x1, uint64_t w,
   x1 = mul_lazy<BS>(t, w, wp, negq);
 }
 
+// ---------------------------------------------------------------------------
+// beta = 2^52 on the FP64 pipe ("D representation").
+//
+// Measured on B200 (tools/pipe_bench.cu): IMAD 64/clk/SM, IMAD.WIDE and
+// IMAD.HI 32/clk/SM, DFMA/DMUL/DADD 64/clk/SM, IADD3/LOP3/SEL ~128/clk/SM.
+// The integer Shoup product above costs ~16 fma-pipe slots (6 wide products);
+// for beta = 2^52 (every operand < 2^52) the same words come out of 8 exact
+// FP64 operations:
+//   a value y in [0, 2^52) is carried as the bit pattern of the double
+//   2^52 + y, i.e. kDBias + y ("D(y)"), so additions, subtractions and the
+//   conditional subtractions stay integer ops (ALU pipe) on the bit patterns,
+//   and the double itself feeds the FMA pipe with no conversion instruction.
+//   mul_lazyD:  v  = D(x) - 2^52                       (exact: x)
+//               hq = fma_rd(W', v, 2^104)             = 2^104 + floor(W'x/2^52)*2^52
+//                    (the sum lies in [2^104, 2^105) where the ulp is 2^52, so
+//                     rounding down IS the reference's mul_hi<52>, modarith.hpp:133-139)
+//               qh = hq - 2^104                       (exact: qhat * 2^52)
+//               h1 = w*v (rn), l1 = fma(w, v, -h1)    (exact TwoProduct: h1 + l1 = w x)
+//               e  = fma(-qh, q*2^-52, h1)            (exact: |h1 - qhat q| < 2^53, integer)
+//               T  = e + l1                           (exact: w x - qhat q in [0, 2q))
+//   and D(T) = T + 2^52. T is the reference's mul_factor_lazy<52> result
+//   (ntt.hpp:97-101): same qhat, same representative.
+// ---------------------------------------------------------------------------
+constexpr uint64_t kDBias = 0x4330000000000000ull;  // bits of 2^52
+constexpr uint64_t kMask52 = (uint64_t{1} << 52) - 1;
+constexpr double kC52 = 4503599627370496.0;                   // 2^52
+constexpr double kC104 = 20282409603651670423947251286016.0;  // 2^104
+
+__device__ __forceinline__ double as_d(uint64_t b) { return __longlong_as_double(static_cast<long long>(b)); }
+__device__ __forceinline__ uint64_t as_u(double d) { return static_cast<uint64_t>(__double_as_longlong(d)); }
+
+// D(y) -> D(y - m) when y >= m else D(y); m <= 2^51.
+__device__ __forceinline__ uint64_t csubD(uint64_t yD, uint64_t m) {
+  const uint64_t d = yD - m;
+#if defined(NK_CSUBD_PLAIN)
+  return (hi32(d) >= 0x43300000u) ? d : yD;
+#else
+  uint64_t r;
+  // one 32-bit compare on the high word (ptxas would otherwise widen it to 64 bits)
+  asm("{\n\t.reg .pred p;\n\t.reg .b32 l, h;\n\t"
+      "mov.b64 {l, h}, %1;\n\t"
+      "setp.ge.u32 p, h, 0x43300000;\n\t"
+      "selp.b64 %0, %1, %2, p;\n\t}"
+      : "=l"(r)
+      : "l"(d), "l"(yD));
+  return r;
+#endif
+}
+
+__device__ __forceinline__ uint64_t mul_lazyD(uint64_t xD, double w, double wp, double qq) {
+  const double v = __dsub_rn(as_d(xD), kC52);
+  const double hq = __fma_rd(wp, v, kC104);
+  const double qh = __dsub_rn(hq, kC104);
+  const double h1 = __dmul_rn(w, v);
+  const double l1 = __fma_rn(w, v, -h1);
+  const double e = __fma_rn(-qh, qq, h1);
+  const double t = __dadd_rn(e, l1);
+  return as_u(__dadd_rn(t, kC52));
+}
+
+// ---------------------------------------------------------------------------
+// Arithmetic policies for the transform kernels. Values live in registers and
+// shared memory in the policy's representation; load()/store() convert at the
+// HBM boundary. Twiddle-table entries are 16 bytes {w, w'} in the policy's
+// format (uint64 for Arith64, the doubles' bit patterns for Arith52F).
+// ---------------------------------------------------------------------------
+struct LimbConstDev {
+  uint64_t q, twoq, negq, ninv, ninvp;  // Arith64: integers; Arith52F: ninv/ninvp are double bits
+  uint64_t twoq_bias;                   // 2q + kDBias
+  double qq;                            // q * 2^-52
+  int32_t bs;
+  int32_t pad;
+};
+
+template <int BS>
+struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)
+  static constexpr bool kFP = false;
+  __device__ static uint64_t load(uint64_t x) { return x; }
+  __device__ static uint64_t store(uint64_t x) { return x; }
+  template <bool ILTM>
+  __device__ static void fwd(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+    fwd_bfly<BS, ILTM>(x0, x1, w.x, w.y, c.twoq, c.negq);
+  }
+  template <bool ILTM>
+  __device__ static void inv(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+    inv_bfly<BS, ILTM>(x0, x1, w.x, w.y, c.twoq, c.negq);
+  }
+  __device__ static uint64_t scale_ninv(uint64_t x, const LimbConstDev& c) {
+    return mul_lazy<BS>(x, c.ninv, c.ninvp, c.negq);
+  }
+  __device__ static uint64_t csub(uint64_t x, uint64_t m) { return nk::csub(x, m); }
+};
+
+struct Arith52F {  // beta = 2^52 on the FP64 pipe (requires 4q < 2^52)
+  static constexpr bool kFP = true;
+  __device__ static uint64_t load(uint64_t x) { return x | kDBias; }
+  __device__ static uint64_t store(uint64_t xD) { return xD & kMask52; }
+  // fwd_butterfly<52, ILTM> (ntt.hpp:103-113) in the D representation
+  template <bool ILTM>
+  __device__ static void fwd(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+    const uint64_t u = ILTM ? x0 : csubD(x0, c.twoq);
+    const uint64_t t = mul_lazyD(x1, as_d(w.x), as_d(w.y), c.qq);
+    x0 = u + t - kDBias;
+    x1 = u + c.twoq_bias - t;
+  }
+  // inv_butterfly<52, ILTM> (ntt.hpp:115-130) in the D representation
+  template <bool ILTM>
+  __device__ static void inv(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+    const uint64_t t = x0 + c.twoq_bias - x1;
+    uint64_t s = x0 + x1 - kDBias;
+    if (!ILTM) s = csubD(s, c.twoq);
+    x0 = s;
+    x1 = mul_lazyD(t, as_d(w.x), as_d(w.y), c.qq);
+  }
+  __device__ static uint64_t scale_ninv(uint64_t xD, const LimbConstDev& c) {
+    return mul_lazyD(xD, as_d(c.ninv), as_d(c.ninvp), c.qq);
+  }
+  __device__ static uint64_t csub(uint64_t xD, uint64_t m) { return csubD(xD, m); }
+};
+
 }  // namespace nk

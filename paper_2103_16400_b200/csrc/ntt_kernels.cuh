@@ -12,33 +12,32 @@
 //   inverse, h = N >> (b+1), t = 2^b:        w_arr[h + (j >> (b+1))]  (ntt.hpp:416-420)
 // The forward runs b = logN-1 .. 0, the inverse b = 0 .. logN-1.
 //
-// Kernels:
-//  * ntt_block<LOGB, LOGV, BS, FWD>: one CTA transforms a contiguous block of
-//    2^LOGB words (a whole row when N <= 2^LOGB, else a sub-block whose high
-//    bits were already handled by ntt_global_pass). Each thread holds 2^LOGV
-//    words in registers; bits are processed in register passes of <= LOGV
-//    stages, with the block exchanged through a padded shared-memory image
-//    between passes (phys(j) = j + j>>4 + j>>8 + j>>12: additive over disjoint
-//    bit fields, so every shared-memory address is a per-thread base plus an
-//    immediate, and every exchange pattern used is bank-conflict free).
-//    Twiddles {w, w'} are one 16-byte load each.
-//  * ntt_global_pass<K, BS, FWD>: K stages on bits [lo, lo+K) of long rows
-//    (N > 2^LOGB), one column of 2^K words per thread, coalesced.
-//  * ntt_small<BS, FWD>: any N <= 2^14, stage-by-stage in shared memory; for the
-//    small sizes the reference tests use.
+// Kernels (A = arithmetic policy, modmath.cuh: Arith52F for beta = 2^52 on the
+// FP64 pipe, ArithInt<BS> otherwise):
+//  * ntt_block14_tma<A, FWD, ILTM0>: the hot kernel. Persistent, one 512-thread
+//    CTA per SM, walks 16384-word blocks (a whole row at N = 16384, or the low
+//    14 bits of a longer row). Each block arrives by TMA (cp.async.bulk.tensor,
+//    128B swizzle) into a shared staging buffer while the previous block is
+//    still being transformed; the block is transformed in registers (32 words
+//    per thread, three register passes of 5/5/4 stages) with two exchanges
+//    through a padded half-size shared buffer; results leave with coalesced
+//    stores.
+//  * ntt_block<LOGB, LOGV, A, FWD, ILTM0>: same register passes for
+//    2^11..2^14-word blocks, loads straight from global (latency-bound sizes).
+//  * ntt_global_pass<K, A, FWD>: K stages on bits [lo, lo+K) of long rows
+//    (N > 2^14), one column of 2^K words per thread, coalesced.
+//  * ntt_small<A, FWD>: any N <= 2^10, stage by stage in shared memory.
 #pragma once
+#include <cuda.h>
+
 #include <cstdint>
+#include <type_traits>
 
 #include "modmath.cuh"
 
 namespace nk {
 
-// Per-limb constants, resident on the device with the tables.
-struct LimbConst {
-  uint64_t q, twoq, negq, ninv, ninvp;
-  int32_t bs;
-  int32_t pad;
-};
+using LimbConst = LimbConstDev;
 
 struct NttArgs {
   uint64_t* out;
@@ -46,22 +45,25 @@ struct NttArgs {
   const ulonglong2* tw;  // [limb][N] {w, w'} of the plan (fwd or inv table)
   const LimbConst* lc;   // [limb]
   uint64_t n;            // row length
-  uint64_t rows;         // npolys * nlimbs
-  uint32_t limb0, nlimbs;  // row r (after remapping) holds limb limb0 + r % nlimbs
+  uint64_t rows;         // launched rows
+  uint32_t limb0, nlimbs;     // row r (after remapping) holds limb limb0 + r % nlimbs
   uint32_t row_mul, row_add;  // launched row i is row i * row_mul + row_add
   uint32_t logn;
   int32_t fin, fout;
+  uint64_t* dbg;  // debug: when set, the TMA kernel dumps each pass's words ([3][N]) for item 0
 };
 
 __device__ __forceinline__ ulonglong2 ldtw(const ulonglong2* p) { return __ldg(p); }
 
-// Shared-memory image index, see header comment.
+// Padded shared-memory image index: additive over disjoint bit fields, so every
+// shared address is a per-thread base plus an immediate, and all exchange
+// patterns below (lane strides 1, 16, 32, ..., 512 words) are conflict free.
 __host__ __device__ constexpr uint32_t smem_phys(uint32_t j) {
   return j + (j >> 4) + (j >> 8) + (j >> 12);
 }
 
 // ---------------------------------------------------------------------------
-// compile-time pass schedule of the block kernel
+// compile-time pass schedule of the block kernels
 // ---------------------------------------------------------------------------
 template <int LOGB, int LOGV>
 struct Sched {
@@ -80,47 +82,11 @@ struct Sched {
   __host__ __device__ static constexpr uint32_t scatter(uint32_t o, int lo_, int k_) {
     return (o & ((1u << lo_) - 1u)) | ((o >> lo_) << (lo_ + k_));
   }
-};
-
-// One pass: K butterfly bits [LO, LO+K) over G = V / 2^K independent groups held
-// in v[g * 2^K + r]. xt = N + block offset + scattered thread index (bits outside
-// the pass only). STAGE0_ILTM: apply the first stage of the pass with
-// InputLessThanMod (reference's fin == 1 specialisation).
-template <int BS, bool FWD, int LOGT, int LOGV, int LO, int K>
-__device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const ulonglong2* __restrict__ tw,
-                                        uint64_t xt, bool first_iltm, uint64_t twoq,
-                                        uint64_t negq) {
-  constexpr int R = 1 << K;
-  constexpr int G = (1 << LOGV) / R;
-#pragma unroll
-  for (int s = 0; s < K; ++s) {
-    const int i = FWD ? (K - 1 - s) : s;  // bit within the pass
-    const int b = LO + i;                 // global bit
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const uint32_t jg = Sched<LOGT + LOGV, LOGV>::scatter(static_cast<uint32_t>(g) << LOGT, LO, K);
-      const uint64_t base = (xt + jg) >> (b + 1);
-#pragma unroll
-      for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
-        const ulonglong2 w = ldtw(tw + base + hi);
-#pragma unroll
-        for (int lo = 0; lo < (1 << i); ++lo) {
-          const int r0 = (hi << (i + 1)) | lo;
-          const int r1 = r0 | (1 << i);
-          uint64_t& x0 = v[g * R + r0];
-          uint64_t& x1 = v[g * R + r1];
-          if (FWD) {
-            if (s == 0 && first_iltm) fwd_bfly<BS, true>(x0, x1, w.x, w.y, twoq, negq);
-            else fwd_bfly<BS, false>(x0, x1, w.x, w.y, twoq, negq);
-          } else {
-            if (s == 0 && first_iltm) inv_bfly<BS, true>(x0, x1, w.x, w.y, twoq, negq);
-            else inv_bfly<BS, false>(x0, x1, w.x, w.y, twoq, negq);
-          }
-        }
-      }
-    }
+  // group g's contribution to the index in pass (lo_, k_)
+  __host__ __device__ static constexpr uint32_t jg(int g, int lo_, int k_) {
+    return scatter(static_cast<uint32_t>(g) << LOGT, lo_, k_);
   }
-}
+};
 
 // P-th pass in processing order.
 template <int LOGB, int LOGV, bool FWD>
@@ -131,45 +97,78 @@ struct PassOf {
   __host__ __device__ static constexpr int k(int p) { return S::k(td(p)); }
 };
 
-template <int LOGB, int LOGV, int BS, bool FWD, int P>
+// One register pass: K butterfly bits [LO, LO+K) over G = V / 2^K independent
+// groups held in v[g * 2^K + r]. xt = N + block offset + this thread's index
+// bits (outside the pass). ILTM0: first stage with InputLessThanMod.
+template <class A, bool FWD, int LOGB, int LOGV, int LO, int K, bool ILTM0>
+__device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const ulonglong2* __restrict__ tw,
+                                        uint64_t xt, const LimbConst& c) {
+  using S = Sched<LOGB, LOGV>;
+  constexpr int R = 1 << K;
+  constexpr int G = (1 << LOGV) / R;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const int i = FWD ? (K - 1 - s) : s;  // bit within the pass
+    const int b = LO + i;                 // bit of the block index
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint64_t base = (xt + S::jg(g, LO, K)) >> (b + 1);
+#pragma unroll
+      for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
+        const ulonglong2 w = ldtw(tw + base + hi);
+#pragma unroll
+        for (int l = 0; l < (1 << i); ++l) {
+          const int r0 = (hi << (i + 1)) | l;
+          const int r1 = r0 | (1 << i);
+          uint64_t& x0 = v[g * R + r0];
+          uint64_t& x1 = v[g * R + r1];
+          if (FWD) {
+            if (ILTM0 && s == 0) A::template fwd<true>(x0, x1, w, c);
+            else A::template fwd<false>(x0, x1, w, c);
+          } else {
+            if (ILTM0 && s == 0) A::template inv<true>(x0, x1, w, c);
+            else A::template inv<false>(x0, x1, w, c);
+          }
+        }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// ntt_block: register passes with full padded shared exchanges (2^11..2^14)
+// ---------------------------------------------------------------------------
+template <int LOGB, int LOGV, class A, bool FWD, int P, bool ILTM0>
 __device__ __forceinline__ void run_passes(uint64_t (&v)[1 << LOGV], uint64_t* sm,
                                            const ulonglong2* __restrict__ tw, uint32_t t,
-                                           uint64_t xbase, bool first_iltm, uint64_t twoq,
-                                           uint64_t negq) {
+                                           uint64_t xbase, const LimbConst& c) {
   using S = Sched<LOGB, LOGV>;
   using PO = PassOf<LOGB, LOGV, FWD>;
   constexpr int LO = PO::lo(P), K = PO::k(P);
   constexpr int R = 1 << K, G = S::V / R;
   const uint32_t jt = S::scatter(t, LO, K);
-  if (P > 0) {
-    // exchange: pass P-1 wrote its values to sm; read this pass's pattern
-    __syncthreads();
+  if constexpr (P > 0) {
+    __syncthreads();  // pass P-1 wrote its image
     const uint32_t bt = smem_phys(jt);
 #pragma unroll
     for (int g = 0; g < G; ++g)
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const uint32_t jc = S::scatter(static_cast<uint32_t>(g) << S::LOGT, LO, K) | (r << LO);
-        v[g * R + r] = sm[bt + smem_phys(jc)];
-      }
+      for (int r = 0; r < R; ++r) v[g * R + r] = sm[bt + smem_phys(S::jg(g, LO, K) | (r << LO))];
   }
-  do_pass<BS, FWD, S::LOGT, LOGV, LO, K>(v, tw, xbase + jt, P == 0 && first_iltm, twoq, negq);
+  do_pass<A, FWD, LOGB, LOGV, LO, K, ILTM0 && P == 0>(v, tw, xbase + jt, c);
   if constexpr (P + 1 < S::NP) {
     __syncthreads();  // every thread has read the previous image
+    const uint32_t bt = smem_phys(jt);
 #pragma unroll
     for (int g = 0; g < G; ++g)
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const uint32_t jc = S::scatter(static_cast<uint32_t>(g) << S::LOGT, LO, K) | (r << LO);
-        sm[smem_phys(jt) + smem_phys(jc)] = v[g * R + r];
-      }
-    run_passes<LOGB, LOGV, BS, FWD, P + 1>(v, sm, tw, t, xbase, false, twoq, negq);
+      for (int r = 0; r < R; ++r) sm[bt + smem_phys(S::jg(g, LO, K) | (r << LO))] = v[g * R + r];
+    run_passes<LOGB, LOGV, A, FWD, P + 1, ILTM0>(v, sm, tw, t, xbase, c);
   }
 }
 
-template <int LOGB, int LOGV, int BS, bool FWD>
-__global__ void __launch_bounds__(1 << (LOGB - LOGV))
-    ntt_block(NttArgs a) {
+template <int LOGB, int LOGV, class A, bool FWD, bool ILTM0>
+__global__ void __launch_bounds__(1 << (LOGB - LOGV)) ntt_block(NttArgs a) {
   using S = Sched<LOGB, LOGV>;
   using PO = PassOf<LOGB, LOGV, FWD>;
   extern __shared__ uint64_t sm[];
@@ -186,58 +185,56 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV))
   const bool whole = (lognb == 0);
 
   uint64_t v[S::V];
-  // ---- load: first pass pattern ----
   {
     constexpr int LO = PO::lo(0), K = PO::k(0);
     constexpr int R = 1 << K, G = S::V / R;
     const uint32_t jt = S::scatter(t, LO, K);
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const uint32_t jg = S::scatter(static_cast<uint32_t>(g) << S::LOGT, LO, K);
+      const uint32_t jg = S::jg(g, LO, K);
       if constexpr (LO == 0 && R >= 2) {
 #pragma unroll
         for (int r = 0; r < R; r += 2) {
           const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(src + jt + jg + r);
-          v[g * R + r] = p.x;
-          v[g * R + r + 1] = p.y;
+          v[g * R + r] = A::load(p.x);
+          v[g * R + r + 1] = A::load(p.y);
         }
       } else {
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[g * R + r] = src[jt + jg + (r << LO)];
+        for (int r = 0; r < R; ++r) v[g * R + r] = A::load(src[jt + jg + (r << LO)]);
       }
     }
   }
-  const bool first_iltm = (a.fin == 1) && (FWD ? whole : true);
-  run_passes<LOGB, LOGV, BS, FWD, 0>(v, sm, tw, t, a.n + boff, first_iltm, c.twoq, c.negq);
+  run_passes<LOGB, LOGV, A, FWD, 0, ILTM0>(v, sm, tw, t, a.n + boff, c);
 
-  // ---- fix-ups of the final pass and store ----
   constexpr int PL = S::NP - 1;
   constexpr int LO = PO::lo(PL), K = PO::k(PL);
   constexpr int R = 1 << K, G = S::V / R;
   if (FWD) {
     if (a.fout == 1) {
 #pragma unroll
-      for (int i = 0; i < S::V; ++i) v[i] = csub(csub(v[i], c.twoq), c.q);  // small_mod(x,q,4)
+      for (int i = 0; i < S::V; ++i) v[i] = A::csub(A::csub(v[i], c.twoq), c.q);  // small_mod(x,q,4)
     }
   } else if (whole) {
 #pragma unroll
-    for (int i = 0; i < S::V; ++i) v[i] = mul_lazy<BS>(v[i], c.ninv, c.ninvp, c.negq);
+    for (int i = 0; i < S::V; ++i) v[i] = A::scale_ninv(v[i], c);
     if (a.fout == 1) {
 #pragma unroll
-      for (int i = 0; i < S::V; ++i) v[i] = csub(v[i], c.q);  // small_mod(x,q,2)
+      for (int i = 0; i < S::V; ++i) v[i] = A::csub(v[i], c.q);  // small_mod(x,q,2)
     }
   }
   const uint32_t jt = S::scatter(t, LO, K);
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    const uint32_t jg = S::scatter(static_cast<uint32_t>(g) << S::LOGT, LO, K);
+    const uint32_t jg = S::jg(g, LO, K);
     if constexpr (LO == 0 && R >= 2) {
 #pragma unroll
       for (int r = 0; r < R; r += 2)
-        *reinterpret_cast<ulonglong2*>(dst + jt + jg + r) = make_ulonglong2(v[g * R + r], v[g * R + r + 1]);
+        *reinterpret_cast<ulonglong2*>(dst + jt + jg + r) =
+            make_ulonglong2(A::store(v[g * R + r]), A::store(v[g * R + r + 1]));
     } else {
 #pragma unroll
-      for (int r = 0; r < R; ++r) dst[jt + jg + (r << LO)] = v[g * R + r];
+      for (int r = 0; r < R; ++r) dst[jt + jg + (r << LO)] = A::store(v[g * R + r]);
     }
   }
 }
@@ -248,11 +245,310 @@ constexpr size_t block_smem_bytes() {
 }
 
 // ---------------------------------------------------------------------------
+// TMA / mbarrier primitives (sm_90+ PTX, sm_100a SASS: UTMALDG, SYNCS.*)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Byte offset of word j in a 128B-swizzled staging tile ([rows][16 words],
+// 16-byte chunk c of row r stored at chunk c ^ (r & 7)), as TMA writes it.
+__device__ __forceinline__ uint32_t swz_off(uint32_t j) {
+  const uint32_t row = j >> 4, col = j & 15;
+  return (row << 7) + ((((col >> 1) ^ (row & 7))) << 4) + ((col & 1) << 3);
+}
+
+// ---------------------------------------------------------------------------
+// ntt_block14_tma: the hot kernel (see the header comment).
+//
+// Pass schedule (each thread holds 32 words; a pass with K = 4 butterfly bits
+// also holds one extra index bit X in registers, as value-index bit 4):
+//   forward: P1 bits 13..9 | P2 bits 8..5 + X = 4  | P3 bits 4..0
+//   inverse: P1 bits 4..0  | P2 bits 8..5 + X = 13 | P3 bits 13..9
+// Exchange 1 (P1 -> P2) is a full exchange: words with index bit 13 clear go
+// to the padded half image B, the others to the staging buffer A (already
+// consumed), so no thread holds pending values while it reads. Only then is
+// the next block's TMA issued into A. Exchange 2 (P2 -> P3) uses B alone in
+// two rounds split on X, which is value-index bit 4 in both passes: a thread
+// writes v[16h..16h+15] and reads back into exactly those registers.
+// Shared: [A: 128 KiB, TMA staging / half image][B: padded half image][mbarrier]
+// ---------------------------------------------------------------------------
+constexpr int kB14 = 14;
+constexpr uint32_t kStageBytes = (1u << kB14) * 8;  // 128 KiB
+constexpr uint32_t kHalfWords = smem_phys((1u << (kB14 - 1)) - 1) + 1;
+constexpr size_t kTmaSmemBytes = 1024 /*align*/ + kStageBytes + kHalfWords * 8 + 16;
+
+// deposit the low bits of t into the set bits of MASK (ascending), like PDEP
+template <uint32_t MASK>
+__host__ __device__ __forceinline__ constexpr uint32_t pdep(uint32_t t) {
+  uint32_t res = 0;
+  int src = 0;
+#pragma unroll
+  for (int b = 0; b < 32;) {
+    if (!((MASK >> b) & 1u)) { ++b; continue; }
+    int len = 0;
+    while (b + len < 32 && ((MASK >> (b + len)) & 1u)) ++len;
+    res |= ((t >> src) & ((len == 32) ? ~0u : ((1u << len) - 1u))) << b;
+    src += len;
+    b += len;
+  }
+  return res;
+}
+
+// remove bit X from a 14-bit index (half-image index for a split on X)
+template <int X>
+__host__ __device__ __forceinline__ constexpr uint32_t squeeze(uint32_t j) {
+  return (j & ((1u << X) - 1u)) | ((j >> (X + 1)) << X);
+}
+
+template <int LO_, int K_, int X_>
+struct PassD {
+  static constexpr int LO = LO_, K = K_, X = X_;
+  static constexpr int R = 1 << K;
+  static constexpr int G = 32 / R;
+  static constexpr uint32_t bmask = ((1u << K) - 1u) << LO;
+  static constexpr uint32_t xmask = (X >= 0) ? (1u << X) : 0u;
+  static constexpr uint32_t tmask = ((1u << kB14) - 1u) & ~(bmask | xmask);
+  __device__ __forceinline__ static uint32_t jt(uint32_t t) { return pdep<tmask>(t); }
+  __host__ __device__ static constexpr uint32_t jc(int g, int r) {
+    return (g ? xmask : 0u) | (static_cast<uint32_t>(r) << LO);
+  }
+};
+
+template <bool FWD>
+struct Sched14 {
+  using P1 = typename std::conditional<FWD, PassD<9, 5, -1>, PassD<0, 5, -1>>::type;
+  using P2 = typename std::conditional<FWD, PassD<5, 4, 4>, PassD<5, 4, 13>>::type;
+  using P3 = typename std::conditional<FWD, PassD<0, 5, -1>, PassD<9, 5, -1>>::type;
+  static constexpr int X = FWD ? 4 : 13;  // split bit of exchange 2
+};
+
+// One register pass over the bits of PD (stage order by direction).
+template <class A, bool FWD, class PD, bool ILTM0>
+__device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __restrict__ tw,
+                                       uint64_t xt, const LimbConst& c) {
+  constexpr int K = PD::K, R = PD::R, G = PD::G;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const int i = FWD ? (K - 1 - s) : s;
+    const int b = PD::LO + i;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint64_t base = (xt + PD::jc(g, 0)) >> (b + 1);
+#pragma unroll
+      for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
+        const ulonglong2 w = ldtw(tw + base + hi);
+#pragma unroll
+        for (int l = 0; l < (1 << i); ++l) {
+          const int r0 = (hi << (i + 1)) | l;
+          const int r1 = r0 | (1 << i);
+          uint64_t& x0 = v[g * R + r0];
+          uint64_t& x1 = v[g * R + r1];
+          if (FWD) {
+            if (ILTM0 && s == 0) A::template fwd<true>(x0, x1, w, c);
+            else A::template fwd<false>(x0, x1, w, c);
+          } else {
+            if (ILTM0 && s == 0) A::template inv<true>(x0, x1, w, c);
+            else A::template inv<false>(x0, x1, w, c);
+          }
+        }
+      }
+    }
+  }
+}
+
+template <class A, bool FWD, bool ILTM0>
+__global__ void __launch_bounds__(512, 1)
+    ntt_block14_tma(const __grid_constant__ CUtensorMap tin, NttArgs a, uint32_t nitems) {
+  using SC = Sched14<FWD>;
+  using P1 = typename SC::P1;
+  using P2 = typename SC::P2;
+  using P3 = typename SC::P3;
+  constexpr int X = SC::X;
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  // 1024-byte alignment for the 128B-swizzle atoms, kept as shared-space pointer arithmetic
+  uint8_t* Astage = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+  uint64_t* Ahalf = reinterpret_cast<uint64_t*>(Astage);
+  uint64_t* B = reinterpret_cast<uint64_t*>(Astage + kStageBytes);
+  uint64_t* bar = B + kHalfWords + (kHalfWords & 1);
+  const uint32_t t = threadIdx.x;
+  const uint32_t lognb = a.logn - kB14;
+  const uint64_t rowwords16 = a.n >> 4;  // tensor rows (of 16 words) per data row
+
+  auto item_row = [&](uint32_t k, uint64_t& row, uint64_t& blk) {
+    row = (static_cast<uint64_t>(k) >> lognb) * a.row_mul + a.row_add;
+    blk = static_cast<uint64_t>(k) & ((uint64_t{1} << lognb) - 1);
+  };
+  auto issue = [&](uint32_t k) {
+    uint64_t row, blk;
+    item_row(k, row, blk);
+    const int32_t y0 = static_cast<int32_t>(row * rowwords16 + (blk << (kB14 - 4)));
+    mbar_expect_tx(bar, kStageBytes);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tma_load_2d(Astage + q * 32768, &tin, 0, y0 + q * 256, bar);
+  };
+
+  if (t == 0) {
+    mbar_init(bar, 1);
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tin)) : "memory");
+  }
+  __syncthreads();
+  if (t == 0 && blockIdx.x < nitems) issue(blockIdx.x);
+  uint32_t phase = 0;
+
+  const uint32_t jt1 = P1::jt(t), jt2 = P2::jt(t), jt3 = P3::jt(t);
+
+  for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
+    uint64_t row, blk;
+    item_row(k, row, blk);
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+    const LimbConst c = a.lc[limb];
+    const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * a.n;
+    const uint64_t boff = blk << kB14;
+    uint64_t* __restrict__ dst = a.out + row * a.n + boff;
+    const uint64_t xbase = a.n + boff;
+    uint64_t v[32];
+
+    // ---- P1 words from the swizzled staging buffer ----
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    if constexpr (P1::LO == 0) {
+      // 32 contiguous words (two tensor rows): 16-byte chunks
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t row16 = (jt1 >> 4) + h;
+        const uint32_t rowoff = row16 << 7, sw = row16 & 7;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Astage + rowoff + ((cc ^ sw) << 4));
+          v[16 * h + 2 * cc] = A::load(p.x);
+          v[16 * h + 2 * cc + 1] = A::load(p.y);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        v[r] = A::load(*reinterpret_cast<const uint64_t*>(Astage + swz_off(jt1 | P1::jc(0, r))));
+    }
+    __syncthreads();  // staging consumed (A is reused as a half image below)
+
+    pass14<A, FWD, P1, ILTM0>(v, tw, xbase + jt1, c);
+
+    // ---- exchange 1: full, through A (index bit 13 set) and B (clear) ----
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const uint32_t j = jt1 | P1::jc(0, r);
+      uint64_t* img = (j >> 13) ? Ahalf : B;
+      img[smem_phys(j & 0x1FFFu)] = v[r];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int g = 0; g < P2::G; ++g)
+#pragma unroll
+      for (int r = 0; r < P2::R; ++r) {
+        const uint32_t j = jt2 | P2::jc(g, r);
+        const uint64_t* img = (j >> 13) ? Ahalf : B;
+        v[g * P2::R + r] = img[smem_phys(j & 0x1FFFu)];
+      }
+    __syncthreads();  // A free: prefetch the next block while P2/P3 compute
+    if (t == 0 && k + gridDim.x < nitems) {
+      fence_proxy_async();
+      issue(k + gridDim.x);
+    }
+
+    pass14<A, FWD, P2, false>(v, tw, xbase + jt2, c);
+
+    // ---- exchange 2: B only, two rounds split on bit X (value-index bit 4) ----
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        B[smem_phys(squeeze<X>(jt2 | P2::jc(h, r)))] = v[16 * h + r];
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const int i = 16 * h + r;  // P3 value index with bit 4 == h
+        v[i] = B[smem_phys(squeeze<X>(jt3 | P3::jc(0, i)))];
+      }
+      __syncthreads();
+    }
+
+    pass14<A, FWD, P3, false>(v, tw, xbase + jt3, c);
+
+    // ---- fix-ups and store ----
+    if (FWD) {
+      if (a.fout == 1) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = A::csub(A::csub(v[i], c.twoq), c.q);  // small_mod(x,q,4)
+      }
+      // P3 holds 32 contiguous words per thread; transpose each half (bit 4)
+      // through B so that the global stores are lane-contiguous.
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) B[smem_phys(squeeze<4>(jt3 | (16 * h + r)))] = A::store(v[16 * h + r]);
+        __syncthreads();
+#pragma unroll
+        for (int s2 = 0; s2 < 16; ++s2) {
+          const uint32_t jq = t + (s2 << 9);  // squeezed index, lane-contiguous
+          const uint32_t j = (jq & 15u) | ((jq >> 4) << 5) | (h << 4);
+          dst[j] = B[smem_phys(jq)];
+        }
+        __syncthreads();
+      }
+    } else {
+      if (lognb == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = A::scale_ninv(v[i], c);
+        if (a.fout == 1) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = A::csub(v[i], c.q);
+        }
+      }
+      // P3 holds j = t + 512 r: coalesced already
+#pragma unroll
+      for (int r = 0; r < 32; ++r) dst[jt3 | P3::jc(0, r)] = A::store(v[r]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K stages over bits [lo, lo+K) of long rows; one column per thread.
 // first_iltm: forward with fin == 1 at the top stage. last: inverse final pass
 // (apply n^-1 and the fout reduction).
 // ---------------------------------------------------------------------------
-template <int K, int BS, bool FWD>
+template <int K, class A, bool FWD>
 __global__ void __launch_bounds__(256) ntt_global_pass(NttArgs a, uint32_t lo, int first_iltm,
                                                        int last) {
   constexpr int R = 1 << K;
@@ -269,7 +565,7 @@ __global__ void __launch_bounds__(256) ntt_global_pass(NttArgs a, uint32_t lo, i
   uint64_t* dst = a.out + row * a.n;
   uint64_t v[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = src[j0 + (static_cast<uint64_t>(r) << lo)];
+  for (int r = 0; r < R; ++r) v[r] = A::load(src[j0 + (static_cast<uint64_t>(r) << lo)]);
   const uint64_t xt = a.n + j0;
 #pragma unroll
   for (int s = 0; s < K; ++s) {
@@ -283,10 +579,10 @@ __global__ void __launch_bounds__(256) ntt_global_pass(NttArgs a, uint32_t lo, i
       for (int l = 0; l < (1 << i); ++l) {
         const int r0 = (hi << (i + 1)) | l, r1 = r0 | (1 << i);
         if (FWD) {
-          if (s == 0 && first_iltm) fwd_bfly<BS, true>(v[r0], v[r1], w.x, w.y, c.twoq, c.negq);
-          else fwd_bfly<BS, false>(v[r0], v[r1], w.x, w.y, c.twoq, c.negq);
+          if (s == 0 && first_iltm) A::template fwd<true>(v[r0], v[r1], w, c);
+          else A::template fwd<false>(v[r0], v[r1], w, c);
         } else {
-          inv_bfly<BS, false>(v[r0], v[r1], w.x, w.y, c.twoq, c.negq);
+          A::template inv<false>(v[r0], v[r1], w, c);
         }
       }
     }
@@ -294,27 +590,27 @@ __global__ void __launch_bounds__(256) ntt_global_pass(NttArgs a, uint32_t lo, i
   if (!FWD && last) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      v[r] = mul_lazy<BS>(v[r], c.ninv, c.ninvp, c.negq);
-      if (a.fout == 1) v[r] = csub(v[r], c.q);
+      v[r] = A::scale_ninv(v[r], c);
+      if (a.fout == 1) v[r] = A::csub(v[r], c.q);
     }
   }
 #pragma unroll
-  for (int r = 0; r < R; ++r) dst[j0 + (static_cast<uint64_t>(r) << lo)] = v[r];
+  for (int r = 0; r < R; ++r) dst[j0 + (static_cast<uint64_t>(r) << lo)] = A::store(v[r]);
 }
 
 // ---------------------------------------------------------------------------
-// Any N <= 2^14: one CTA per row, whole row in shared memory, one stage at a
+// Any N <= 2^10: one CTA per row, whole row in shared memory, one stage at a
 // time. Used for the small sizes of the reference's tests.
 // ---------------------------------------------------------------------------
-template <int BS, bool FWD>
+template <class A, bool FWD>
 __global__ void __launch_bounds__(256) ntt_small(NttArgs a) {
-  extern __shared__ uint64_t sm[];
+  extern __shared__ uint64_t smw[];
   const uint64_t row = static_cast<uint64_t>(blockIdx.x) * a.row_mul + a.row_add;
   const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
   const LimbConst c = a.lc[limb];
   const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * a.n;
   const uint32_t n = static_cast<uint32_t>(a.n);
-  for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) sm[j] = a.in[row * a.n + j];
+  for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) smw[j] = A::load(a.in[row * a.n + j]);
   __syncthreads();
   for (uint32_t s = 0; s < a.logn; ++s) {
     const uint32_t b = FWD ? (a.logn - 1 - s) : s;
@@ -322,28 +618,28 @@ __global__ void __launch_bounds__(256) ntt_small(NttArgs a) {
     for (uint32_t p = threadIdx.x; p < n / 2; p += blockDim.x) {
       const uint32_t j = ((p >> b) << (b + 1)) | (p & ((1u << b) - 1u));
       const ulonglong2 w = ldtw(tw + ((a.n + j) >> (b + 1)));
-      uint64_t x0 = sm[j], x1 = sm[j + (1u << b)];
+      uint64_t x0 = smw[j], x1 = smw[j + (1u << b)];
       if (FWD) {
-        if (iltm) fwd_bfly<BS, true>(x0, x1, w.x, w.y, c.twoq, c.negq);
-        else fwd_bfly<BS, false>(x0, x1, w.x, w.y, c.twoq, c.negq);
+        if (iltm) A::template fwd<true>(x0, x1, w, c);
+        else A::template fwd<false>(x0, x1, w, c);
       } else {
-        if (iltm) inv_bfly<BS, true>(x0, x1, w.x, w.y, c.twoq, c.negq);
-        else inv_bfly<BS, false>(x0, x1, w.x, w.y, c.twoq, c.negq);
+        if (iltm) A::template inv<true>(x0, x1, w, c);
+        else A::template inv<false>(x0, x1, w, c);
       }
-      sm[j] = x0;
-      sm[j + (1u << b)] = x1;
+      smw[j] = x0;
+      smw[j + (1u << b)] = x1;
     }
     __syncthreads();
   }
   for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) {
-    uint64_t x = sm[j];
+    uint64_t x = smw[j];
     if (FWD) {
-      if (a.fout == 1) x = csub(csub(x, c.twoq), c.q);
+      if (a.fout == 1) x = A::csub(A::csub(x, c.twoq), c.q);
     } else {
-      x = mul_lazy<BS>(x, c.ninv, c.ninvp, c.negq);
-      if (a.fout == 1) x = csub(x, c.q);
+      x = A::scale_ninv(x, c);
+      if (a.fout == 1) x = A::csub(x, c.q);
     }
-    a.out[row * a.n + j] = x;
+    a.out[row * a.n + j] = A::store(x);
   }
 }
 

@@ -62,6 +62,7 @@ class Oracle:
                 "oc_ntt_inverse": (C.c_int, [u64, u64p, C.c_uint32, C.c_int, u64p, u64p, u64,
                                              u64, u64, C.c_int]),
                 "oc_ntt_root": (C.c_int, [u64, u64, u64, C.c_int, C.c_int, u64p, u64p, u64, u64]),
+                "oc_ntt_stages": (C.c_int, [u64, u64, C.c_int, u64p, u64, C.c_int]),
                 "oc_reference_ntt": (C.c_int, [u64, u64, u64, C.c_int, u64p, u64p]),
                 "oc_eltwise_add_mod": (C.c_int, [u64p, u64p, u64p, u64, u64]),
                 "oc_eltwise_neg_mod": (C.c_int, [u64p, u64p, u64, u64]),
