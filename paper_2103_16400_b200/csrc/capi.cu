@@ -86,6 +86,8 @@ struct nk_plan {
   std::vector<int> bs;
   ulonglong2* tw_fwd = nullptr;  // [limb][n]
   ulonglong2* tw_inv = nullptr;  // [limb][n]
+  ulonglong2* twl_fwd = nullptr;  // [limb][n] low-bit-stage tables, transposed (nk::low_index)
+  ulonglong2* twl_inv = nullptr;
   nk::LimbConst* lc = nullptr;   // [limb]
   nk::MultConst* mc[3] = {nullptr, nullptr, nullptr};  // fin = 1, 2, 4
 };
@@ -266,6 +268,7 @@ int ntt_dispatch(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, 
   a.out = res;
   a.in = op;
   a.tw = fwd ? p->tw_fwd : p->tw_inv;
+  a.twl = fwd ? p->twl_fwd : p->twl_inv;
   a.lc = p->lc;
   a.n = p->n;
   a.logn = p->logn;
@@ -370,6 +373,8 @@ void nk_plan_destroy(nk_plan* p) {
   cudaSetDevice(p->device);
   cudaFree(p->tw_fwd);
   cudaFree(p->tw_inv);
+  cudaFree(p->twl_fwd);
+  cudaFree(p->twl_inv);
   cudaFree(p->lc);
   for (auto* m : p->mc) cudaFree(m);
   cudaSetDevice(cur);
@@ -394,7 +399,7 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
   p->n = n;
   p->logn = tabs[0].logn;
   p->nlimbs = nlimbs;
-  std::vector<ulonglong2> hf(n * nlimbs), hi(n * nlimbs);
+  std::vector<ulonglong2> hf(n * nlimbs), hi(n * nlimbs), hlf(n * nlimbs), hli(n * nlimbs);
   std::vector<nk::LimbConst> hl(nlimbs);
   std::vector<nk::MultConst> hm[3];
   for (auto& v : hm) v.resize(nlimbs);
@@ -411,6 +416,16 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
       hf[l * n + i] = make_ulonglong2(enc(t.w[i]), enc(t.wp[i]));
       hi[l * n + i] = make_ulonglong2(enc(t.wi[i]), enc(t.wip[i]));
     }
+    if (n >= 32) {
+      for (int b = 0; b < 5; ++b)
+        for (uint64_t d = 0; d < (uint64_t{1} << (4 - b)); ++d)
+          for (uint64_t jhi = 0; jhi < (n >> 5); ++jhi) {
+            const uint64_t src = (n >> (b + 1)) + (jhi << (4 - b)) + d;
+            const uint64_t dst = nk::low_index(n, b, static_cast<int>(d), jhi);
+            hlf[l * n + dst] = hf[l * n + src];
+            hli[l * n + dst] = hi[l * n + src];
+          }
+    }
     // -q modulo 2^64 (the 52-bit negated modulus of ntt.hpp:85-92 agrees modulo 2^52,
     // see modmath.cuh)
     hl[l] = nk::LimbConst{t.q, 2 * t.q, ~t.q + 1, enc(t.ninv), enc(t.ninvp), 2 * t.q + nk::kDBias,
@@ -424,12 +439,16 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
   cudaError_t e;
   if ((e = cudaMalloc(&p->tw_fwd, hf.size() * sizeof(ulonglong2))) ||
       (e = cudaMalloc(&p->tw_inv, hi.size() * sizeof(ulonglong2))) ||
+      (e = cudaMalloc(&p->twl_fwd, hlf.size() * sizeof(ulonglong2))) ||
+      (e = cudaMalloc(&p->twl_inv, hli.size() * sizeof(ulonglong2))) ||
       (e = cudaMalloc(&p->lc, hl.size() * sizeof(nk::LimbConst))))
     return cleanup(cuda_fail(e, "cudaMalloc(plan tables)"));
   for (int f = 0; f < 3; ++f)
     if ((e = cudaMalloc(&p->mc[f], nlimbs * sizeof(nk::MultConst))))
       return cleanup(cuda_fail(e, "cudaMalloc(plan consts)"));
-  if ((e = cudaMemcpy(p->tw_fwd, hf.data(), hf.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice)) ||
+  if ((e = cudaMemcpy(p->twl_fwd, hlf.data(), hlf.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(p->twl_inv, hli.data(), hli.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(p->tw_fwd, hf.data(), hf.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(p->tw_inv, hi.data(), hi.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(p->lc, hl.data(), hl.size() * sizeof(nk::LimbConst), cudaMemcpyHostToDevice)))
     return cleanup(cuda_fail(e, "cudaMemcpy(plan tables)"));

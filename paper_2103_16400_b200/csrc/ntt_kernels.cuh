@@ -42,8 +42,9 @@ using LimbConst = LimbConstDev;
 struct NttArgs {
   uint64_t* out;
   const uint64_t* in;
-  const ulonglong2* tw;  // [limb][N] {w, w'} of the plan (fwd or inv table)
-  const LimbConst* lc;   // [limb]
+  const ulonglong2* tw;   // [limb][N] {w, w'} of the plan (fwd or inv table)
+  const ulonglong2* twl;  // [limb][N] the same entries for bits 0..4, lane-contiguous (see low_index)
+  const LimbConst* lc;    // [limb]
   uint64_t n;            // row length
   uint64_t rows;         // launched rows
   uint32_t limb0, nlimbs;     // row r (after remapping) holds limb limb0 + r % nlimbs
@@ -332,6 +333,12 @@ __host__ __device__ __forceinline__ constexpr uint32_t squeeze(uint32_t j) {
   return (j & ((1u << X) - 1u)) | ((j >> (X + 1)) << X);
 }
 
+// Low table: for stage bit b < 5, entry (d, jhi) with d < 2^(4-b), jhi < N/32
+// holds psi_rev[(N >> (b+1)) + (jhi << (4-b)) + d]; segment b starts at N - (N >> b).
+__host__ __device__ __forceinline__ uint64_t low_index(uint64_t n, int b, int d, uint64_t jhi) {
+  return (n - (n >> b)) + static_cast<uint64_t>(d) * (n >> 5) + jhi;
+}
+
 template <int LO_, int K_, int X_>
 struct PassD {
   static constexpr int LO = LO_, K = K_, X = X_;
@@ -357,8 +364,13 @@ struct Sched14 {
 // One register pass over the bits of PD (stage order by direction).
 template <class A, bool FWD, class PD, bool ILTM0>
 __device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __restrict__ tw,
+                                       const ulonglong2* __restrict__ twl, uint64_t n,
                                        uint64_t xt, const LimbConst& c) {
   constexpr int K = PD::K, R = PD::R, G = PD::G;
+  // the pass over bits 0..4 reads the transposed low table: lanes differ in
+  // jhi = j >> 5, so loads of one (stage, d) are lane-contiguous
+  constexpr bool kLow = (PD::LO == 0 && PD::K == 5);
+  const uint64_t jhi = (xt - n) >> 5;
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     const int i = FWD ? (K - 1 - s) : s;
@@ -368,7 +380,7 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __re
       const uint64_t base = (xt + PD::jc(g, 0)) >> (b + 1);
 #pragma unroll
       for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
-        const ulonglong2 w = ldtw(tw + base + hi);
+        const ulonglong2 w = kLow ? ldtw(twl + low_index(n, b, hi, jhi)) : ldtw(tw + base + hi);
 #pragma unroll
         for (int l = 0; l < (1 << i); ++l) {
           const int r0 = (hi << (i + 1)) | l;
@@ -435,6 +447,7 @@ __global__ void __launch_bounds__(512, 1)
     const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
     const LimbConst c = a.lc[limb];
     const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * a.n;
+    const ulonglong2* __restrict__ twl = a.twl + static_cast<uint64_t>(limb) * a.n;
     const uint64_t boff = blk << kB14;
     uint64_t* __restrict__ dst = a.out + row * a.n + boff;
     const uint64_t xbase = a.n + boff;
@@ -463,7 +476,7 @@ __global__ void __launch_bounds__(512, 1)
     }
     __syncthreads();  // staging consumed (A is reused as a half image below)
 
-    pass14<A, FWD, P1, ILTM0>(v, tw, xbase + jt1, c);
+    pass14<A, FWD, P1, ILTM0>(v, tw, twl, a.n, xbase + jt1, c);
 
     // ---- exchange 1: full, through A (index bit 13 set) and B (clear) ----
 #pragma unroll
@@ -487,7 +500,7 @@ __global__ void __launch_bounds__(512, 1)
       issue(k + gridDim.x);
     }
 
-    pass14<A, FWD, P2, false>(v, tw, xbase + jt2, c);
+    pass14<A, FWD, P2, false>(v, tw, twl, a.n, xbase + jt2, c);
 
     // ---- exchange 2: B only, two rounds split on bit X (value-index bit 4) ----
 #pragma unroll
@@ -504,7 +517,7 @@ __global__ void __launch_bounds__(512, 1)
       __syncthreads();
     }
 
-    pass14<A, FWD, P3, false>(v, tw, xbase + jt3, c);
+    pass14<A, FWD, P3, false>(v, tw, twl, a.n, xbase + jt3, c);
 
     // ---- fix-ups and store ----
     if (FWD) {
