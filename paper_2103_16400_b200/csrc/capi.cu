@@ -416,20 +416,22 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
       hf[l * n + i] = make_ulonglong2(enc(t.w[i]), enc(t.wp[i]));
       hi[l * n + i] = make_ulonglong2(enc(t.wi[i]), enc(t.wip[i]));
     }
-    if (n >= 32) {
-      for (int b = 0; b < 5; ++b)
-        for (uint64_t d = 0; d < (uint64_t{1} << (4 - b)); ++d)
-          for (uint64_t jhi = 0; jhi < (n >> 5); ++jhi) {
-            const uint64_t src = (n >> (b + 1)) + (jhi << (4 - b)) + d;
-            const uint64_t dst = nk::low_index(n, b, static_cast<int>(d), jhi);
-            hlf[l * n + dst] = hf[l * n + src];
-            hli[l * n + dst] = hi[l * n + src];
-          }
+    if (n >= (uint64_t{1} << 14)) {  // per 16384-word block (nk::low_index)
+      for (uint64_t blk = 0; blk < (n >> 14); ++blk)
+        for (int b = 0; b < 5; ++b)
+          for (uint64_t d = 0; d < (uint64_t{1} << (4 - b)); ++d)
+            for (uint64_t jhi = 0; jhi < 512; ++jhi) {
+              const uint64_t src = (n >> (b + 1)) + (((blk << 9) + jhi) << (4 - b)) + d;
+              const uint64_t dst = (blk << 14) + nk::low_index(b, static_cast<int>(d), static_cast<uint32_t>(jhi));
+              hlf[l * n + dst] = hf[l * n + src];
+              hli[l * n + dst] = hi[l * n + src];
+            }
     }
     // -q modulo 2^64 (the 52-bit negated modulus of ntt.hpp:85-92 agrees modulo 2^52,
     // see modmath.cuh)
     hl[l] = nk::LimbConst{t.q, 2 * t.q, ~t.q + 1, enc(t.ninv), enc(t.ninvp), 2 * t.q + nk::kDBias,
-                          std::ldexp(static_cast<double>(t.q), -52), t.bs, 0};
+                          std::ldexp(static_cast<double>(t.q), -52), static_cast<double>(2 * t.q),
+                          t.bs, 0};
     nk::host::Modulus m;
     nk::host::make_modulus(t.q, &m);
     const int fins[3] = {1, 2, 4};

@@ -151,15 +151,20 @@ __device__ __forceinline__ uint64_t csubD(uint64_t yD, uint64_t m) {
 #endif
 }
 
-__device__ __forceinline__ uint64_t mul_lazyD(uint64_t xD, double w, double wp, double qq) {
-  const double v = __dsub_rn(as_d(xD), kC52);
+// w*v - floor(w'v/2^52)*q as a plain double (exact integer in [0, 2q)) for a
+// plain double v < 2^52.
+__device__ __forceinline__ double mul_lazy_plain(double v, double w, double wp, double qq) {
   const double hq = __fma_rd(wp, v, kC104);
   const double qh = __dsub_rn(hq, kC104);
   const double h1 = __dmul_rn(w, v);
   const double l1 = __fma_rn(w, v, -h1);
   const double e = __fma_rn(-qh, qq, h1);
-  const double t = __dadd_rn(e, l1);
-  return as_u(__dadd_rn(t, kC52));
+  return __dadd_rn(e, l1);
+}
+
+__device__ __forceinline__ uint64_t mul_lazyD(uint64_t xD, double w, double wp, double qq) {
+  const double v = __dsub_rn(as_d(xD), kC52);
+  return as_u(__dadd_rn(mul_lazy_plain(v, w, wp, qq), kC52));
 }
 
 // ---------------------------------------------------------------------------
@@ -172,6 +177,7 @@ struct LimbConstDev {
   uint64_t q, twoq, negq, ninv, ninvp;  // Arith64: integers; Arith52F: ninv/ninvp are double bits
   uint64_t twoq_bias;                   // 2q + kDBias
   double qq;                            // q * 2^-52
+  double twoq_d;                        // 2q as a double
   int32_t bs;
   int32_t pad;
 };
@@ -199,22 +205,27 @@ struct Arith52F {  // beta = 2^52 on the FP64 pipe (requires 4q < 2^52)
   static constexpr bool kFP = true;
   __device__ static uint64_t load(uint64_t x) { return x | kDBias; }
   __device__ static uint64_t store(uint64_t xD) { return xD & kMask52; }
-  // fwd_butterfly<52, ILTM> (ntt.hpp:103-113) in the D representation
+  // fwd_butterfly<52, ILTM> (ntt.hpp:103-113) in the D representation. The
+  // output sums are formed on the FP64 pipe: D(u) + T and D(u) + 2q - T are
+  // exact (every intermediate is an integer below 2^53).
   template <bool ILTM>
   __device__ static void fwd(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
     const uint64_t u = ILTM ? x0 : csubD(x0, c.twoq);
-    const uint64_t t = mul_lazyD(x1, as_d(w.x), as_d(w.y), c.qq);
-    x0 = u + t - kDBias;
-    x1 = u + c.twoq_bias - t;
+    const double t = mul_lazy_plain(__dsub_rn(as_d(x1), kC52), as_d(w.x), as_d(w.y), c.qq);
+    const double du = as_d(u);
+    x0 = as_u(__dadd_rn(du, t));
+    x1 = as_u(__dsub_rn(__dadd_rn(du, c.twoq_d), t));
   }
-  // inv_butterfly<52, ILTM> (ntt.hpp:115-130) in the D representation
+  // inv_butterfly<52, ILTM> (ntt.hpp:115-130) in the D representation:
+  // t = x0 - x1 + 2q = (D(x0) - D(x1)) + 2q on the FP64 pipe (exact), the sum
+  // x0 + x1 on the integer pipe (D(x0) + D(x1) - 2^52).
   template <bool ILTM>
   __device__ static void inv(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
-    const uint64_t t = x0 + c.twoq_bias - x1;
+    const double t = __dadd_rn(__dsub_rn(as_d(x0), as_d(x1)), c.twoq_d);
     uint64_t s = x0 + x1 - kDBias;
     if (!ILTM) s = csubD(s, c.twoq);
     x0 = s;
-    x1 = mul_lazyD(t, as_d(w.x), as_d(w.y), c.qq);
+    x1 = as_u(__dadd_rn(mul_lazy_plain(t, as_d(w.x), as_d(w.y), c.qq), kC52));
   }
   __device__ static uint64_t scale_ninv(uint64_t xD, const LimbConstDev& c) {
     return mul_lazyD(xD, as_d(c.ninv), as_d(c.ninvp), c.qq);

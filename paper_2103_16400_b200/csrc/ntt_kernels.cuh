@@ -333,10 +333,12 @@ __host__ __device__ __forceinline__ constexpr uint32_t squeeze(uint32_t j) {
   return (j & ((1u << X) - 1u)) | ((j >> (X + 1)) << X);
 }
 
-// Low table: for stage bit b < 5, entry (d, jhi) with d < 2^(4-b), jhi < N/32
-// holds psi_rev[(N >> (b+1)) + (jhi << (4-b)) + d]; segment b starts at N - (N >> b).
-__host__ __device__ __forceinline__ uint64_t low_index(uint64_t n, int b, int d, uint64_t jhi) {
-  return (n - (n >> b)) + static_cast<uint64_t>(d) * (n >> 5) + jhi;
+// Low table (per 16384-word block, blocks contiguous per limb): for stage bit
+// b < 5, entry (d, jhi) with d < 2^(4-b), jhi < 512 (block-local j >> 5) holds
+// psi_rev[(N >> (b+1)) + ((boff >> 5) + jhi) * 2^(4-b) + d]; segment b starts at
+// 16384 - (16384 >> b). Offsets are compile-time constants in the kernel.
+__host__ __device__ constexpr uint32_t low_index(int b, int d, uint32_t jhi) {
+  return (16384u - (16384u >> b)) + static_cast<uint32_t>(d) * 512u + jhi;
 }
 
 template <int LO_, int K_, int X_>
@@ -367,10 +369,10 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __re
                                        const ulonglong2* __restrict__ twl, uint64_t n,
                                        uint64_t xt, const LimbConst& c) {
   constexpr int K = PD::K, R = PD::R, G = PD::G;
-  // the pass over bits 0..4 reads the transposed low table: lanes differ in
-  // jhi = j >> 5, so loads of one (stage, d) are lane-contiguous
+  // the pass over bits 0..4 reads the transposed low table (twl points at this
+  // block's segment plus this thread's jhi): loads of one (stage, d) are
+  // lane-contiguous and their offsets are immediates
   constexpr bool kLow = (PD::LO == 0 && PD::K == 5);
-  const uint64_t jhi = (xt - n) >> 5;
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     const int i = FWD ? (K - 1 - s) : s;
@@ -380,7 +382,7 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __re
       const uint64_t base = (xt + PD::jc(g, 0)) >> (b + 1);
 #pragma unroll
       for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
-        const ulonglong2 w = kLow ? ldtw(twl + low_index(n, b, hi, jhi)) : ldtw(tw + base + hi);
+        const ulonglong2 w = kLow ? ldtw(twl + low_index(b, hi, 0)) : ldtw(tw + base + hi);
 #pragma unroll
         for (int l = 0; l < (1 << i); ++l) {
           const int r0 = (hi << (i + 1)) | l;
@@ -440,6 +442,12 @@ __global__ void __launch_bounds__(512, 1)
   uint32_t phase = 0;
 
   const uint32_t jt1 = P1::jt(t), jt2 = P2::jt(t), jt3 = P3::jt(t);
+  const uint32_t jtlow = FWD ? jt3 : jt1;  // thread index bits of the pass over bits 0..4
+  // per-thread shared-memory bases (index bits of t and of the registers are
+  // disjoint, so every access below is base + immediate)
+  const uint32_t e1w = smem_phys(jt1 & 0x1FFFu), e1r = smem_phys(jt2 & 0x1FFFu);
+  const bool e1w_hi = (jt1 >> 13) & 1, e1r_hi = (jt2 >> 13) & 1;
+  const uint32_t e2w = smem_phys(squeeze<X>(jt2)), e2r = smem_phys(squeeze<X>(jt3));
 
   for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
     uint64_t row, blk;
@@ -447,7 +455,9 @@ __global__ void __launch_bounds__(512, 1)
     const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
     const LimbConst c = a.lc[limb];
     const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * a.n;
-    const ulonglong2* __restrict__ twl = a.twl + static_cast<uint64_t>(limb) * a.n;
+    // low table: this block's segment, offset by this thread's jhi in the low pass
+    const ulonglong2* __restrict__ twl =
+        a.twl + static_cast<uint64_t>(limb) * a.n + (blk << kB14) + (jtlow >> 5);
     const uint64_t boff = blk << kB14;
     uint64_t* __restrict__ dst = a.out + row * a.n + boff;
     const uint64_t xbase = a.n + boff;
@@ -481,18 +491,18 @@ __global__ void __launch_bounds__(512, 1)
     // ---- exchange 1: full, through A (index bit 13 set) and B (clear) ----
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
-      const uint32_t j = jt1 | P1::jc(0, r);
-      uint64_t* img = (j >> 13) ? Ahalf : B;
-      img[smem_phys(j & 0x1FFFu)] = v[r];
+      const uint32_t jc = P1::jc(0, r);
+      uint64_t* img = (((jc >> 13) & 1) | e1w_hi) ? Ahalf : B;
+      img[e1w + smem_phys(jc & 0x1FFFu)] = v[r];
     }
     __syncthreads();
 #pragma unroll
     for (int g = 0; g < P2::G; ++g)
 #pragma unroll
       for (int r = 0; r < P2::R; ++r) {
-        const uint32_t j = jt2 | P2::jc(g, r);
-        const uint64_t* img = (j >> 13) ? Ahalf : B;
-        v[g * P2::R + r] = img[smem_phys(j & 0x1FFFu)];
+        const uint32_t jc = P2::jc(g, r);
+        const uint64_t* img = (((jc >> 13) & 1) | e1r_hi) ? Ahalf : B;
+        v[g * P2::R + r] = img[e1r + smem_phys(jc & 0x1FFFu)];
       }
     __syncthreads();  // A free: prefetch the next block while P2/P3 compute
     if (t == 0 && k + gridDim.x < nitems) {
@@ -506,13 +516,12 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r)
-        B[smem_phys(squeeze<X>(jt2 | P2::jc(h, r)))] = v[16 * h + r];
+      for (int r = 0; r < 16; ++r) B[e2w + smem_phys(squeeze<X>(P2::jc(h, r)))] = v[16 * h + r];
       __syncthreads();
 #pragma unroll
       for (int r = 0; r < 16; ++r) {
         const int i = 16 * h + r;  // P3 value index with bit 4 == h
-        v[i] = B[smem_phys(squeeze<X>(jt3 | P3::jc(0, i)))];
+        v[i] = B[e2r + smem_phys(squeeze<X>(P3::jc(0, i)))];
       }
       __syncthreads();
     }
@@ -526,17 +535,23 @@ __global__ void __launch_bounds__(512, 1)
         for (int i = 0; i < 32; ++i) v[i] = A::csub(A::csub(v[i], c.twoq), c.q);  // small_mod(x,q,4)
       }
       // P3 holds 32 contiguous words per thread; transpose each half (bit 4)
-      // through B so that the global stores are lane-contiguous.
+      // through B so the global stores are lane-contiguous: B holds the half as
+      // 512 rows of 16 words (row = t) in the 128B-swizzled arrangement, so
+      // both the 16-byte writes (8 lanes, 8 rows) and the row reads (8 lanes,
+      // one row) are conflict free.
+      uint8_t* Bb = reinterpret_cast<uint8_t*>(B);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
 #pragma unroll
-        for (int r = 0; r < 16; ++r) B[smem_phys(squeeze<4>(jt3 | (16 * h + r)))] = A::store(v[16 * h + r]);
+        for (int cc = 0; cc < 8; ++cc)
+          *reinterpret_cast<ulonglong2*>(Bb + (t << 7) + ((cc ^ (t & 7)) << 4)) =
+              make_ulonglong2(A::store(v[16 * h + 2 * cc]), A::store(v[16 * h + 2 * cc + 1]));
         __syncthreads();
 #pragma unroll
-        for (int s2 = 0; s2 < 16; ++s2) {
-          const uint32_t jq = t + (s2 << 9);  // squeezed index, lane-contiguous
-          const uint32_t j = (jq & 15u) | ((jq >> 4) << 5) | (h << 4);
-          dst[j] = B[smem_phys(jq)];
+        for (int s2 = 0; s2 < 8; ++s2) {
+          const uint32_t rowi = (t >> 3) + (s2 << 6), cc = t & 7;  // squeezed row, chunk
+          const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Bb + (rowi << 7) + ((cc ^ (rowi & 7)) << 4));
+          *reinterpret_cast<ulonglong2*>(dst + (rowi << 5) + (h << 4) + (cc << 1)) = p;
         }
         __syncthreads();
       }
