@@ -1,0 +1,239 @@
+// nttkit_b200.hpp — header-only C++ facade over the C-ABI (nttkit_b200.h),
+// mirroring the reference's C++ API (/root/reference/proj/include/nttkit/) so
+// a caller of the reference can switch by changing the namespace:
+//
+//   reference (nttkit::)                        this facade (nttkit_b200::)
+//   Modulus(q)                modarith.hpp:106  Modulus(q)
+//   NttTables(n, m[, root])   ntt.hpp:210-217   NttTables(n, m[, root][, bit_shift])
+//   NttTables::forward        ntt.hpp:268-285   NttTables::forward (host spans)
+//   NttTables::inverse        ntt.hpp:289-306   NttTables::inverse (host spans)
+//   eltwise_mult_mod          eltwise.hpp:180   eltwise_mult_mod
+//   eltwise_fma_mod           eltwise.hpp:263   eltwise_fma_mod (std::optional addend)
+//   poly_mult_mod             ring.hpp:28-43    poly_mult_mod
+//   HEXL: hexl::NTT{ComputeForward, ComputeInverse},
+//                            hexl::EltwiseMultMod, hexl::EltwiseFMAMod
+//
+// Host-span calls copy to the GPU, run the sm_100a kernels and copy back before
+// returning (the reference's calls are blocking). Argument errors throw
+// std::invalid_argument with the reference's message; CUDA failures throw
+// std::runtime_error. RnsNtt exposes the batched device-pointer entry points.
+#ifndef NTTKIT_B200_HPP
+#define NTTKIT_B200_HPP
+
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "nttkit_b200.h"
+
+namespace nttkit_b200 {
+
+inline void check(int rc) {
+  if (rc == NK_OK) return;
+  const std::string msg = nk_last_error();
+  if (rc == NK_ERR_CUDA) throw std::runtime_error(msg);
+  throw std::invalid_argument(msg);
+}
+
+class Modulus {
+ public:
+  explicit Modulus(uint64_t q) : q_(q) { check(nk_modulus(q, &bits_, &barrett_)); }
+  uint64_t value() const noexcept { return q_; }
+  unsigned bits() const noexcept { return bits_; }
+  unsigned barrett_shift() const noexcept { return 63 + bits_; }
+  uint64_t barrett_factor() const noexcept { return barrett_; }
+  friend bool operator==(const Modulus& a, const Modulus& b) { return a.q_ == b.q_; }
+
+ private:
+  uint64_t q_;
+  uint32_t bits_ = 0;
+  uint64_t barrett_ = 0;
+};
+
+// Tables of many RNS limbs on one device; batched data is [npolys][nlimbs][n].
+class RnsNtt {
+ public:
+  RnsNtt(uint64_t n, std::span<const uint64_t> moduli, int device = 0, int bit_shift = 0,
+         std::optional<std::span<const uint64_t>> roots = std::nullopt) {
+    nk_plan* p = nullptr;
+    check(nk_plan_create(&p, device, n, moduli.data(), roots ? roots->data() : nullptr,
+                         static_cast<uint32_t>(moduli.size()), bit_shift));
+    plan_.reset(p);
+    n_ = n;
+    nlimbs_ = static_cast<uint32_t>(moduli.size());
+  }
+  uint64_t size() const noexcept { return n_; }
+  uint32_t limbs() const noexcept { return nlimbs_; }
+  const nk_plan* plan() const noexcept { return plan_.get(); }
+
+  // device pointers, asynchronous on `stream` (cudaStream_t)
+  void forward_device(uint64_t* d_result, const uint64_t* d_operand, uint32_t npolys,
+                      uint64_t in, uint64_t out, void* stream = nullptr) const {
+    check(nk_ntt_forward(plan_.get(), d_result, d_operand, 0, nlimbs_, npolys, in, out, stream));
+  }
+  void inverse_device(uint64_t* d_result, const uint64_t* d_operand, uint32_t npolys,
+                      uint64_t in, uint64_t out, void* stream = nullptr) const {
+    check(nk_ntt_inverse(plan_.get(), d_result, d_operand, 0, nlimbs_, npolys, in, out, stream));
+  }
+  void poly_mult_device(uint64_t* d_result, const uint64_t* d_f, const uint64_t* d_g,
+                        uint32_t npolys, void* stream = nullptr) const {
+    check(nk_poly_mult_mod(plan_.get(), d_result, d_f, d_g, 0, nlimbs_, npolys, stream));
+  }
+
+  // host buffers, blocking
+  void forward(std::span<uint64_t> result, std::span<const uint64_t> operand, uint64_t in,
+               uint64_t out) const {
+    host_call(true, result, operand, in, out);
+  }
+  void inverse(std::span<uint64_t> result, std::span<const uint64_t> operand, uint64_t in,
+               uint64_t out) const {
+    host_call(false, result, operand, in, out);
+  }
+
+ protected:
+  void host_call(bool fwd, std::span<uint64_t> result, std::span<const uint64_t> operand,
+                 uint64_t in, uint64_t out) const {
+    const uint64_t row = n_ * nlimbs_;
+    if (operand.size() != result.size() || row == 0 || operand.size() % row != 0)
+      throw std::invalid_argument("transform: buffer length must equal n");
+    const uint32_t npolys = static_cast<uint32_t>(operand.size() / row);
+    auto fn = fwd ? nk_ntt_forward_host : nk_ntt_inverse_host;
+    check(fn(plan_.get(), result.data(), operand.data(), operand.size(), 0, nlimbs_, npolys, in,
+             out, nullptr));
+  }
+
+  struct Deleter {
+    void operator()(nk_plan* p) const { nk_plan_destroy(p); }
+  };
+  std::unique_ptr<nk_plan, Deleter> plan_;
+  uint64_t n_ = 0;
+  uint32_t nlimbs_ = 0;
+};
+
+// NttTables(n, Modulus[, root][, bit_shift]) — one limb, reference semantics.
+class NttTables : public RnsNtt {
+ public:
+  NttTables(uint64_t n, const Modulus& m) : RnsNtt(n, one(m)), m_(m) {}
+  NttTables(uint64_t n, const Modulus& m, uint64_t root)
+      : RnsNtt(n, one(m), 0, 0, std::span<const uint64_t>(&root_holder(root), 1)), m_(m) {}
+  NttTables(uint64_t n, const Modulus& m, std::optional<uint64_t> root, int bit_shift)
+      : RnsNtt(n, one(m), 0, bit_shift,
+               root ? std::optional<std::span<const uint64_t>>(
+                          std::span<const uint64_t>(&root_holder(*root), 1))
+                    : std::nullopt),
+        m_(m) {
+    // the reference validates the width before it looks at a root (ntt.hpp:226-231);
+    // nk_plan_create applies the same order.
+  }
+  const Modulus& modulus() const noexcept { return m_; }
+  uint64_t root() const {
+    uint64_t psi = 0;
+    check(nk_plan_info(plan(), 0, nullptr, nullptr, &psi, nullptr, nullptr));
+    return psi;
+  }
+  int bit_shift() const {
+    int bs = 0;
+    check(nk_plan_info(plan(), 0, nullptr, nullptr, nullptr, &bs, nullptr));
+    return bs;
+  }
+  void forward(std::span<uint64_t> result, std::span<const uint64_t> operand, uint64_t in,
+               uint64_t out) const {
+    if (result.size() != size() || operand.size() != size())
+      throw std::invalid_argument("transform: buffer length must equal n");
+    host_call(true, result, operand, in, out);
+  }
+  void inverse(std::span<uint64_t> result, std::span<const uint64_t> operand, uint64_t in,
+               uint64_t out) const {
+    if (result.size() != size() || operand.size() != size())
+      throw std::invalid_argument("transform: buffer length must equal n");
+    host_call(false, result, operand, in, out);
+  }
+
+ private:
+  static std::span<const uint64_t> one(const Modulus& m) {
+    thread_local uint64_t q;
+    q = m.value();
+    return std::span<const uint64_t>(&q, 1);
+  }
+  static uint64_t& root_holder(uint64_t r) {
+    thread_local uint64_t v;
+    v = r;
+    return v;
+  }
+  Modulus m_;
+};
+
+inline void eltwise_mult_mod(std::span<uint64_t> result, std::span<const uint64_t> a,
+                             std::span<const uint64_t> b, const Modulus& m,
+                             uint64_t input_mod_factor) {
+  if (result.size() != a.size() || a.size() != b.size())
+    throw std::invalid_argument("eltwise: operand lengths must match");
+  check(nk_eltwise_mult_mod_host(result.data(), a.data(), b.data(), a.size(), m.value(),
+                                 input_mod_factor, 0, nullptr));
+}
+
+inline void eltwise_fma_mod(std::span<uint64_t> result, std::span<const uint64_t> a, uint64_t y,
+                            std::optional<std::span<const uint64_t>> z, const Modulus& m,
+                            uint64_t input_mod_factor) {
+  if (result.size() != a.size() || (z && z->size() != a.size()))
+    throw std::invalid_argument("eltwise: operand lengths must match");
+  check(nk_eltwise_fma_mod_host(result.data(), a.data(), y, z ? z->data() : nullptr, a.size(),
+                                m.value(), input_mod_factor, 0, 0, nullptr));
+}
+
+inline void poly_mult_mod(std::span<uint64_t> result, std::span<const uint64_t> f,
+                          std::span<const uint64_t> g, const NttTables& tables) {
+  if (result.size() != tables.size() || f.size() != tables.size() || g.size() != tables.size())
+    throw std::invalid_argument("poly_mult_mod: operand lengths must equal n");
+  check(nk_poly_mult_mod_host(tables.plan(), result.data(), f.data(), g.data(), f.size(), 0, 1, 1,
+                              nullptr));
+}
+
+// ---- Intel HEXL names ----
+namespace hexl {
+
+class NTT {
+ public:
+  NTT(uint64_t degree, uint64_t q) : t_(degree, Modulus(q)) {}
+  NTT(uint64_t degree, uint64_t q, uint64_t root_of_unity) : t_(degree, Modulus(q), root_of_unity) {}
+  void ComputeForward(uint64_t* result, const uint64_t* operand, uint64_t input_mod_factor,
+                      uint64_t output_mod_factor) const {
+    t_.forward(std::span<uint64_t>(result, t_.size()), std::span<const uint64_t>(operand, t_.size()),
+               input_mod_factor, output_mod_factor);
+  }
+  void ComputeInverse(uint64_t* result, const uint64_t* operand, uint64_t input_mod_factor,
+                      uint64_t output_mod_factor) const {
+    t_.inverse(std::span<uint64_t>(result, t_.size()), std::span<const uint64_t>(operand, t_.size()),
+               input_mod_factor, output_mod_factor);
+  }
+  uint64_t GetDegree() const { return t_.size(); }
+  uint64_t GetModulus() const { return t_.modulus().value(); }
+
+ private:
+  NttTables t_;
+};
+
+inline void EltwiseMultMod(uint64_t* result, const uint64_t* operand1, const uint64_t* operand2,
+                           uint64_t n, uint64_t modulus, uint64_t input_mod_factor) {
+  eltwise_mult_mod(std::span<uint64_t>(result, n), std::span<const uint64_t>(operand1, n),
+                   std::span<const uint64_t>(operand2, n), Modulus(modulus), input_mod_factor);
+}
+
+// arg3 == nullptr: vector-scalar multiply
+inline void EltwiseFMAMod(uint64_t* result, const uint64_t* arg1, uint64_t arg2,
+                          const uint64_t* arg3, uint64_t n, uint64_t modulus,
+                          uint64_t input_mod_factor) {
+  std::optional<std::span<const uint64_t>> z;
+  if (arg3) z = std::span<const uint64_t>(arg3, n);
+  eltwise_fma_mod(std::span<uint64_t>(result, n), std::span<const uint64_t>(arg1, n), arg2, z,
+                  Modulus(modulus), input_mod_factor);
+}
+
+}  // namespace hexl
+}  // namespace nttkit_b200
+
+#endif

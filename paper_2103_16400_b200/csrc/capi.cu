@@ -554,15 +554,38 @@ int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const u
 // ---------------------------------------------------------------------------
 // element-wise (single modulus)
 // ---------------------------------------------------------------------------
-int nk_eltwise_mult_mod(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
-                        uint64_t fin, void* stream) {
-  nk::host::Modulus m;
-  if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
-  // dispatch of eltwise.hpp:180-188 and the checks of the path it picks
+namespace {
+// Modulus(q) plus the dispatch of eltwise.hpp:180-188 and the checks of the path it picks
+int validate_mult(uint64_t q, uint64_t fin, nk::host::Modulus* m) {
+  if (!valid_modulus(q, m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (fin != 1 && fin != 2 && fin != 4)
     return fail(NK_ERR_MULT_FACTOR, "eltwise_mult_mod: input_mod_factor must be 1, 2 or 4");
   if (q >= (uint64_t{1} << 50) && u128{fin} * q >= (u128{1} << 63))
     return fail(NK_ERR_MULT_INT_RANGE, "eltwise_mult_mod_int: requires input_mod_factor*q < 2^63");
+  return 0;
+}
+
+// eltwise.hpp:236-251 (+ the automatic width of eltwise.hpp:263-271); *bs receives the width
+int validate_fma(uint64_t q, uint64_t y, uint64_t fin, int bit_shift, int* bs) {
+  nk::host::Modulus m;
+  if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
+  *bs = bit_shift;
+  if (*bs == 0) *bs = (u128{fin} * q < (u128{1} << 52)) ? 52 : 64;
+  if (*bs != 52 && *bs != 64) return fail(NK_ERR_BIT_SHIFT, "eltwise_fma_mod: accumulator width must be 52 or 64");
+  if (fin != 1 && fin != 2 && fin != 4 && fin != 8)
+    return fail(NK_ERR_FMA_FACTOR, "eltwise_fma_mod: input_mod_factor must be 1, 2, 4 or 8");
+  if (q >= (uint64_t{1} << 61)) return fail(NK_ERR_FMA_MODULUS, "eltwise_fma_mod: requires q < 2^61");
+  if (y >= q) return fail(NK_ERR_FMA_SCALAR, "eltwise_fma_mod: scalar must be < q");
+  if (u128{fin} * q >= (u128{1} << *bs))
+    return fail(NK_ERR_FMA_WIDTH, "eltwise_fma_mod: requires input_mod_factor*q < 2^BitShift");
+  return 0;
+}
+}  // namespace
+
+int nk_eltwise_mult_mod(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
+                        uint64_t fin, void* stream) {
+  nk::host::Modulus m;
+  if (int rc = validate_mult(q, fin, &m)) return rc;
   if (n == 0) return 0;
   if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_mult_mod: NULL buffer");
   const nk::MultConst c{q, 2 * q, m.barrett, m.bits - 1, static_cast<int>(fin)};
@@ -575,17 +598,8 @@ int nk_eltwise_mult_mod(uint64_t* res, const uint64_t* a, const uint64_t* b, uin
 
 int nk_eltwise_fma_mod(uint64_t* res, const uint64_t* a, uint64_t y, const uint64_t* z, uint64_t n,
                        uint64_t q, uint64_t fin, int bit_shift, void* stream) {
-  nk::host::Modulus m;
-  if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
-  int bs = bit_shift;
-  if (bs == 0) bs = (u128{fin} * q < (u128{1} << 52)) ? 52 : 64;  // eltwise.hpp:266
-  if (bs != 52 && bs != 64) return fail(NK_ERR_BIT_SHIFT, "eltwise_fma_mod: accumulator width must be 52 or 64");
-  if (fin != 1 && fin != 2 && fin != 4 && fin != 8)
-    return fail(NK_ERR_FMA_FACTOR, "eltwise_fma_mod: input_mod_factor must be 1, 2, 4 or 8");
-  if (q >= (uint64_t{1} << 61)) return fail(NK_ERR_FMA_MODULUS, "eltwise_fma_mod: requires q < 2^61");
-  if (y >= q) return fail(NK_ERR_FMA_SCALAR, "eltwise_fma_mod: scalar must be < q");
-  if (u128{fin} * q >= (u128{1} << bs))
-    return fail(NK_ERR_FMA_WIDTH, "eltwise_fma_mod: requires input_mod_factor*q < 2^BitShift");
+  int bs = 0;
+  if (int rc = validate_fma(q, y, fin, bit_shift, &bs)) return rc;
   if (n == 0) return 0;
   if (!res || !a) return fail(NK_ERR_NULL, "eltwise_fma_mod: NULL buffer");
   const nk::FmaConst c{q, y, static_cast<uint64_t>((static_cast<u128>(y) << bs) / q),
@@ -711,6 +725,9 @@ int nk_poly_mult_mod_host(const nk_plan* p, uint64_t* res, const uint64_t* f, co
 int nk_eltwise_mult_mod_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n,
                              uint64_t q, uint64_t fin, int device, void* stream) {
   if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_mult_mod: NULL buffer");
+  nk::host::Modulus m;
+  if (int rc = validate_mult(q, fin, &m)) return rc;
+  if (n == 0) return 0;
   if (int rc = ensure_device(device)) return rc;
   cudaStream_t st = S(stream);
   DevBuf da, db;
@@ -724,6 +741,9 @@ int nk_eltwise_fma_mod_host(uint64_t* res, const uint64_t* a, uint64_t y, const 
                             uint64_t n, uint64_t q, uint64_t fin, int bit_shift, int device,
                             void* stream) {
   if (!res || !a) return fail(NK_ERR_NULL, "eltwise_fma_mod: NULL buffer");
+  int bs = 0;
+  if (int rc = validate_fma(q, y, fin, bit_shift, &bs)) return rc;
+  if (n == 0) return 0;
   if (int rc = ensure_device(device)) return rc;
   cudaStream_t st = S(stream);
   DevBuf da, dz;

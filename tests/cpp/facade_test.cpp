@@ -1,0 +1,88 @@
+// Exercises the C++ facade (include/nttkit_b200.hpp) the way a caller of the
+// reference's C++ API would. `--cpu`: only the argument-error behaviour (no
+// device needed). Default: also transforms, element-wise and ring calls on the
+// GPU, checked against known answers of the reference's tests.
+#include <cstdio>
+#include <cstring>
+#include <optional>
+#include <random>
+#include <stdexcept>
+#include <vector>
+
+#include "../../include/nttkit_b200.hpp"
+
+namespace nb = nttkit_b200;
+
+static int failures = 0;
+#define EXPECT(cond)                                                   \
+  do {                                                                 \
+    if (!(cond)) {                                                     \
+      std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+      ++failures;                                                      \
+    }                                                                  \
+  } while (0)
+
+template <class F>
+static bool throws_invalid(F&& f) {
+  try {
+    f();
+  } catch (const std::invalid_argument&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+
+int main(int argc, char** argv) {
+  const bool cpu_only = argc > 1 && std::strcmp(argv[1], "--cpu") == 0;
+  // modarith.hpp:109-111 / test_modarith.cpp:31-42
+  EXPECT(throws_invalid([] { nb::Modulus m(15); }));
+  EXPECT(throws_invalid([] { nb::Modulus m(2); }));
+  EXPECT(nb::Modulus(17).bits() == 5);
+  // ntt.hpp:219-236 / test_ntt.cpp:57-70 (validated before any device work)
+  EXPECT(throws_invalid([] { nb::NttTables t(4, nb::Modulus(13)); }));
+  EXPECT(throws_invalid([] { nb::NttTables t(3, nb::Modulus(17)); }));
+  EXPECT(throws_invalid([] { nb::NttTables t(4, nb::Modulus(17), std::nullopt, 48); }));
+  EXPECT(throws_invalid([] { nb::NttTables t(4, nb::Modulus(17), uint64_t{3}); }));
+  if (cpu_only) {
+    std::printf(failures ? "facade cpu checks FAILED\n" : "facade cpu checks ok\n");
+    return failures ? 1 : 0;
+  }
+  // test_ntt.cpp:94-114: n=2, q=5
+  nb::NttTables t2(2, nb::Modulus(5));
+  EXPECT(t2.root() == 2);
+  std::vector<uint64_t> a{1, 1}, out(2);
+  t2.forward(out, a, 1, 1);
+  EXPECT(out[0] == 3 && out[1] == 4);
+  t2.inverse(out, out, 1, 1);
+  EXPECT(out[0] == 1 && out[1] == 1);
+  EXPECT(throws_invalid([&] { t2.forward(out, a, 3, 1); }));
+  // round trip at cfg1 size through the HEXL names
+  const uint64_t q = 1125899906826241ull;
+  nb::hexl::NTT ntt(4096, q);
+  std::mt19937_64 eng(1 ^ 20260809);
+  std::vector<uint64_t> x(4096), y(4096), z(4096);
+  for (auto& v : x) v = eng() % q;
+  ntt.ComputeForward(y.data(), x.data(), 1, 1);
+  ntt.ComputeInverse(z.data(), y.data(), 1, 1);
+  EXPECT(z == x);
+  // test_eltwise.cpp:180-186: 2*3+4 mod 17 = 10
+  uint64_t r = 0, two = 2, four = 4;
+  nb::hexl::EltwiseFMAMod(&r, &two, 3, &four, 1, 17, 1);
+  EXPECT(r == 10);
+  // (q-1)^2 == 1
+  std::vector<uint64_t> top(64, q - 1), one(64);
+  nb::hexl::EltwiseMultMod(one.data(), top.data(), top.data(), 64, q, 1);
+  for (auto v : one) EXPECT(v == 1);
+  // test_ring.cpp:41-54: X * X^(n-1) = -1 mod (X^8 + 1, 97)
+  nb::NttTables t8(8, nb::Modulus(97));
+  std::vector<uint64_t> xa(8, 0), xb(8, 0), xc(8);
+  xa[1] = 1;
+  xb[7] = 1;
+  nb::poly_mult_mod(xc, xa, xb, t8);
+  EXPECT(xc[0] == 96);
+  for (int i = 1; i < 8; ++i) EXPECT(xc[i] == 0);
+  std::printf(failures ? "facade gpu checks FAILED\n" : "facade gpu checks ok\n");
+  return failures ? 1 : 0;
+}
