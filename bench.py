@@ -14,7 +14,7 @@ Multi-GPU: one process per GPU, each rank transforms its own cfg3 batch
 
 --impl reference: the reference's own CPU code (oracle/_ref/libnttref.so, built
 from the unmodified nttkit headers) on all host threads, same config/metric, on
-a bounded sample of rows per step.
+the full cfg3 batch per step.
 """
 from __future__ import annotations
 
@@ -113,20 +113,24 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_reference(moduli, rows, reps, threads):
-    """The reference's NttTables::forward/inverse on `rows` rows, all threads."""
+def cpu_reference(moduli, rows, reps, threads, min_seconds=0.0):
+    """The reference's NttTables::forward/inverse (oracle/_ref, the unmodified
+    nttkit headers) on `rows` rows with `threads` host threads; returns the
+    per-step times (at least `reps` steps and at least `min_seconds` total)."""
+    import ctypes as C
+
     from oracle_lib import Ref
 
     ref = Ref()
-    x = make_inputs(moduli, rows // len(moduli) or 1, SEED)[: rows * N]
+    npolys = max(1, rows // len(moduli))
+    x = make_inputs(moduli, npolys, SEED)[: rows * N]
     out = np.empty_like(x)
-    import ctypes as C
-
     mods = np.asarray(moduli, np.uint64)
     p = ref.lib.ref_plan_create(N, mods.ctypes.data_as(C.POINTER(C.c_uint64)), mods.size)
     ptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint64))  # noqa: E731
     times = []
-    for _ in range(reps):
+    t_start = time.perf_counter()
+    while len(times) < reps or time.perf_counter() - t_start < min_seconds:
         t0 = time.perf_counter()
         ref.lib.ref_plan_ntt(p, 0, ptr(out), ptr(x), rows, 1, 1, threads)
         ref.lib.ref_plan_ntt(p, 1, ptr(out), ptr(out), rows, 1, 1, threads)
@@ -137,29 +141,75 @@ def cpu_reference(moduli, rows, reps, threads):
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path
+    (nttkit NttTables::forward + inverse, compiled -O3 -DNDEBUG into
+    oracle/_ref/libnttref.so) on all host threads, the full cfg3 batch per step.
+    Under torchrun only rank 0 runs it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     moduli = cfg3_moduli()
     threads = os.cpu_count() or 1
-    rows = max(len(moduli), min(2048, 64 * threads))  # bounded sample per step
-    rows -= rows % len(moduli)
+    rows = NPOLYS * NLIMBS
     cpu_reference(moduli, rows, max(1, args.warmup), threads)  # warm-up
     times = cpu_reference(moduli, rows, args.steps, threads)
     t = statistics.median(times)
     v = 2 * rows * N / t / 1e6
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "Mcoeff/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (mt19937_64, uniform [0,q))",
         "config": {"workload": "cfg3: N=16384, 32 limbs x 64 polys, fwd(1,1)+inv(1,1)",
-                   "sample_rows_per_step": rows},
+                   "rows_per_step": rows},
         "cpu_baseline": {"value": v, "unit": "Mcoeff/s", "cores": threads, "kind": "reference",
-                         "sample": f"{rows} rows of N=16384 (of 2048), fwd+inv per step"},
+                         "sample": f"full cfg3 batch ({rows} rows of N=16384) fwd+inv per step"},
         "e2e": {"value": v, "unit": "Mcoeff/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def ncu_traffic():
+    """dram read+write bytes per forward launch from the committed ncu capture
+    (profiles/ncu_summary.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        k = d["kernels"]["ntt_block14_tma<Arith52F,fwd>"]
+        return float(k["dram_bytes_read"]) + float(k["dram_bytes_write"])
+    except Exception:
+        return None
+
+
+def modmul_bench(stream, reps=20):
+    """cfg2 vector-vector EltwiseMultMod, 2^20 words, 60-bit q, on 16 rotating
+    buffer sets (16 x 24 MiB > 126 MB L2): GB/s at 24 B/word."""
+    import torch
+
+    import paper_2103_16400_b200 as nk
+    from primes import cfg2_modulus
+
+    q = cfg2_modulus()
+    n = 1 << 20
+    sets = 16
+    g = torch.Generator(device="cuda").manual_seed(2)
+    a = torch.randint(0, 1 << 59, (sets, n), dtype=torch.int64, device="cuda", generator=g)
+    b = torch.randint(0, 1 << 59, (sets, n), dtype=torch.int64, device="cuda", generator=g)
+    r = torch.empty_like(a)
+    for i in range(sets):
+        nk.eltwise_mult_mod(r[i], a[i], b[i], q, 1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for k in range(reps * sets):
+        i = k % sets
+        nk.eltwise_mult_mod(r[i], a[i], b[i], q, 1)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / (reps * sets)
+    return {"metric": "EltwiseMultMod GB/s (cfg2: 2^20 x 60-bit, 24 B/word)",
+            "value": 24 * n / (us * 1e-6) / 1e9, "us_per_call": us,
+            "l2": "16 rotating buffer sets of 24 MiB (384 MiB > 126 MB L2)"}
 
 
 def run_gpu(args):
@@ -266,12 +316,14 @@ def run_gpu(args):
         cpu = None
         if not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
-            rows = 2 * NLIMBS
-            times = cpu_reference(moduli, rows, 3, threads)
+            rows = NPOLYS * NLIMBS
+            times = cpu_reference(moduli, rows, 2, threads, min_seconds=10.0)
             tt = statistics.median(times)
             cpu = {"value": 2 * rows * N / tt / 1e6, "unit": "Mcoeff/s", "cores": threads,
                    "kind": "reference",
-                   "sample": f"{rows} rows of N=16384 fwd+inv (reference NttTables, -O3 -DNDEBUG)"}
+                   "sample": f"full cfg3 batch fwd+inv, {len(times)} steps (~10 s), reference "
+                             f"NttTables (-O3 -DNDEBUG) on {threads} threads"}
+        modmul = modmul_bench(stream)
         line = {
             "metric": METRIC, "value": value, "unit": "Mcoeff/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -283,7 +335,7 @@ def run_gpu(args):
             "fwd_ms": fwd_ms, "inv_ms": inv_ms,
             "fwd_mcoeff_s": words / fwd_ms / 1e3, "inv_mcoeff_s": words / inv_ms / 1e3,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "kernel": "ntt_block<14,5,52,fwd>",
+                         "frac": achieved / hbm, "traffic": None, "kernel": "ntt_block14_tma<Arith52F,fwd>",
                          "peak_kind": peak_kind, "algorithmic_bytes_per_launch": fwd_bytes},
             "int_pipe": {"butterflies_per_launch": butterflies,
                          "gbfly_s": butterflies / (fwd_ms * 1e-3) / 1e9},
@@ -292,6 +344,7 @@ def run_gpu(args):
                     "d2h_bytes_per_step": 2 * 8 * words,
                     "path": "nk_ntt_forward_host + nk_ntt_inverse_host (pinned host buffers)"},
             "gpu_launches": launches, "clocks": clocks,
+            "modmul": modmul,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -301,8 +354,8 @@ def run_gpu(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
