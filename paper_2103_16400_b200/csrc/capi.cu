@@ -307,10 +307,38 @@ int ntt_dispatch(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, 
 }
 
 unsigned eltwise_grid(uint64_t work) {
-  // enough CTAs for every SM to stream; grid-stride covers the rest
-  uint64_t g = (work + 255) / 256;
-  const uint64_t cap = 148ull * 16;
+  // work = 16-byte chunks; each thread takes nk::kU chunks per sweep. Enough
+  // CTAs for ~2 waves of 8 resident 256-thread CTAs per SM; grid-stride beyond.
+  uint64_t g = (work + 256 * nk::kU - 1) / (256 * nk::kU);
+  const uint64_t cap = static_cast<uint64_t>(sm_count()) * 16;
   return static_cast<unsigned>(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+template <int FIN, bool SMALLQ, bool BATCHED>
+void launch_mult_t(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t total, uint32_t logn,
+                   nk::MultConst c0, const nk::MultConst* consts, uint32_t nlimbs, cudaStream_t st) {
+  nk::eltwise_mult_kernel<FIN, SMALLQ, BATCHED>
+      <<<eltwise_grid(total / 2 + 1), 256, 0, st>>>(r, a, b, total, logn, c0, consts, nlimbs);
+}
+
+int launch_mult(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t total, uint32_t logn,
+                nk::MultConst c0, const nk::MultConst* consts, uint32_t nlimbs, int fin, bool small,
+                cudaStream_t st) {
+  const bool batched = consts != nullptr;
+#define NK_M(F, S, B) launch_mult_t<F, S, B>(r, a, b, total, logn, c0, consts, nlimbs, st)
+#define NK_M2(F)                                                      \
+  if (small) { if (batched) NK_M(F, true, true); else NK_M(F, true, false); } \
+  else { if (batched) NK_M(F, false, true); else NK_M(F, false, false); }
+  switch (fin) {
+    case 1: NK_M2(1) break;
+    case 2: NK_M2(2) break;
+    default: NK_M2(4) break;
+  }
+#undef NK_M2
+#undef NK_M
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
 }
 
 }  // namespace
@@ -518,11 +546,10 @@ int nk_plan_eltwise_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* a,
   if (int rc = ensure_device(p->device)) return rc;
   const int fi = fin == 1 ? 0 : (fin == 2 ? 1 : 2);
   const uint64_t rows = static_cast<uint64_t>(npolys) * nlimbs;
-  nk::eltwise_mult_kernel<<<eltwise_grid(rows * p->n / 2), 256, 0, S(stream)>>>(
-      res, a, b, p->n, rows, nk::MultConst{}, p->mc[fi] + limb0, nlimbs);
-  g_launches++;
-  NK_CUDA(cudaGetLastError());
-  return 0;
+  bool small = true;
+  for (uint32_t l = 0; l < nlimbs; ++l) small &= p->q[limb0 + l] < (uint64_t{1} << 61);
+  return launch_mult(res, a, b, rows * p->n, p->logn, nk::MultConst{}, p->mc[fi] + limb0, nlimbs,
+                     static_cast<int>(fin), small, S(stream));
 }
 
 int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const uint64_t* g,
@@ -589,11 +616,8 @@ int nk_eltwise_mult_mod(uint64_t* res, const uint64_t* a, const uint64_t* b, uin
   if (n == 0) return 0;
   if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_mult_mod: NULL buffer");
   const nk::MultConst c{q, 2 * q, m.barrett, m.bits - 1, static_cast<int>(fin)};
-  cudaStream_t st = S(stream);
-  nk::eltwise_mult_kernel<<<eltwise_grid(n / 2 + 1), 256, 0, st>>>(res, a, b, n, 1, c, nullptr, 1);
-  g_launches++;
-  NK_CUDA(cudaGetLastError());
-  return 0;
+  return launch_mult(res, a, b, n, 0, c, nullptr, 1, static_cast<int>(fin), q < (uint64_t{1} << 61),
+                     S(stream));
 }
 
 int nk_eltwise_fma_mod(uint64_t* res, const uint64_t* a, uint64_t y, const uint64_t* z, uint64_t n,
@@ -606,13 +630,21 @@ int nk_eltwise_fma_mod(uint64_t* res, const uint64_t* a, uint64_t y, const uint6
                        static_cast<int>(fin), bs};
   cudaStream_t st = S(stream);
   const unsigned grid = eltwise_grid(n / 2 + 1);
-  if (bs == 52) {
-    if (z) nk::eltwise_fma_kernel<52, true><<<grid, 256, 0, st>>>(res, a, z, n, c);
-    else nk::eltwise_fma_kernel<52, false><<<grid, 256, 0, st>>>(res, a, z, n, c);
-  } else {
-    if (z) nk::eltwise_fma_kernel<64, true><<<grid, 256, 0, st>>>(res, a, z, n, c);
-    else nk::eltwise_fma_kernel<64, false><<<grid, 256, 0, st>>>(res, a, z, n, c);
+#define NK_FMA(BS, Z, F) nk::eltwise_fma_kernel<BS, Z, F><<<grid, 256, 0, st>>>(res, a, z, n, c)
+#define NK_FMA_F(BS, Z)                          \
+  switch (fin) {                                 \
+    case 1: NK_FMA(BS, Z, 1); break;             \
+    case 2: NK_FMA(BS, Z, 2); break;             \
+    case 4: NK_FMA(BS, Z, 4); break;             \
+    default: NK_FMA(BS, Z, 8); break;            \
   }
+  if (bs == 52) {
+    if (z) { NK_FMA_F(52, true) } else { NK_FMA_F(52, false) }
+  } else {
+    if (z) { NK_FMA_F(64, true) } else { NK_FMA_F(64, false) }
+  }
+#undef NK_FMA_F
+#undef NK_FMA
   g_launches++;
   NK_CUDA(cudaGetLastError());
   return 0;
