@@ -159,6 +159,11 @@ uint64_t nk_launch_count(void);
  * kernel writes the words of its first block after each of its three register
  * passes. NULL (the default) disables it. */
 void nk_debug_dump_to(uint64_t* d_buf);
+/* Testing aid: when on, every beta = 2^52 transform uses the exact lazy
+ * arithmetic (the reference's representatives) even where only the canonical
+ * result is observable, so the tests can cover both arithmetic paths. Off by
+ * default. */
+void nk_debug_exact_only(int on);
 
 #ifdef __cplusplus
 }

@@ -52,6 +52,7 @@ _SIGS = {
     "nk_version": (C.c_char_p, []),
     "nk_launch_count": (u64, []),
     "nk_debug_dump_to": (None, [vp]),
+    "nk_debug_exact_only": (None, [C.c_int]),
     "nk_modulus": (C.c_int, [u64, C.POINTER(C.c_uint32), u64p]),
     "nk_minimal_primitive_root": (C.c_int, [u64, u64, u64p]),
     "nk_tables_host": (C.c_int, [u64, u64, u64p, C.c_int, u64p, u64p, u64p, u64p, u64p, u64p,
@@ -206,6 +207,12 @@ def tables_host(n, q, root=None, bit_shift=0):
 
 def launch_count():
     return lib().nk_launch_count()
+
+
+def set_exact_only(on):
+    """Testing aid (nk_debug_exact_only): force the exact lazy arithmetic on
+    every beta = 2^52 transform, including canonical-output ones."""
+    lib().nk_debug_exact_only(1 if on else 0)
 
 
 # ---------------------------------------------------------------------------

@@ -25,6 +25,7 @@ namespace {
 
 thread_local std::string g_err;
 uint64_t* g_dbg = nullptr;  // nk_debug_dump_to()
+bool g_exact_only = false;  // nk_debug_exact_only()
 std::atomic<uint64_t> g_launches{0};
 
 int fail(int code, const std::string& msg) {
@@ -296,8 +297,14 @@ int ntt_dispatch(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, 
     const int bs = p->bs[limb0 + (uniform ? 0 : l)];
     const uint64_t words = static_cast<uint64_t>(npolys) * nlimbs * p->n;
     int rc;
-    if (bs == 52)
-      rc = fwd ? run_ntt<nk::Arith52F, true>(b, words, st) : run_ntt<nk::Arith52F, false>(b, words, st);
+    // beta = 2^52: signed FP64 arithmetic when only the canonical result is
+    // observable (fout == 1 and one kernel holds the whole row), else the
+    // reference's exact lazy representatives (nk::Arith52P)
+    const bool canon = (b.fout == 1) && (b.logn <= kLogBlock) && !g_exact_only;
+    if (bs == 52 && canon)
+      rc = fwd ? run_ntt<nk::Arith52S, true>(b, words, st) : run_ntt<nk::Arith52S, false>(b, words, st);
+    else if (bs == 52)
+      rc = fwd ? run_ntt<nk::Arith52P, true>(b, words, st) : run_ntt<nk::Arith52P, false>(b, words, st);
     else
       rc = fwd ? run_ntt<nk::ArithInt<64>, true>(b, words, st)
                : run_ntt<nk::ArithInt<64>, false>(b, words, st);
@@ -352,6 +359,7 @@ const char* nk_last_error(void) { return g_err.c_str(); }
 const char* nk_version(void) { return "nttkit_b200 0.1 (sm_100a)"; }
 uint64_t nk_launch_count(void) { return g_launches.load(); }
 void nk_debug_dump_to(uint64_t* d_buf) { g_dbg = d_buf; }
+void nk_debug_exact_only(int on) { g_exact_only = on != 0; }
 
 int nk_modulus(uint64_t q, uint32_t* bits, uint64_t* barrett_factor) {
   nk::host::Modulus m;
@@ -436,7 +444,7 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
     p->q.push_back(t.q);
     p->psi.push_back(t.psi);
     p->bs.push_back(t.bs);
-    // beta = 2^52 limbs run on the FP64 pipe (nk::Arith52F): table words hold the
+    // beta = 2^52 limbs run on the FP64 pipe (nk::Arith52P / Arith52S): table words hold the
     // doubles' bit patterns (exact: every value is below 2^52)
     const bool fp = (t.bs == 52);
     auto enc = [fp](uint64_t x) { return fp ? dbits(static_cast<double>(x)) : x; };
@@ -459,7 +467,8 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
     // see modmath.cuh)
     hl[l] = nk::LimbConst{t.q, 2 * t.q, ~t.q + 1, enc(t.ninv), enc(t.ninvp), 2 * t.q + nk::kDBias,
                           std::ldexp(static_cast<double>(t.q), -52), static_cast<double>(2 * t.q),
-                          t.bs, 0};
+                          t.bs, 0, static_cast<double>(t.q), 1.0 / static_cast<double>(t.q),
+                          static_cast<double>(t.q) + 4503599627370496.0};
     nk::host::Modulus m;
     nk::host::make_modulus(t.q, &m);
     const int fins[3] = {1, 2, 4};

@@ -180,7 +180,11 @@ struct LimbConstDev {
   double twoq_d;                        // 2q as a double
   int32_t bs;
   int32_t pad;
+  double q_d;     // q as a double
+  double qinv;    // 1/q rounded (Arith52S canonicalisation)
+  double q_bias;  // q + 2^52
 };
+constexpr double kC52x15 = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer constant
 
 template <int BS>
 struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)
@@ -199,6 +203,9 @@ struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)
     return mul_lazy<BS>(x, c.ninv, c.ninvp, c.negq);
   }
   __device__ static uint64_t csub(uint64_t x, uint64_t m) { return nk::csub(x, m); }
+  static constexpr bool kSigned = false;
+  __device__ static uint64_t red4(uint64_t x, const LimbConstDev& c) { return nk::csub(nk::csub(x, c.twoq), c.q); }
+  __device__ static uint64_t red2(uint64_t x, const LimbConstDev& c) { return nk::csub(x, c.q); }
 };
 
 struct Arith52F {  // beta = 2^52 on the FP64 pipe (requires 4q < 2^52)
@@ -231,6 +238,154 @@ struct Arith52F {  // beta = 2^52 on the FP64 pipe (requires 4q < 2^52)
     return mul_lazyD(xD, as_d(c.ninv), as_d(c.ninvp), c.qq);
   }
   __device__ static uint64_t csub(uint64_t xD, uint64_t m) { return csubD(xD, m); }
+  static constexpr bool kSigned = false;
+  __device__ static uint64_t red4(uint64_t x, const LimbConstDev& c) { return csubD(csubD(x, c.twoq), c.q); }
+  __device__ static uint64_t red2(uint64_t x, const LimbConstDev& c) { return csubD(x, c.q); }
 };
+
+// ---------------------------------------------------------------------------
+// beta = 2^52 on the FP64 pipe, values as plain doubles ("P representation").
+//
+// Same butterflies and the same representatives as Arith52F (so lazy outputs
+// stay bit-exact), but a word is carried as the double whose value it is, so
+// the Shoup product needs no unbiasing and the conditional subtraction is one
+// DADD plus a sign test: no 64-bit integer add (which ptxas issues as
+// IADD3 + IMAD.X, and IMAD shares issue bandwidth with the FP64 pipe).
+// Registers hold the double's bit pattern (uint64_t) so the kernels stay
+// policy-agnostic.
+// ---------------------------------------------------------------------------
+// y >= m ? y - m : y on plain doubles (y, m exact integers below 2^53)
+__device__ __forceinline__ double csubP(double y, double m) {
+  const double d = __dsub_rn(y, m);
+  return (static_cast<int32_t>(hi32(as_u(d))) >= 0) ? d : y;
+}
+
+struct Arith52P {
+  static constexpr bool kFP = true;
+  __device__ static uint64_t load(uint64_t x) { return as_u(__dsub_rn(as_d(x | kDBias), kC52)); }
+  __device__ static uint64_t store(uint64_t x) { return as_u(__dadd_rn(as_d(x), kC52)) & kMask52; }
+  template <bool ILTM>
+  __device__ static void fwd(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+    const double u = ILTM ? as_d(x0) : csubP(as_d(x0), c.twoq_d);
+    const double t = mul_lazy_plain(as_d(x1), as_d(w.x), as_d(w.y), c.qq);
+    x0 = as_u(__dadd_rn(u, t));
+    x1 = as_u(__dsub_rn(__dadd_rn(u, c.twoq_d), t));
+  }
+  template <bool ILTM>
+  __device__ static void inv(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+    const double a = as_d(x0), b = as_d(x1);
+    const double t = __dadd_rn(__dsub_rn(a, b), c.twoq_d);
+    double s = __dadd_rn(a, b);
+    if (!ILTM) s = csubP(s, c.twoq_d);
+    x0 = as_u(s);
+    x1 = as_u(mul_lazy_plain(t, as_d(w.x), as_d(w.y), c.qq));
+  }
+  __device__ static uint64_t scale_ninv(uint64_t x, const LimbConstDev& c) {
+    return as_u(mul_lazy_plain(as_d(x), as_d(c.ninv), as_d(c.ninvp), c.qq));
+  }
+  static constexpr bool kSigned = false;
+  __device__ static uint64_t red4(uint64_t x, const LimbConstDev& c) {
+    return as_u(csubP(csubP(as_d(x), c.twoq_d), c.q_d));
+  }
+  __device__ static uint64_t red2(uint64_t x, const LimbConstDev& c) { return as_u(csubP(as_d(x), c.q_d)); }
+};
+
+// ---------------------------------------------------------------------------
+// beta = 2^52 on the FP64 pipe, SIGNED values (canonical-output transforms
+// only: fout == 1). Requires q < 2^50 (so 4q <= 2^52).
+//
+// Signed Shoup product for |v| < 4q (so |W' v| < 2^104):
+//   hq = fma_rn(W', v, 3*2^104)   in [1.25, 1.75]*2^105, ulp 2^53, so
+//        hq - 3*2^104 = 2^53 * round(W' v / 2^53) = k * 2^52, k even, exact
+//   T  = w v - k q   (same TwoProduct/FMA steps as mul_lazy_plain, exact)
+// With W' = w 2^52/q - d (0 <= d < 1): T = q (W'v/2^52 - k) + q d v/2^52, and
+// |W'v/2^52 - k| <= 1, |d v/2^52| < 1, so |T| < 2q.
+// (The floor-with-2^104 form of mul_lazy_plain is unsigned-only: a negative
+// W'v drops the sum into the binade below 2^104, where the ulp is 2^51.)
+// Signed words drop Harvey's "+2q" (x1' = u - T) and the GS "+2q" (t = x0 - x1):
+//   forward: |x| < 4q in, u = x0 - 2q sgn(x0) [|x0| >= 2q] in (-2q, 2q),
+//            x0' = u + T, x1' = u - T in (-4q, 4q)
+//   inverse: |x| < 2q in, s = x0 + x1 in (-4q, 4q) -> (-2q, 2q) by the same
+//            signed conditional subtraction, x1' = T(x0 - x1) in (-2q, 2q)
+// Representatives differ from the reference's lazy ones; canonical results
+// (every value reduced to [0, q) at the end) are identical.
+// ---------------------------------------------------------------------------
+constexpr double kC104x3 = 60847228810955011271841753858048.0;  // 3 * 2^104
+
+__device__ __forceinline__ double mul_signed(double v, double w, double wp, double qq) {
+  const double hq = __fma_rn(wp, v, kC104x3);
+  const double qh = __dsub_rn(hq, kC104x3);
+  const double h1 = __dmul_rn(w, v);
+  const double l1 = __fma_rn(w, v, -h1);
+  const double e = __fma_rn(-qh, qq, h1);
+  return __dadd_rn(e, l1);
+}
+// |y| >= m ? y - m sgn(y) : y  (one DADD on |y|, sign copied on the integer pipe)
+__device__ __forceinline__ double csubS(double y, double m) {
+  const double d = __dsub_rn(fabs(y), m);
+  const uint64_t yb = as_u(y), db = as_u(d);
+  const uint64_t r = db | (yb & 0x8000000000000000ull);
+  return (static_cast<int32_t>(hi32(db)) >= 0) ? as_d(r) : y;
+}
+
+struct Arith52S {
+  static constexpr bool kFP = true;
+  static constexpr bool kSigned = true;
+  __device__ static uint64_t load(uint64_t x) { return as_u(__dsub_rn(as_d(x | kDBias), kC52)); }
+  // raw bits; the dispatcher never runs this policy where an intermediate
+  // (non-canonical) result is written to memory
+  __device__ static uint64_t store(uint64_t x) { return x; }
+  // canonical integer of a value x in (-8q, 8q): k = round(x/q) (x*qinv is
+  // within 2^-49 of x/q), r = x - kq exact in (-q/2 - 1, q/2 + 1); the result
+  // is r + q or r, formed in the biased domain (2^52 + r + q, then minus q
+  // when that stays >= 2^52), so no signed-zero case can arise.
+  __device__ static uint64_t canon(double x, const LimbConstDev& c) {
+    const double k = __dsub_rn(__fma_rn(x, c.qinv, kC52x15), kC52x15);
+    const double r = __fma_rn(-k, c.q_d, x);
+    const uint64_t rb = as_u(__dadd_rn(r, c.q_bias));  // 2^52 + r + q
+    const uint64_t db = as_u(__dsub_rn(as_d(rb), c.q_d));
+    return ((hi32(db) >= 0x43300000u) ? db : rb) & kMask52;
+  }
+  template <bool ILTM>
+  __device__ static void fwd(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+    const double u = ILTM ? as_d(x0) : csubS(as_d(x0), c.twoq_d);
+    const double t = mul_signed(as_d(x1), as_d(w.x), as_d(w.y), c.qq);
+    x0 = as_u(__dadd_rn(u, t));
+    x1 = as_u(__dsub_rn(u, t));
+  }
+  template <bool ILTM>
+  __device__ static void inv(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+    const double a = as_d(x0), b = as_d(x1);
+    const double t = __dsub_rn(a, b);
+    double s = __dadd_rn(a, b);
+    if (!ILTM) s = csubS(s, c.twoq_d);
+    x0 = as_u(s);
+    x1 = as_u(mul_signed(t, as_d(w.x), as_d(w.y), c.qq));
+  }
+  __device__ static uint64_t scale_ninv(uint64_t x, const LimbConstDev& c) {
+    return as_u(mul_signed(as_d(x), as_d(c.ninv), as_d(c.ninvp), c.qq));
+  }
+};
+
+// Final word of a forward transform (small_mod(x, q, 4) when fout == 1,
+// ntt.hpp:282-284) and of an inverse (n^-1 Shoup pass, ntt.hpp:429-432, then
+// small_mod(x, q, 2) when fout == 1, ntt.hpp:303-305), as stored integers.
+template <class A>
+__device__ __forceinline__ uint64_t fwd_out(uint64_t x, const LimbConstDev& c, int fout) {
+  if constexpr (A::kSigned) {
+    return A::canon(as_d(x), c);
+  } else {
+    return A::store(fout == 1 ? A::red4(x, c) : x);
+  }
+}
+template <class A>
+__device__ __forceinline__ uint64_t inv_out(uint64_t x, const LimbConstDev& c, int fout) {
+  const uint64_t y = A::scale_ninv(x, c);
+  if constexpr (A::kSigned) {
+    return A::canon(as_d(y), c);
+  } else {
+    return A::store(fout == 1 ? A::red2(y, c) : y);
+  }
+}
 
 }  // namespace nk

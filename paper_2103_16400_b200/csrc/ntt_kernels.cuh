@@ -211,19 +211,9 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV)) ntt_block(NttArgs a) {
   constexpr int PL = S::NP - 1;
   constexpr int LO = PO::lo(PL), K = PO::k(PL);
   constexpr int R = 1 << K, G = S::V / R;
-  if (FWD) {
-    if (a.fout == 1) {
+  // ntt_block always transforms whole rows: final words
 #pragma unroll
-      for (int i = 0; i < S::V; ++i) v[i] = A::csub(A::csub(v[i], c.twoq), c.q);  // small_mod(x,q,4)
-    }
-  } else if (whole) {
-#pragma unroll
-    for (int i = 0; i < S::V; ++i) v[i] = A::scale_ninv(v[i], c);
-    if (a.fout == 1) {
-#pragma unroll
-      for (int i = 0; i < S::V; ++i) v[i] = A::csub(v[i], c.q);  // small_mod(x,q,2)
-    }
-  }
+  for (int i = 0; i < S::V; ++i) v[i] = FWD ? fwd_out<A>(v[i], c, a.fout) : inv_out<A>(v[i], c, a.fout);
   const uint32_t jt = S::scatter(t, LO, K);
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -232,10 +222,10 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV)) ntt_block(NttArgs a) {
 #pragma unroll
       for (int r = 0; r < R; r += 2)
         *reinterpret_cast<ulonglong2*>(dst + jt + jg + r) =
-            make_ulonglong2(A::store(v[g * R + r]), A::store(v[g * R + r + 1]));
+            make_ulonglong2(v[g * R + r], v[g * R + r + 1]);
     } else {
 #pragma unroll
-      for (int r = 0; r < R; ++r) dst[jt + jg + (r << LO)] = A::store(v[g * R + r]);
+      for (int r = 0; r < R; ++r) dst[jt + jg + (r << LO)] = v[g * R + r];
     }
   }
 }
@@ -530,10 +520,8 @@ __global__ void __launch_bounds__(512, 1)
 
     // ---- fix-ups and store ----
     if (FWD) {
-      if (a.fout == 1) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = A::csub(A::csub(v[i], c.twoq), c.q);  // small_mod(x,q,4)
-      }
+      for (int i = 0; i < 32; ++i) v[i] = fwd_out<A>(v[i], c, a.fout);
       // P3 holds 32 contiguous words per thread; transpose each half (bit 4)
       // through B so the global stores are lane-contiguous: B holds the half as
       // 512 rows of 16 words (row = t) in the 128B-swizzled arrangement, so
@@ -545,7 +533,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
         for (int cc = 0; cc < 8; ++cc)
           *reinterpret_cast<ulonglong2*>(Bb + (t << 7) + ((cc ^ (t & 7)) << 4)) =
-              make_ulonglong2(A::store(v[16 * h + 2 * cc]), A::store(v[16 * h + 2 * cc + 1]));
+              make_ulonglong2(v[16 * h + 2 * cc], v[16 * h + 2 * cc + 1]);
         __syncthreads();
 #pragma unroll
         for (int s2 = 0; s2 < 8; ++s2) {
@@ -558,15 +546,14 @@ __global__ void __launch_bounds__(512, 1)
     } else {
       if (lognb == 0) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = A::scale_ninv(v[i], c);
-        if (a.fout == 1) {
+        for (int i = 0; i < 32; ++i) v[i] = inv_out<A>(v[i], c, a.fout);
+      } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = A::csub(v[i], c.q);
-        }
+        for (int i = 0; i < 32; ++i) v[i] = A::store(v[i]);  // intermediate of a long row
       }
       // P3 holds j = t + 512 r: coalesced already
 #pragma unroll
-      for (int r = 0; r < 32; ++r) dst[jt3 | P3::jc(0, r)] = A::store(v[r]);
+      for (int r = 0; r < 32; ++r) dst[jt3 | P3::jc(0, r)] = v[r];
     }
   }
 }
@@ -615,15 +602,9 @@ __global__ void __launch_bounds__(256) ntt_global_pass(NttArgs a, uint32_t lo, i
       }
     }
   }
-  if (!FWD && last) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      v[r] = A::scale_ninv(v[r], c);
-      if (a.fout == 1) v[r] = A::csub(v[r], c.q);
-    }
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) dst[j0 + (static_cast<uint64_t>(r) << lo)] = A::store(v[r]);
+  for (int r = 0; r < R; ++r)
+    dst[j0 + (static_cast<uint64_t>(r) << lo)] = (!FWD && last) ? inv_out<A>(v[r], c, a.fout) : A::store(v[r]);
 }
 
 // ---------------------------------------------------------------------------
@@ -660,14 +641,7 @@ __global__ void __launch_bounds__(256) ntt_small(NttArgs a) {
     __syncthreads();
   }
   for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) {
-    uint64_t x = smw[j];
-    if (FWD) {
-      if (a.fout == 1) x = A::csub(A::csub(x, c.twoq), c.q);
-    } else {
-      x = A::scale_ninv(x, c);
-      if (a.fout == 1) x = A::csub(x, c.q);
-    }
-    a.out[row * a.n + j] = A::store(x);
+    a.out[row * a.n + j] = FWD ? fwd_out<A>(smw[j], c, a.fout) : inv_out<A>(smw[j], c, a.fout);
   }
 }
 

@@ -74,18 +74,57 @@ def check_dir(nk, oracle, n, moduli, npolys, seed, fwd_factors=FWD_FACTORS,
 
 @pytest.mark.parametrize("logn", list(range(1, 11)))
 @pytest.mark.parametrize("bits", [20, 30, 50, 61])
-def test_small_sizes_match_oracle(nk, oracle, logn, bits):
+def test_small_sizes_match_oracle(nk, oracle, logn, bits, arith):
     n = 1 << logn
     moduli = smallest_ntt_primes(bits, n, 2)
     check_dir(nk, oracle, n, moduli, 3, 100 + logn * 7 + bits)
 
 
+@pytest.fixture(params=[False, True], ids=["auto", "exact_only"])
+def arith(request, nk):
+    """Canonical-output beta = 2^52 transforms run signed FP64 arithmetic by
+    default; exact_only forces the lazy-exact arithmetic on them too."""
+    nk.set_exact_only(request.param)
+    yield request.param
+    nk.set_exact_only(False)
+
+
 @pytest.mark.parametrize("logn", [11, 12, 13, 14])
 @pytest.mark.parametrize("bits", [30, 50, 60, 61])
-def test_block_sizes_match_oracle(nk, oracle, logn, bits):
+def test_block_sizes_match_oracle(nk, oracle, logn, bits, arith):
     n = 1 << logn
     moduli = largest_ntt_primes(bits, n, 3)
     check_dir(nk, oracle, n, moduli, 2, 300 + logn * 7 + bits)
+
+
+@pytest.mark.parametrize("logn", [1, 3, 10, 12, 14])
+@pytest.mark.parametrize("pattern", ["max", "zero", "alt", "top"])
+def test_extreme_inputs(nk, oracle, logn, pattern, arith):
+    """Worst-case magnitudes for the lazy/signed bounds: all q-1 (lifted to
+    fin*q - 1), zeros, alternating 0 / max, and max in the top half only."""
+    n = 1 << logn
+    moduli = largest_ntt_primes(50, n, 2)
+    plan = nk.RnsNtt(n, moduli)
+    q = np.repeat(np.asarray(moduli, dtype=np.uint64), n)
+    for fin, fout in FWD_FACTORS + [(f, o) for f, o in INV_FACTORS]:
+        top = q * np.uint64(fin) - np.uint64(1)
+        if pattern == "max":
+            x = top
+        elif pattern == "zero":
+            x = np.zeros_like(q)
+        elif pattern == "alt":
+            x = np.where(np.arange(q.size) % 2 == 0, top, np.uint64(0)).astype(np.uint64)
+        else:
+            x = np.where((np.arange(q.size) % n) >= n // 2, top, np.uint64(0)).astype(np.uint64)
+        d = dev(x)
+        if (fin, fout) in FWD_FACTORS:
+            got = host(plan.forward(torch.empty_like(d), d, fin, fout))
+            want = oracle.forward(n, moduli, x, fin, fout)
+            assert np.array_equal(got, want), f"fwd {pattern} fin={fin} fout={fout}"
+        if (fin, fout) in INV_FACTORS:
+            got = host(plan.inverse(torch.empty_like(d), d, fin, fout))
+            want = oracle.inverse(n, moduli, x, fin, fout)
+            assert np.array_equal(got, want), f"inv {pattern} fin={fin} fout={fout}"
 
 
 @pytest.mark.parametrize("logn", [15, 16, 17, 18])
@@ -169,7 +208,7 @@ def test_definitional_transform(nk, oracle):
     assert np.array_equal(t.inverse(None, f, 1, 1), x)
 
 
-def test_cfg3_full(nk, oracle):
+def test_cfg3_full(nk, oracle, arith):
     """BASELINE cfg3: N=16384, 32 limbs x 64 polys, forward(1,1) and inverse(1,1)."""
     c = cfg3()
     n, moduli, npolys = c["n"], c["moduli"], c["npolys"]
