@@ -34,6 +34,11 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 METRIC = "fwd/inv NTT Mcoeff/s (N=16384, batched limbs)"
+FWD_KERNEL = "ntt_pair14<Arith52S,fwd>"  # the forward's only launch at cfg3
+# FP64 operations per butterfly of the signed canonical arithmetic
+# (modmath.cuh Arith52S: 6 for the Shoup product, 2 output adds, 1 for the
+# conditional subtraction), the floor the transform kernels are bound by
+DP_PER_BFLY = 9
 N = 16384
 NLIMBS = 32
 NPOLYS = 64
@@ -78,7 +83,27 @@ class ClockSampler:
         self._t = None
 
     def start(self):
+        def run_nvml():
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+                    ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4)]
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                self.samples.append([str(sm), str(mx), f"{pw:.1f}", hex(r)] +
+                                    ["Active" if r & b else "Not Active" for _, b in bits])
+                self._stop.wait(0.02)
+
         def run():
+            try:
+                return run_nvml()
+            except Exception:
+                pass
             q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -175,7 +200,7 @@ def ncu_traffic():
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        k = d["kernels"]["ntt_block14_tma<Arith52F,fwd>"]
+        k = d["kernels"][FWD_KERNEL]
         return float(k["dram_bytes_read"]) + float(k["dram_bytes_write"])
     except Exception:
         return None
@@ -317,6 +342,9 @@ def run_gpu(args):
     fwd_bytes = 16 * words  # read + write each coefficient once
     achieved = fwd_bytes / (fwd_ms * 1e-3) / 1e9
     butterflies = (N // 2) * 14 * NPOLYS * NLIMBS
+    sm_clock = clocks.get("sm_mhz") or smmax
+    dp_floor_us = butterflies * DP_PER_BFLY / (64 * 148 * sm_clock * 1e6) * 1e6
+    survey_int_us = butterflies * 30 / (128 * 148 * smmax * 1e6) * 1e6
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
@@ -340,10 +368,23 @@ def run_gpu(args):
             "fwd_ms": fwd_ms, "inv_ms": inv_ms,
             "fwd_mcoeff_s": words / fwd_ms / 1e3, "inv_mcoeff_s": words / inv_ms / 1e3,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "kernel": "ntt_block14_tma<Arith52F,fwd>",
-                         "peak_kind": peak_kind, "algorithmic_bytes_per_launch": fwd_bytes},
+                         "frac": achieved / hbm, "traffic": ncu_traffic(), "kernel": FWD_KERNEL,
+                         "peak_kind": peak_kind, "algorithmic_bytes_per_launch": fwd_bytes,
+                         "note": "traffic: dram read+write of one ncu --set full capture "
+                                 "(profiles/ncu_summary.json); the kernel is FP64-pipe bound, "
+                                 "see compute"},
+            # the binding roofline of the transform: FP64 issue (64 DP ops/clk/SM,
+            # tools/pipe_bench.cu) at the run's SM clock
+            "compute": {"pipe": "fp64", "dp_ops_per_butterfly": DP_PER_BFLY,
+                        "butterflies_per_launch": butterflies,
+                        "t_floor_us": dp_floor_us, "t_measured_us": fwd_ms * 1e3,
+                        "frac": dp_floor_us / (fwd_ms * 1e3),
+                        "sm_mhz": sm_clock},
             "int_pipe": {"butterflies_per_launch": butterflies,
-                         "gbfly_s": butterflies / (fwd_ms * 1e-3) / 1e9},
+                         "gbfly_s": butterflies / (fwd_ms * 1e-3) / 1e9,
+                         "survey_int_model_frac": survey_int_us / (fwd_ms * 1e3),
+                         "survey_int_model": "30 integer instr/butterfly at 128 lanes/clk/SM "
+                                             "(SURVEY.md 8(d))"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "Mcoeff/s", "h2d_bytes_per_step": 2 * 8 * words,
                     "d2h_bytes_per_step": 2 * 8 * words,
@@ -359,7 +400,7 @@ def run_gpu(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -164,6 +164,9 @@ void nk_debug_dump_to(uint64_t* d_buf);
  * result is observable, so the tests can cover both arithmetic paths. Off by
  * default. */
 void nk_debug_exact_only(int on);
+/* Testing aid: which kernel transforms 16384-word blocks. -1 (default) = the
+ * faster one per direction, 0 = the CTA-pair kernel, 1 = the single-CTA kernel. */
+void nk_debug_block_kernel(int which);
 
 #ifdef __cplusplus
 }

@@ -53,6 +53,7 @@ _SIGS = {
     "nk_launch_count": (u64, []),
     "nk_debug_dump_to": (None, [vp]),
     "nk_debug_exact_only": (None, [C.c_int]),
+    "nk_debug_block_kernel": (None, [C.c_int]),
     "nk_modulus": (C.c_int, [u64, C.POINTER(C.c_uint32), u64p]),
     "nk_minimal_primitive_root": (C.c_int, [u64, u64, u64p]),
     "nk_tables_host": (C.c_int, [u64, u64, u64p, C.c_int, u64p, u64p, u64p, u64p, u64p, u64p,
@@ -213,6 +214,12 @@ def set_exact_only(on):
     """Testing aid (nk_debug_exact_only): force the exact lazy arithmetic on
     every beta = 2^52 transform, including canonical-output ones."""
     lib().nk_debug_exact_only(1 if on else 0)
+
+
+def set_block_kernel(which):
+    """Testing aid (nk_debug_block_kernel): -1 = per-direction default,
+    0 = CTA-pair kernel, 1 = single-CTA kernel, for 16384-word blocks."""
+    lib().nk_debug_block_kernel(int(which))
 
 
 # ---------------------------------------------------------------------------

@@ -18,6 +18,7 @@
 #include "eltwise_kernels.cuh"
 #include "host_math.hpp"
 #include "ntt_kernels.cuh"
+#include "ntt_pair.cuh"
 
 using nk::host::u128;
 
@@ -135,6 +136,22 @@ int make_row_map(CUtensorMap* map, const uint64_t* base, uint64_t words) {
   return 0;
 }
 
+// 3D view [words/512][32 lines][16 words] (no swizzle), boxes 16 x 16 x 32:
+// one box = the 8192 words of a 16384-word block with index bit 8 fixed.
+int make_superline_map(CUtensorMap* map, const uint64_t* base, uint64_t words) {
+  EncodeTiledFn fn;
+  if (int rc = encode_fn(&fn)) return rc;
+  const cuuint64_t dims[3] = {16, 32, words / 512};
+  const cuuint64_t strides[2] = {128, 4096};
+  const cuuint32_t box[3] = {16, 16, 32};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NK_ERR_CUDA, "cuTensorMapEncodeTiled(3D) failed (" + std::to_string(r) + ")");
+  return 0;
+}
+
 int sm_count() {
   static int n[64] = {};
   int dev = 0;
@@ -163,8 +180,52 @@ int launch_tma_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cuda
   return 0;
 }
 
+// CTA-pair kernel (ntt_pair.cuh): persistent, one cluster of 2 per block in
+// flight, as many clusters as fit (2 CTAs per SM).
+template <class A, bool FWD, bool IL>
+int launch_pair_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
+  CUtensorMap map;
+  if (int rc = FWD ? make_superline_map(&map, a.in, buf_words) : make_row_map(&map, a.in, buf_words)) return rc;
+  auto kern = nk::ntt_pair14<A, FWD, IL>;
+  if (int rc = set_smem(kern, nk::kPairSmemBytes)) return rc;
+  static int max_clusters[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!max_clusters[dev & 63]) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * sm_count());
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = nk::kPairSmemBytes;
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 2;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    NK_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
+    max_clusters[dev & 63] = n > 0 ? n : sm_count();
+  }
+  const uint64_t mc = static_cast<uint64_t>(max_clusters[dev & 63]);
+  const uint64_t g = nitems < mc ? nitems : mc;
+  kern<<<static_cast<unsigned>(2 * g), 256, nk::kPairSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int g_block_kernel = -1;  // nk_debug_block_kernel(): -1 auto, 0 pair, 1 single
+
 template <class A, bool FWD>
 int launch_tma(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm, cudaStream_t st) {
+  // measured on B200 (cfg3): the CTA-pair kernel is the faster forward, the
+  // single-CTA kernel the faster inverse (the pair inverse exchanges late,
+  // so its next TMA overlaps less compute)
+  const bool pair = g_block_kernel < 0 ? FWD : g_block_kernel == 0;
+  if (pair)
+    return iltm ? launch_pair_t<A, FWD, true>(a, nitems, buf_words, st)
+                : launch_pair_t<A, FWD, false>(a, nitems, buf_words, st);
   return iltm ? launch_tma_t<A, FWD, true>(a, nitems, buf_words, st)
               : launch_tma_t<A, FWD, false>(a, nitems, buf_words, st);
 }
@@ -360,6 +421,7 @@ const char* nk_version(void) { return "nttkit_b200 0.1 (sm_100a)"; }
 uint64_t nk_launch_count(void) { return g_launches.load(); }
 void nk_debug_dump_to(uint64_t* d_buf) { g_dbg = d_buf; }
 void nk_debug_exact_only(int on) { g_exact_only = on != 0; }
+void nk_debug_block_kernel(int which) { g_block_kernel = which; }
 
 int nk_modulus(uint64_t q, uint32_t* bits, uint64_t* barrett_factor) {
   nk::host::Modulus m;

@@ -363,6 +363,9 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __re
   // block's segment plus this thread's jhi): loads of one (stage, d) are
   // lane-contiguous and their offsets are immediates
   constexpr bool kLow = (PD::LO == 0 && PD::K == 5);
+#if defined(NK_DBG_NO_COMPUTE)  // perf experiment only: data movement without butterflies
+  return;
+#endif
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     const int i = FWD ? (K - 1 - s) : s;
@@ -372,7 +375,11 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __re
       const uint64_t base = (xt + PD::jc(g, 0)) >> (b + 1);
 #pragma unroll
       for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
+#if defined(NK_DBG_TW_SMALL)  // perf experiment only: L1-resident twiddles (wrong results)
+        const ulonglong2 w = ldtw(tw + ((base + hi) & 63));
+#else
         const ulonglong2 w = kLow ? ldtw(twl + low_index(b, hi, 0)) : ldtw(tw + base + hi);
+#endif
 #pragma unroll
         for (int l = 0; l < (1 << i); ++l) {
           const int r0 = (hi << (i + 1)) | l;

@@ -236,3 +236,17 @@ def test_cfg4_full(nk, oracle):
     x2 = lifted(oracle, fh, moduli, n, 2, 45)
     b = plan.inverse(torch.empty_like(d), dev(x2), 2, 1)
     assert np.array_equal(host(b), x)
+
+
+@pytest.mark.parametrize("kernel", [0, 1], ids=["pair", "single"])
+@pytest.mark.parametrize("logn,bits,npolys", [(14, 50, 3), (14, 60, 2), (15, 50, 1), (16, 60, 1)])
+def test_block_kernels_match_oracle(nk, oracle, kernel, logn, bits, npolys, arith):
+    """Both 16384-word block kernels (CTA pair / single CTA), both arithmetic
+    paths, whole rows and the low 14 bits of long rows, odd block counts."""
+    nk.set_block_kernel(kernel)
+    try:
+        n = 1 << logn
+        moduli = largest_ntt_primes(bits, n, 3)
+        check_dir(nk, oracle, n, moduli, npolys, 900 + logn + bits + kernel)
+    finally:
+        nk.set_block_kernel(-1)

@@ -1,0 +1,101 @@
+// Microbenchmark: the register passes of the block kernels (pass14, real
+// twiddle tables and index patterns), without exchanges or HBM traffic.
+// Separates the compute-phase efficiency from the data movement.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2103_16400_b200/csrc \
+//        -o tools/pass_bench tools/pass_bench.cu
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "ntt_kernels.cuh"
+
+using namespace nk;
+
+template <class A, bool FWD, int WHICH>
+__global__ void __launch_bounds__(256, 2) kern(const ulonglong2* tw, const ulonglong2* twl, LimbConstDev c,
+                                               uint32_t nlimbs, uint32_t iters, uint64_t* out) {
+  using P1 = typename std::conditional<FWD, PassD<9, 5, -1>, PassD<0, 5, -1>>::type;
+  using P2 = PassD<5, 4, 4>;
+  using P3 = typename std::conditional<FWD, PassD<0, 5, -1>, PassD<9, 5, -1>>::type;
+  const uint32_t t = threadIdx.x, l = t & 31, w = t >> 5, cta = blockIdx.x & 1;
+  const uint32_t jt_p2 = (l & 15u) | ((l >> 4) << 9) | (w << 10) | (cta << 13);
+  const uint32_t jt_low = (l << 5) | (w << 10) | (cta << 13);
+  const uint32_t jt_hi = t | (cta << 8);
+  const uint64_t n = 16384;
+  uint64_t v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = A::load((t * 977u + i * 131u) % 1000003u);
+  for (uint32_t it = 0; it < iters; ++it) {
+    const uint32_t limb = (blockIdx.x / 2 + it * 148) % nlimbs;
+    const ulonglong2* tl = tw + limb * n;
+    const ulonglong2* tll = twl + limb * n + (jt_low >> 5);
+    if (WHICH & 1) pass14<A, FWD, P1, false>(v, tl, tll, n, n + (FWD ? jt_hi : jt_low), c);
+    if (WHICH & 2) pass14<A, FWD, P2, false>(v, tl, tll, n, n + jt_p2, c);
+    if (WHICH & 4) pass14<A, FWD, P3, false>(v, tl, tll, n, n + (FWD ? jt_low : jt_hi), c);
+  }
+  uint64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) s ^= v[i];
+  if (s == 0x12345) out[t] = s;
+}
+
+static uint64_t dbits(double d) {
+  uint64_t u;
+  memcpy(&u, &d, 8);
+  return u;
+}
+
+template <class A, bool FWD, int WHICH>
+void run(const char* name, const ulonglong2* tw, const ulonglong2* twl, const LimbConstDev& c, int bfly_per_iter) {
+  uint64_t* out;
+  cudaMalloc(&out, 1 << 16);
+  const uint32_t iters = 200;
+  kern<A, FWD, WHICH><<<296, 256>>>(tw, twl, c, 32, 10, out);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  kern<A, FWD, WHICH><<<296, 256>>>(tw, twl, c, 32, iters, out);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double bf = 296.0 * 256 * iters * bfly_per_iter;
+  printf("%-26s %s: %8.3f ms  %5.2f bfly/clk/SM (1965 MHz)  %s\n", name, FWD ? "fwd" : "inv", ms,
+         bf / (ms * 1e-3) / 148 / 1.965e9, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(out);
+}
+
+int main() {
+  const uint64_t q = 1125899904679937ull, n = 16384;
+  LimbConstDev c{};
+  c.q = q;
+  c.twoq = 2 * q;
+  c.negq = 0 - q;
+  c.qq = double(q) / 4503599627370496.0;
+  c.twoq_d = double(2 * q);
+  c.q_d = double(q);
+  c.qinv = 1.0 / double(q);
+  c.q_bias = double(q) + 4503599627370496.0;
+  c.bs = 52;
+  std::vector<ulonglong2> h(n * 32);
+  for (size_t i = 0; i < h.size(); ++i) {
+    const uint64_t w = (i * 0x9E3779B97F4A7C15ull) % q;
+    const uint64_t wp = (uint64_t)(((unsigned __int128)w << 52) / q);
+    h[i] = make_ulonglong2(dbits(double(w)), dbits(double(wp)));
+  }
+  ulonglong2 *tw, *twl;
+  cudaMalloc(&tw, h.size() * 16);
+  cudaMalloc(&twl, h.size() * 16);
+  cudaMemcpy(tw, h.data(), h.size() * 16, cudaMemcpyHostToDevice);
+  cudaMemcpy(twl, h.data(), h.size() * 16, cudaMemcpyHostToDevice);
+  run<Arith52S, true, 7>("S all passes", tw, twl, c, 224);
+  run<Arith52S, true, 1>("S P1 (13..9)", tw, twl, c, 80);
+  run<Arith52S, true, 2>("S P2 (8..5)", tw, twl, c, 64);
+  run<Arith52S, true, 4>("S P3 (4..0, low table)", tw, twl, c, 80);
+  run<Arith52S, false, 7>("S all passes", tw, twl, c, 224);
+  run<Arith52S, false, 1>("S P1 (0..4, low table)", tw, twl, c, 80);
+  run<Arith52S, false, 2>("S P2", tw, twl, c, 64);
+  run<Arith52S, false, 4>("S P3 (9..13)", tw, twl, c, 80);
+  return 0;
+}
