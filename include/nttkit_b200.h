@@ -165,7 +165,8 @@ void nk_debug_dump_to(uint64_t* d_buf);
  * default. */
 void nk_debug_exact_only(int on);
 /* Testing aid: which kernel transforms 16384-word blocks. -1 (default) = the
- * faster one per direction, 0 = the CTA-pair kernel, 1 = the single-CTA kernel. */
+ * faster one per direction, 0 = the CTA-pair kernel, 1 = the single-CTA kernel,
+ * 2 = the warp-per-item kernel (whole N = 16384 rows only). */
 void nk_debug_block_kernel(int which);
 
 #ifdef __cplusplus

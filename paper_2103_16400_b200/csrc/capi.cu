@@ -19,6 +19,7 @@
 #include "host_math.hpp"
 #include "ntt_kernels.cuh"
 #include "ntt_pair.cuh"
+#include "ntt_warp.cuh"
 
 using nk::host::u128;
 
@@ -215,14 +216,46 @@ int launch_pair_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cud
   return 0;
 }
 
-int g_block_kernel = -1;  // nk_debug_block_kernel(): -1 auto, 0 pair, 1 single
+int g_block_kernel = -1;  // nk_debug_block_kernel(): -1 auto, 0 pair, 1 single, 2 warp
+
+// Warp-per-item kernel (ntt_warp.cuh) for whole 16384-word rows: persistent,
+// every warp resident; per-row phase counters live in a stream-ordered
+// allocation of this call (tables stay shareable across concurrent calls).
+template <class A, bool FWD, bool IL>
+int launch_warp_t(const nk::NttArgs& a, cudaStream_t st) {
+  auto kern = nk::ntt_warp14<A, FWD, IL>;
+  if (int rc = set_smem(kern, nk::kWarpSmemBytes)) return rc;
+  static int per_sm[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!per_sm[dev & 63]) {
+    int n = 0;
+    NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 256, nk::kWarpSmemBytes));
+    per_sm[dev & 63] = n > 0 ? n : 1;
+  }
+  const uint64_t items = a.rows * 32;
+  uint64_t grid = static_cast<uint64_t>(per_sm[dev & 63]) * sm_count();
+  const uint64_t need = (items + nk::kWarpsPerCta - 1) / nk::kWarpsPerCta;
+  if (grid > need) grid = need;
+  uint32_t* cnt = nullptr;
+  const size_t cbytes = (a.rows + 1) * sizeof(uint32_t);
+  NK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cnt), cbytes, st));
+  NK_CUDA(cudaMemsetAsync(cnt, 0, cbytes, st));
+  nk::WarpNttArgs wa{a, cnt, cnt + a.rows, static_cast<uint32_t>(grid * nk::kWarpsPerCta / 16 + 1)};
+  kern<<<static_cast<unsigned>(grid), 256, nk::kWarpSmemBytes, st>>>(wa);
+  g_launches++;
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(cnt, st);
+  if (e != cudaSuccess) return cuda_fail(e, "ntt_warp14 launch");
+  return 0;
+}
 
 template <class A, bool FWD>
 int launch_tma(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm, cudaStream_t st) {
   // measured on B200 (cfg3): the CTA-pair kernel is the faster forward, the
   // single-CTA kernel the faster inverse (the pair inverse exchanges late,
   // so its next TMA overlaps less compute)
-  const bool pair = g_block_kernel < 0 ? FWD : g_block_kernel == 0;
+  const bool pair = (g_block_kernel < 0 || g_block_kernel == 2) ? FWD : g_block_kernel == 0;
   if (pair)
     return iltm ? launch_pair_t<A, FWD, true>(a, nitems, buf_words, st)
                 : launch_pair_t<A, FWD, false>(a, nitems, buf_words, st);
@@ -289,7 +322,13 @@ int run_ntt(nk::NttArgs a, uint64_t buf_words, cudaStream_t st) {
   const uint32_t logn = a.logn;
   if (logn <= 10) return launch_small<A, FWD>(a, st);
   if (logn < kLogBlock) return launch_block<A, FWD>(logn, a, a.rows, a.fin == 1, st);
-  if (logn == kLogBlock) return launch_tma<A, FWD>(a, a.rows, buf_words, a.fin == 1, st);
+  if (logn == kLogBlock) {
+    // the warp-per-item kernel is correct but not (yet) the faster one on
+    // B200 (profiles/ncu_r01_session2_warp.txt): selected only explicitly
+    if (g_block_kernel == 2)
+      return a.fin == 1 ? launch_warp_t<A, FWD, true>(a, st) : launch_warp_t<A, FWD, false>(a, st);
+    return launch_tma<A, FWD>(a, a.rows, buf_words, a.fin == 1, st);
+  }
   // long rows: high bits in global passes of <= 3 stages, low 14 bits per block
   const uint32_t gbits = logn - kLogBlock;
   uint32_t ks[2] = {gbits, 0};

@@ -260,7 +260,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
       for (int r = 0; r < 32; ++r)
         if ((r >> 4) != static_cast<int>(c)) st_async_u64(s_peer + (t + 256u * c + 512u * (r & 15)) * 8u, v[r], x_peer);
 #endif
-      mbar_wait(bar_x, phase);  // acquire.cta: st.async data is ordered by complete_tx (no L1 invalidate)
+      NK_XWAIT(bar_x, phase);  // acquire.cta: st.async data is ordered by complete_tx (no L1 invalidate)
 #pragma unroll
       for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -343,7 +343,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
             st_async_u64(s_peer + ((j & 255u) | ((j >> 9) << 8)) * 8u, v[16 * g + r], x_peer);
         }
 #endif
-      mbar_wait(bar_x, phase);  // acquire.cta: st.async data is ordered by complete_tx (no L1 invalidate)
+      NK_XWAIT(bar_x, phase);  // acquire.cta: st.async data is ordered by complete_tx (no L1 invalidate)
 #pragma unroll
       for (int r = 0; r < 32; ++r) v[r] = S[t + 256 * r];
       __syncwarp();
