@@ -76,6 +76,17 @@ int ensure_device(int dev) {
   int cur = -1;
   NK_CUDA(cudaGetDevice(&cur));
   if (cur != dev) NK_CUDA(cudaSetDevice(dev));
+  // stream-ordered scratch (poly_mult_mod's g^, per-call counters) comes from
+  // the device's default pool; keep freed blocks in the pool instead of
+  // returning them to the driver at every synchronisation
+  static std::once_flag pool_once[64];
+  std::call_once(pool_once[dev & 63], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  });
   return 0;
 }
 
@@ -364,8 +375,10 @@ int check_limbs(const nk_plan* p, uint32_t limb0, uint32_t nlimbs) {
 }
 
 int ntt_dispatch(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, uint32_t limb0,
-                 uint32_t nlimbs, uint32_t npolys, uint64_t fin, uint64_t fout, cudaStream_t st) {
+                 uint32_t nlimbs, uint32_t npolys, uint64_t fin, uint64_t fout, cudaStream_t st,
+                 const uint64_t* mulb = nullptr) {
   nk::NttArgs a{};
+  a.mulb = mulb;
   a.out = res;
   a.in = op;
   a.tw = fwd ? p->tw_fwd : p->tw_inv;
@@ -677,6 +690,22 @@ int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const u
   cudaStream_t st = S(stream);
   uint64_t* gh = nullptr;
   NK_CUDA(cudaMallocAsync(&gh, bytes, st));
+  // Fused sequence when every limb takes the signed FP64 arithmetic and the
+  // forward is the CTA-pair kernel: canonical g^, then f^ with the dyadic
+  // product applied in the forward's store, then the inverse. The result is
+  // canonical and unique, so it equals the reference's fwd(1,4) x2 /
+  // mult(4) / inv(1,1) sequence (ring.hpp:28-43) word for word.
+  bool fused = p->logn == kLogBlock && !g_exact_only && (g_block_kernel < 0 || g_block_kernel == 0);
+  for (uint32_t l = 0; l < nlimbs; ++l) fused &= p->bs[limb0 + l] == 52;
+  if (fused) {
+    int rc = ntt_dispatch(p, true, gh, g, limb0, nlimbs, npolys, 1, 1, st);
+    if (!rc) rc = ntt_dispatch(p, true, res, f, limb0, nlimbs, npolys, 1, 1, st, gh);
+    if (!rc) rc = ntt_dispatch(p, false, res, res, limb0, nlimbs, npolys, 1, 1, st);
+    cudaError_t e = cudaFreeAsync(gh, st);
+    if (rc) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
+    return 0;
+  }
   // ring.hpp:39-42: g^ = fwd(g,1,4) first so that result may alias g
   int rc = ntt_dispatch(p, true, gh, g, limb0, nlimbs, npolys, 1, 4, st);
   if (!rc) rc = ntt_dispatch(p, true, res, f, limb0, nlimbs, npolys, 1, 4, st);

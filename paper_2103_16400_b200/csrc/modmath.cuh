@@ -367,6 +367,22 @@ struct Arith52S {
   }
 };
 
+// a * b mod q, canonical, for canonical integers a, b < q < 2^50 on the FP64
+// pipe: h + l = a b exactly (TwoProduct), k = round(h / q) through the
+// rounded reciprocal (|h/q - k| <= 0.75), r = h - k q + l exact in
+// (-0.76q, 0.76q), one conditional add of q. The product is unique, so this
+// equals the reference's eltwise_mult_mod (eltwise.hpp:180-188) result.
+__device__ __forceinline__ uint64_t mulmod_canon(uint64_t a, uint64_t b, const LimbConstDev& c) {
+  const double x = __dsub_rn(as_d(a | kDBias), kC52), y = __dsub_rn(as_d(b | kDBias), kC52);
+  const double h = __dmul_rn(x, y);
+  const double l = __fma_rn(x, y, -h);
+  const double k = __dsub_rn(__fma_rn(h, c.qinv, kC52x15), kC52x15);
+  const double r = __dadd_rn(__fma_rn(-k, c.q_d, h), l);
+  const uint64_t rb = as_u(__dadd_rn(r, c.q_bias));  // 2^52 + r + q
+  const uint64_t db = as_u(__dsub_rn(as_d(rb), c.q_d));
+  return ((hi32(db) >= 0x43300000u) ? db : rb) & kMask52;
+}
+
 // Final word of a forward transform (small_mod(x, q, 4) when fout == 1,
 // ntt.hpp:282-284) and of an inverse (n^-1 Shoup pass, ntt.hpp:429-432, then
 // small_mod(x, q, 2) when fout == 1, ntt.hpp:303-305), as stored integers.

@@ -52,6 +52,8 @@ struct NttArgs {
   uint32_t logn;
   int32_t fin, fout;
   uint64_t* dbg;  // debug: when set, the TMA kernel dumps each pass's words ([3][N]) for item 0
+  const uint64_t* mulb;  // forward (CTA-pair kernel, fout == 1): multiply the canonical
+                         // result by these canonical words (same layout) before storing
 };
 
 __device__ __forceinline__ ulonglong2 ldtw(const ulonglong2* p) { return __ldg(p); }

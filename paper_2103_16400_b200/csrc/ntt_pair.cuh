@@ -371,6 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
       // image (32 rows of 16 words, 128B swizzle), one round per bit 4
       uint8_t* Wb = reinterpret_cast<uint8_t*>(W);
       uint64_t* wdst = dst + (w << 10) + (c << 13);
+      const uint64_t* mulb = a.mulb ? a.mulb + row * a.n + boff + (w << 10) + (c << 13) : nullptr;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -381,8 +382,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
 #pragma unroll
         for (int s2 = 0; s2 < 8; ++s2) {  // 32 rows, 4 per warp instruction
           const uint32_t rw = (l >> 3) + 4 * s2, cc = l & 7;
-          const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Wb + (rw << 7) + ((cc ^ (rw & 7)) << 4));
-          *reinterpret_cast<ulonglong2*>(wdst + (rw << 5) + (h << 4) + (cc << 1)) = p;
+          ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Wb + (rw << 7) + ((cc ^ (rw & 7)) << 4));
+          const uint32_t off = (rw << 5) + (h << 4) + (cc << 1);
+          if constexpr (A::kSigned) {
+            if (mulb) {  // fused dyadic product of poly_mult_mod (ring.hpp:39-41)
+              const ulonglong2 gb = __ldg(reinterpret_cast<const ulonglong2*>(mulb + off));
+              p.x = mulmod_canon(p.x, gb.x, cst);
+              p.y = mulmod_canon(p.y, gb.y, cst);
+            }
+          }
+          *reinterpret_cast<ulonglong2*>(wdst + off) = p;
         }
         __syncwarp();
       }

@@ -221,3 +221,36 @@ def test_cfg5_sample(nk, oracle):
     for r in sample:
         want = oracle.poly_mult_mod(n, [moduli[r % L]], f[r], g[r])
         assert np.array_equal(got[r], want), r
+
+
+@pytest.mark.parametrize("exact", [False, True], ids=["fused", "unfused"])
+def test_poly_16384_paths_and_aliasing(nk, oracle, exact):
+    """N = 16384 with 50-bit limbs runs the fused sequence (forward g, forward f
+    with the dyadic product in its store, inverse); exact_only forces the
+    reference's fwd(1,4)/mult(4)/inv(1,1) sequence. Both must equal the
+    oracle, also when the result aliases f or g and for all-(q-1) inputs."""
+    from primes import largest_ntt_primes
+
+    n = 16384
+    moduli = largest_ntt_primes(50, n, 3)
+    plan = nk.RnsNtt(n, moduli)
+    nk.set_exact_only(exact)
+    try:
+        npolys = 2
+        rows = npolys * len(moduli)
+        f = np.stack([oracle.mt19937_64(70 + r, n, moduli[r % 3]) for r in range(rows)]).reshape(-1)
+        g = np.stack([oracle.mt19937_64(170 + r, n, moduli[r % 3]) for r in range(rows)]).reshape(-1)
+        g[:n] = moduli[0] - 1  # extreme row
+        want = np.concatenate([oracle.poly_mult_mod(n, [moduli[r % 3]], f[r * n:(r + 1) * n],
+                                                    g[r * n:(r + 1) * n]) for r in range(rows)])
+        df, dg = dev(f), dev(g)
+        out = torch.empty_like(df)
+        plan.poly_mult_mod(out, df, dg)
+        assert np.array_equal(host(out), want)
+        plan.poly_mult_mod(df, df, dg)  # result aliases f
+        assert np.array_equal(host(df), want)
+        df = dev(f)
+        plan.poly_mult_mod(dg, df, dg)  # result aliases g
+        assert np.array_equal(host(dg), want)
+    finally:
+        nk.set_exact_only(False)
