@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <initializer_list>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -374,9 +375,41 @@ int check_limbs(const nk_plan* p, uint32_t limb0, uint32_t nlimbs) {
   return 0;
 }
 
+int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, uint32_t limb0,
+                         uint32_t nlimbs, uint32_t npolys, uint64_t fin, uint64_t fout, cudaStream_t st,
+                         const uint64_t* mulb);
+
+// The transform kernels use 16/32-byte vector accesses and TMA on row
+// starts: buffers that are not 32-byte aligned (e.g. a view starting at an odd
+// word) run through an aligned stream-ordered copy instead of faulting.
 int ntt_dispatch(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, uint32_t limb0,
                  uint32_t nlimbs, uint32_t npolys, uint64_t fin, uint64_t fout, cudaStream_t st,
                  const uint64_t* mulb = nullptr) {
+  const uintptr_t mis = (reinterpret_cast<uintptr_t>(res) | reinterpret_cast<uintptr_t>(op) |
+                         reinterpret_cast<uintptr_t>(mulb)) & 31;
+  if (!mis || npolys == 0)
+    return ntt_dispatch_aligned(p, fwd, res, op, limb0, nlimbs, npolys, fin, fout, st, mulb);
+  const size_t bytes = static_cast<size_t>(npolys) * nlimbs * p->n * 8;
+  uint64_t *t = nullptr, *tm = nullptr;
+  NK_CUDA(cudaMallocAsync(&t, bytes, st));
+  NK_CUDA(cudaMemcpyAsync(t, op, bytes, cudaMemcpyDeviceToDevice, st));
+  if (mulb) {
+    NK_CUDA(cudaMallocAsync(&tm, bytes, st));
+    NK_CUDA(cudaMemcpyAsync(tm, mulb, bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  int rc = ntt_dispatch_aligned(p, fwd, t, t, limb0, nlimbs, npolys, fin, fout, st, mulb ? tm : nullptr);
+  if (!rc) {
+    cudaError_t e = cudaMemcpyAsync(res, t, bytes, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync(unaligned result)");
+  }
+  cudaFreeAsync(t, st);
+  if (tm) cudaFreeAsync(tm, st);
+  return rc;
+}
+
+int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, uint32_t limb0,
+                         uint32_t nlimbs, uint32_t npolys, uint64_t fin, uint64_t fout, cudaStream_t st,
+                         const uint64_t* mulb) {
   nk::NttArgs a{};
   a.mulb = mulb;
   a.out = res;
@@ -427,25 +460,56 @@ int ntt_dispatch(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, 
 }
 
 unsigned eltwise_grid(uint64_t work) {
-  // work = 16-byte chunks; each thread takes nk::kU chunks per sweep. Enough
+  // work = vector chunks; each thread takes nk::kU chunks per sweep. Enough
   // CTAs for ~2 waves of 8 resident 256-thread CTAs per SM; grid-stride beyond.
   uint64_t g = (work + 256 * nk::kU - 1) / (256 * nk::kU);
   const uint64_t cap = static_cast<uint64_t>(sm_count()) * 16;
   return static_cast<unsigned>(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
+// widest vector access all pointers allow (32 / 16 / 8 bytes)
+int vec_of(std::initializer_list<const void*> ptrs) {
+  uintptr_t x = 0;
+  for (const void* p : ptrs) x |= reinterpret_cast<uintptr_t>(p);
+  return (x & 31) == 0 ? 4 : ((x & 15) == 0 ? 2 : 1);
+}
+
+// launch with programmatic stream serialisation (the kernels call
+// griddepcontrol.wait before touching memory, nk::pdl_enter)
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 template <int FIN, bool SMALLQ, bool BATCHED>
-void launch_mult_t(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t total, uint32_t logn,
-                   nk::MultConst c0, const nk::MultConst* consts, uint32_t nlimbs, cudaStream_t st) {
-  nk::eltwise_mult_kernel<FIN, SMALLQ, BATCHED>
-      <<<eltwise_grid(total / 2 + 1), 256, 0, st>>>(r, a, b, total, logn, c0, consts, nlimbs);
+cudaError_t launch_mult_t(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t total, uint32_t logn,
+                          nk::MultConst c0, const nk::MultConst* consts, uint32_t nlimbs, cudaStream_t st) {
+  const int vec = vec_of({r, a, b});
+#define NK_MV(V)                                                                                          \
+  return launch_pdl(nk::eltwise_mult_kernel<FIN, SMALLQ, BATCHED, V>, eltwise_grid(total / V + 1), 256, st, \
+                    r, a, b, total, logn, c0, consts, nlimbs)
+  if (vec == 4) NK_MV(4);
+  if (vec == 2) NK_MV(2);
+  NK_MV(1);
+#undef NK_MV
 }
 
 int launch_mult(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t total, uint32_t logn,
                 nk::MultConst c0, const nk::MultConst* consts, uint32_t nlimbs, int fin, bool small,
                 cudaStream_t st) {
   const bool batched = consts != nullptr;
-#define NK_M(F, S, B) launch_mult_t<F, S, B>(r, a, b, total, logn, c0, consts, nlimbs, st)
+  cudaError_t e;
+#define NK_M(F, S, B) e = launch_mult_t<F, S, B>(r, a, b, total, logn, c0, consts, nlimbs, st)
 #define NK_M2(F)                                                      \
   if (small) { if (batched) NK_M(F, true, true); else NK_M(F, true, false); } \
   else { if (batched) NK_M(F, false, true); else NK_M(F, false, false); }
@@ -457,6 +521,7 @@ int launch_mult(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t tota
 #undef NK_M2
 #undef NK_M
   g_launches++;
+  if (e != cudaSuccess) return cuda_fail(e, "eltwise_mult_kernel launch");
   NK_CUDA(cudaGetLastError());
   return 0;
 }
@@ -768,8 +833,14 @@ int nk_eltwise_fma_mod(uint64_t* res, const uint64_t* a, uint64_t y, const uint6
   const nk::FmaConst c{q, y, static_cast<uint64_t>((static_cast<u128>(y) << bs) / q),
                        static_cast<int>(fin), bs};
   cudaStream_t st = S(stream);
-  const unsigned grid = eltwise_grid(n / 2 + 1);
-#define NK_FMA(BS, Z, F) nk::eltwise_fma_kernel<BS, Z, F><<<grid, 256, 0, st>>>(res, a, z, n, c)
+  const int vec = z ? vec_of({res, a, z}) : vec_of({res, a});
+  cudaError_t e = cudaSuccess;
+#define NK_FMAV(BS, Z, F, V) \
+  e = launch_pdl(nk::eltwise_fma_kernel<BS, Z, F, V>, eltwise_grid(n / V + 1), 256, st, res, a, z, n, c)
+#define NK_FMA(BS, Z, F)                            \
+  if (vec == 4) NK_FMAV(BS, Z, F, 4);               \
+  else if (vec == 2) NK_FMAV(BS, Z, F, 2);          \
+  else NK_FMAV(BS, Z, F, 1)
 #define NK_FMA_F(BS, Z)                          \
   switch (fin) {                                 \
     case 1: NK_FMA(BS, Z, 1); break;             \
@@ -784,6 +855,8 @@ int nk_eltwise_fma_mod(uint64_t* res, const uint64_t* a, uint64_t y, const uint6
   }
 #undef NK_FMA_F
 #undef NK_FMA
+#undef NK_FMAV
+  if (e != cudaSuccess) return cuda_fail(e, "eltwise_fma_kernel launch");
   g_launches++;
   NK_CUDA(cudaGetLastError());
   return 0;
@@ -795,8 +868,9 @@ int nk_eltwise_add_mod(uint64_t* res, const uint64_t* a, const uint64_t* b, uint
   if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (n == 0) return 0;
   if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_add_mod: NULL buffer");
-  nk::eltwise_add_kernel<<<eltwise_grid(n), 256, 0, S(stream)>>>(res, a, b, n, q);
+  cudaError_t e = launch_pdl(nk::eltwise_add_kernel, eltwise_grid(n), 256, S(stream), res, a, b, n, q);
   g_launches++;
+  if (e != cudaSuccess) return cuda_fail(e, "eltwise_add_kernel launch");
   NK_CUDA(cudaGetLastError());
   return 0;
 }
@@ -806,8 +880,9 @@ int nk_eltwise_neg_mod(uint64_t* res, const uint64_t* a, uint64_t n, uint64_t q,
   if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (n == 0) return 0;
   if (!res || !a) return fail(NK_ERR_NULL, "eltwise_neg_mod: NULL buffer");
-  nk::eltwise_neg_kernel<<<eltwise_grid(n), 256, 0, S(stream)>>>(res, a, n, q);
+  cudaError_t e = launch_pdl(nk::eltwise_neg_kernel, eltwise_grid(n), 256, S(stream), res, a, n, q);
   g_launches++;
+  if (e != cudaSuccess) return cuda_fail(e, "eltwise_neg_kernel launch");
   NK_CUDA(cudaGetLastError());
   return 0;
 }

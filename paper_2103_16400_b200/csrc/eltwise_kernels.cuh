@@ -1,5 +1,5 @@
-// Element-wise modular kernels for sm_100a: HBM-bound streaming, 16-byte
-// vector loads/stores (two words per access), grid-stride over the vector.
+// Element-wise modular kernels for sm_100a: HBM-bound streaming, 32-byte
+// vector loads/stores (four words per access) when aligned, grid-stride.
 //
 // Outputs are canonical ([0, q)), so any exact algorithm gives the
 // reference's words. We follow the reference's integer formulas:
@@ -48,12 +48,57 @@ __device__ __forceinline__ uint64_t mult_barrett(uint64_t a, uint64_t b, const M
   return c4;
 }
 
+// Vector access of VEC consecutive words (VEC = 4: one 256-bit LDG/STG,
+// sm_100; 2: 128-bit; 1: scalar), streaming cache hints (each word is touched
+// once). The launcher picks VEC from the pointers' alignment.
+template <int VEC>
+struct WordVec {
+  uint64_t w[VEC];
+};
+template <int VEC>
+__device__ __forceinline__ WordVec<VEC> ld_stream(const uint64_t* p) {
+  WordVec<VEC> v;
+  if constexpr (VEC == 4) {
+    asm volatile("ld.global.cs.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(v.w[0]), "=l"(v.w[1]), "=l"(v.w[2]), "=l"(v.w[3])
+                 : "l"(p));
+  } else if constexpr (VEC == 2) {
+    const ulonglong2 t = __ldcs(reinterpret_cast<const ulonglong2*>(p));
+    v.w[0] = t.x;
+    v.w[1] = t.y;
+  } else {
+    v.w[0] = __ldcs(p);
+  }
+  return v;
+}
+template <int VEC>
+__device__ __forceinline__ void st_stream(uint64_t* p, const WordVec<VEC>& v) {
+  if constexpr (VEC == 4) {
+    asm volatile("st.global.cs.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(v.w[0]), "l"(v.w[1]), "l"(v.w[2]),
+                 "l"(v.w[3])
+                 : "memory");
+  } else if constexpr (VEC == 2) {
+    __stcs(reinterpret_cast<ulonglong2*>(p), make_ulonglong2(v.w[0], v.w[1]));
+  } else {
+    __stcs(p, v.w[0]);
+  }
+}
+
+// Programmatic dependent launch: the kernels are launched with programmatic
+// stream serialisation, so the next kernel's launch overlaps this one's tail;
+// each kernel still waits for its predecessor's memory before touching data.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
 // Rows of `n` = 2^logn words (BATCHED: row r uses consts[r % nlimbs]) or one
-// vector under c0. Each thread streams kU 16-byte chunks per iteration with all
-// loads issued before any arithmetic (memory-level parallelism for an
-// HBM-bound loop); grid-stride over a few waves of resident CTAs.
-constexpr int kU = 4;
-template <int FIN, bool SMALLQ, bool BATCHED>
+// vector under c0. Each thread streams kU chunks of VEC words per iteration
+// with all loads issued before any arithmetic (memory-level parallelism for an
+// HBM-bound loop); grid-stride over a few waves of resident CTAs; the last
+// total % VEC words are done by thread 0.
+constexpr int kU = 2;
+template <int FIN, bool SMALLQ, bool BATCHED, int VEC>
 __global__ void __launch_bounds__(256) eltwise_mult_kernel(uint64_t* __restrict__ r,
                                                            const uint64_t* __restrict__ a,
                                                            const uint64_t* __restrict__ b,
@@ -61,39 +106,38 @@ __global__ void __launch_bounds__(256) eltwise_mult_kernel(uint64_t* __restrict_
                                                            MultConst c0,
                                                            const MultConst* __restrict__ consts,
                                                            uint32_t nlimbs) {
-  const uint64_t total2 = total >> 1;
+  pdl_enter();
+  const uint64_t chunks = total / VEC;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  const ulonglong2* __restrict__ a2 = reinterpret_cast<const ulonglong2*>(a);
-  const ulonglong2* __restrict__ b2 = reinterpret_cast<const ulonglong2*>(b);
-  ulonglong2* __restrict__ r2 = reinterpret_cast<ulonglong2*>(r);
-  for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < total2;
+  auto cst = [&](uint64_t word) { return BATCHED ? consts[(word >> logn) % nlimbs] : c0; };
+  for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < chunks;
        i0 += kU * stride) {
-    ulonglong2 x[kU], y[kU];
+    WordVec<VEC> x[kU], y[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint64_t i = i0 + u * stride;
-      if (i < total2) {
-        x[u] = __ldcs(a2 + i);  // streamed once: evict-first
-        y[u] = __ldcs(b2 + i);
+      if (i < chunks) {
+        x[u] = ld_stream<VEC>(a + i * VEC);
+        y[u] = ld_stream<VEC>(b + i * VEC);
       }
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint64_t i = i0 + u * stride;
-      if (i < total2) {
-        MultConst c = c0;
-        if (BATCHED) c = consts[((2 * i) >> logn) % nlimbs];  // n even: both words in one row
-        ulonglong2 o;
-        o.x = mult_barrett<FIN, SMALLQ>(x[u].x, y[u].x, c);
-        o.y = mult_barrett<FIN, SMALLQ>(x[u].y, y[u].y, c);
-        __stcs(r2 + i, o);
+      if (i < chunks) {
+        WordVec<VEC> o;
+        // rows are >= VEC words whenever logn >= log2(VEC): one constant per chunk
+        const bool one_row = !BATCHED || (VEC == 1) || ((1u << logn) >= static_cast<uint32_t>(VEC));
+        const MultConst c = cst(i * VEC);
+#pragma unroll
+        for (int k = 0; k < VEC; ++k)
+          o.w[k] = mult_barrett<FIN, SMALLQ>(x[u].w[k], y[u].w[k], one_row ? c : cst(i * VEC + k));
+        st_stream<VEC>(r + i * VEC, o);
       }
     }
   }
-  if (!BATCHED && (total & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint64_t k = total - 1;
-    r[k] = mult_barrett<FIN, SMALLQ>(a[k], b[k], c0);
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (uint64_t k = chunks * VEC; k < total; ++k) r[k] = mult_barrett<FIN, SMALLQ>(a[k], b[k], cst(k));
 }
 
 struct FmaConst {
@@ -116,49 +160,47 @@ __device__ __forceinline__ uint64_t fma_one(uint64_t a, uint64_t z, const FmaCon
   return v;
 }
 
-template <int BS, bool HAS_Z, int FIN>
+template <int BS, bool HAS_Z, int FIN, int VEC>
 __global__ void __launch_bounds__(256) eltwise_fma_kernel(uint64_t* __restrict__ r,
                                                           const uint64_t* __restrict__ a,
                                                           const uint64_t* __restrict__ z,
                                                           uint64_t n, FmaConst c) {
-  const uint64_t n2 = n >> 1;
+  pdl_enter();
+  const uint64_t chunks = n / VEC;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  const ulonglong2* __restrict__ a2 = reinterpret_cast<const ulonglong2*>(a);
-  const ulonglong2* __restrict__ z2 = reinterpret_cast<const ulonglong2*>(z);
-  ulonglong2* __restrict__ r2 = reinterpret_cast<ulonglong2*>(r);
-  for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < n2;
+  for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < chunks;
        i0 += kU * stride) {
-    ulonglong2 x[kU], zz[kU];
+    WordVec<VEC> x[kU], zz[kU];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint64_t i = i0 + u * stride;
-      zz[u] = make_ulonglong2(0, 0);
-      if (i < n2) {
-        x[u] = __ldcs(a2 + i);
-        if (HAS_Z) zz[u] = __ldcs(z2 + i);
+#pragma unroll
+      for (int k = 0; k < VEC; ++k) zz[u].w[k] = 0;
+      if (i < chunks) {
+        x[u] = ld_stream<VEC>(a + i * VEC);
+        if (HAS_Z) zz[u] = ld_stream<VEC>(z + i * VEC);
       }
     }
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
       const uint64_t i = i0 + u * stride;
-      if (i < n2) {
-        ulonglong2 o;
-        o.x = fma_one<BS, HAS_Z, FIN>(x[u].x, zz[u].x, c);
-        o.y = fma_one<BS, HAS_Z, FIN>(x[u].y, zz[u].y, c);
-        __stcs(r2 + i, o);
+      if (i < chunks) {
+        WordVec<VEC> o;
+#pragma unroll
+        for (int k = 0; k < VEC; ++k) o.w[k] = fma_one<BS, HAS_Z, FIN>(x[u].w[k], zz[u].w[k], c);
+        st_stream<VEC>(r + i * VEC, o);
       }
     }
   }
-  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-    const uint64_t k = n - 1;
-    r[k] = fma_one<BS, HAS_Z, FIN>(a[k], HAS_Z ? z[k] : 0, c);
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (uint64_t k = chunks * VEC; k < n; ++k) r[k] = fma_one<BS, HAS_Z, FIN>(a[k], HAS_Z ? z[k] : 0, c);
 }
 
 __global__ void __launch_bounds__(256) eltwise_add_kernel(uint64_t* __restrict__ r,
                                                           const uint64_t* __restrict__ a,
                                                           const uint64_t* __restrict__ b,
                                                           uint64_t n, uint64_t q) {
+  pdl_enter();
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += stride)
@@ -168,6 +210,7 @@ __global__ void __launch_bounds__(256) eltwise_add_kernel(uint64_t* __restrict__
 __global__ void __launch_bounds__(256) eltwise_neg_kernel(uint64_t* __restrict__ r,
                                                           const uint64_t* __restrict__ a,
                                                           uint64_t n, uint64_t q) {
+  pdl_enter();
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += stride) {

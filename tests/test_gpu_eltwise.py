@@ -254,3 +254,36 @@ def test_poly_16384_paths_and_aliasing(nk, oracle, exact):
         assert np.array_equal(host(dg), want)
     finally:
         nk.set_exact_only(False)
+
+
+@pytest.mark.parametrize("offset", [0, 1, 2, 3])
+def test_unaligned_views(nk, oracle, offset):
+    """Device views that start at any word (8/16/32-byte alignment): the
+    element-wise kernels pick their vector width, the transforms stage through
+    an aligned copy; results equal the aligned ones."""
+    from primes import cfg2_modulus, largest_ntt_primes
+
+    q = cfg2_modulus()
+    n = 4099
+    a = oracle.mt19937_64(91, n, q)
+    b = oracle.mt19937_64(92, n, q)
+    base_a = torch.zeros(n + 8, dtype=torch.int64, device="cuda")
+    base_b = torch.zeros(n + 8, dtype=torch.int64, device="cuda")
+    base_r = torch.zeros(n + 8, dtype=torch.int64, device="cuda")
+    da, db, dr = base_a[offset:offset + n], base_b[offset:offset + n], base_r[offset:offset + n]
+    da.copy_(dev(a))
+    db.copy_(dev(b))
+    nk.eltwise_mult_mod(dr, da, db, q, 1)
+    assert np.array_equal(host(dr), oracle.eltwise_mult_mod(a, b, q, 1))
+    nk.eltwise_fma_mod(dr, da, 12345, db, q, 1)
+    assert np.array_equal(host(dr), oracle.eltwise_fma_mod(a, 12345, b, q, 1))
+    nn = 16384
+    qq = largest_ntt_primes(50, nn, 1)[0]
+    plan = nk.RnsNtt(nn, [qq])
+    x = oracle.mt19937_64(93, nn, qq)
+    bx = torch.zeros(nn + 8, dtype=torch.int64, device="cuda")
+    bo = torch.zeros(nn + 8, dtype=torch.int64, device="cuda")
+    dx, do = bx[offset:offset + nn], bo[offset:offset + nn]
+    dx.copy_(dev(x))
+    plan.forward(do, dx, 1, 1)
+    assert np.array_equal(host(do), oracle.forward(nn, [qq], x, 1, 1))
