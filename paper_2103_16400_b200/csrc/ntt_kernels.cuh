@@ -365,26 +365,25 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __re
   // block's segment plus this thread's jhi): loads of one (stage, d) are
   // lane-contiguous and their offsets are immediates
   constexpr bool kLow = (PD::LO == 0 && PD::K == 5);
-#if defined(NK_DBG_NO_COMPUTE)  // perf experiment only: data movement without butterflies
-  return;
-#endif
+  // a passenger bit below the pass's bits does not reach the twiddle index
+  // ((N + j) >> (b+1) with b > X): both groups share each twiddle
+  constexpr bool kShared = (G == 2) && (PD::X >= 0) && (PD::X < PD::LO);
+  constexpr int GL = kShared ? 1 : G;  // groups with their own twiddles
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     const int i = FWD ? (K - 1 - s) : s;
     const int b = PD::LO + i;
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const uint64_t base = (xt + PD::jc(g, 0)) >> (b + 1);
+    for (int gl = 0; gl < GL; ++gl) {
+      const uint64_t base = (xt + PD::jc(gl, 0)) >> (b + 1);
 #pragma unroll
       for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
-#if defined(NK_DBG_TW_SMALL)  // perf experiment only: L1-resident twiddles (wrong results)
-        const ulonglong2 w = ldtw(tw + ((base + hi) & 63));
-#else
         const ulonglong2 w = kLow ? ldtw(twl + low_index(b, hi, 0)) : ldtw(tw + base + hi);
-#endif
 #pragma unroll
-        for (int l = 0; l < (1 << i); ++l) {
-          const int r0 = (hi << (i + 1)) | l;
+        for (int l = 0; l < ((1 << i) * (G / GL)); ++l) {
+          const int g = kShared ? (l >> i) : gl;
+          const int ll = l & ((1 << i) - 1);
+          const int r0 = (hi << (i + 1)) | ll;
           const int r1 = r0 | (1 << i);
           uint64_t& x0 = v[g * R + r0];
           uint64_t& x1 = v[g * R + r1];

@@ -87,9 +87,6 @@ __device__ __forceinline__ void mbar_arrive_relaxed_remote(uint32_t rbar) {
   asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
-#if defined(NK_DBG_NO_XWAIT)
-  return;
-#endif
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
@@ -121,10 +118,14 @@ __host__ __device__ constexpr uint32_t wimg(uint32_t j) {
   return idx + 2u * (idx >> 4);
 }
 
-#if defined(NK_DBG_NO_XWAIT)  // perf experiment only: exchanges without waits (wrong results)
-#define NK_XWAIT(b, p) ((void)0)
+#if defined(NK_DBG_TIMELINE)  // perf experiment: per-warp phase timestamps into a.dbg
+#define NK_TS(id)                                                                            \
+  do {                                                                                       \
+    if (a.dbg && l == 0 && it_ < 32)                                                         \
+      a.dbg[((static_cast<uint64_t>(blockIdx.x) * 8 + w) * 32 + it_) * 16 + (id)] = clock64(); \
+  } while (0)
 #else
-#define NK_XWAIT(b, p) mbar_wait(b, p)
+#define NK_TS(id) ((void)0)
 #endif
 
 template <class A, bool FWD, bool ILTM0>
@@ -193,9 +194,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
   const uint32_t jt1 = FWD ? jt_hi : jt_low;
   const uint32_t jt3 = FWD ? jt_low : jt_hi;
 
+  uint32_t it_ = 0;
+  (void)it_;
   for (uint32_t k = k0; k < nitems; k += kstep) {
     uint64_t row, blk;
     item_row(k, row, blk);
+    NK_TS(0);
     const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
     const LimbConst cst = a.lc[limb];
     const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * a.n;
@@ -208,6 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
 
     // ---- P1 words from the staging buffer ----
     mbar_wait(bar, phase);
+    NK_TS(1);
     if (FWD) {
 #pragma unroll
       for (int r = 0; r < 32; ++r) v[r] = A::load(S[t + 256 * r]);  // local = j & 255 | (j >> 9) << 8
@@ -226,41 +231,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
       }
     }
 
-#if defined(NK_DBG_COMPUTE_X3)  // perf experiment only: every pass three times (wrong results)
-#pragma unroll 1
-    for (int rep = 0; rep < 2; ++rep)
-      pass14<A, FWD, P1, ILTM0>(v, tw, twl, a.n, xbase + jt1, cst);
-#endif
+    NK_TS(2);
     pass14<A, FWD, P1, ILTM0>(v, tw, twl, a.n, xbase + jt1, cst);
+    NK_TS(3);
     // every P1 word has been consumed: the staging buffer may be overwritten
     __syncwarp();
     if (l == 0) {
       mbar_arrive_relaxed_local(bar_free_mine);
-#if !defined(NK_DBG_LOCAL_X)
       mbar_arrive_relaxed_remote(free_peer_remote);
-#endif
     }
 
     if (FWD) {
       // ---- DSMEM exchange P1 -> P2: word j goes to CTA bit13(j), index j & 0x1FFF ----
-      NK_XWAIT(bar_free_mine, phase);
+      mbar_wait(bar_free_mine, phase);
 #pragma unroll
       for (int r = 0; r < 32; ++r)
         if ((r >> 4) == static_cast<int>(c)) S[t + 256u * c + 512u * (r & 15)] = v[r];
-#if defined(NK_DBG_LOCAL_X)  // perf experiment only: no cross-CTA traffic (wrong results)
-#pragma unroll
-      for (int r = 0; r < 32; ++r)
-        if ((r >> 4) != static_cast<int>(c)) S[t + 256u * c + 512u * (r & 15)] = v[r];
-      mbar_arrive_local(bar_x);
-#else
       if (t == 0) mbar_arrive_expect_local(bar_x, kPairStageBytes / 2);
       else mbar_arrive_local(bar_x);
-      NK_XWAIT(bar_free_peer, phase);
+      mbar_wait(bar_free_peer, phase);
 #pragma unroll
       for (int r = 0; r < 32; ++r)
         if ((r >> 4) != static_cast<int>(c)) st_async_u64(s_peer + (t + 256u * c + 512u * (r & 15)) * 8u, v[r], x_peer);
-#endif
-      NK_XWAIT(bar_x, phase);  // acquire.cta: st.async data is ordered by complete_tx (no L1 invalidate)
+      mbar_wait(bar_x, phase);  // acquire.cta: st.async data is ordered by complete_tx (no L1 invalidate)
+      NK_TS(4);
 #pragma unroll
       for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -268,7 +262,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
       __syncwarp();
       if (l == 0) mbar_arrive_local(bar_sfree);  // release: the image reads are performed
       if (t == 0) {
-        NK_XWAIT(bar_sfree, phase);
+        mbar_wait(bar_sfree, phase);
         if (k + kstep < nitems) {
           fence_proxy_async();
           issue(k + kstep);
@@ -289,12 +283,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
       }
     }
 
-#if defined(NK_DBG_COMPUTE_X3)  // perf experiment only: every pass three times (wrong results)
-#pragma unroll 1
-    for (int rep = 0; rep < 2; ++rep)
-      pass14<A, FWD, P2, false>(v, tw, twl, a.n, xbase + jt_p2, cst);
-#endif
+    NK_TS(5);
     pass14<A, FWD, P2, false>(v, tw, twl, a.n, xbase + jt_p2, cst);
+    NK_TS(6);
 
     if (FWD) {
       // ---- warp-local exchange P2 -> P3 (rounds on bit 4) ----
@@ -313,7 +304,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
       }
     } else {
       // ---- DSMEM exchange P2 -> P3: word j goes to CTA bit8(j), index (j & 255) | (j >> 9) << 8 ----
-      NK_XWAIT(bar_free_mine, phase);
+      mbar_wait(bar_free_mine, phase);
 #pragma unroll
       for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -321,19 +312,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
           const uint32_t j = jt_p2 + (g << 4) + (r << 5);
           if (((r >> 3) & 1) == static_cast<int>(c)) S[(j & 255u) | ((j >> 9) << 8)] = v[16 * g + r];
         }
-#if defined(NK_DBG_LOCAL_X)
-#pragma unroll
-      for (int g = 0; g < 2; ++g)
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-          const uint32_t j = jt_p2 + (g << 4) + (r << 5);
-          if (((r >> 3) & 1) != static_cast<int>(c)) S[(j & 255u) | ((j >> 9) << 8)] = v[16 * g + r];
-        }
-      mbar_arrive_local(bar_x);
-#else
       if (t == 0) mbar_arrive_expect_local(bar_x, kPairStageBytes / 2);
       else mbar_arrive_local(bar_x);
-      NK_XWAIT(bar_free_peer, phase);
+      mbar_wait(bar_free_peer, phase);
 #pragma unroll
       for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -342,14 +323,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
           if (((r >> 3) & 1) != static_cast<int>(c))
             st_async_u64(s_peer + ((j & 255u) | ((j >> 9) << 8)) * 8u, v[16 * g + r], x_peer);
         }
-#endif
-      NK_XWAIT(bar_x, phase);  // acquire.cta: st.async data is ordered by complete_tx (no L1 invalidate)
+      mbar_wait(bar_x, phase);  // acquire.cta: st.async data is ordered by complete_tx (no L1 invalidate)
 #pragma unroll
       for (int r = 0; r < 32; ++r) v[r] = S[t + 256 * r];
       __syncwarp();
       if (l == 0) mbar_arrive_local(bar_sfree);
       if (t == 0) {
-        NK_XWAIT(bar_sfree, phase);
+        mbar_wait(bar_sfree, phase);
         if (k + kstep < nitems) {
           fence_proxy_async();
           issue(k + kstep);
@@ -357,12 +337,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
       }
     }
 
-#if defined(NK_DBG_COMPUTE_X3)  // perf experiment only: every pass three times (wrong results)
-#pragma unroll 1
-    for (int rep = 0; rep < 2; ++rep)
-      pass14<A, FWD, P3, false>(v, tw, twl, a.n, xbase + jt3, cst);
-#endif
+    NK_TS(7);
     pass14<A, FWD, P3, false>(v, tw, twl, a.n, xbase + jt3, cst);
+    NK_TS(8);
 
     if (FWD) {
 #pragma unroll
@@ -406,7 +383,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
 #pragma unroll
       for (int r = 0; r < 32; ++r) dst[jt_hi + 512 * r] = v[r];
     }
+    NK_TS(9);
     phase ^= 1;
+    ++it_;
   }
   // no CTA may exit while its peer can still signal or write into it: every
   // remote operation of the last item precedes the peer's wait on bar_x
