@@ -380,19 +380,21 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __re
       for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
         const ulonglong2 w = kLow ? ldtw(twl + low_index(b, hi, 0)) : ldtw(tw + base + hi);
 #pragma unroll
-        for (int l = 0; l < ((1 << i) * (G / GL)); ++l) {
-          const int g = kShared ? (l >> i) : gl;
-          const int ll = l & ((1 << i) - 1);
-          const int r0 = (hi << (i + 1)) | ll;
-          const int r1 = r0 | (1 << i);
-          uint64_t& x0 = v[g * R + r0];
-          uint64_t& x1 = v[g * R + r1];
-          if (FWD) {
-            if (ILTM0 && s == 0) A::template fwd<true>(x0, x1, w, c);
-            else A::template fwd<false>(x0, x1, w, c);
-          } else {
-            if (ILTM0 && s == 0) A::template inv<true>(x0, x1, w, c);
-            else A::template inv<false>(x0, x1, w, c);
+        for (int gg = 0; gg < G / GL; ++gg) {
+#pragma unroll
+          for (int l = 0; l < (1 << i); ++l) {
+            const int g = kShared ? gg : gl;
+            const int r0 = (hi << (i + 1)) | l;
+            const int r1 = r0 | (1 << i);
+            uint64_t& x0 = v[g * R + r0];
+            uint64_t& x1 = v[g * R + r1];
+            if (FWD) {
+              if (ILTM0 && s == 0) A::template fwd<true>(x0, x1, w, c);
+              else A::template fwd<false>(x0, x1, w, c);
+            } else {
+              if (ILTM0 && s == 0) A::template inv<true>(x0, x1, w, c);
+              else A::template inv<false>(x0, x1, w, c);
+            }
           }
         }
       }

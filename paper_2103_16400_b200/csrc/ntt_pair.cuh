@@ -172,6 +172,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
     }
   };
 
+  // the same boxes as issue(), prefetched into L2 only: the real TMA (which
+  // must wait until the staging buffer is free) then reads from L2
+  auto prefetch_l2 = [&](uint32_t k) {
+    uint64_t row, blk;
+    item_row(k, row, blk);
+    const uint64_t word0 = row * a.n + (blk << kB14);
+    if (FWD) {
+      asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                       reinterpret_cast<uint64_t>(&tin)),
+                   "r"(0), "r"(static_cast<int32_t>(16 * c)), "r"(static_cast<int32_t>(word0 >> 9))
+                   : "memory");
+    } else {
+      const int32_t line0 = static_cast<int32_t>((word0 >> 4) + 512 * c);
+      asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                       reinterpret_cast<uint64_t>(&tin)),
+                   "r"(0), "r"(line0)
+                   : "memory");
+      asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                       reinterpret_cast<uint64_t>(&tin)),
+                   "r"(0), "r"(line0 + 256)
+                   : "memory");
+    }
+  };
+
   const uint32_t k0 = cluster_id_x(), kstep = ncluster_x();
   if (t == 0) {
     mbar_init(bar, 1);
@@ -212,6 +236,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
 
     // ---- P1 words from the staging buffer ----
     mbar_wait(bar, phase);
+    if (FWD && t == 0 && k + kstep < nitems) prefetch_l2(k + kstep);
     NK_TS(1);
     if (FWD) {
 #pragma unroll
