@@ -46,22 +46,23 @@ static uint64_t dbits(double d) {
 }
 
 template <class A, bool FWD, int WHICH>
-void run(const char* name, const ulonglong2* tw, const ulonglong2* twl, const LimbConstDev& c, int bfly_per_iter) {
+void run(const char* name, const ulonglong2* tw, const ulonglong2* twl, const LimbConstDev& c, int bfly_per_iter,
+         int grid = 296) {
   uint64_t* out;
   cudaMalloc(&out, 1 << 16);
   const uint32_t iters = 200;
-  kern<A, FWD, WHICH><<<296, 256>>>(tw, twl, c, 32, 10, out);
+  kern<A, FWD, WHICH><<<grid, 256>>>(tw, twl, c, 32, 10, out);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  kern<A, FWD, WHICH><<<296, 256>>>(tw, twl, c, 32, iters, out);
+  kern<A, FWD, WHICH><<<grid, 256>>>(tw, twl, c, 32, iters, out);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
-  const double bf = 296.0 * 256 * iters * bfly_per_iter;
-  printf("%-26s %s: %8.3f ms  %5.2f bfly/clk/SM (1965 MHz)  %s\n", name, FWD ? "fwd" : "inv", ms,
+  const double bf = double(grid) * 256 * iters * bfly_per_iter;
+  printf("%-26s grid %3d %s: %8.3f ms  %5.2f bfly/clk/SM (1965 MHz)  %s\n", name, grid, FWD ? "fwd" : "inv", ms,
          bf / (ms * 1e-3) / 148 / 1.965e9, cudaGetErrorString(cudaGetLastError()));
   cudaFree(out);
 }
@@ -90,6 +91,8 @@ int main() {
   cudaMemcpy(tw, h.data(), h.size() * 16, cudaMemcpyHostToDevice);
   cudaMemcpy(twl, h.data(), h.size() * 16, cudaMemcpyHostToDevice);
   run<Arith52S, true, 7>("S all passes", tw, twl, c, 224);
+  run<Arith52S, true, 7>("S all passes, 1 CTA/SM", tw, twl, c, 224, 148);
+  run<Arith52S, true, 4>("S P3, 1 CTA/SM", tw, twl, c, 80, 148);
   run<Arith52S, true, 1>("S P1 (13..9)", tw, twl, c, 80);
   run<Arith52S, true, 2>("S P2 (8..5)", tw, twl, c, 64);
   run<Arith52S, true, 4>("S P3 (4..0, low table)", tw, twl, c, 80);
