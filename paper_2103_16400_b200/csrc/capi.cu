@@ -275,9 +275,11 @@ int launch_tma(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, bool i
               : launch_tma_t<A, FWD, false>(a, nitems, buf_words, st);
 }
 
-template <int LOGB, class A, bool FWD, bool IL>
+// LOGV = log2(words per thread): 32 words per thread for batches that fill
+// the GPU, 8 for small ones (cfg1: one row), where the row's latency is the
+// metric and 4x more threads per row cut it.
+template <int LOGB, int LOGV, class A, bool FWD, bool IL>
 int launch_block_t(const nk::NttArgs& a, uint64_t grid, cudaStream_t st) {
-  constexpr int LOGV = 5;
   constexpr size_t smem = nk::block_smem_bytes<LOGB, LOGV>();
   auto kern = nk::ntt_block<LOGB, LOGV, A, FWD, IL>;
   if (smem > 48 * 1024)
@@ -290,14 +292,19 @@ int launch_block_t(const nk::NttArgs& a, uint64_t grid, cudaStream_t st) {
 
 template <class A, bool FWD>
 int launch_block(uint32_t logb, const nk::NttArgs& a, uint64_t grid, bool iltm, cudaStream_t st) {
+  const bool small = a.rows < static_cast<uint64_t>(sm_count());
+#define NK_LB2(L, V) \
+  return iltm ? launch_block_t<L, V, A, FWD, true>(a, grid, st) : launch_block_t<L, V, A, FWD, false>(a, grid, st)
 #define NK_LB(L) \
-  return iltm ? launch_block_t<L, A, FWD, true>(a, grid, st) : launch_block_t<L, A, FWD, false>(a, grid, st)
+  if (small) NK_LB2(L, 3); \
+  NK_LB2(L, 5)
   switch (logb) {
     case 11: NK_LB(11);
     case 12: NK_LB(12);
     default: NK_LB(13);
   }
 #undef NK_LB
+#undef NK_LB2
 }
 
 template <class A, bool FWD>

@@ -250,3 +250,13 @@ def test_block_kernels_match_oracle(nk, oracle, kernel, logn, bits, npolys, arit
         check_dir(nk, oracle, n, moduli, npolys, 900 + logn + bits + kernel)
     finally:
         nk.set_block_kernel(-1)
+
+
+@pytest.mark.parametrize("logn", [11, 12, 13])
+def test_block_sizes_large_batches(nk, oracle, logn, arith):
+    """Batches of >= #SMs rows take the 32-words-per-thread block kernels (small
+    batches take the 8-words-per-thread ones, test_block_sizes_match_oracle)."""
+    n = 1 << logn
+    moduli = largest_ntt_primes(50, n, 3)
+    check_dir(nk, oracle, n, moduli, 52, 700 + logn, fwd_factors=[(1, 1), (4, 4), (2, 1)],
+              inv_factors=[(1, 1), (2, 2)])
