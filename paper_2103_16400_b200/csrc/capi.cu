@@ -894,30 +894,89 @@ int nk_eltwise_neg_mod(uint64_t* res, const uint64_t* a, uint64_t n, uint64_t q,
   return 0;
 }
 
+}  // extern "C"
+
 // ---------------------------------------------------------------------------
-// host-buffer wrappers: H2D, kernels, D2H on `stream`, then wait.
+// host-buffer wrappers: chunked H2D / kernels / D2H pipeline, then wait.
 // ---------------------------------------------------------------------------
 namespace {
 
-struct DevBuf {
-  uint64_t* p = nullptr;
-  cudaStream_t st = nullptr;
-  ~DevBuf() {
-    if (p) cudaFreeAsync(p, st);
-  }
+// Pipelined host-buffer execution. The work is cut into chunks of whole
+// units (polynomials for transforms, words for element-wise ops) of about
+// kChunkBytes; chunk i is uploaded, computed and downloaded on internal stream
+// i % 2, so the upload of one chunk, the kernels of another and the download of
+// a third overlap (PCIe is full duplex and the kernels are ~50x faster than
+// the copies). Blocking: returns when the results are in host memory. Work
+// previously queued on the caller's stream is ordered before the chunks.
+constexpr uint64_t kChunkBytes = 16ull << 20;
+
+struct HostPipe {
+  cudaStream_t s[2] = {nullptr, nullptr};
+  cudaEvent_t start = nullptr;
 };
 
-int h2d(DevBuf& d, const uint64_t* h, uint64_t words, cudaStream_t st) {
-  d.st = st;
-  NK_CUDA(cudaMallocAsync(&d.p, words * 8, st));
-  if (h) NK_CUDA(cudaMemcpyAsync(d.p, h, words * 8, cudaMemcpyHostToDevice, st));
+int host_pipe(int dev, HostPipe** out) {
+  static HostPipe pipes[64];
+  static std::once_flag once[64];
+  static cudaError_t err[64];
+  std::call_once(once[dev & 63], [dev] {
+    HostPipe& hp = pipes[dev & 63];
+    cudaError_t e = cudaSuccess;
+    for (auto& st : hp.s)
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp.start, cudaEventDisableTiming);
+    err[dev & 63] = e;
+  });
+  if (err[dev & 63] != cudaSuccess) return cuda_fail(err[dev & 63], "host pipeline streams");
+  *out = &pipes[dev & 63];
   return 0;
 }
 
-int finish(uint64_t* h, const DevBuf& d, uint64_t words, cudaStream_t st) {
-  NK_CUDA(cudaMemcpyAsync(h, d.p, words * 8, cudaMemcpyDeviceToHost, st));
-  NK_CUDA(cudaStreamSynchronize(st));
-  return 0;
+// fn(device buffers of the chunk (inputs; the first is also the output),
+//    first unit, units in chunk, stream) -> int
+template <class Fn>
+int run_pipelined(int dev, cudaStream_t user, uint64_t units, uint64_t unit_words,
+                  std::initializer_list<const uint64_t*> hin, uint64_t* hout, Fn&& fn) {
+  HostPipe* hp = nullptr;
+  if (int rc = host_pipe(dev, &hp)) return rc;
+  const int nin = static_cast<int>(hin.size());
+  const uint64_t unit_bytes = unit_words * 8;
+  uint64_t per = kChunkBytes / unit_bytes;
+  if (per < 1) per = 1;
+  if (per > units) per = units;
+  const uint64_t nchunks = (units + per - 1) / per;
+  NK_CUDA(cudaEventRecord(hp->start, user));
+  uint64_t* buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  int rc = 0;
+  const int nst = nchunks > 1 ? 2 : 1;
+  for (int k = 0; k < nst && !rc; ++k) {
+    cudaError_t e = cudaStreamWaitEvent(hp->s[k], hp->start, 0);
+    for (int j = 0; j < nin && e == cudaSuccess; ++j)
+      e = cudaMallocAsync(&buf[k][j], per * unit_bytes, hp->s[k]);
+    if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline buffers");
+  }
+  for (uint64_t c = 0; c < nchunks && !rc; ++c) {
+    const int k = static_cast<int>(c % nst);
+    const uint64_t u0 = c * per, nu = (u0 + per <= units) ? per : units - u0;
+    const uint64_t off = u0 * unit_words, bytes = nu * unit_bytes;
+    cudaError_t e = cudaSuccess;
+    int j = 0;
+    for (const uint64_t* h : hin) {
+      if (e == cudaSuccess && h) e = cudaMemcpyAsync(buf[k][j], h + off, bytes, cudaMemcpyHostToDevice, hp->s[k]);
+      ++j;
+    }
+    if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMemcpyAsync(H2D)"); break; }
+    if ((rc = fn(buf[k], u0, nu, hp->s[k]))) break;
+    e = cudaMemcpyAsync(hout + off, buf[k][0], bytes, cudaMemcpyDeviceToHost, hp->s[k]);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync(D2H)");
+  }
+  for (int k = 0; k < nst; ++k) {
+    for (int j = 0; j < nin; ++j)
+      if (buf[k][j]) cudaFreeAsync(buf[k][j], hp->s[k]);
+    cudaError_t e = cudaStreamSynchronize(hp->s[k]);
+    if (!rc && e != cudaSuccess) rc = cuda_fail(e, "cudaStreamSynchronize(host pipeline)");
+  }
+  return rc;
 }
 
 int ntt_host(bool fwd, const nk_plan* p, uint64_t* res, const uint64_t* op, uint64_t length,
@@ -927,17 +986,19 @@ int ntt_host(bool fwd, const nk_plan* p, uint64_t* res, const uint64_t* op, uint
   const uint64_t words = static_cast<uint64_t>(npolys) * nlimbs * p->n;
   if (length != words) return fail(NK_ERR_LENGTH, "transform: buffer length must equal n");
   if (!res || !op) return fail(NK_ERR_NULL, "transform: NULL buffer");
+  if (npolys == 0) return 0;
   if (int rc = ensure_device(p->device)) return rc;
-  cudaStream_t st = S(stream);
-  DevBuf d;
-  if (int rc = h2d(d, op, words, st)) return rc;
-  int rc = fwd ? nk_ntt_forward(p, d.p, d.p, limb0, nlimbs, npolys, fin, fout, stream)
-               : nk_ntt_inverse(p, d.p, d.p, limb0, nlimbs, npolys, fin, fout, stream);
-  if (rc) return rc;
-  return finish(res, d, words, st);
+  return run_pipelined(p->device, S(stream), npolys, static_cast<uint64_t>(nlimbs) * p->n, {op}, res,
+                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
+                         const uint32_t np = static_cast<uint32_t>(nu);
+                         return fwd ? nk_ntt_forward(p, d[0], d[0], limb0, nlimbs, np, fin, fout, st)
+                                    : nk_ntt_inverse(p, d[0], d[0], limb0, nlimbs, np, fin, fout, st);
+                       });
 }
 
 }  // namespace
+
+extern "C" {
 
 int nk_ntt_forward_host(const nk_plan* p, uint64_t* res, const uint64_t* op, uint64_t length,
                         uint32_t limb0, uint32_t nlimbs, uint32_t npolys, uint64_t fin,
@@ -966,13 +1027,16 @@ int nk_poly_mult_mod_host(const nk_plan* p, uint64_t* res, const uint64_t* f, co
   const uint64_t words = static_cast<uint64_t>(npolys) * nlimbs * p->n;
   if (length != words) return fail(NK_ERR_LENGTH, "poly_mult_mod: operand lengths must equal n");
   if (!res || !f || !g) return fail(NK_ERR_NULL, "poly_mult_mod: NULL buffer");
+  for (uint32_t l = 0; l < nlimbs && limb0 + l < p->nlimbs; ++l)
+    if (p->q[limb0 + l] >= (uint64_t{1} << 61))
+      return fail(NK_ERR_POLY_MODULUS, "poly_mult_mod: requires q < 2^61");
+  if (npolys == 0) return 0;
   if (int rc = ensure_device(p->device)) return rc;
-  cudaStream_t st = S(stream);
-  DevBuf df, dg;
-  if (int rc = h2d(df, f, words, st)) return rc;
-  if (int rc = h2d(dg, g, words, st)) return rc;
-  if (int rc = nk_poly_mult_mod(p, df.p, df.p, dg.p, limb0, nlimbs, npolys, stream)) return rc;
-  return finish(res, df, words, st);
+  return run_pipelined(p->device, S(stream), npolys, static_cast<uint64_t>(nlimbs) * p->n, {f, g}, res,
+                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
+                         return nk_poly_mult_mod(p, d[0], d[0], d[1], limb0, nlimbs,
+                                                 static_cast<uint32_t>(nu), st);
+                       });
 }
 
 int nk_eltwise_mult_mod_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n,
@@ -982,12 +1046,10 @@ int nk_eltwise_mult_mod_host(uint64_t* res, const uint64_t* a, const uint64_t* b
   if (int rc = validate_mult(q, fin, &m)) return rc;
   if (n == 0) return 0;
   if (int rc = ensure_device(device)) return rc;
-  cudaStream_t st = S(stream);
-  DevBuf da, db;
-  if (int rc = h2d(da, a, n, st)) return rc;
-  if (int rc = h2d(db, b, n, st)) return rc;
-  if (int rc = nk_eltwise_mult_mod(da.p, da.p, db.p, n, q, fin, stream)) return rc;
-  return finish(res, da, n, st);
+  return run_pipelined(device, S(stream), n, 1, {a, b}, res,
+                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
+                         return nk_eltwise_mult_mod(d[0], d[0], d[1], nu, q, fin, st);
+                       });
 }
 
 int nk_eltwise_fma_mod_host(uint64_t* res, const uint64_t* a, uint64_t y, const uint64_t* z,
@@ -998,14 +1060,11 @@ int nk_eltwise_fma_mod_host(uint64_t* res, const uint64_t* a, uint64_t y, const 
   if (int rc = validate_fma(q, y, fin, bit_shift, &bs)) return rc;
   if (n == 0) return 0;
   if (int rc = ensure_device(device)) return rc;
-  cudaStream_t st = S(stream);
-  DevBuf da, dz;
-  if (int rc = h2d(da, a, n, st)) return rc;
-  if (z)
-    if (int rc = h2d(dz, z, n, st)) return rc;
-  if (int rc = nk_eltwise_fma_mod(da.p, da.p, y, z ? dz.p : nullptr, n, q, fin, bit_shift, stream))
-    return rc;
-  return finish(res, da, n, st);
+  return run_pipelined(device, S(stream), n, 1, {a, z}, res,
+                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
+                         return nk_eltwise_fma_mod(d[0], d[0], y, z ? d[1] : nullptr, nu, q, fin, bit_shift,
+                                                   st);
+                       });
 }
 
 }  // extern "C"

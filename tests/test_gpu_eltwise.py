@@ -287,3 +287,27 @@ def test_unaligned_views(nk, oracle, offset):
     dx.copy_(dev(x))
     plan.forward(do, dx, 1, 1)
     assert np.array_equal(host(do), oracle.forward(nn, [qq], x, 1, 1))
+
+
+def test_host_pipeline_multi_chunk(nk, oracle):
+    """Host-buffer entry points cut large inputs into ~16 MiB chunks that are
+    uploaded / computed / downloaded on two streams: results must not depend on
+    the chunking (odd chunk counts, a short last chunk)."""
+    from primes import cfg2_modulus, largest_ntt_primes
+
+    q = cfg2_modulus()
+    n = 5 * (1 << 20) + 12345  # 3 chunks, the last one short
+    a = oracle.mt19937_64(301, n, q)
+    b = oracle.mt19937_64(302, n, q)
+    got = nk.eltwise_mult_mod(None, a, b, q, 1)
+    assert np.array_equal(got, oracle.eltwise_mult_mod(a, b, q, 1))
+    got = nk.eltwise_fma_mod(None, a, 987654321, b, q, 1)
+    assert np.array_equal(got, oracle.eltwise_fma_mod(a, 987654321, b, q, 1))
+    nn = 16384
+    moduli = largest_ntt_primes(50, nn, 3)
+    plan = nk.RnsNtt(nn, moduli)
+    npolys = 45  # 135 rows = 17.6 MiB: two chunks
+    x = np.concatenate([oracle.mt19937_64(400 + r, nn, moduli[r % 3]) for r in range(3 * npolys)])
+    f = plan.forward(None, x, 1, 1)
+    assert np.array_equal(f, oracle.forward(nn, moduli, x, 1, 1, threads=8))
+    assert np.array_equal(plan.inverse(None, f, 1, 1), x)
