@@ -391,7 +391,7 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "Mcoeff/s", "h2d_bytes_per_step": 2 * 8 * words,
                     "d2h_bytes_per_step": 2 * 8 * words,
-                    "path": "nk_ntt_forward_host + nk_ntt_inverse_host (pinned host buffers)"},
+                    "path": "nk_ntt_forward_host + nk_ntt_inverse_host (pinned host buffers; chunked upload / compute / download pipeline, 4 PCIe transfers of 256 MiB per step)"},
             "gpu_launches": launches, "clocks": clocks,
             "modmul": modmul,
         }
