@@ -228,11 +228,62 @@ int launch_pair_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cud
   return 0;
 }
 
-int g_block_kernel = -1;  // nk_debug_block_kernel(): -1 auto, 0 pair, 1 single, 2 warp
+int g_block_kernel = -1;  // nk_debug_block_kernel(): -1 auto, 0 pair, 1 single, 2 warp, 4 staged warp (fwd)
 
 // Warp-per-item kernel (ntt_warp.cuh) for whole 16384-word rows: persistent,
 // every warp resident; per-row phase counters live in a stream-ordered
 // allocation of this call (tables stay shareable across concurrent calls).
+// 2D view [words/128][128] of a row buffer (no swizzle), boxes of 8 x 128:
+// the 8-column items of the warp-per-item forward
+int make_cols_map(CUtensorMap* map, const uint64_t* base, uint64_t words) {
+  EncodeTiledFn fn;
+  if (int rc = encode_fn(&fn)) return rc;
+  const cuuint64_t dims[2] = {128, words / 128};
+  const cuuint64_t strides[1] = {1024};
+  const cuuint32_t box[2] = {8, 128};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint64_t*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NK_ERR_CUDA, "cuTensorMapEncodeTiled(cols) failed (" + std::to_string(r) + ")");
+  return 0;
+}
+
+// staged warp-per-item forward (ntt_warp14s)
+template <class A>
+int launch_warps_t(const nk::NttArgs& a, uint64_t buf_words, cudaStream_t st) {
+  CUtensorMap map;
+  if (int rc = make_cols_map(&map, a.in, buf_words)) return rc;
+  auto kern = nk::ntt_warp14s<A, false>;
+  if (int rc = set_smem(kern, nk::kWarpSSmemBytes)) return rc;
+  static int per_sm[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!per_sm[dev & 63]) {
+    int n = 0;
+    NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 256, nk::kWarpSSmemBytes));
+    per_sm[dev & 63] = n > 0 ? n : 1;
+  }
+  const uint64_t items = a.rows * 32;
+  uint64_t grid = static_cast<uint64_t>(per_sm[dev & 63]) * sm_count();
+  const uint64_t need = (items + nk::kWarpsPerCta - 1) / nk::kWarpsPerCta;
+  if (grid > need) grid = need;
+  uint32_t* cnt = nullptr;
+  const size_t cbytes = (a.rows + 1) * sizeof(uint32_t);
+  NK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cnt), cbytes, st));
+  NK_CUDA(cudaMemsetAsync(cnt, 0, cbytes, st));
+  // lag: a row's phase-1 items sit more than one round (grid warps) behind its
+  // phase-0 items, so no warp ever waits on an item of its own
+  const uint32_t lag = static_cast<uint32_t>(grid * nk::kWarpsPerCta / 16 + 2);
+  nk::WarpNttArgs wa{a, cnt, cnt + a.rows, lag};
+  kern<<<static_cast<unsigned>(grid), 256, nk::kWarpSSmemBytes, st>>>(map, wa);
+  g_launches++;
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(cnt, st);
+  if (e != cudaSuccess) return cuda_fail(e, "ntt_warp14s launch");
+  return 0;
+}
+
 template <class A, bool FWD, bool IL>
 int launch_warp_t(const nk::NttArgs& a, cudaStream_t st) {
   auto kern = nk::ntt_warp14<A, FWD, IL>;
@@ -346,6 +397,7 @@ int run_ntt(nk::NttArgs a, uint64_t buf_words, cudaStream_t st) {
     // B200 (profiles/ncu_r01_session2_warp.txt): selected only explicitly
     if (g_block_kernel == 2)
       return a.fin == 1 ? launch_warp_t<A, FWD, true>(a, st) : launch_warp_t<A, FWD, false>(a, st);
+    if (g_block_kernel == 4 && FWD) return launch_warps_t<A>(a, buf_words, st);
     return launch_tma<A, FWD>(a, a.rows, buf_words, a.fin == 1, st);
   }
   // long rows: high bits in global passes of <= 3 stages, low 14 bits per block

@@ -366,3 +366,232 @@ __global__ void __launch_bounds__(256, 2) ntt_warp14(WarpNttArgs wa) {
 }
 
 }  // namespace nk
+
+namespace nk {
+
+// ---------------------------------------------------------------------------
+// ntt_warp14s: the forward warp-per-item transform with asynchronous staging.
+// Each warp owns a 12.4 KiB shared region: an item image (the TMA / bulk-copy
+// landing zone, reused as the exchange image) and the phase-1 items' twiddle
+// segments. The next item's data is requested as soon as the current item's
+// exchange has been read, so the copy overlaps the last two stages, the
+// stores and the other warps' work; phase-0 input is also prefetched into L2
+// one item ahead. A phase-1 item's copy is only issued once the row counter
+// shows all 16 phase-0 items of the row published; if it is not ready at the
+// exchange, the warp finishes and publishes its own item first, so a waiting
+// warp never holds unpublished work (no cycle of waits).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kWSWords = 1056;                    // image (8448 B)
+constexpr uint32_t kWRegionBytes = 8448 + 4096 + 128;  // + twiddles (4 KiB) + mbarrier
+constexpr size_t kWarpSSmemBytes = 128 + kWarpsPerCta * kWRegionBytes;
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// twiddle segment of part-1 stage i (index bit 2 + i) inside the region
+__host__ __device__ constexpr uint32_t twseg(int i) {
+  return i == 4 ? 0 : (i == 3 ? 8 : (i == 2 ? 24 : (i == 1 ? 56 : 120)));
+}
+
+template <class A, bool ILTM0_UNUSED>
+__global__ void __launch_bounds__(256, 2)
+    ntt_warp14s(const __grid_constant__ CUtensorMap tin_cols, WarpNttArgs wa) {
+  extern __shared__ __align__(128) uint8_t wraw[];
+  const NttArgs& a = wa.a;
+  const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  uint8_t* region = wraw + ((128u - (smem_u32(wraw) & 127u)) & 127u) + wid * kWRegionBytes;
+  uint64_t* SW = reinterpret_cast<uint64_t*>(region);
+  ulonglong2* TWB = reinterpret_cast<ulonglong2*>(region + 8448);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(region + 8448 + 4096);
+  const uint32_t nw = gridDim.x * kWarpsPerCta;
+  const uint32_t rows = static_cast<uint32_t>(a.rows);
+  const uint32_t total = rows * 32u;
+  const uint32_t blo = lane & 7u, g = lane >> 3, b01 = lane & 3u, alo = lane >> 2;
+  const uint64_t pol_keep = policy_evict_last(), pol_stream = policy_evict_first();
+
+  auto row_of = [&](uint32_t rl) { return static_cast<uint64_t>(rl) * a.row_mul + a.row_add; };
+  auto limb_of = [&](uint64_t row) { return a.limb0 + static_cast<uint32_t>(row % a.nlimbs); };
+  // lane 0 only: is the row's phase 0 complete (non-blocking / blocking)
+  auto row_ready = [&](uint32_t rl) { return ld_relaxed_gpu(wa.cnt + rl) >= 16u; };
+  auto wait_row = [&](uint32_t rl) {
+    uint32_t spins = 0;
+    while (!row_ready(rl)) {
+      __nanosleep(64);
+      if (++spins > (1u << 24)) {  // give up (wrong result, no hang)
+        atomicOr(wa.err, 1u);
+        break;
+      }
+    }
+  };
+  // lane 0 only: request item p's data into this warp's region
+  auto issue = [&](uint32_t p) {
+    int ph;
+    uint32_t rl, sub;
+    warp_item(p, rows, wa.lag, ph, rl, sub);
+    const uint64_t row = row_of(rl);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (ph == 0) {
+      mbar_expect_tx(bar, 8192);
+      tma_load_2d(SW, &tin_cols, static_cast<int32_t>(8 * sub), static_cast<int32_t>(row * 128), bar);
+    } else {
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      const ulonglong2* tw = a.tw + static_cast<uint64_t>(limb_of(row)) * 16384u;
+      const uint32_t ab = 8 * sub;
+      mbar_expect_tx(bar, 8192 + 248 * 16);
+      for (int q = 0; q < 8; ++q)
+        bulk_g2s(SW + 132 * q, a.out + row * 16384u + 128u * (ab + q), 1024, bar);
+      for (int i = 4; i >= 0; --i)
+        bulk_g2s(TWB + twseg(i), tw + (2048 >> i) + (ab << (4 - i)), (8u << (4 - i)) * 16u, bar);
+    }
+  };
+  auto prefetch_in = [&](uint32_t p) {  // L2 prefetch of a phase-0 item's input
+    int ph;
+    uint32_t rl, sub;
+    warp_item(p, rows, wa.lag, ph, rl, sub);
+    if (ph != 0) return;
+    const uint64_t* s2 = a.in + row_of(rl) * 16384u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) prefetch_l2(s2 + 128u * (lane + 32u * k) + 8u * sub);
+  };
+
+  uint32_t pending = ~0u;
+  auto publish = [&]() {
+    if (pending != ~0u) {
+      __syncwarp();
+      if (lane == 0) red_release_gpu(wa.cnt + pending);
+      pending = ~0u;
+    }
+  };
+
+  const uint32_t p0 = blockIdx.x * kWarpsPerCta + wid;
+  if (lane == 0) mbar_init(bar, 1);
+  __syncwarp();
+  // the first request: phase-0 items at once; a phase-1 first item (small
+  // batches, rows < lag) goes through the deferred path (wait for its row)
+  bool loaded = false;
+  if (p0 < total) {
+    int ph;
+    uint32_t rl0, sub0;
+    warp_item(p0, rows, wa.lag, ph, rl0, sub0);
+    loaded = (ph == 0);
+    if (loaded && lane == 0) issue(p0);
+  }
+  uint32_t parity = 0;
+
+  for (uint32_t p = p0; p < total; p += nw) {
+    int phase;
+    uint32_t rl, sub;
+    warp_item(p, rows, wa.lag, phase, rl, sub);
+    const uint64_t row = row_of(rl);
+    const uint32_t limb = limb_of(row);
+    const LimbConst c = a.lc[limb];
+    const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * 16384u;
+    uint64_t* __restrict__ dst = a.out + row * 16384u;
+    const uint32_t pn = p + nw;
+    if (!loaded) {  // deferred request (the row was not ready at the last exchange)
+      if (lane == 0) {
+        int ph;
+        uint32_t rl2, sub2;
+        warp_item(p, rows, wa.lag, ph, rl2, sub2);
+        if (ph == 1) wait_row(rl2);
+        issue(p);
+      }
+      __syncwarp();
+    }
+    if (pn < total) prefetch_in(pn);
+    mbar_wait(bar, parity);
+    parity ^= 1;
+    uint64_t v[32];
+    bool next_issued = false;
+    auto request_next = [&]() {  // after the exchange reads: the region is free
+      __syncwarp();
+      bool ok = true;
+      if (lane == 0 && pn < total) {
+        int ph;
+        uint32_t rl2, sub2;
+        warp_item(pn, rows, wa.lag, ph, rl2, sub2);
+        ok = (ph == 0) || row_ready(rl2);
+        if (ok) issue(pn);
+      }
+      next_issued = __shfl_sync(0xffffffffu, ok ? 1 : 0, 0) != 0;
+    };
+
+    if (phase == 0) {
+      // ---- columns: stages 13..9, a bits 6..2 in registers ----
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = A::load(SW[32 * r + lane]);
+      {
+        auto t = [&](int i, int hi) { return ldtw(tw + (16 >> i) + hi); };
+        stage32<A, true, false, 4>(v, c, [&](int hi) { return t(4, hi); });
+        publish();  // the previous item's stores have had a stage to drain
+        stage32<A, true, false, 3>(v, c, [&](int hi) { return t(3, hi); });
+        stage32<A, true, false, 2>(v, c, [&](int hi) { return t(2, hi); });
+        stage32<A, true, false, 1>(v, c, [&](int hi) { return t(1, hi); });
+        stage32<A, true, false, 0>(v, c, [&](int hi) { return t(0, hi); });
+      }
+      __syncwarp();  // every lane has read the landing image
+#pragma unroll
+      for (int r = 0; r < 32; ++r) SW[cidx(4u * r + g, blo)] = v[r];
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = SW[cidx(r + 32u * g, blo)];
+      request_next();
+      {
+        auto t = [&](int i, int hi) { return ldtw(tw + (64 >> i) + hi + (g << (4 - i))); };
+        stage32<A, true, false, 1>(v, c, [&](int hi) { return t(1, hi); });
+        stage32<A, true, false, 0>(v, c, [&](int hi) { return t(0, hi); });
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r) st_hint(dst + 128u * (r + 32u * g) + 8u * sub + blo, v[r], pol_keep);
+      pending = rl;
+    } else {
+      // ---- rows: stages 6..2, b bits 2..6 in registers; twiddles staged ----
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = SW[132 * alo + 4 * r + b01];
+      {
+        auto t = [&](int i, int hi) { return TWB[twseg(i) + (alo << (4 - i)) + hi]; };
+        stage32<A, true, false, 4>(v, c, [&](int hi) { return t(4, hi); });
+        publish();  // the previous item's stores have had a stage to drain
+        stage32<A, true, false, 3>(v, c, [&](int hi) { return t(3, hi); });
+        stage32<A, true, false, 2>(v, c, [&](int hi) { return t(2, hi); });
+        stage32<A, true, false, 1>(v, c, [&](int hi) { return t(1, hi); });
+        stage32<A, true, false, 0>(v, c, [&](int hi) { return t(0, hi); });
+      }
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < 32; ++r) SW[ridx(alo, 4u * r + b01)] = v[r];
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const ulonglong2 p2 = *reinterpret_cast<const ulonglong2*>(SW + ridx(q, 4u * lane + 2 * h));
+          v[4 * q + 2 * h] = p2.x;
+          v[4 * q + 2 * h + 1] = p2.y;
+        }
+      request_next();
+      const uint32_t ab = 8u * sub;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t ar = ab + q;
+        const ulonglong2 w1 = ldtw(tw + 4096u + 32u * ar + lane);
+        A::template fwd<false>(v[4 * q + 0], v[4 * q + 2], w1, c);
+        A::template fwd<false>(v[4 * q + 1], v[4 * q + 3], w1, c);
+        const ulonglong2 w0a = ldtw(tw + 8192u + 64u * ar + 2u * lane);
+        const ulonglong2 w0b = ldtw(tw + 8192u + 64u * ar + 2u * lane + 1u);
+        A::template fwd<false>(v[4 * q + 0], v[4 * q + 1], w0a, c);
+        A::template fwd<false>(v[4 * q + 2], v[4 * q + 3], w0b, c);
+        st_v4(dst + 128u * ar + 4u * lane, fwd_out<A>(v[4 * q], c, a.fout), fwd_out<A>(v[4 * q + 1], c, a.fout),
+              fwd_out<A>(v[4 * q + 2], c, a.fout), fwd_out<A>(v[4 * q + 3], c, a.fout));
+      }
+    }
+    loaded = next_issued;
+    if (!loaded) publish();  // nothing of ours may be pending while we wait for a row
+  }
+  publish();
+}
+
+}  // namespace nk
