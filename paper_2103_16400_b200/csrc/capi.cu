@@ -195,10 +195,27 @@ int launch_tma_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cuda
 
 // CTA-pair kernel (ntt_pair.cuh): persistent, one cluster of 2 per block in
 // flight, as many clusters as fit (2 CTAs per SM).
+// 3D view [words/32][2][16] (128B swizzle), boxes 16 x 1 x 32: one half of 32
+// consecutive 32-word runs = one warp's output round of ntt_pair14 (forward)
+int make_out_map(CUtensorMap* map, const uint64_t* base, uint64_t words) {
+  EncodeTiledFn fn;
+  if (int rc = encode_fn(&fn)) return rc;
+  const cuuint64_t dims[3] = {16, 2, words / 32};
+  const cuuint64_t strides[2] = {128, 256};
+  const cuuint32_t box[3] = {16, 1, 32};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(NK_ERR_CUDA, "cuTensorMapEncodeTiled(out) failed (" + std::to_string(r) + ")");
+  return 0;
+}
+
 template <class A, bool FWD, bool IL>
 int launch_pair_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
-  CUtensorMap map;
+  CUtensorMap map, omap;
   if (int rc = FWD ? make_superline_map(&map, a.in, buf_words) : make_row_map(&map, a.in, buf_words)) return rc;
+  if (int rc = make_out_map(&omap, a.out, buf_words)) return rc;
   auto kern = nk::ntt_pair14<A, FWD, IL>;
   if (int rc = set_smem(kern, nk::kPairSmemBytes)) return rc;
   static int max_clusters[64] = {};
@@ -222,7 +239,7 @@ int launch_pair_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cud
   }
   const uint64_t mc = static_cast<uint64_t>(max_clusters[dev & 63]);
   const uint64_t g = nitems < mc ? nitems : mc;
-  kern<<<static_cast<unsigned>(2 * g), 256, nk::kPairSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));
+  kern<<<static_cast<unsigned>(2 * g), 256, nk::kPairSmemBytes, st>>>(map, omap, a, static_cast<uint32_t>(nitems));
   g_launches++;
   NK_CUDA(cudaGetLastError());
   return 0;

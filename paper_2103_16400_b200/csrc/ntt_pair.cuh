@@ -36,7 +36,7 @@ namespace nk {
 
 constexpr uint32_t kPairHalfWords = 8192;
 constexpr uint32_t kPairStageBytes = kPairHalfWords * 8;  // 64 KiB
-constexpr uint32_t kWarpImgWords = 576;                   // 512 + 2 * 32 pad
+constexpr uint32_t kWarpImgWords = 640;                   // 512 + 2 * 32 pad, rounded to 1 KiB (TMA-store swizzle atoms)
 // barriers: full (TMA), x (exchange landed), free_mine / free_peer (staging
 // consumed by this CTA's / the peer's warps), sfree (image read: TMA may refill)
 constexpr size_t kPairSmemBytes = 1024 + kPairStageBytes + 8 * kWarpImgWords * 8 + 5 * 8;
@@ -112,6 +112,18 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
+                                             const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // warp-image position of a word (index bits 0..3 and 5..9; bit 4 is the round)
 __host__ __device__ constexpr uint32_t wimg(uint32_t j) {
   const uint32_t idx = (j & 15u) | (((j >> 5) & 31u) << 4);
@@ -128,9 +140,12 @@ __host__ __device__ constexpr uint32_t wimg(uint32_t j) {
 #define NK_TS(id) ((void)0)
 #endif
 
+// tout (forward): 3D view [words/32][2][16] of the result, boxes 16 x 1 x 32
+// with 128B swizzle = one warp's output round straight from its image.
 template <class A, bool FWD, bool ILTM0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
-    ntt_pair14(const __grid_constant__ CUtensorMap tin, NttArgs a, uint32_t nitems) {
+    ntt_pair14(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, NttArgs a,
+               uint32_t nitems) {
   using P1 = typename std::conditional<FWD, PassD<9, 5, -1>, PassD<0, 5, -1>>::type;
   using P2 = PassD<5, 4, 4>;
   using P3 = typename std::conditional<FWD, PassD<0, 5, -1>, PassD<9, 5, -1>>::type;
@@ -314,6 +329,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
 
     if (FWD) {
       // ---- warp-local exchange P2 -> P3 (rounds on bit 4) ----
+      if (l == 0) bulk_wait_read();  // the last item's output store has read the image
+      __syncwarp();
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -374,6 +391,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
       uint8_t* Wb = reinterpret_cast<uint8_t*>(W);
       uint64_t* wdst = dst + (w << 10) + (c << 13);
       const uint64_t* mulb = a.mulb ? a.mulb + row * a.n + boff + (w << 10) + (c << 13) : nullptr;
+      if (!mulb) {
+        // the image rows are the TMA box rows: one bulk tensor store per round
+        const int32_t srow = static_cast<int32_t>((row * a.n + boff + (w << 10) + (c << 13)) >> 5);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1) {
+            if (l == 0) bulk_wait_read();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc)
+            *reinterpret_cast<ulonglong2*>(Wb + (l << 7) + ((cc ^ (l & 7)) << 4)) =
+                make_ulonglong2(v[16 * h + 2 * cc], v[16 * h + 2 * cc + 1]);
+          fence_proxy_async();
+          __syncwarp();
+          if (l == 0) tma_store_3d(&tout, 0, h, srow, Wb);
+        }
+      } else
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -412,6 +447,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
     phase ^= 1;
     ++it_;
   }
+  if (FWD && l == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   // no CTA may exit while its peer can still signal or write into it: every
   // remote operation of the last item precedes the peer's wait on bar_x
   cluster_arrive();
