@@ -155,9 +155,10 @@ int nk_eltwise_fma_mod_host(uint64_t* result, const uint64_t* a, uint64_t y, con
 /* Number of kernels the library has launched in this process (for the bench's
  * gpu_launches claim). */
 uint64_t nk_launch_count(void);
-/* Debug aid: when d_buf (device, 3*16384 words) is non-NULL, the N = 2^14 transform
- * kernel writes the words of its first block after each of its three register
- * passes. NULL (the default) disables it. */
+/* Debug aid: device buffer that a library built with -DNK_DBG_TIMELINE fills
+ * with per-warp phase timestamps of the CTA-pair forward kernel
+ * (tools/timeline.py; 296 x 8 x 32 x 16 words). NULL (the default) disables it;
+ * the normal build ignores it. */
 void nk_debug_dump_to(uint64_t* d_buf);
 /* Testing aid: when on, every beta = 2^52 transform uses the exact lazy
  * arithmetic (the reference's representatives) even where only the canonical

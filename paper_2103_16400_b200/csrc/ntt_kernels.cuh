@@ -51,7 +51,7 @@ struct NttArgs {
   uint32_t row_mul, row_add;  // launched row i is row i * row_mul + row_add
   uint32_t logn;
   int32_t fin, fout;
-  uint64_t* dbg;  // debug: when set, the TMA kernel dumps each pass's words ([3][N]) for item 0
+  uint64_t* dbg;  // debug: per-warp phase timestamps of an NK_DBG_TIMELINE build (tools/timeline.py)
   const uint64_t* mulb;  // forward (CTA-pair kernel, fout == 1): multiply the canonical
                          // result by these canonical words (same layout) before storing
 };
