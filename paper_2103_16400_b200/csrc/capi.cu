@@ -245,7 +245,7 @@ int launch_pair_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cud
   return 0;
 }
 
-int g_block_kernel = -1;  // nk_debug_block_kernel(): -1 auto, 0 pair, 1 single, 2 warp, 4 staged warp (fwd)
+int g_block_kernel = -1;  // nk_debug_block_kernel(): -1 auto, 0 pair, 1 single, 2 warp, 4 staged warp (fwd), 5 3-barrier inverse
 
 // Warp-per-item kernel (ntt_warp.cuh) for whole 16384-word rows: persistent,
 // every warp resident; per-row phase counters live in a stream-ordered
@@ -330,8 +330,23 @@ int launch_warp_t(const nk::NttArgs& a, cudaStream_t st) {
   return 0;
 }
 
+template <class A, bool IL>
+int launch_inv2_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
+  CUtensorMap map;
+  if (int rc = make_row_map(&map, a.in, buf_words)) return rc;
+  auto kern = nk::ntt_inv14_tma<A, IL>;
+  if (int rc = set_smem(kern, nk::kTmaSmemBytes)) return rc;
+  const uint64_t g = nitems < static_cast<uint64_t>(sm_count()) ? nitems : sm_count();
+  kern<<<static_cast<unsigned>(g), 512, nk::kTmaSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
 template <class A, bool FWD>
 int launch_tma(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm, cudaStream_t st) {
+  if (!FWD && g_block_kernel == 5)
+    return iltm ? launch_inv2_t<A, true>(a, nitems, buf_words, st) : launch_inv2_t<A, false>(a, nitems, buf_words, st);
   // measured on B200 (cfg3): the CTA-pair kernel is the faster forward, the
   // single-CTA kernel the faster inverse (the pair inverse exchanges late,
   // so its next TMA overlaps less compute)

@@ -124,11 +124,6 @@ __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
-// warp-image position of a word (index bits 0..3 and 5..9; bit 4 is the round)
-__host__ __device__ constexpr uint32_t wimg(uint32_t j) {
-  const uint32_t idx = (j & 15u) | (((j >> 5) & 31u) << 4);
-  return idx + 2u * (idx >> 4);
-}
 
 #if defined(NK_DBG_TIMELINE)  // perf experiment: per-warp phase timestamps into a.dbg
 #define NK_TS(id)                                                                            \
