@@ -19,6 +19,10 @@ if [ "${SKIP_NCU:-0}" = "0" ]; then
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:${PROF_K:-ntt} -s ${PROF_S:-2} -c ${PROF_C:-2} \
       -o $O/prof python tools/prof_ntt.py --op ${PROF_OP:-both} --iters 2 > $O/ncu_full.log 2>&1
   echo "ncu_full=$?" | tee -a $O/status
+  timeout 120 python tools/prof_eltwise.py > $O/prof_elt_plain.log 2>&1 && \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:eltwise -s 3 -c 3 \
+      -o $O/prof_elt python tools/prof_eltwise.py > $O/ncu_elt.log 2>&1
+  echo "ncu_elt=$?" | tee -a $O/status
 fi
 cat $O/status
 tail -3 $O/pytest_gpu.log
