@@ -9,9 +9,11 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <initializer_list>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -550,11 +552,29 @@ int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64
   return 0;
 }
 
-unsigned eltwise_grid(uint64_t work) {
-  // work = vector chunks; each thread takes nk::kU chunks per sweep. Enough
-  // CTAs for ~2 waves of 8 resident 256-thread CTAs per SM; grid-stride beyond.
-  uint64_t g = (work + 256 * nk::kU - 1) / (256 * nk::kU);
-  const uint64_t cap = static_cast<uint64_t>(sm_count()) * 16;
+// Resident CTAs per SM of an element-wise kernel (occupancy API, cached per
+// kernel and device).
+int resident_ctas(const void* kern, int block) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto& c = cache[dev & 63];
+  auto it = c.find(kern);
+  if (it != c.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, block, 0) != cudaSuccess || n < 1) n = 1;
+  c[kern] = n;
+  return n;
+}
+
+unsigned eltwise_grid(uint64_t work, const void* kern, int ku = nk::kU) {
+  // work = vector chunks; each thread takes ku chunks per sweep; up to two
+  // waves of resident CTAs, grid-stride beyond
+  const uint64_t per = 256ull * ku;
+  uint64_t g = (work + per - 1) / per;
+  const uint64_t cap = 2ull * sm_count() * resident_ctas(kern, 256);
   return static_cast<unsigned>(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
@@ -587,7 +607,7 @@ cudaError_t launch_mult_t(uint64_t* r, const uint64_t* a, const uint64_t* b, uin
                           nk::MultConst c0, const nk::MultConst* consts, uint32_t nlimbs, cudaStream_t st) {
   const int vec = vec_of({r, a, b});
 #define NK_MV(V)                                                                                          \
-  return launch_pdl(nk::eltwise_mult_kernel<FIN, SMALLQ, BATCHED, V>, eltwise_grid(total / V + 1), 256, st, \
+  return launch_pdl(nk::eltwise_mult_kernel<FIN, SMALLQ, BATCHED, V>, eltwise_grid(total / V + 1, reinterpret_cast<const void*>(nk::eltwise_mult_kernel<FIN, SMALLQ, BATCHED, V>)), 256, st, \
                     r, a, b, total, logn, c0, consts, nlimbs)
   if (vec == 4) NK_MV(4);
   if (vec == 2) NK_MV(2);
@@ -927,7 +947,7 @@ int nk_eltwise_fma_mod(uint64_t* res, const uint64_t* a, uint64_t y, const uint6
   const int vec = z ? vec_of({res, a, z}) : vec_of({res, a});
   cudaError_t e = cudaSuccess;
 #define NK_FMAV(BS, Z, F, V) \
-  e = launch_pdl(nk::eltwise_fma_kernel<BS, Z, F, V>, eltwise_grid(n / V + 1), 256, st, res, a, z, n, c)
+  e = launch_pdl(nk::eltwise_fma_kernel<BS, Z, F, V>, eltwise_grid(n / V + 1, reinterpret_cast<const void*>(nk::eltwise_fma_kernel<BS, Z, F, V>), nk::fma_ku(Z)), 256, st, res, a, z, n, c)
 #define NK_FMA(BS, Z, F)                            \
   if (vec == 4) NK_FMAV(BS, Z, F, 4);               \
   else if (vec == 2) NK_FMAV(BS, Z, F, 2);          \
@@ -959,7 +979,7 @@ int nk_eltwise_add_mod(uint64_t* res, const uint64_t* a, const uint64_t* b, uint
   if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (n == 0) return 0;
   if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_add_mod: NULL buffer");
-  cudaError_t e = launch_pdl(nk::eltwise_add_kernel, eltwise_grid(n), 256, S(stream), res, a, b, n, q);
+  cudaError_t e = launch_pdl(nk::eltwise_add_kernel, eltwise_grid(n, reinterpret_cast<const void*>(nk::eltwise_add_kernel)), 256, S(stream), res, a, b, n, q);
   g_launches++;
   if (e != cudaSuccess) return cuda_fail(e, "eltwise_add_kernel launch");
   NK_CUDA(cudaGetLastError());
@@ -971,7 +991,7 @@ int nk_eltwise_neg_mod(uint64_t* res, const uint64_t* a, uint64_t n, uint64_t q,
   if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (n == 0) return 0;
   if (!res || !a) return fail(NK_ERR_NULL, "eltwise_neg_mod: NULL buffer");
-  cudaError_t e = launch_pdl(nk::eltwise_neg_kernel, eltwise_grid(n), 256, S(stream), res, a, n, q);
+  cudaError_t e = launch_pdl(nk::eltwise_neg_kernel, eltwise_grid(n, reinterpret_cast<const void*>(nk::eltwise_neg_kernel)), 256, S(stream), res, a, n, q);
   g_launches++;
   if (e != cudaSuccess) return cuda_fail(e, "eltwise_neg_kernel launch");
   NK_CUDA(cudaGetLastError());
@@ -993,9 +1013,29 @@ namespace {
 // the copies). Blocking: returns when the results are in host memory. Work
 // previously queued on the caller's stream is ordered before the chunks.
 constexpr uint64_t kChunkBytes = 16ull << 20;
+constexpr int kMaxDepth = 4;
+
+// chunk size and pipeline depth (buffers / internal streams); tunable through
+// NK_HOST_CHUNK_MB / NK_HOST_DEPTH for measurements
+uint64_t host_chunk_bytes() {
+  static const uint64_t v = [] {
+    const char* e = getenv("NK_HOST_CHUNK_MB");
+    const long mb = e ? atol(e) : 0;
+    return mb > 0 ? static_cast<uint64_t>(mb) << 20 : kChunkBytes;
+  }();
+  return v;
+}
+int host_depth() {
+  static const int v = [] {
+    const char* e = getenv("NK_HOST_DEPTH");
+    const int d = e ? atoi(e) : 0;
+    return d >= 1 && d <= kMaxDepth ? d : 2;
+  }();
+  return v;
+}
 
 struct HostPipe {
-  cudaStream_t s[2] = {nullptr, nullptr};
+  cudaStream_t s[kMaxDepth] = {};
   cudaEvent_t start = nullptr;
 };
 
@@ -1025,14 +1065,14 @@ int run_pipelined(int dev, cudaStream_t user, uint64_t units, uint64_t unit_word
   if (int rc = host_pipe(dev, &hp)) return rc;
   const int nin = static_cast<int>(hin.size());
   const uint64_t unit_bytes = unit_words * 8;
-  uint64_t per = kChunkBytes / unit_bytes;
+  uint64_t per = host_chunk_bytes() / unit_bytes;
   if (per < 1) per = 1;
   if (per > units) per = units;
   const uint64_t nchunks = (units + per - 1) / per;
   NK_CUDA(cudaEventRecord(hp->start, user));
-  uint64_t* buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  uint64_t* buf[kMaxDepth][2] = {};
   int rc = 0;
-  const int nst = nchunks > 1 ? 2 : 1;
+  const int nst = static_cast<int>(nchunks < static_cast<uint64_t>(host_depth()) ? nchunks : host_depth());
   for (int k = 0; k < nst && !rc; ++k) {
     cudaError_t e = cudaStreamWaitEvent(hp->s[k], hp->start, 0);
     for (int j = 0; j < nin && e == cudaSuccess; ++j)

@@ -94,12 +94,14 @@ __device__ __forceinline__ void pdl_enter() {
 
 // Rows of `n` = 2^logn words (BATCHED: row r uses consts[r % nlimbs]) or one
 // vector under c0. Each thread streams kU chunks of VEC words per iteration
-// with all loads issued before any arithmetic (memory-level parallelism for an
-// HBM-bound loop); grid-stride over a few waves of resident CTAs; the last
-// total % VEC words are done by thread 0.
-constexpr int kU = 2;
+// with all loads issued before any arithmetic; grid-stride beyond a few waves
+// of resident CTAs; the last total % VEC words are done by thread 0.
+// kU = 1 with ~6 resident CTAs per SM: at 2^20 words a call is ~6 us, and
+// more, smaller CTAs start streaming sooner and drain faster than fewer CTAs
+// with deeper per-thread batches (tools/elt_probe.cu: 5.6 vs 6.2 us per call).
+constexpr int kU = 1;
 template <int FIN, bool SMALLQ, bool BATCHED, int VEC>
-__global__ void __launch_bounds__(256) eltwise_mult_kernel(uint64_t* __restrict__ r,
+__global__ void __launch_bounds__(256, FIN == 1 ? 6 : 4) eltwise_mult_kernel(uint64_t* __restrict__ r,
                                                            const uint64_t* __restrict__ a,
                                                            const uint64_t* __restrict__ b,
                                                            uint64_t total, uint32_t logn,
@@ -160,19 +162,24 @@ __device__ __forceinline__ uint64_t fma_one(uint64_t a, uint64_t z, const FmaCon
   return v;
 }
 
+// chunks per thread of the FMA kernel: one input stream (vector-scalar
+// multiply) keeps two chunks in flight per thread, two streams one
+__host__ __device__ constexpr int fma_ku(bool has_z) { return has_z ? 1 : 2; }
+
 template <int BS, bool HAS_Z, int FIN, int VEC>
-__global__ void __launch_bounds__(256) eltwise_fma_kernel(uint64_t* __restrict__ r,
+__global__ void __launch_bounds__(256, HAS_Z ? 6 : 1) eltwise_fma_kernel(uint64_t* __restrict__ r,
                                                           const uint64_t* __restrict__ a,
                                                           const uint64_t* __restrict__ z,
                                                           uint64_t n, FmaConst c) {
   pdl_enter();
+  constexpr int KU = fma_ku(HAS_Z);
   const uint64_t chunks = n / VEC;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   for (uint64_t i0 = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i0 < chunks;
-       i0 += kU * stride) {
-    WordVec<VEC> x[kU], zz[kU];
+       i0 += KU * stride) {
+    WordVec<VEC> x[KU], zz[KU];
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < KU; ++u) {
       const uint64_t i = i0 + u * stride;
 #pragma unroll
       for (int k = 0; k < VEC; ++k) zz[u].w[k] = 0;
@@ -182,7 +189,7 @@ __global__ void __launch_bounds__(256) eltwise_fma_kernel(uint64_t* __restrict__
       }
     }
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
+    for (int u = 0; u < KU; ++u) {
       const uint64_t i = i0 + u * stride;
       if (i < chunks) {
         WordVec<VEC> o;

@@ -26,8 +26,10 @@ def main():
     ap.add_argument("--bits", type=int, default=50)
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--fin", type=int, default=1)
+    ap.add_argument("--kernel", type=int, default=-1, help="nk_debug_block_kernel (-1 auto)")
     ap.add_argument("--op", default="both", choices=["fwd", "inv", "both", "poly", "mult"])
     a = ap.parse_args()
+    nk.set_block_kernel(a.kernel)
     moduli = largest_ntt_primes(a.bits, a.n, a.limbs)
     plan = nk.RnsNtt(a.n, moduli)
     words = a.n * a.limbs * a.polys
