@@ -755,10 +755,13 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
     }
     // -q modulo 2^64 (the 52-bit negated modulus of ntt.hpp:85-92 agrees modulo 2^52,
     // see modmath.cuh)
+    // folded last inverse stage: n^-1 * w_1 (w_1 = inverse table entry 1)
+    const uint64_t nw = static_cast<uint64_t>(static_cast<u128>(t.ninv) * t.wi[1] % t.q);
+    const uint64_t nwp = static_cast<uint64_t>((static_cast<u128>(nw) << t.bs) / t.q);
     hl[l] = nk::LimbConst{t.q, 2 * t.q, ~t.q + 1, enc(t.ninv), enc(t.ninvp), 2 * t.q + nk::kDBias,
                           std::ldexp(static_cast<double>(t.q), -52), static_cast<double>(2 * t.q),
                           t.bs, 0, static_cast<double>(t.q), 1.0 / static_cast<double>(t.q),
-                          static_cast<double>(t.q) + 4503599627370496.0};
+                          static_cast<double>(t.q) + 4503599627370496.0, enc(nw), enc(nwp)};
     nk::host::Modulus m;
     nk::host::make_modulus(t.q, &m);
     const int fins[3] = {1, 2, 4};

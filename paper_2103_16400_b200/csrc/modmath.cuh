@@ -183,6 +183,10 @@ struct LimbConstDev {
   double q_d;     // q as a double
   double qinv;    // 1/q rounded (Arith52S canonicalisation)
   double q_bias;  // q + 2^52
+  // n^-1 * w_1 mod q and its Shoup quotient (policy encoding like ninv): the
+  // last inverse stage's single twiddle (table index 1) times n^-1, for the
+  // folded last stage of canonical inverses (inv_fold)
+  uint64_t nw, nwp;
 };
 constexpr double kC52x15 = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer constant
 
@@ -206,6 +210,16 @@ struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)
   static constexpr bool kSigned = false;
   __device__ static uint64_t red4(uint64_t x, const LimbConstDev& c) { return nk::csub(nk::csub(x, c.twoq), c.q); }
   __device__ static uint64_t red2(uint64_t x, const LimbConstDev& c) { return nk::csub(x, c.q); }
+  // last GS stage (twiddle w_1) with the n^-1 pass folded in, canonical words
+  // out: x0 = n^-1 (x0 + x1), x1 = (n^-1 w_1)(x0 - x1), inputs in [0, 2q).
+  // Only for fout == 1, where the result is unique (not the reference's
+  // operation sequence: two Shoup products per butterfly instead of three).
+  static constexpr bool kFold = true;
+  __device__ static void inv_fold(uint64_t& x0, uint64_t& x1, const LimbConstDev& c) {
+    const uint64_t s = x0 + x1, t = x0 + c.twoq - x1;  // [0, 4q), (0, 4q): below beta
+    x0 = nk::csub(mul_lazy<BS>(s, c.ninv, c.ninvp, c.negq), c.q);
+    x1 = nk::csub(mul_lazy<BS>(t, c.nw, c.nwp, c.negq), c.q);
+  }
 };
 
 struct Arith52F {  // beta = 2^52 on the FP64 pipe (requires 4q < 2^52)
@@ -241,6 +255,8 @@ struct Arith52F {  // beta = 2^52 on the FP64 pipe (requires 4q < 2^52)
   static constexpr bool kSigned = false;
   __device__ static uint64_t red4(uint64_t x, const LimbConstDev& c) { return csubD(csubD(x, c.twoq), c.q); }
   __device__ static uint64_t red2(uint64_t x, const LimbConstDev& c) { return csubD(x, c.q); }
+  static constexpr bool kFold = false;
+  __device__ static void inv_fold(uint64_t&, uint64_t&, const LimbConstDev&) {}
 };
 
 // ---------------------------------------------------------------------------
@@ -288,6 +304,14 @@ struct Arith52P {
     return as_u(csubP(csubP(as_d(x), c.twoq_d), c.q_d));
   }
   __device__ static uint64_t red2(uint64_t x, const LimbConstDev& c) { return as_u(csubP(as_d(x), c.q_d)); }
+  // see ArithInt::inv_fold; plain doubles in [0, 2q) in, stored words out
+  static constexpr bool kFold = true;
+  __device__ static void inv_fold(uint64_t& x0, uint64_t& x1, const LimbConstDev& c) {
+    const double a = as_d(x0), b = as_d(x1);
+    const double s = __dadd_rn(a, b), t = __dadd_rn(__dsub_rn(a, b), c.twoq_d);  // exact, < 4q
+    x0 = store(as_u(csubP(mul_lazy_plain(s, as_d(c.ninv), as_d(c.ninvp), c.qq), c.q_d)));
+    x1 = store(as_u(csubP(mul_lazy_plain(t, as_d(c.nw), as_d(c.nwp), c.qq), c.q_d)));
+  }
 };
 
 // ---------------------------------------------------------------------------
@@ -364,6 +388,13 @@ struct Arith52S {
   }
   __device__ static uint64_t scale_ninv(uint64_t x, const LimbConstDev& c) {
     return as_u(mul_signed(as_d(x), as_d(c.ninv), as_d(c.ninvp), c.qq));
+  }
+  // see ArithInt::inv_fold; signed doubles |x| < 2q in, canonical words out
+  static constexpr bool kFold = true;
+  __device__ static void inv_fold(uint64_t& x0, uint64_t& x1, const LimbConstDev& c) {
+    const double a = as_d(x0), b = as_d(x1);
+    x0 = canon(mul_signed(__dadd_rn(a, b), as_d(c.ninv), as_d(c.ninvp), c.qq), c);
+    x1 = canon(mul_signed(__dsub_rn(a, b), as_d(c.nw), as_d(c.nwp), c.qq), c);
   }
 };
 

@@ -592,11 +592,19 @@ __global__ void __launch_bounds__(256) ntt_global_pass(NttArgs a, uint32_t lo, i
 #pragma unroll
   for (int r = 0; r < R; ++r) v[r] = A::load(src[j0 + (static_cast<uint64_t>(r) << lo)]);
   const uint64_t xt = a.n + j0;
+  // canonical inverse: the last stage (bit logn - 1, one twiddle) takes the
+  // n^-1 factor (A::inv_fold) and stores canonical words directly
+  const bool fold = !FWD && A::kFold && last && a.fout == 1;
 #pragma unroll
   for (int s = 0; s < K; ++s) {
     const int i = FWD ? (K - 1 - s) : s;
     const uint32_t b = lo + i;
     const uint64_t base = xt >> (b + 1);
+    if (!FWD && s == K - 1 && fold) {
+#pragma unroll
+      for (int r0 = 0; r0 < R / 2; ++r0) A::inv_fold(v[r0], v[r0 + R / 2], c);
+      break;
+    }
 #pragma unroll
     for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
       const ulonglong2 w = ldtw(tw + base + hi);
@@ -614,7 +622,8 @@ __global__ void __launch_bounds__(256) ntt_global_pass(NttArgs a, uint32_t lo, i
   }
 #pragma unroll
   for (int r = 0; r < R; ++r)
-    dst[j0 + (static_cast<uint64_t>(r) << lo)] = (!FWD && last) ? inv_out<A>(v[r], c, a.fout) : A::store(v[r]);
+    dst[j0 + (static_cast<uint64_t>(r) << lo)] =
+        fold ? v[r] : ((!FWD && last) ? inv_out<A>(v[r], c, a.fout) : A::store(v[r]));
 }
 
 // ---------------------------------------------------------------------------
