@@ -468,6 +468,13 @@ int check_limbs(const nk_plan* p, uint32_t limb0, uint32_t nlimbs) {
   return 0;
 }
 
+// largest modulus of limbs [l0, l0 + cnt)
+uint64_t max_q(const nk_plan* p, uint32_t l0, uint32_t cnt) {
+  uint64_t m = 0;
+  for (uint32_t l = l0; l < l0 + cnt; ++l) m = p->q[l] > m ? p->q[l] : m;
+  return m;
+}
+
 int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, uint32_t limb0,
                          uint32_t nlimbs, uint32_t npolys, uint64_t fin, uint64_t fout, cudaStream_t st,
                          const uint64_t* mulb);
@@ -544,6 +551,9 @@ int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64
       rc = fwd ? run_ntt<nk::Arith52S, true>(b, words, st) : run_ntt<nk::Arith52S, false>(b, words, st);
     else if (bs == 52)
       rc = fwd ? run_ntt<nk::Arith52P, true>(b, words, st) : run_ntt<nk::Arith52P, false>(b, words, st);
+    else if (b.fout == 1 && !g_exact_only && max_q(p, limb0 + (uniform ? 0 : l), uniform ? nlimbs : 1) < (uint64_t{1} << 61))
+      // beta = 2^64, canonical result only: loose Shoup quotients (nk::ArithIntL)
+      rc = fwd ? run_ntt<nk::ArithIntL, true>(b, words, st) : run_ntt<nk::ArithIntL, false>(b, words, st);
     else
       rc = fwd ? run_ntt<nk::ArithInt<64>, true>(b, words, st)
                : run_ntt<nk::ArithInt<64>, false>(b, words, st);
@@ -761,7 +771,7 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
     hl[l] = nk::LimbConst{t.q, 2 * t.q, ~t.q + 1, enc(t.ninv), enc(t.ninvp), 2 * t.q + nk::kDBias,
                           std::ldexp(static_cast<double>(t.q), -52), static_cast<double>(2 * t.q),
                           t.bs, 0, static_cast<double>(t.q), 1.0 / static_cast<double>(t.q),
-                          static_cast<double>(t.q) + 4503599627370496.0, enc(nw), enc(nwp)};
+                          static_cast<double>(t.q) + 4503599627370496.0, enc(nw), enc(nwp), 4 * t.q};
     nk::host::Modulus m;
     nk::host::make_modulus(t.q, &m);
     const int fins[3] = {1, 2, 4};

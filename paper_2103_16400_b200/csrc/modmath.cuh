@@ -187,11 +187,13 @@ struct LimbConstDev {
   // last inverse stage's single twiddle (table index 1) times n^-1, for the
   // folded last stage of canonical inverses (inv_fold)
   uint64_t nw, nwp;
+  uint64_t fourq;  // 4q (ArithIntL)
 };
 constexpr double kC52x15 = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer constant
 
 template <int BS>
 struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)
+  static constexpr bool kLoose = false;
   static constexpr bool kFP = false;
   __device__ static uint64_t load(uint64_t x) { return x; }
   __device__ static uint64_t store(uint64_t x) { return x; }
@@ -223,6 +225,7 @@ struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)
 };
 
 struct Arith52F {  // beta = 2^52 on the FP64 pipe (requires 4q < 2^52)
+  static constexpr bool kLoose = false;
   static constexpr bool kFP = true;
   __device__ static uint64_t load(uint64_t x) { return x | kDBias; }
   __device__ static uint64_t store(uint64_t xD) { return xD & kMask52; }
@@ -277,6 +280,7 @@ __device__ __forceinline__ double csubP(double y, double m) {
 }
 
 struct Arith52P {
+  static constexpr bool kLoose = false;
   static constexpr bool kFP = true;
   __device__ static uint64_t load(uint64_t x) { return as_u(__dsub_rn(as_d(x | kDBias), kC52)); }
   __device__ static uint64_t store(uint64_t x) { return as_u(__dadd_rn(as_d(x), kC52)) & kMask52; }
@@ -353,6 +357,7 @@ __device__ __forceinline__ double csubS(double y, double m) {
 }
 
 struct Arith52S {
+  static constexpr bool kLoose = false;
   static constexpr bool kFP = true;
   static constexpr bool kSigned = true;
   __device__ static uint64_t load(uint64_t x) { return as_u(__dsub_rn(as_d(x | kDBias), kC52)); }
@@ -398,6 +403,74 @@ struct Arith52S {
   }
 };
 
+// ---------------------------------------------------------------------------
+// ArithIntL: beta = 2^64 limbs with q < 2^61, canonical outputs only (fout ==
+// 1, like Arith52S for beta = 2^52).
+//
+// The Shoup quotient drops the low x low partial product and the carries of
+// the two cross products' low halves:
+//   qh = a1 b1 + hi32(a1 b0) + hi32(a0 b1)     (w' = a1:a0, x = b1:b0)
+// The dropped terms sum to less than 3 * 2^64, so qh = floor(w'x / 2^64) - d
+// with d in {0, 1, 2}, and T = w x - qh q (mod 2^64) = T_exact + d q lies in
+// [0, 4q). Cost: one IMAD.WIDE and two IMAD.HI instead of four IMAD.WIDE
+// (IMAD.WIDE issues at half the IMAD rate).
+// Ranges (8q < 2^64): forward words in [0, 8q): u = x0 reduced by 4q once
+// ([0, 4q)), x0' = u + T, x1' = u + 4q - T, both in [0, 8q). Inverse words
+// in [0, 4q): x0' = x0 + x1 reduced by 4q once, x1' = T(x0 + 4q - x1).
+// Representatives differ from the reference's lazy ones; canonical results
+// are identical (they are unique).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t qhat64_loose(uint64_t wp, uint64_t x) {
+  const uint32_t a0 = lo32(wp), a1 = hi32(wp), b0 = lo32(x), b1 = hi32(x);
+  const uint64_t cross = static_cast<uint64_t>(__umulhi(a1, b0)) + __umulhi(a0, b1);
+  return mad_wide(a1, b1, cross);
+}
+__device__ __forceinline__ uint64_t mul_loose(uint64_t x, uint64_t w, uint64_t wp, uint64_t negq) {
+  return lo_sum(w, x, qhat64_loose(wp, x), negq);
+}
+
+struct ArithIntL {
+  using Tw = ulonglong2;
+  static constexpr bool kFP = false;
+  static constexpr bool kSigned = false;
+  static constexpr bool kLoose = true;
+  __device__ static uint64_t load(uint64_t x) { return x; }
+  __device__ static uint64_t store(uint64_t x) { return x; }
+  // inputs below 4q (fin <= 4): the first stage's reduction is a value no-op
+  template <bool ILTM>
+  __device__ static void fwd(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+    const uint64_t u = ILTM ? x0 : nk::csub(x0, c.fourq);
+    const uint64_t t = mul_loose(x1, w.x, w.y, c.negq);
+    x0 = u + t;
+    x1 = u + c.fourq - t;
+  }
+  template <bool ILTM>
+  __device__ static void inv(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+    const uint64_t t = x0 + c.fourq - x1;
+    uint64_t s = x0 + x1;
+    if (!ILTM) s = nk::csub(s, c.fourq);
+    x0 = s;
+    x1 = mul_loose(t, w.x, w.y, c.negq);
+  }
+  __device__ static uint64_t scale_ninv(uint64_t x, const LimbConstDev& c) {
+    return mul_loose(x, c.ninv, c.ninvp, c.negq);
+  }
+  // [0, 8q) -> [0, q)
+  __device__ static uint64_t red8(uint64_t x, const LimbConstDev& c) {
+    return nk::csub(nk::csub(nk::csub(x, c.fourq), c.twoq), c.q);
+  }
+  // [0, 4q) -> [0, q)
+  __device__ static uint64_t red4(uint64_t x, const LimbConstDev& c) {
+    return nk::csub(nk::csub(x, c.twoq), c.q);
+  }
+  static constexpr bool kFold = true;
+  __device__ static void inv_fold(uint64_t& x0, uint64_t& x1, const LimbConstDev& c) {
+    const uint64_t s = x0 + x1, t = x0 + c.fourq - x1;  // both below 8q
+    x0 = red4(mul_loose(s, c.ninv, c.ninvp, c.negq), c);
+    x1 = red4(mul_loose(t, c.nw, c.nwp, c.negq), c);
+  }
+};
+
 // a * b mod q, canonical, for canonical integers a, b < q < 2^50 on the FP64
 // pipe: h + l = a b exactly (TwoProduct), k = round(h / q) through the
 // rounded reciprocal (|h/q - k| <= 0.75), r = h - k q + l exact in
@@ -419,7 +492,9 @@ __device__ __forceinline__ uint64_t mulmod_canon(uint64_t a, uint64_t b, const L
 // small_mod(x, q, 2) when fout == 1, ntt.hpp:303-305), as stored integers.
 template <class A>
 __device__ __forceinline__ uint64_t fwd_out(uint64_t x, const LimbConstDev& c, int fout) {
-  if constexpr (A::kSigned) {
+  if constexpr (A::kLoose) {
+    return A::red8(x, c);  // canonical-only policy
+  } else if constexpr (A::kSigned) {
     return A::canon(as_d(x), c);
   } else {
     return A::store(fout == 1 ? A::red4(x, c) : x);
@@ -428,7 +503,9 @@ __device__ __forceinline__ uint64_t fwd_out(uint64_t x, const LimbConstDev& c, i
 template <class A>
 __device__ __forceinline__ uint64_t inv_out(uint64_t x, const LimbConstDev& c, int fout) {
   const uint64_t y = A::scale_ninv(x, c);
-  if constexpr (A::kSigned) {
+  if constexpr (A::kLoose) {
+    return A::red4(y, c);  // canonical-only policy
+  } else if constexpr (A::kSigned) {
     return A::canon(as_d(y), c);
   } else {
     return A::store(fout == 1 ? A::red2(y, c) : y);
