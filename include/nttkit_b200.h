@@ -20,6 +20,8 @@
  *   nk_ntt_inverse[_host]   NttTables::inverse(result, operand, in, out)  ntt.hpp:289-306
  *                           (HEXL: NTT::ComputeInverse            PAPER.md:495-496)
  *   nk_eltwise_mult_mod[_host]  eltwise_mult_mod(r, a, b, Modulus, f)     eltwise.hpp:180-188
+ *   nk_eltwise_mult_mod_int[_host]    eltwise_mult_mod_int            eltwise.hpp:137-154
+ *   nk_eltwise_mult_mod_float[_host]  eltwise_mult_mod_float          eltwise.hpp:158-175
  *                           (HEXL: EltwiseMultMod                 PAPER.md:542-544)
  *   nk_eltwise_fma_mod[_host]   eltwise_fma_mod(r, a, y, z?, Modulus, f)  eltwise.hpp:263-271
  *                           and eltwise_fma_mod<B>                eltwise.hpp:231-259
@@ -122,8 +124,15 @@ int nk_poly_mult_mod(const nk_plan* plan, uint64_t* d_result, const uint64_t* d_
                      const uint64_t* d_g, uint32_t limb0, uint32_t nlimbs, uint32_t npolys,
                      void* stream);
 
+/* eltwise_mult_mod picks the path like the reference (eltwise.hpp:180-188): FP64
+ * (DFMA) for q < 2^50, integer Barrett otherwise; _int / _float force one path
+ * with that path's checks (eltwise.hpp:137-154 / 158-175). Results are identical. */
 int nk_eltwise_mult_mod(uint64_t* d_result, const uint64_t* d_a, const uint64_t* d_b,
                         uint64_t n, uint64_t q, uint64_t input_mod_factor, void* stream);
+int nk_eltwise_mult_mod_int(uint64_t* d_result, const uint64_t* d_a, const uint64_t* d_b,
+                            uint64_t n, uint64_t q, uint64_t input_mod_factor, void* stream);
+int nk_eltwise_mult_mod_float(uint64_t* d_result, const uint64_t* d_a, const uint64_t* d_b,
+                              uint64_t n, uint64_t q, uint64_t input_mod_factor, void* stream);
 /* d_z may be NULL (vector-scalar multiply). bit_shift: 0 = automatic, 52 or 64. */
 int nk_eltwise_fma_mod(uint64_t* d_result, const uint64_t* d_a, uint64_t y, const uint64_t* d_z,
                        uint64_t n, uint64_t q, uint64_t input_mod_factor, int bit_shift,
@@ -148,6 +157,10 @@ int nk_poly_mult_mod_host(const nk_plan* plan, uint64_t* result, const uint64_t*
                           uint32_t npolys, void* stream);
 int nk_eltwise_mult_mod_host(uint64_t* result, const uint64_t* a, const uint64_t* b, uint64_t n,
                              uint64_t q, uint64_t input_mod_factor, int device, void* stream);
+int nk_eltwise_mult_mod_int_host(uint64_t* result, const uint64_t* a, const uint64_t* b, uint64_t n,
+                                 uint64_t q, uint64_t input_mod_factor, int device, void* stream);
+int nk_eltwise_mult_mod_float_host(uint64_t* result, const uint64_t* a, const uint64_t* b, uint64_t n,
+                                   uint64_t q, uint64_t input_mod_factor, int device, void* stream);
 int nk_eltwise_fma_mod_host(uint64_t* result, const uint64_t* a, uint64_t y, const uint64_t* z,
                             uint64_t n, uint64_t q, uint64_t input_mod_factor, int bit_shift,
                             int device, void* stream);

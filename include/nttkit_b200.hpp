@@ -8,6 +8,8 @@
 //   NttTables::forward        ntt.hpp:268-285   NttTables::forward (host spans)
 //   NttTables::inverse        ntt.hpp:289-306   NttTables::inverse (host spans)
 //   eltwise_mult_mod          eltwise.hpp:180   eltwise_mult_mod
+//   eltwise_mult_mod_int      eltwise.hpp:137   eltwise_mult_mod_int
+//   eltwise_mult_mod_float    eltwise.hpp:158   eltwise_mult_mod_float
 //   eltwise_fma_mod           eltwise.hpp:263   eltwise_fma_mod (std::optional addend)
 //   poly_mult_mod             ring.hpp:28-43    poly_mult_mod
 //   HEXL: hexl::NTT{ComputeForward, ComputeInverse},
@@ -174,6 +176,24 @@ inline void eltwise_mult_mod(std::span<uint64_t> result, std::span<const uint64_
     throw std::invalid_argument("eltwise: operand lengths must match");
   check(nk_eltwise_mult_mod_host(result.data(), a.data(), b.data(), a.size(), m.value(),
                                  input_mod_factor, 0, nullptr));
+}
+
+inline void eltwise_mult_mod_int(std::span<uint64_t> result, std::span<const uint64_t> a,
+                                 std::span<const uint64_t> b, const Modulus& m,
+                                 uint64_t input_mod_factor) {
+  if (result.size() != a.size() || a.size() != b.size())
+    throw std::invalid_argument("eltwise: operand lengths must match");
+  check(nk_eltwise_mult_mod_int_host(result.data(), a.data(), b.data(), a.size(), m.value(),
+                                     input_mod_factor, 0, nullptr));
+}
+
+inline void eltwise_mult_mod_float(std::span<uint64_t> result, std::span<const uint64_t> a,
+                                   std::span<const uint64_t> b, const Modulus& m,
+                                   uint64_t input_mod_factor) {
+  if (result.size() != a.size() || a.size() != b.size())
+    throw std::invalid_argument("eltwise: operand lengths must match");
+  check(nk_eltwise_mult_mod_float_host(result.data(), a.data(), b.data(), a.size(), m.value(),
+                                       input_mod_factor, 0, nullptr));
 }
 
 inline void eltwise_fma_mod(std::span<uint64_t> result, std::span<const uint64_t> a, uint64_t y,

@@ -14,6 +14,8 @@ this module                    reference (/root/reference/proj/include/nttkit/)
 ``NttTables.forward``          ``NttTables::forward`` ntt.hpp:268-285
 ``NttTables.inverse``          ``NttTables::inverse`` ntt.hpp:289-306
 ``eltwise_mult_mod``           eltwise.hpp:180-188
+``eltwise_mult_mod_int``       eltwise.hpp:137-154
+``eltwise_mult_mod_float``     eltwise.hpp:158-175
 ``eltwise_fma_mod``            eltwise.hpp:263-271 (``z=None``: vector-scalar)
 ``eltwise_add_mod`` / ``_neg`` eltwise.hpp:47-70
 ``poly_mult_mod``              ring.hpp:28-43
@@ -68,6 +70,8 @@ _SIGS = {
                                            u64, vp]),
     "nk_poly_mult_mod": (C.c_int, [vp, vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, vp]),
     "nk_eltwise_mult_mod": (C.c_int, [vp, vp, vp, u64, u64, u64, vp]),
+    "nk_eltwise_mult_mod_int": (C.c_int, [vp, vp, vp, u64, u64, u64, vp]),
+    "nk_eltwise_mult_mod_float": (C.c_int, [vp, vp, vp, u64, u64, u64, vp]),
     "nk_eltwise_fma_mod": (C.c_int, [vp, vp, u64, vp, u64, u64, u64, C.c_int, vp]),
     "nk_eltwise_add_mod": (C.c_int, [vp, vp, vp, u64, u64, vp]),
     "nk_eltwise_neg_mod": (C.c_int, [vp, vp, u64, u64, vp]),
@@ -78,6 +82,8 @@ _SIGS = {
     "nk_poly_mult_mod_host": (C.c_int, [vp, vp, vp, vp, u64, C.c_uint32, C.c_uint32, C.c_uint32,
                                         vp]),
     "nk_eltwise_mult_mod_host": (C.c_int, [vp, vp, vp, u64, u64, u64, C.c_int, vp]),
+    "nk_eltwise_mult_mod_int_host": (C.c_int, [vp, vp, vp, u64, u64, u64, C.c_int, vp]),
+    "nk_eltwise_mult_mod_float_host": (C.c_int, [vp, vp, vp, u64, u64, u64, C.c_int, vp]),
     "nk_eltwise_fma_mod_host": (C.c_int, [vp, vp, u64, vp, u64, u64, u64, C.c_int, C.c_int, vp]),
 }
 
@@ -383,24 +389,43 @@ def _device_of_default():
         return 0
 
 
-def eltwise_mult_mod(result, a, b, m, input_mod_factor=1, stream=None):
-    """result[i] = a[i]*b[i] mod q; inputs in [0, input_mod_factor*q) (eltwise.hpp:180-188)."""
+def _eltwise_mult(path, result, a, b, m, input_mod_factor, stream):
     q = _q_of(m)
+    dev_fn, host_fn = {
+        "auto": ("nk_eltwise_mult_mod", "nk_eltwise_mult_mod_host"),
+        "int": ("nk_eltwise_mult_mod_int", "nk_eltwise_mult_mod_int_host"),
+        "float": ("nk_eltwise_mult_mod_float", "nk_eltwise_mult_mod_float_host"),
+    }[path]
     if _is_torch(a):
         if not (a.numel() == b.numel() == result.numel()):
             raise ValueError("eltwise: operand lengths must match")
         st = _stream_of(a) if stream is None else C.c_void_p(stream)
-        _check(lib().nk_eltwise_mult_mod(_dev_ptr(result), _dev_ptr(a), _dev_ptr(b), a.numel(), q,
-                                         int(input_mod_factor), st))
+        _check(getattr(lib(), dev_fn)(_dev_ptr(result), _dev_ptr(a), _dev_ptr(b), a.numel(), q,
+                                      int(input_mod_factor), st))
         return result
     aa, bb = _host_arr(a, "a"), _host_arr(b, "b")
     out = np.empty_like(aa) if result is None else result
     if not (aa.size == bb.size == out.size):
         raise ValueError("eltwise: operand lengths must match")
-    _check(lib().nk_eltwise_mult_mod_host(_hp(out), _hp(aa), _hp(bb), aa.size, q,
-                                          int(input_mod_factor), _device_of_default(),
-                                          None if stream is None else C.c_void_p(stream)))
+    _check(getattr(lib(), host_fn)(_hp(out), _hp(aa), _hp(bb), aa.size, q, int(input_mod_factor),
+                                   _device_of_default(), None if stream is None else C.c_void_p(stream)))
     return out
+
+
+def eltwise_mult_mod(result, a, b, m, input_mod_factor=1, stream=None):
+    """result[i] = a[i]*b[i] mod q; inputs in [0, input_mod_factor*q) (eltwise.hpp:180-188:
+    the FP64 path for q < 2^50, the integer path otherwise)."""
+    return _eltwise_mult("auto", result, a, b, m, input_mod_factor, stream)
+
+
+def eltwise_mult_mod_int(result, a, b, m, input_mod_factor=1, stream=None):
+    """The integer-Barrett path (eltwise.hpp:137-154); requires input_mod_factor*q < 2^63."""
+    return _eltwise_mult("int", result, a, b, m, input_mod_factor, stream)
+
+
+def eltwise_mult_mod_float(result, a, b, m, input_mod_factor=1, stream=None):
+    """The FP64 path (eltwise.hpp:158-175); requires q < 2^50."""
+    return _eltwise_mult("float", result, a, b, m, input_mod_factor, stream)
 
 
 def eltwise_fma_mod(result, a, y, z, m, input_mod_factor=1, bit_shift=0, stream=None):

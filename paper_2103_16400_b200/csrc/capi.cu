@@ -910,14 +910,70 @@ int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const u
 // element-wise (single modulus)
 // ---------------------------------------------------------------------------
 namespace {
-// Modulus(q) plus the dispatch of eltwise.hpp:180-188 and the checks of the path it picks
-int validate_mult(uint64_t q, uint64_t fin, nk::host::Modulus* m) {
+// element-wise multiply paths: the dispatch of eltwise.hpp:180-188 (FP64 for
+// q < 2^50, else integer Barrett) or one path forced, as the reference's
+// eltwise_mult_mod_int / eltwise_mult_mod_float (eltwise.hpp:137-175)
+enum MultPath { kMultAuto = 0, kMultInt = 1, kMultFloat = 2 };
+constexpr uint64_t kFloatPathBound = uint64_t{1} << 50;  // eltwise.hpp:132
+
+MultPath resolve_path(MultPath path, uint64_t q) {
+  return path != kMultAuto ? path : (q < kFloatPathBound ? kMultFloat : kMultInt);
+}
+
+// Modulus(q) plus the checks of the path that runs (eltwise.hpp:141-146, 162-167)
+int validate_mult(uint64_t q, uint64_t fin, nk::host::Modulus* m, MultPath path = kMultAuto) {
   if (!valid_modulus(q, m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (fin != 1 && fin != 2 && fin != 4)
     return fail(NK_ERR_MULT_FACTOR, "eltwise_mult_mod: input_mod_factor must be 1, 2 or 4");
-  if (q >= (uint64_t{1} << 50) && u128{fin} * q >= (u128{1} << 63))
+  path = resolve_path(path, q);
+  if (path == kMultInt && u128{fin} * q >= (u128{1} << 63))
     return fail(NK_ERR_MULT_INT_RANGE, "eltwise_mult_mod_int: requires input_mod_factor*q < 2^63");
+  if (path == kMultFloat && q >= kFloatPathBound)
+    return fail(NK_ERR_MULT_FLOAT_RANGE, "eltwise_mult_mod_float: requires q < 2^50");
   return 0;
+}
+
+int launch_mult_float(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q, int fin,
+                      cudaStream_t st) {
+  nk::LimbConstDev c{};
+  c.q = q;
+  c.q_d = static_cast<double>(q);
+  c.qinv = 1.0 / static_cast<double>(q);
+  c.q_bias = static_cast<double>(q) + 4503599627370496.0;
+  const int vec = vec_of({r, a, b});
+  cudaError_t e;
+#define NK_MFV(F, V)                                                                                    \
+  e = launch_pdl(nk::eltwise_mult_float_kernel<F, V>,                                                   \
+                 eltwise_grid(n / V + 1, reinterpret_cast<const void*>(nk::eltwise_mult_float_kernel<F, V>)), \
+                 256, st, r, a, b, n, c)
+#define NK_MF(F)                 \
+  if (vec == 4) NK_MFV(F, 4);    \
+  else if (vec == 2) NK_MFV(F, 2); \
+  else NK_MFV(F, 1)
+  switch (fin) {
+    case 1: NK_MF(1); break;
+    case 2: NK_MF(2); break;
+    default: NK_MF(4); break;
+  }
+#undef NK_MF
+#undef NK_MFV
+  g_launches++;
+  if (e != cudaSuccess) return cuda_fail(e, "eltwise_mult_float_kernel launch");
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int eltwise_mult_path(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
+                      uint64_t fin, MultPath path, void* stream) {
+  nk::host::Modulus m;
+  if (int rc = validate_mult(q, fin, &m, path)) return rc;
+  if (n == 0) return 0;
+  if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_mult_mod: NULL buffer");
+  if (resolve_path(path, q) == kMultFloat)
+    return launch_mult_float(res, a, b, n, q, static_cast<int>(fin), S(stream));
+  const nk::MultConst c{q, 2 * q, m.barrett, m.bits - 1, static_cast<int>(fin)};
+  return launch_mult(res, a, b, n, 0, c, nullptr, 1, static_cast<int>(fin), q < (uint64_t{1} << 61),
+                     S(stream));
 }
 
 // eltwise.hpp:236-251 (+ the automatic width of eltwise.hpp:263-271); *bs receives the width
@@ -939,13 +995,17 @@ int validate_fma(uint64_t q, uint64_t y, uint64_t fin, int bit_shift, int* bs) {
 
 int nk_eltwise_mult_mod(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
                         uint64_t fin, void* stream) {
-  nk::host::Modulus m;
-  if (int rc = validate_mult(q, fin, &m)) return rc;
-  if (n == 0) return 0;
-  if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_mult_mod: NULL buffer");
-  const nk::MultConst c{q, 2 * q, m.barrett, m.bits - 1, static_cast<int>(fin)};
-  return launch_mult(res, a, b, n, 0, c, nullptr, 1, static_cast<int>(fin), q < (uint64_t{1} << 61),
-                     S(stream));
+  return eltwise_mult_path(res, a, b, n, q, fin, kMultAuto, stream);
+}
+
+int nk_eltwise_mult_mod_int(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
+                            uint64_t fin, void* stream) {
+  return eltwise_mult_path(res, a, b, n, q, fin, kMultInt, stream);
+}
+
+int nk_eltwise_mult_mod_float(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
+                              uint64_t fin, void* stream) {
+  return eltwise_mult_path(res, a, b, n, q, fin, kMultFloat, stream);
 }
 
 int nk_eltwise_fma_mod(uint64_t* res, const uint64_t* a, uint64_t y, const uint64_t* z, uint64_t n,
@@ -1176,17 +1236,32 @@ int nk_poly_mult_mod_host(const nk_plan* p, uint64_t* res, const uint64_t* f, co
                        });
 }
 
-int nk_eltwise_mult_mod_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n,
-                             uint64_t q, uint64_t fin, int device, void* stream) {
+namespace {
+int eltwise_mult_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
+                      uint64_t fin, MultPath path, int device, void* stream) {
   if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_mult_mod: NULL buffer");
   nk::host::Modulus m;
-  if (int rc = validate_mult(q, fin, &m)) return rc;
+  if (int rc = validate_mult(q, fin, &m, path)) return rc;
   if (n == 0) return 0;
   if (int rc = ensure_device(device)) return rc;
   return run_pipelined(device, S(stream), n, 1, {a, b}, res,
                        [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
-                         return nk_eltwise_mult_mod(d[0], d[0], d[1], nu, q, fin, st);
+                         return eltwise_mult_path(d[0], d[0], d[1], nu, q, fin, path, st);
                        });
+}
+}  // namespace
+
+int nk_eltwise_mult_mod_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n,
+                             uint64_t q, uint64_t fin, int device, void* stream) {
+  return eltwise_mult_host(res, a, b, n, q, fin, kMultAuto, device, stream);
+}
+int nk_eltwise_mult_mod_int_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n,
+                                 uint64_t q, uint64_t fin, int device, void* stream) {
+  return eltwise_mult_host(res, a, b, n, q, fin, kMultInt, device, stream);
+}
+int nk_eltwise_mult_mod_float_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n,
+                                   uint64_t q, uint64_t fin, int device, void* stream) {
+  return eltwise_mult_host(res, a, b, n, q, fin, kMultFloat, device, stream);
 }
 
 int nk_eltwise_fma_mod_host(uint64_t* res, const uint64_t* a, uint64_t y, const uint64_t* z,

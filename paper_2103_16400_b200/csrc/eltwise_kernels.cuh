@@ -142,6 +142,33 @@ __global__ void __launch_bounds__(256, FIN == 1 ? 6 : 4) eltwise_mult_kernel(uin
     for (uint64_t k = chunks * VEC; k < total; ++k) r[k] = mult_barrett<FIN, SMALLQ>(a[k], b[k], cst(k));
 }
 
+// eltwise_mult_mod_float (eltwise.hpp:158-175, loop 106-125) for q < 2^50 on
+// the FP64 pipe: small_mod both inputs, then mulmod_canon (modmath.cuh):
+// TwoProduct h + l = x y, quotient round(h / q) through the rounded reciprocal,
+// r = (h - k q) + l exact, one correction. The reference takes floor(h u) with
+// u = 1/q rounded up and corrects in both directions; the canonical product is
+// unique, so the words are the same.
+template <int FIN, int VEC>
+__global__ void __launch_bounds__(256, 6) eltwise_mult_float_kernel(uint64_t* __restrict__ r,
+                                                                    const uint64_t* __restrict__ a,
+                                                                    const uint64_t* __restrict__ b,
+                                                                    uint64_t total, LimbConstDev c) {
+  pdl_enter();
+  const uint64_t chunks = total / VEC;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < chunks; i += stride) {
+    const WordVec<VEC> x = ld_stream<VEC>(a + i * VEC), y = ld_stream<VEC>(b + i * VEC);
+    WordVec<VEC> o;
+#pragma unroll
+    for (int k = 0; k < VEC; ++k)
+      o.w[k] = mulmod_canon(small_mod(x.w[k], c.q, FIN), small_mod(y.w[k], c.q, FIN), c);
+    st_stream<VEC>(r + i * VEC, o);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (uint64_t k = chunks * VEC; k < total; ++k)
+      r[k] = mulmod_canon(small_mod(a[k], c.q, FIN), small_mod(b[k], c.q, FIN), c);
+}
+
 struct FmaConst {
   uint64_t q, y, ybarr;
   int32_t fin, bs;

@@ -133,6 +133,14 @@ def test_eltwise_errors_before_device(nk):
         nk.eltwise_fma_mod(None, np.zeros(4, np.uint64), 1, None, q50, 8, bit_shift=52)
     with pytest.raises(ValueError, match="operand lengths must match"):
         nk.eltwise_mult_mod(None, np.zeros(8, np.uint64), np.zeros(7, np.uint64), q50, 1)
+    # the explicit paths carry their own checks (eltwise.hpp:144-146, 165-167)
+    q60 = smallest_ntt_primes(60, 1, 1)[0]
+    with pytest.raises(ValueError, match=re.escape("eltwise_mult_mod_float: requires q < 2^50")):
+        nk.eltwise_mult_mod_float(None, np.zeros(8, np.uint64), np.zeros(8, np.uint64), q60, 1)
+    with pytest.raises(ValueError, match=re.escape("eltwise_mult_mod_int: requires input_mod_factor*q < 2^63")):
+        nk.eltwise_mult_mod_int(None, np.zeros(8, np.uint64), np.zeros(8, np.uint64), q62, 4)
+    with pytest.raises(ValueError, match="input_mod_factor must be 1, 2 or 4"):
+        nk.eltwise_mult_mod_float(None, np.zeros(8, np.uint64), np.zeros(8, np.uint64), q50, 8)
 
 
 def test_no_cpu_fallback_without_device(nk):

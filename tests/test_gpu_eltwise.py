@@ -56,6 +56,24 @@ def test_mult_matches_oracle(nk, oracle, q, fin, n):
         assert np.array_equal(want, oracle.eltwise_mult_mod(a, b, q, fin, path=1))
 
 
+@pytest.mark.parametrize("q", [17, 97] + [primes_with_bits(b, 1)[0] for b in (20, 30, 49, 50)])
+@pytest.mark.parametrize("fin", [1, 2, 4])
+@pytest.mark.parametrize("n", [1, 5, 4097])
+def test_mult_explicit_paths(nk, oracle, q, fin, n):
+    """eltwise_mult_mod_int / _float (eltwise.hpp:137-175): both paths give the
+    reference's words wherever they apply."""
+    a = sample_inputs(oracle, q, fin, n, 31 + n)
+    b = sample_inputs(oracle, q, fin, n, 32 + n)
+    want = oracle.eltwise_mult_mod(a, b, q, fin)
+    for fn in (nk.eltwise_mult_mod_int, nk.eltwise_mult_mod_float):
+        if fn is nk.eltwise_mult_mod_float and q >= (1 << 50):
+            continue
+        r = torch.empty(n, dtype=torch.int64, device="cuda")
+        fn(r, dev(a), dev(b), q, fin)
+        assert np.array_equal(host(r), want), fn.__name__
+        assert np.array_equal(fn(None, a, b, q, fin), want), fn.__name__ + " (host buffers)"
+
+
 def test_float_path_correction_cases(nk, oracle):
     """test_eltwise.cpp:117-133: quotient estimate overshoot triples."""
     cases = [(1125899906842597, 1006683697935267, 1120468225943409),

@@ -78,6 +78,17 @@ def main():
         us = 1e3 * timed(step, 20, 3) / sets
         out.append({"cfg": 2, "op": name, "us_per_call": us, "GB_s": bpw * n2 / us / 1e3})
     del a, c, r
+    # f-3: the two multiply paths at q < 2^50 (the reference takes the FP64 one)
+    q50 = largest_ntt_primes(50, 2, 1)[0]
+    a = torch.stack([rnd(n2, q50, gen) for _ in range(sets)])
+    c = torch.stack([rnd(n2, q50, gen) for _ in range(sets)])
+    r = torch.empty_like(a)
+    for name, fn in (("int", nk.eltwise_mult_mod_int), ("float", nk.eltwise_mult_mod_float)):
+        step = graphed(lambda: [fn(r[i], a[i], c[i], q50, 1) for i in range(sets)])
+        us = 1e3 * timed(step, 20, 3) / sets
+        out.append({"cfg": "2b", "op": f"EltwiseMultMod 50-bit q, {name} path", "us_per_call": us,
+                    "GB_s": 24 * n2 / us / 1e3})
+    del a, c, r
     # cfg3
     n = 16384
     m3 = largest_ntt_primes(50, n, 32)
