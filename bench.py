@@ -245,6 +245,38 @@ def modmul_bench(stream, reps=20):
             "timing": "one CUDA graph of 16 back-to-back calls (programmatic dependent launch)"}
 
 
+def pcie_probe(reps=4, nbytes=256 << 20):
+    """Pinned-memory PCIe bandwidth on this box: H2D, D2H and both at once
+    (GB/s per direction) -- the ceiling of the e2e number."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    h2 = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d2 = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def rate(fn):
+        fn()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        return reps * nbytes / (time.perf_counter() - t0) / 1e9
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+
+    out = {"h2d_gbs": rate(lambda: d.copy_(h, non_blocking=True)),
+           "d2h_gbs": rate(lambda: h2.copy_(d2, non_blocking=True)),
+           "duplex_gbs_per_direction": rate(both)}
+    del h, h2, d, d2
+    return out
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -340,6 +372,11 @@ def run_gpu(args):
         e2e_s = float(t.item())
     e2e_value = coeffs_step / e2e_s / 1e6
 
+    pcie = pcie_probe() if rank == 0 else None
+    if pcie:
+        # each step moves 2 x 8 B/coeff each way per direction-op: the duplex ceiling
+        pcie["e2e_ceiling_mcoeff_s"] = coeffs_step / (2 * 8 * words / (pcie["duplex_gbs_per_direction"] * 1e9)) / 1e6
+
     hbm, smmax, peak_kind = peaks()
     # dominant kernel: the forward block kernel (one launch per forward)
     fwd_bytes = 16 * words  # read + write each coefficient once
@@ -391,7 +428,8 @@ def run_gpu(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "Mcoeff/s", "h2d_bytes_per_step": 2 * 8 * words,
                     "d2h_bytes_per_step": 2 * 8 * words,
-                    "path": "nk_ntt_forward_host + nk_ntt_inverse_host (pinned host buffers; chunked upload / compute / download pipeline, 4 PCIe transfers of 256 MiB per step)"},
+                    "path": "nk_ntt_forward_host + nk_ntt_inverse_host (pinned host buffers; chunked upload / compute / download pipeline, 4 PCIe transfers of 256 MiB per step)",
+                    "pcie": pcie},
             "gpu_launches": launches, "clocks": clocks,
             "modmul": modmul,
         }

@@ -27,3 +27,24 @@ fi
 cat $O/status
 tail -3 $O/pytest_gpu.log
 cat $O/bench.json $O/bench_ref.json
+# all-config device times, and the launch list of the cfg4 / cfg5 kernels
+timeout 300 python tools/time_cfgs.py > $O/cfgs.jsonl 2>&1; echo "cfgs=$?" | tee -a $O/status
+if [ "${SKIP_NCU:-0}" = "0" ]; then
+  timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__issue_active.avg.pct_of_peak_sustained_active --clock-control none --csv \
+      --log-file $O/launches_cfg4.csv python tools/prof_ntt.py --n 65536 --limbs 24 --polys 16 --bits 60 --fin 4 --iters 1 > $O/ncu_cfg4.log 2>&1
+  timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+      --log-file $O/launches_cfg5.csv python tools/prof_ntt.py --n 16384 --limbs 16 --polys 128 --op poly --iters 1 > $O/ncu_cfg5.log 2>&1
+  echo "ncu_cfg45=$?" | tee -a $O/status
+fi
+cat $O/cfgs.jsonl
+# keep the merge-back under gpurun's 64 MiB cap: text exports of every report,
+# the binary reports only when small
+for r in $O/*.ncu-rep; do
+  [ -f "$r" ] || continue
+  ncu -i "$r" --page raw --csv > "${r%.ncu-rep}_raw.csv" 2>/dev/null
+  ncu -i "$r" --page details --csv > "${r%.ncu-rep}_details.csv" 2>/dev/null
+  ncu -i "$r" --page source --csv --print-source sass > "${r%.ncu-rep}_source.csv" 2>/dev/null
+  gzip -f "${r%.ncu-rep}_source.csv"
+  [ $(stat -c %s "$r") -gt 15000000 ] && rm -f "$r"
+done
+du -sh $O

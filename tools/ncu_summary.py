@@ -1,8 +1,12 @@
 #!/usr/bin/env python
-"""Print the key metrics of an ncu report (run here, on the CPU box)."""
+"""Print the key metrics of an ncu report (run here, on the CPU box), or of
+its `--page raw --csv` export (tools/gpu_check.sh writes *_raw.csv)."""
 import csv, subprocess, sys
 rep = sys.argv[1]
-out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep.endswith(".csv"):
+    out = open(rep).read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 r = list(csv.reader(out.splitlines()))
 hdr, units = r[0], r[1]
 keys = ['Kernel Name', 'gpu__time_duration.sum', 'sm__throughput.avg.pct_of_peak_sustained_elapsed',
