@@ -612,18 +612,21 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cu
   return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
-template <int FIN, bool SMALLQ, bool BATCHED>
+template <int FIN, bool LOOSE, bool BATCHED>
 cudaError_t launch_mult_t(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t total, uint32_t logn,
                           nk::MultConst c0, const nk::MultConst* consts, uint32_t nlimbs, cudaStream_t st) {
   const int vec = vec_of({r, a, b});
 #define NK_MV(V)                                                                                          \
-  return launch_pdl(nk::eltwise_mult_kernel<FIN, SMALLQ, BATCHED, V>, eltwise_grid(total / V + 1, reinterpret_cast<const void*>(nk::eltwise_mult_kernel<FIN, SMALLQ, BATCHED, V>)), 256, st, \
+  return launch_pdl(nk::eltwise_mult_kernel<FIN, LOOSE, BATCHED, V>, eltwise_grid(total / V + 1, reinterpret_cast<const void*>(nk::eltwise_mult_kernel<FIN, LOOSE, BATCHED, V>)), 256, st, \
                     r, a, b, total, logn, c0, consts, nlimbs)
   if (vec == 4) NK_MV(4);
   if (vec == 2) NK_MV(2);
   NK_MV(1);
 #undef NK_MV
 }
+
+// loose Barrett quotients (eltwise_kernels.cuh) need 5q < 2^63
+bool loose_barrett(uint64_t q) { return u128{5} * q < (u128{1} << 63); }
 
 int launch_mult(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t total, uint32_t logn,
                 nk::MultConst c0, const nk::MultConst* consts, uint32_t nlimbs, int fin, bool small,
@@ -859,7 +862,7 @@ int nk_plan_eltwise_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* a,
   const int fi = fin == 1 ? 0 : (fin == 2 ? 1 : 2);
   const uint64_t rows = static_cast<uint64_t>(npolys) * nlimbs;
   bool small = true;
-  for (uint32_t l = 0; l < nlimbs; ++l) small &= p->q[limb0 + l] < (uint64_t{1} << 61);
+  for (uint32_t l = 0; l < nlimbs; ++l) small &= loose_barrett(p->q[limb0 + l]);
   return launch_mult(res, a, b, rows * p->n, p->logn, nk::MultConst{}, p->mc[fi] + limb0, nlimbs,
                      static_cast<int>(fin), small, S(stream));
 }
@@ -972,8 +975,7 @@ int eltwise_mult_path(uint64_t* res, const uint64_t* a, const uint64_t* b, uint6
   if (resolve_path(path, q) == kMultFloat)
     return launch_mult_float(res, a, b, n, q, static_cast<int>(fin), S(stream));
   const nk::MultConst c{q, 2 * q, m.barrett, m.bits - 1, static_cast<int>(fin)};
-  return launch_mult(res, a, b, n, 0, c, nullptr, 1, static_cast<int>(fin), q < (uint64_t{1} << 61),
-                     S(stream));
+  return launch_mult(res, a, b, n, 0, c, nullptr, 1, static_cast<int>(fin), loose_barrett(q), S(stream));
 }
 
 // eltwise.hpp:236-251 (+ the automatic width of eltwise.hpp:263-271); *bs receives the width

@@ -28,17 +28,22 @@ __device__ __forceinline__ uint64_t csub63(uint64_t x, uint64_t m) {
   return (static_cast<int32_t>(hi32(d)) < 0) ? x : d;
 }
 
-// mult_mod_int_loop<F> body (eltwise.hpp:82-90). SMALLQ: q < 2^61, so every
-// intermediate of the tail is below 2^63 and the cheaper sign test applies.
-template <int FIN, bool SMALLQ>
+// mult_mod_int_loop<F> body (eltwise.hpp:82-90). LOOSE (5q < 2^63): the
+// Barrett quotient c3 = mulhi(c1, k) takes three of the four 32-bit partial
+// products (qhat64_loose, modmath.cuh: floor minus 0..2), so c4 < 5q and one
+// more conditional subtraction follows; every intermediate stays below 2^63
+// and the sign test on the high word suffices. The canonical product is
+// unique, so the words are the reference's.
+template <int FIN, bool LOOSE>
 __device__ __forceinline__ uint64_t mult_barrett(uint64_t a, uint64_t b, const MultConst& c) {
   const uint64_t x = small_mod(a, c.q, FIN);
   const uint64_t y = small_mod(b, c.q, FIN);
   const uint64_t plo = x * y, phi = __umul64hi(x, y);
   const uint64_t c1 = (plo >> c.shift) | (phi << (64 - c.shift));  // shift in [1, 61]
-  const uint64_t c3 = __umul64hi(c1, c.barrett);
-  uint64_t c4 = plo - c3 * c.q;  // true value < 3q, wraps exactly
-  if (SMALLQ) {
+  const uint64_t c3 = LOOSE ? qhat64_loose(c1, c.barrett) : __umul64hi(c1, c.barrett);
+  uint64_t c4 = plo - c3 * c.q;  // true value < 3q (exact) / 5q (loose), wraps exactly
+  if (LOOSE) {
+    c4 = csub63(c4, c.twoq << 1);
     c4 = csub63(c4, c.twoq);
     c4 = csub63(c4, c.q);
   } else {
@@ -100,7 +105,7 @@ __device__ __forceinline__ void pdl_enter() {
 // more, smaller CTAs start streaming sooner and drain faster than fewer CTAs
 // with deeper per-thread batches (tools/elt_probe.cu: 5.6 vs 6.2 us per call).
 constexpr int kU = 1;
-template <int FIN, bool SMALLQ, bool BATCHED, int VEC>
+template <int FIN, bool LOOSE, bool BATCHED, int VEC>
 __global__ void __launch_bounds__(256, FIN == 1 ? 6 : 4) eltwise_mult_kernel(uint64_t* __restrict__ r,
                                                            const uint64_t* __restrict__ a,
                                                            const uint64_t* __restrict__ b,
@@ -133,13 +138,13 @@ __global__ void __launch_bounds__(256, FIN == 1 ? 6 : 4) eltwise_mult_kernel(uin
         const MultConst c = cst(i * VEC);
 #pragma unroll
         for (int k = 0; k < VEC; ++k)
-          o.w[k] = mult_barrett<FIN, SMALLQ>(x[u].w[k], y[u].w[k], one_row ? c : cst(i * VEC + k));
+          o.w[k] = mult_barrett<FIN, LOOSE>(x[u].w[k], y[u].w[k], one_row ? c : cst(i * VEC + k));
         st_stream<VEC>(r + i * VEC, o);
       }
     }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0)
-    for (uint64_t k = chunks * VEC; k < total; ++k) r[k] = mult_barrett<FIN, SMALLQ>(a[k], b[k], cst(k));
+    for (uint64_t k = chunks * VEC; k < total; ++k) r[k] = mult_barrett<FIN, LOOSE>(a[k], b[k], cst(k));
 }
 
 // eltwise_mult_mod_float (eltwise.hpp:158-175, loop 106-125) for q < 2^50 on
@@ -179,8 +184,14 @@ template <int BS, bool HAS_Z, int FIN>
 __device__ __forceinline__ uint64_t fma_one(uint64_t a, uint64_t z, const FmaConst& c) {
   // q < 2^61 (eltwise.hpp:243-245): every value below is < 2^63
   const uint64_t x = small_mod(a, c.q, FIN);
-  const uint64_t qh = (BS == 52) ? qhat52(c.ybarr, x) : __umul64hi(x, c.ybarr);
-  uint64_t v = x * c.y - qh * c.q;  // in [0, 2q)
+  // beta = 2^64 with an addend: the loose quotient (qhat64_loose, floor minus
+  // 0..2) leaves v in [0, 4q) < 2^63 for one more conditional subtraction
+  // (cfg2 FMA 5.51 -> 5.27 us; the one-stream vector-scalar form measured
+  // 4.28 -> 4.36 us with it, so it keeps the exact quotient)
+  constexpr bool kLoose = (BS == 64) && HAS_Z;
+  const uint64_t qh = (BS == 52) ? qhat52(c.ybarr, x) : (kLoose ? qhat64_loose(c.ybarr, x) : __umul64hi(x, c.ybarr));
+  uint64_t v = x * c.y - qh * c.q;  // in [0, 2q) / [0, 4q) (loose)
+  if (kLoose) v = csub63(v, 2 * c.q);
   v = csub63(v, c.q);
   if (HAS_Z) {
     v += small_mod(z, c.q, FIN);
