@@ -74,6 +74,29 @@ def test_mult_explicit_paths(nk, oracle, q, fin, n):
         assert np.array_equal(fn(None, a, b, q, fin), want), fn.__name__ + " (host buffers)"
 
 
+def _prime_near(oracle, x, step):
+    c = x | 1
+    while not oracle.is_prime(c):
+        c += step
+    return c
+
+
+@pytest.mark.parametrize("fin", [1, 2, 4])
+def test_mult_loose_barrett_boundary(nk, oracle, fin):
+    """The integer multiply takes loose Barrett quotients for 5q < 2^63 and the
+    exact ones above: primes on both sides of 2^63 / 5, boundary-heavy inputs."""
+    edge = (1 << 63) // 5
+    for q in (_prime_near(oracle, edge, -2), _prime_near(oracle, edge + 2, 2)):
+        if fin * q >= (1 << 63):
+            continue
+        n = 4099
+        a = sample_inputs(oracle, q, fin, n, 41)
+        b = sample_inputs(oracle, q, fin, n, 42)
+        r = torch.empty(n, dtype=torch.int64, device="cuda")
+        nk.eltwise_mult_mod(r, dev(a), dev(b), q, fin)
+        assert np.array_equal(host(r), oracle.eltwise_mult_mod(a, b, q, fin)), hex(q)
+
+
 def test_float_path_correction_cases(nk, oracle):
     """test_eltwise.cpp:117-133: quotient estimate overshoot triples."""
     cases = [(1125899906842597, 1006683697935267, 1120468225943409),
@@ -96,7 +119,7 @@ def test_mult_identities(nk, oracle):
     assert np.all(nk.eltwise_mult_mod(None, top, top, q, 1) == 1)
 
 
-FMA_QS = [17] + [primes_with_bits(b, 1)[0] for b in (20, 30, 48, 50, 60)]
+FMA_QS = [17] + [primes_with_bits(b, 1)[0] for b in (20, 30, 48, 50, 60)] + [(1 << 61) - 1]  # 2^61 - 1: largest allowed q
 
 
 @pytest.mark.parametrize("q", FMA_QS)

@@ -260,3 +260,17 @@ def test_block_sizes_large_batches(nk, oracle, logn, arith):
     moduli = largest_ntt_primes(50, n, 3)
     check_dir(nk, oracle, n, moduli, 52, 700 + logn, fwd_factors=[(1, 1), (4, 4), (2, 1)],
               inv_factors=[(1, 1), (2, 2)])
+
+
+@pytest.mark.parametrize("logn", [12, 14, 15, 16])
+def test_loose_quotient_boundary(nk, oracle, logn):
+    """Canonical beta = 2^64 transforms take the loose-quotient policy
+    (ArithIntL) for q < 2^61 and the exact one above: a plan holding the
+    largest 61-bit and the smallest 62-bit NTT primes runs both, limb by limb,
+    plus single-width plans of each."""
+    n = 1 << logn
+    q61 = largest_ntt_primes(61, n, 1)
+    q62 = smallest_ntt_primes(62, n, 1)
+    for moduli in (q61 + q62, q61, q62):
+        check_dir(nk, oracle, n, moduli, 1, 900 + logn,
+                  fwd_factors=[(1, 1), (4, 1)], inv_factors=[(1, 1), (2, 1)])
