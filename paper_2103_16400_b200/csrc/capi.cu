@@ -1109,9 +1109,15 @@ int host_depth() {
   return v;
 }
 
+// One pipeline (streams + ordering event) per device. Host-buffer calls from
+// several threads (the reference allows concurrent calls on shared tables,
+// ntt.hpp:203-205, test_ntt.cpp:349-375) take turns on it: they are
+// PCIe-bound, so serialising them costs no throughput, and the ordering event
+// is never re-recorded by one call while another waits on it.
 struct HostPipe {
   cudaStream_t s[kMaxDepth] = {};
   cudaEvent_t start = nullptr;
+  std::mutex mu;
 };
 
 int host_pipe(int dev, HostPipe** out) {
@@ -1138,6 +1144,7 @@ int run_pipelined(int dev, cudaStream_t user, uint64_t units, uint64_t unit_word
                   std::initializer_list<const uint64_t*> hin, uint64_t* hout, Fn&& fn) {
   HostPipe* hp = nullptr;
   if (int rc = host_pipe(dev, &hp)) return rc;
+  std::lock_guard<std::mutex> lock(hp->mu);
   const int nin = static_cast<int>(hin.size());
   const uint64_t unit_bytes = unit_words * 8;
   uint64_t per = host_chunk_bytes() / unit_bytes;

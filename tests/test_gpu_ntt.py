@@ -274,3 +274,45 @@ def test_loose_quotient_boundary(nk, oracle, logn):
     for moduli in (q61 + q62, q61, q62):
         check_dir(nk, oracle, n, moduli, 1, 900 + logn,
                   fwd_factors=[(1, 1), (4, 1)], inv_factors=[(1, 1), (2, 1)])
+
+
+def test_shared_tables_across_threads(nk, oracle):
+    """test_ntt.cpp:349-375: four threads transform through one shared plan,
+    50 times each; here both through the blocking host-buffer calls and
+    through device buffers on per-thread streams."""
+    import threading
+
+    n = 1024
+    q = smallest_ntt_primes(50, n, 1)[0]
+    plan = nk.RnsNtt(n, [q])
+    k = 4
+    inputs = [oracle.mt19937_64(1500 + i, n, q) for i in range(k)]
+    expected = [oracle.forward(n, [q], x, 1, 1) for x in inputs]
+    host_out = [np.zeros(n, np.uint64) for _ in range(k)]
+    dev_out = [None] * k
+    errors = []
+
+    def work(i):
+        try:
+            for _ in range(50):
+                plan.forward(host_out[i], inputs[i], 1, 1)
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                d = dev(inputs[i])
+                o = torch.empty_like(d)
+                for _ in range(50):
+                    plan.forward(o, d, 1, 1)
+                st.synchronize()
+                dev_out[i] = o.cpu().numpy().view(np.uint64)
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(k)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+    for i in range(k):
+        assert np.array_equal(host_out[i], expected[i])
+        assert np.array_equal(dev_out[i], expected[i])
