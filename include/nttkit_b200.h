@@ -180,7 +180,10 @@ void nk_debug_dump_to(uint64_t* d_buf);
 void nk_debug_exact_only(int on);
 /* Testing aid: which kernel transforms 16384-word blocks. -1 (default) = the
  * faster one per direction, 0 = the CTA-pair kernel, 1 = the single-CTA kernel,
- * 2 = the warp-per-item kernel (whole N = 16384 rows only). */
+ * 2 = the warp-per-item kernel (whole N = 16384 rows only), 4 = the staged
+ * warp-per-item forward, 5 = the 3-barrier inverse; 6 = defaults, but batches
+ * of 2^11..2^13-word rows smaller than the SM count take the plain block kernel
+ * instead of the latency kernel (ntt_block_lat). */
 void nk_debug_block_kernel(int which);
 
 #ifdef __cplusplus

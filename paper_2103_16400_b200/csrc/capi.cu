@@ -247,6 +247,7 @@ int launch_pair_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cud
   return 0;
 }
 
+bool g_no_lat = false;     // nk_debug_block_kernel(6): small batches take ntt_block instead of ntt_block_lat
 int g_block_kernel = -1;  // nk_debug_block_kernel(): -1 auto, 0 pair, 1 single, 2 warp, 4 staged warp (fwd), 5 3-barrier inverse
 
 // Warp-per-item kernel (ntt_warp.cuh) for whole 16384-word rows: persistent,
@@ -375,9 +376,40 @@ int launch_block_t(const nk::NttArgs& a, uint64_t grid, cudaStream_t st) {
   return 0;
 }
 
+// latency path (ntt_block_lat): programmatic dependent launch, twiddle row
+// staged into shared memory before griddepcontrol.wait
+template <int LOGB, int LOGV, class A, bool FWD, bool IL>
+int launch_block_lat_t(const nk::NttArgs& a, uint64_t grid, cudaStream_t st) {
+  constexpr size_t smem = nk::lat_smem_bytes<LOGB, LOGV>();
+  auto kern = nk::ntt_block_lat<LOGB, LOGV, A, FWD, IL>;
+  if (int rc = set_smem(kern, smem)) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(1u << (LOGB - LOGV));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  g_launches++;
+  if (e != cudaSuccess) return cuda_fail(e, "ntt_block_lat launch");
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
 template <class A, bool FWD>
 int launch_block(uint32_t logb, const nk::NttArgs& a, uint64_t grid, bool iltm, cudaStream_t st) {
   const bool small = a.rows < static_cast<uint64_t>(sm_count());
+  if (small && a.logn == logb && !g_no_lat) {  // whole rows, few of them: the latency path
+    switch (logb) {
+      case 11: return iltm ? launch_block_lat_t<11, 3, A, FWD, true>(a, grid, st) : launch_block_lat_t<11, 3, A, FWD, false>(a, grid, st);
+      case 12: return iltm ? launch_block_lat_t<12, 3, A, FWD, true>(a, grid, st) : launch_block_lat_t<12, 3, A, FWD, false>(a, grid, st);
+      default: return iltm ? launch_block_lat_t<13, 3, A, FWD, true>(a, grid, st) : launch_block_lat_t<13, 3, A, FWD, false>(a, grid, st);
+    }
+  }
 #define NK_LB2(L, V) \
   return iltm ? launch_block_t<L, V, A, FWD, true>(a, grid, st) : launch_block_t<L, V, A, FWD, false>(a, grid, st)
 #define NK_LB(L) \
@@ -662,7 +694,10 @@ const char* nk_version(void) { return "nttkit_b200 0.1 (sm_100a)"; }
 uint64_t nk_launch_count(void) { return g_launches.load(); }
 void nk_debug_dump_to(uint64_t* d_buf) { g_dbg = d_buf; }
 void nk_debug_exact_only(int on) { g_exact_only = on != 0; }
-void nk_debug_block_kernel(int which) { g_block_kernel = which; }
+void nk_debug_block_kernel(int which) {
+  g_no_lat = (which == 6);
+  g_block_kernel = which == 6 ? -1 : which;
+}
 
 int nk_modulus(uint64_t q, uint32_t* bits, uint64_t* barrett_factor) {
   nk::host::Modulus m;

@@ -103,7 +103,8 @@ struct PassOf {
 // One register pass: K butterfly bits [LO, LO+K) over G = V / 2^K independent
 // groups held in v[g * 2^K + r]. xt = N + block offset + this thread's index
 // bits (outside the pass). ILTM0: first stage with InputLessThanMod.
-template <class A, bool FWD, int LOGB, int LOGV, int LO, int K, bool ILTM0>
+// TWS: tw points at a copy of the twiddle row in shared memory (ntt_block_lat).
+template <class A, bool FWD, int LOGB, int LOGV, int LO, int K, bool ILTM0, bool TWS = false>
 __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const ulonglong2* __restrict__ tw,
                                         uint64_t xt, const LimbConst& c) {
   using S = Sched<LOGB, LOGV>;
@@ -118,7 +119,7 @@ __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const ulonglon
       const uint64_t base = (xt + S::jg(g, LO, K)) >> (b + 1);
 #pragma unroll
       for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
-        const ulonglong2 w = ldtw(tw + base + hi);
+        const ulonglong2 w = TWS ? tw[base + hi] : ldtw(tw + base + hi);
 #pragma unroll
         for (int l = 0; l < (1 << i); ++l) {
           const int r0 = (hi << (i + 1)) | l;
@@ -141,7 +142,7 @@ __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const ulonglon
 // ---------------------------------------------------------------------------
 // ntt_block: register passes with full padded shared exchanges (2^11..2^14)
 // ---------------------------------------------------------------------------
-template <int LOGB, int LOGV, class A, bool FWD, int P, bool ILTM0>
+template <int LOGB, int LOGV, class A, bool FWD, int P, bool ILTM0, bool TWS = false>
 __device__ __forceinline__ void run_passes(uint64_t (&v)[1 << LOGV], uint64_t* sm,
                                            const ulonglong2* __restrict__ tw, uint32_t t,
                                            uint64_t xbase, const LimbConst& c) {
@@ -158,7 +159,7 @@ __device__ __forceinline__ void run_passes(uint64_t (&v)[1 << LOGV], uint64_t* s
 #pragma unroll
       for (int r = 0; r < R; ++r) v[g * R + r] = sm[bt + smem_phys(S::jg(g, LO, K) | (r << LO))];
   }
-  do_pass<A, FWD, LOGB, LOGV, LO, K, ILTM0 && P == 0>(v, tw, xbase + jt, c);
+  do_pass<A, FWD, LOGB, LOGV, LO, K, ILTM0 && P == 0, TWS>(v, tw, xbase + jt, c);
   if constexpr (P + 1 < S::NP) {
     __syncthreads();  // every thread has read the previous image
     const uint32_t bt = smem_phys(jt);
@@ -166,7 +167,7 @@ __device__ __forceinline__ void run_passes(uint64_t (&v)[1 << LOGV], uint64_t* s
     for (int g = 0; g < G; ++g)
 #pragma unroll
       for (int r = 0; r < R; ++r) sm[bt + smem_phys(S::jg(g, LO, K) | (r << LO))] = v[g * R + r];
-    run_passes<LOGB, LOGV, A, FWD, P + 1, ILTM0>(v, sm, tw, t, xbase, c);
+    run_passes<LOGB, LOGV, A, FWD, P + 1, ILTM0, TWS>(v, sm, tw, t, xbase, c);
   }
 }
 
@@ -280,6 +281,95 @@ __device__ __forceinline__ void fence_proxy_async() {
 __device__ __forceinline__ uint32_t swz_off(uint32_t j) {
   const uint32_t row = j >> 4, col = j & 15;
   return (row << 7) + ((((col >> 1) ^ (row & 7))) << 4) + ((col & 1) << 3);
+}
+
+// ---------------------------------------------------------------------------
+// ntt_block_lat: whole rows of 2^11..2^13 words for batches smaller than the
+// SM count (cfg1: one row), where a transform's latency is the metric. Same
+// passes as ntt_block, plus:
+//  * the row's twiddle table (plan data, read-only since plan creation) is
+//    copied into shared memory by one bulk copy BEFORE griddepcontrol.wait, so
+//    under programmatic dependent launch it lands while the previous kernel in
+//    the stream is still running, and every pass reads its twiddles from
+//    shared memory instead of waiting on L2;
+//  * griddepcontrol.launch_dependents right away, so the next transform can
+//    stage its own table during this one.
+// Inputs are read and outputs written only after griddepcontrol.wait.
+// ---------------------------------------------------------------------------
+template <int LOGB, int LOGV>
+constexpr size_t lat_smem_bytes() {
+  return ((block_smem_bytes<LOGB, LOGV>() + 15) & ~size_t{15}) + (size_t{16} << LOGB) + 16;
+}
+
+template <int LOGB, int LOGV, class A, bool FWD, bool ILTM0>
+__global__ void __launch_bounds__(1 << (LOGB - LOGV)) ntt_block_lat(NttArgs a) {
+  using S = Sched<LOGB, LOGV>;
+  using PO = PassOf<LOGB, LOGV, FWD>;
+  extern __shared__ __align__(16) uint64_t sm[];
+  constexpr size_t kImgWords = ((block_smem_bytes<LOGB, LOGV>() + 15) & ~size_t{15}) / 8;
+  ulonglong2* tws = reinterpret_cast<ulonglong2*>(sm + kImgWords);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(tws + (1u << LOGB));
+  const uint32_t t = threadIdx.x;
+  const uint64_t row = static_cast<uint64_t>(blockIdx.x) * a.row_mul + a.row_add;
+  const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+  if (t == 0) {
+    mbar_init(bar, 1);
+    mbar_expect_tx(bar, 16u << LOGB);
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(tws)),
+        "l"(a.tw + static_cast<uint64_t>(limb) * a.n), "r"(16u << LOGB), "r"(smem_u32(bar))
+        : "memory");
+  }
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+  const LimbConst c = a.lc[limb];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const uint64_t* __restrict__ src = a.in + row * a.n;
+  uint64_t* __restrict__ dst = a.out + row * a.n;
+
+  uint64_t v[S::V];
+  {
+    constexpr int LO = PO::lo(0), K = PO::k(0);
+    constexpr int R = 1 << K, G = S::V / R;
+    const uint32_t jt = S::scatter(t, LO, K);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t jg = S::jg(g, LO, K);
+      if constexpr (LO == 0 && R >= 2) {
+#pragma unroll
+        for (int r = 0; r < R; r += 2) {
+          const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(src + jt + jg + r);
+          v[g * R + r] = A::load(p.x);
+          v[g * R + r + 1] = A::load(p.y);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[g * R + r] = A::load(src[jt + jg + (r << LO)]);
+      }
+    }
+  }
+  __syncthreads();  // the barrier's initialisation is visible to every thread
+  mbar_wait(bar, 0);
+  run_passes<LOGB, LOGV, A, FWD, 0, ILTM0, true>(v, sm, tws, t, a.n, c);
+
+  constexpr int PL = S::NP - 1;
+  constexpr int LO = PO::lo(PL), K = PO::k(PL);
+  constexpr int R = 1 << K, G = S::V / R;
+#pragma unroll
+  for (int i = 0; i < S::V; ++i) v[i] = FWD ? fwd_out<A>(v[i], c, a.fout) : inv_out<A>(v[i], c, a.fout);
+  const uint32_t jt = S::scatter(t, LO, K);
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const uint32_t jg = S::jg(g, LO, K);
+    if constexpr (LO == 0 && R >= 2) {
+#pragma unroll
+      for (int r = 0; r < R; r += 2)
+        *reinterpret_cast<ulonglong2*>(dst + jt + jg + r) = make_ulonglong2(v[g * R + r], v[g * R + r + 1]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[jt + jg + (r << LO)] = v[g * R + r];
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

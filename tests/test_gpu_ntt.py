@@ -316,3 +316,18 @@ def test_shared_tables_across_threads(nk, oracle):
     for i in range(k):
         assert np.array_equal(host_out[i], expected[i])
         assert np.array_equal(dev_out[i], expected[i])
+
+
+@pytest.mark.parametrize("logn", [11, 12, 13])
+@pytest.mark.parametrize("bits", [50, 60])
+def test_small_batch_plain_block_kernel(nk, oracle, logn, bits):
+    """Small batches of 2^11..2^13-word rows normally take the latency kernel
+    (ntt_block_lat: staged twiddles, programmatic dependent launch); mode 6
+    forces the plain block kernel, which must agree as well."""
+    n = 1 << logn
+    moduli = largest_ntt_primes(bits, n, 2)
+    nk.set_block_kernel(6)
+    try:
+        check_dir(nk, oracle, n, moduli, 1, 950 + logn + bits)
+    finally:
+        nk.set_block_kernel(-1)

@@ -61,6 +61,12 @@ def main():
     f, b = torch.empty_like(x), torch.empty_like(x)
     step = graphed(lambda: (p1.forward(f, x, 1, 1), p1.inverse(b, f, 1, 1)))
     out.append({"cfg": 1, "op": "fwd(1,1)+inv(1,1) latency, CUDA graph", "us": 1e3 * timed(step, 200, 10)})
+    nk.set_block_kernel(6)  # plain block kernel for comparison
+    step = graphed(lambda: (p1.forward(f, x, 1, 1), p1.inverse(b, f, 1, 1)))
+    out.append({"cfg": 1, "op": "fwd+inv latency, plain block kernel (mode 6)", "us": 1e3 * timed(step, 200, 10)})
+    nk.set_block_kernel(-1)
+    out.append({"cfg": 1, "op": "fwd+inv latency, stream launches (no graph)",
+                "us": 1e3 * timed(lambda: (p1.forward(f, x, 1, 1), p1.inverse(b, f, 1, 1)), 200, 10)})
     # cfg2
     q = cfg2_modulus()
     n2, sets = 1 << 20, 16
