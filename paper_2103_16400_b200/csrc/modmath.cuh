@@ -171,10 +171,12 @@ __device__ __forceinline__ uint64_t mul_lazyD(uint64_t xD, double w, double wp, 
 // Arithmetic policies for the transform kernels. Values live in registers and
 // shared memory in the policy's representation; load()/store() convert at the
 // HBM boundary. Twiddle-table entries are 16 bytes {w, w'} in the policy's
-// format (uint64 for Arith64, the doubles' bit patterns for Arith52F).
+// format (uint64 for the integer policies, the doubles' bit patterns for the
+// FP64 ones). Arith52F (biased doubles) is the first FP64 form, kept for
+// tools/bfly_bench.cu; the dispatcher uses Arith52S / Arith52P.
 // ---------------------------------------------------------------------------
 struct LimbConstDev {
-  uint64_t q, twoq, negq, ninv, ninvp;  // Arith64: integers; Arith52F: ninv/ninvp are double bits
+  uint64_t q, twoq, negq, ninv, ninvp;  // integer policies: integers; FP64 policies: ninv/ninvp are double bits
   uint64_t twoq_bias;                   // 2q + kDBias
   double qq;                            // q * 2^-52
   double twoq_d;                        // 2q as a double

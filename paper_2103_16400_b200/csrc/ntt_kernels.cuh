@@ -12,9 +12,12 @@
 //   inverse, h = N >> (b+1), t = 2^b:        w_arr[h + (j >> (b+1))]  (ntt.hpp:416-420)
 // The forward runs b = logN-1 .. 0, the inverse b = 0 .. logN-1.
 //
-// Kernels (A = arithmetic policy, modmath.cuh: Arith52F for beta = 2^52 on the
-// FP64 pipe, ArithInt<BS> otherwise):
-//  * ntt_block14_tma<A, FWD, ILTM0>: the hot kernel. Persistent, one 512-thread
+// Kernels (A = arithmetic policy, modmath.cuh: Arith52S / Arith52P on the FP64
+// pipe for beta = 2^52, ArithIntL / ArithInt<64> on the integer pipes for
+// beta = 2^64; capi.cu: ntt_dispatch_aligned picks one per call):
+//  * ntt_pair14<A, FWD, ILTM0> (ntt_pair.cuh): the forward's 16384-word block
+//    kernel, one block per CTA pair (cluster of 2), two pairs per SM.
+//  * ntt_block14_tma<A, FWD, ILTM0>: the inverse's. Persistent, one 512-thread
 //    CTA per SM, walks 16384-word blocks (a whole row at N = 16384, or the low
 //    14 bits of a longer row). Each block arrives by TMA (cp.async.bulk.tensor,
 //    128B swizzle) into a shared staging buffer while the previous block is
@@ -23,10 +26,15 @@
 //    through a padded half-size shared buffer; results leave with coalesced
 //    stores.
 //  * ntt_block<LOGB, LOGV, A, FWD, ILTM0>: same register passes for
-//    2^11..2^14-word blocks, loads straight from global (latency-bound sizes).
+//    2^11..2^14-word blocks, loads straight from global; ntt_block_lat: the
+//    same for batches smaller than the SM count, twiddle row staged in shared
+//    memory before griddepcontrol.wait (programmatic dependent launch).
 //  * ntt_global_pass<K, A, FWD>: K stages on bits [lo, lo+K) of long rows
 //    (N > 2^14), one column of 2^K words per thread, coalesced.
 //  * ntt_small<A, FWD>: any N <= 2^10, stage by stage in shared memory.
+//  * ntt_warp14 / ntt_warp14s (ntt_warp.cuh) and ntt_inv14_tma (below):
+//    alternative 16384-word kernels, correct and selectable
+//    (nk_debug_block_kernel), not faster on B200 today.
 #pragma once
 #include <cuda.h>
 

@@ -11,6 +11,45 @@
 
 using namespace nk;
 
+
+// pass14 with twiddles read from a 4096-entry shared-memory table (indices
+// masked): what the compute phases would reach if twiddle loads had shared
+// memory latency (the access pattern differs, the latency question does not)
+template <class A, bool FWD, class PD>
+__device__ __forceinline__ void pass14_smem(uint64_t (&v)[32], const ulonglong2* tws, uint64_t xt,
+                                            const LimbConstDev& c) {
+  constexpr int K = PD::K, R = PD::R, G = PD::G;
+  constexpr bool kLow = (PD::LO == 0 && PD::K == 5);
+  constexpr bool kShared = (G == 2) && (PD::X >= 0) && (PD::X < PD::LO);
+  constexpr int GL = kShared ? 1 : G;
+  const uint32_t jhi = static_cast<uint32_t>(xt >> 5) & 511u;
+#pragma unroll
+  for (int s = 0; s < K; ++s) {
+    const int i = FWD ? (K - 1 - s) : s;
+    const int b = PD::LO + i;
+#pragma unroll
+    for (int gl = 0; gl < GL; ++gl) {
+      const uint64_t base = (xt + PD::jc(gl, 0)) >> (b + 1);
+#pragma unroll
+      for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
+        const uint32_t idx = kLow ? (low_index(b, hi, 0) + jhi) : static_cast<uint32_t>(base + hi);
+        const ulonglong2 w = tws[idx & 4095u];
+#pragma unroll
+        for (int gg = 0; gg < G / GL; ++gg) {
+#pragma unroll
+          for (int l = 0; l < (1 << i); ++l) {
+            const int g = kShared ? gg : gl;
+            const int r0 = (hi << (i + 1)) | l;
+            const int r1 = r0 | (1 << i);
+            if (FWD) A::template fwd<false>(v[g * R + r0], v[g * R + r1], w, c);
+            else A::template inv<false>(v[g * R + r0], v[g * R + r1], w, c);
+          }
+        }
+      }
+    }
+  }
+}
+
 template <class A, bool FWD, int WHICH>
 __global__ void __launch_bounds__(256, 2) kern(const ulonglong2* tw, const ulonglong2* twl, LimbConstDev c,
                                                uint32_t nlimbs, uint32_t iters, uint64_t* out) {
@@ -32,6 +71,16 @@ __global__ void __launch_bounds__(256, 2) kern(const ulonglong2* tw, const ulong
     if (WHICH & 1) pass14<A, FWD, P1, false>(v, tl, tll, n, n + (FWD ? jt_hi : jt_low), c);
     if (WHICH & 2) pass14<A, FWD, P2, false>(v, tl, tll, n, n + jt_p2, c);
     if (WHICH & 4) pass14<A, FWD, P3, false>(v, tl, tll, n, n + (FWD ? jt_low : jt_hi), c);
+    if (WHICH & 8) {
+      extern __shared__ __align__(16) ulonglong2 tws[];
+      if (it == 0) {
+        for (uint32_t k = t; k < 4096; k += 256) tws[k] = tl[k];
+        __syncthreads();
+      }
+      pass14_smem<A, FWD, P1>(v, tws, n + (FWD ? jt_hi : jt_low), c);
+      pass14_smem<A, FWD, P2>(v, tws, n + jt_p2, c);
+      pass14_smem<A, FWD, P3>(v, tws, n + (FWD ? jt_low : jt_hi), c);
+    }
   }
   uint64_t s = 0;
 #pragma unroll
@@ -47,16 +96,19 @@ static uint64_t dbits(double d) {
 
 template <class A, bool FWD, int WHICH>
 void run(const char* name, const ulonglong2* tw, const ulonglong2* twl, const LimbConstDev& c, int bfly_per_iter,
-         int grid = 296) {
+         int grid = 296, int smem = 0) {
+  // smem > 0: that much dynamic shared memory per CTA, so L1 shrinks to what
+  // the real kernels leave it (~44 KiB per SM at two 106 KiB CTAs)
+  cudaFuncSetAttribute(kern<A, FWD, WHICH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   uint64_t* out;
   cudaMalloc(&out, 1 << 16);
   const uint32_t iters = 200;
-  kern<A, FWD, WHICH><<<grid, 256>>>(tw, twl, c, 32, 10, out);
+  kern<A, FWD, WHICH><<<grid, 256, smem>>>(tw, twl, c, 32, 10, out);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  kern<A, FWD, WHICH><<<grid, 256>>>(tw, twl, c, 32, iters, out);
+  kern<A, FWD, WHICH><<<grid, 256, smem>>>(tw, twl, c, 32, iters, out);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
@@ -90,6 +142,11 @@ int main() {
   cudaMalloc(&twl, h.size() * 16);
   cudaMemcpy(tw, h.data(), h.size() * 16, cudaMemcpyHostToDevice);
   cudaMemcpy(twl, h.data(), h.size() * 16, cudaMemcpyHostToDevice);
+  const int sm = 106 * 1024;
+  run<Arith52S, true, 7>("S all passes, small L1", tw, twl, c, 224, 296, sm);
+  run<Arith52S, true, 8>("S all passes, smem twiddles", tw, twl, c, 224, 296, sm);
+  run<Arith52S, false, 7>("S all inv, small L1", tw, twl, c, 224, 296, sm);
+  run<Arith52S, false, 8>("S all inv, smem twiddles", tw, twl, c, 224, 296, sm);
   run<Arith52S, true, 7>("S all passes", tw, twl, c, 224);
   run<Arith52S, true, 7>("S all passes, 1 CTA/SM", tw, twl, c, 224, 148);
   run<Arith52S, true, 4>("S P3, 1 CTA/SM", tw, twl, c, 80, 148);
