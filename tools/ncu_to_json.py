@@ -8,7 +8,10 @@ import csv, json, re, subprocess, sys
 
 rep, out = sys.argv[1], sys.argv[2]
 note = sys.argv[3] if len(sys.argv) > 3 else ""
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if rep.endswith(".csv"):  # a --page raw --csv export (tools/gpu_check.sh)
+    raw = open(rep).read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, units = rows[0], rows[1]
 keep = {"gpu__time_duration.sum": "duration", "dram__bytes_read.sum": "dram_bytes_read",
