@@ -267,6 +267,29 @@ static inline void inv_bfly(uint64_t* x0, uint64_t* x1, uint64_t w, uint64_t wp,
   *x1 = mul_factor_lazy(v, w, wp, t->neg_q, t->bs);
 }
 
+/* the scalar butterflies of the public API, harvey_forward_butterfly /
+ * harvey_inverse_butterfly (ntt.hpp:137-166): one butterfly per element pair,
+ * twiddle w with its precon for width bs, ILTM off */
+int oc_butterflies(int fwd, uint64_t q, int bs, uint64_t w, const uint64_t* x0, const uint64_t* x1,
+                   uint64_t n, uint64_t* y0, uint64_t* y1) {
+  if (bs != 52 && bs != 64) return -1;
+  tables_t t;
+  memset(&t, 0, sizeof t);
+  t.q = q;
+  t.twice_q = 2 * q;
+  t.bs = bs;
+  t.neg_q = bs == 52 ? (((uint64_t)1 << 52) - q) : (~q + 1);
+  const uint64_t wp = (uint64_t)(((u128)w << bs) / q);
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t a = x0[i], b = x1[i];
+    if (fwd) fwd_bfly(&a, &b, w, wp, &t, 0);
+    else inv_bfly(&a, &b, w, wp, &t, 0);
+    y0[i] = a;
+    y1[i] = b;
+  }
+  return 0;
+}
+
 /* forward_impl<B>, ntt.hpp:363-394, then the fout==1 pass ntt.hpp:282-284 */
 static void forward_row(const tables_t* t, uint64_t* a, uint64_t fin, uint64_t fout) {
   const uint64_t n = t->n;

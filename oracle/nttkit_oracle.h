@@ -39,6 +39,9 @@ uint64_t oc_inv_mod(uint64_t x, uint64_t q);
 uint64_t oc_small_mod(uint64_t x, uint64_t q, uint64_t factor);
 uint64_t oc_precompute_factor(uint64_t w, uint64_t q, int bit_shift);
 uint64_t oc_bit_reverse(uint64_t i, unsigned log2n);
+/* harvey_forward/inverse_butterfly (ntt.hpp:137-166) on n element pairs */
+int oc_butterflies(int fwd, uint64_t q, int bs, uint64_t w, const uint64_t* x0, const uint64_t* x1,
+                   uint64_t n, uint64_t* y0, uint64_t* y1);
 
 /* ---- tables (ntt.hpp) ---- */
 /* minimal primitive `order`-th root; 0 on error (ntt.hpp:172-197) */

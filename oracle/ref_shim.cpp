@@ -231,4 +231,25 @@ int ref_naive_negacyclic(uint64_t n, uint64_t q, const uint64_t* f, const uint64
 
 int ref_is_prime(uint64_t n) { return is_prime(n) ? 1 : 0; }
 
+// harvey_forward_butterfly / harvey_inverse_butterfly (ntt.hpp:137-166) on
+// element pairs, twiddle w with precompute_factor<bs>(w) (modarith.hpp:176-183)
+int ref_butterflies(int fwd, uint64_t q, int bs, uint64_t w, const uint64_t* x0, const uint64_t* x1,
+                    uint64_t n, uint64_t* y0, uint64_t* y1) {
+  return guarded([&] {
+    const Modulus m(q);
+    for (uint64_t i = 0; i < n; ++i) {
+      std::pair<uint64_t, uint64_t> r;
+      if (bs == 52) {
+        const MultiplyFactor f = precompute_factor<52>(w, m);
+        r = fwd ? harvey_forward_butterfly<52>(x0[i], x1[i], f, m) : harvey_inverse_butterfly<52>(x0[i], x1[i], f, m);
+      } else {
+        const MultiplyFactor f = precompute_factor<64>(w, m);
+        r = fwd ? harvey_forward_butterfly<64>(x0[i], x1[i], f, m) : harvey_inverse_butterfly<64>(x0[i], x1[i], f, m);
+      }
+      y0[i] = r.first;
+      y1[i] = r.second;
+    }
+  });
+}
+
 }  // extern "C"

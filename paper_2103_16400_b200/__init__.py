@@ -56,6 +56,7 @@ _SIGS = {
     "nk_debug_dump_to": (None, [vp]),
     "nk_debug_exact_only": (None, [C.c_int]),
     "nk_debug_block_kernel": (None, [C.c_int]),
+    "nk_debug_butterflies": (C.c_int, [C.c_int, C.c_int, u64, u64, vp, vp, u64, vp, vp]),
     "nk_modulus": (C.c_int, [u64, C.POINTER(C.c_uint32), u64p]),
     "nk_minimal_primitive_root": (C.c_int, [u64, u64, u64p]),
     "nk_tables_host": (C.c_int, [u64, u64, u64p, C.c_int, u64p, u64p, u64p, u64p, u64p, u64p,
@@ -220,6 +221,16 @@ def set_exact_only(on):
     """Testing aid (nk_debug_exact_only): force the exact lazy arithmetic on
     every beta = 2^52 transform, including canonical-output ones."""
     lib().nk_debug_exact_only(1 if on else 0)
+
+
+def debug_butterflies(policy, fwd, q, w, x0, x1):
+    """Testing aid (nk_debug_butterflies): one butterfly per element pair of the
+    int64 CUDA tensors x0, x1 in a kernel arithmetic policy; returns (y0, y1)."""
+    import torch
+    y0, y1 = torch.empty_like(x0), torch.empty_like(x1)
+    _check(lib().nk_debug_butterflies(int(policy), int(bool(fwd)), int(q), int(w), _dev_ptr(x0),
+                                      _dev_ptr(x1), x0.numel(), _dev_ptr(y0), _dev_ptr(y1)))
+    return y0, y1
 
 
 def set_block_kernel(which):

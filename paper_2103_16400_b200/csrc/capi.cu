@@ -685,6 +685,48 @@ int launch_mult(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t tota
 }  // namespace
 
 // ---------------------------------------------------------------------------
+// testing aid: single butterflies in each arithmetic policy (nk_debug_butterflies)
+// ---------------------------------------------------------------------------
+namespace nk {
+template <class A, bool FWD, bool SIGNED_IO>
+__global__ void bfly_test_kernel(const uint64_t* x0, const uint64_t* x1, uint64_t n, ulonglong2 w,
+                                 LimbConstDev c, uint64_t* y0, uint64_t* y1) {
+  const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t a, b;
+  if (SIGNED_IO) {  // Arith52S words are signed doubles: int64 in and out
+    a = as_u(static_cast<double>(static_cast<int64_t>(x0[i])));
+    b = as_u(static_cast<double>(static_cast<int64_t>(x1[i])));
+  } else {
+    a = A::load(x0[i]);
+    b = A::load(x1[i]);
+  }
+  if (FWD) A::template fwd<false>(a, b, w, c);
+  else A::template inv<false>(a, b, w, c);
+  if (SIGNED_IO) {
+    y0[i] = static_cast<uint64_t>(static_cast<int64_t>(as_d(a)));
+    y1[i] = static_cast<uint64_t>(static_cast<int64_t>(as_d(b)));
+  } else {
+    y0[i] = A::store(a);
+    y1[i] = A::store(b);
+  }
+}
+}  // namespace nk
+
+namespace {
+template <class A, bool SIGNED_IO>
+int run_bfly_test(bool fwd, const uint64_t* x0, const uint64_t* x1, uint64_t n, ulonglong2 w,
+                  const nk::LimbConstDev& c, uint64_t* y0, uint64_t* y1) {
+  const unsigned grid = static_cast<unsigned>((n + 255) / 256);
+  if (fwd) nk::bfly_test_kernel<A, true, SIGNED_IO><<<grid, 256>>>(x0, x1, n, w, c, y0, y1);
+  else nk::bfly_test_kernel<A, false, SIGNED_IO><<<grid, 256>>>(x0, x1, n, w, c, y0, y1);
+  g_launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
 // host-only entry points
 // ---------------------------------------------------------------------------
 extern "C" {
@@ -694,6 +736,47 @@ const char* nk_version(void) { return "nttkit_b200 0.1 (sm_100a)"; }
 uint64_t nk_launch_count(void) { return g_launches.load(); }
 void nk_debug_dump_to(uint64_t* d_buf) { g_dbg = d_buf; }
 void nk_debug_exact_only(int on) { g_exact_only = on != 0; }
+int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint64_t* d_x0, const uint64_t* d_x1,
+                         uint64_t n, uint64_t* d_y0, uint64_t* d_y1) {
+  nk::host::Modulus m;
+  if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
+  if (w >= q) return fail(NK_ERR_ROOT, "debug_butterflies: twiddle must be < q");
+  const bool b52 = policy == 1 || policy == 2 || policy == 3 || policy == 5;
+  if (policy < 0 || policy > 5) return fail(NK_ERR_BIT_SHIFT, "debug_butterflies: policy must be 0..5");
+  if (b52 && u128{4} * q >= (u128{1} << 52))
+    return fail(NK_ERR_BIT_SHIFT_52, "NttTables: 52-bit accumulator requires 4q < 2^52");
+  if (policy == 4 && q >= (uint64_t{1} << 61))
+    return fail(NK_ERR_MODULUS, "debug_butterflies: the loose policy requires q < 2^61");
+  if (n == 0) return 0;
+  if (!d_x0 || !d_x1 || !d_y0 || !d_y1) return fail(NK_ERR_NULL, "debug_butterflies: NULL buffer");
+  const int bs = b52 ? 52 : 64;
+  const uint64_t wp = static_cast<uint64_t>((static_cast<u128>(w) << bs) / q);
+  const bool fp = policy == 2 || policy == 3 || policy == 5;
+  auto enc = [fp](uint64_t x) { return fp ? dbits(static_cast<double>(x)) : x; };
+  nk::LimbConstDev c{};
+  c.q = q;
+  c.twoq = 2 * q;
+  c.negq = ~q + 1;
+  c.twoq_bias = 2 * q + nk::kDBias;
+  c.qq = std::ldexp(static_cast<double>(q), -52);
+  c.twoq_d = static_cast<double>(2 * q);
+  c.bs = bs;
+  c.q_d = static_cast<double>(q);
+  c.qinv = 1.0 / static_cast<double>(q);
+  c.q_bias = static_cast<double>(q) + 4503599627370496.0;
+  c.fourq = 4 * q;
+  const ulonglong2 tw = make_ulonglong2(enc(w), enc(wp));
+  const bool f = fwd != 0;
+  switch (policy) {
+    case 0: return run_bfly_test<nk::ArithInt<64>, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
+    case 1: return run_bfly_test<nk::ArithInt<52>, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
+    case 2: return run_bfly_test<nk::Arith52P, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
+    case 3: return run_bfly_test<nk::Arith52S, true>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
+    case 4: return run_bfly_test<nk::ArithIntL, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
+    default: return run_bfly_test<nk::Arith52F, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
+  }
+}
+
 void nk_debug_block_kernel(int which) {
   g_no_lat = (which == 6);
   g_block_kernel = which == 6 ? -1 : which;

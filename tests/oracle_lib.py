@@ -72,6 +72,7 @@ class Oracle:
                                                C.c_int]),
                 "oc_naive_negacyclic": (C.c_int, [u64, u64, u64p, u64p, u64p]),
                 "oc_mt19937_64_fill": (None, [u64, u64p, u64, u64]),
+                "oc_butterflies": (C.c_int, [C.c_int, u64, C.c_int, u64, u64p, u64p, u64, u64p, u64p]),
             }
             for name, (res, args) in sig.items():
                 f = getattr(lib, name)
@@ -91,6 +92,16 @@ class Oracle:
         if rc:
             raise ValueError("Modulus: value must be a prime in [3, 2^62)")
         return bits.value, k.value
+
+    def butterflies(self, fwd, q, bs, w, x0, x1):
+        """harvey_forward/inverse_butterfly (ntt.hpp:137-166) on element pairs."""
+        x0 = np.ascontiguousarray(x0, np.uint64)
+        x1 = np.ascontiguousarray(x1, np.uint64)
+        y0, y1 = np.empty_like(x0), np.empty_like(x1)
+        P = lambda a: a.ctypes.data_as(u64p)  # noqa: E731
+        rc = self.lib.oc_butterflies(int(fwd), q, bs, w, P(x0), P(x1), x0.size, P(y0), P(y1))
+        assert rc == 0
+        return y0, y1
 
     def minimal_primitive_root(self, order, q):
         return self.lib.oc_minimal_primitive_root(order, q)
@@ -232,6 +243,10 @@ class Ref:
                 "ref_naive_negacyclic": (C.c_int, [u64, u64, u64p, u64p, u64p]),
                 "ref_is_prime": (C.c_int, [u64]),
             }
+            # added later in the round: bound only when the prebuilt library has it
+            if hasattr(lib, "ref_butterflies"):
+                sig["ref_butterflies"] = (C.c_int, [C.c_int, u64, C.c_int, u64, u64p, u64p, u64,
+                                                    u64p, u64p])
             for name, (res, args) in sig.items():
                 f = getattr(lib, name)
                 f.restype = res
@@ -266,6 +281,14 @@ class Ref:
 
     def inverse(self, n, moduli, x, fin=1, fout=1, bit_shift=0, threads=1):
         return self._ntt(self.lib.ref_ntt_inverse, n, moduli, x, fin, fout, bit_shift, threads)
+
+    def butterflies(self, fwd, q, bs, w, x0, x1):
+        x0 = np.ascontiguousarray(x0, np.uint64)
+        x1 = np.ascontiguousarray(x1, np.uint64)
+        y0, y1 = np.empty_like(x0), np.empty_like(x1)
+        self._check(self.lib.ref_butterflies(int(fwd), q, bs, w, _ptr(x0), _ptr(x1), x0.size,
+                                             _ptr(y0), _ptr(y1)))
+        return y0, y1
 
     def eltwise_mult_mod(self, a, b, q, fin=1, path=0, threads=1):
         a = np.ascontiguousarray(a, np.uint64)
