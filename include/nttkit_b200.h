@@ -32,6 +32,8 @@
  *   nk_poly_mult_mod[_host] poly_mult_mod(result, f, g, tables)   ring.hpp:28-43
  *   nk_modulus              Modulus(q)                            modarith.hpp:106-129
  *   nk_minimal_primitive_root  minimal_primitive_root             ntt.hpp:172-197
+ *   nk_precompute_factor    precompute_factor<B>                  modarith.hpp:176-183
+ *   nk_harvey_butterflies   harvey_forward/inverse_butterfly<B>   ntt.hpp:137-166
  *   nk_tables_host          NttTables table accessors             ntt.hpp:249-261
  *
  * Batched layout (device entry points): `npolys * nlimbs` contiguous rows of n
@@ -78,6 +80,9 @@ enum {
   NK_ERR_OVERLAP = -20,         /* result/operand partially overlap (ntt.hpp:267-268 contract) */
   NK_ERR_LIMB = -21,            /* limb range outside the plan */
   NK_ERR_NULL = -22,            /* NULL pointer where a buffer is required */
+  NK_ERR_FACTOR_OPERAND = -23,  /* "precompute_factor: operand must be < q"                   modarith.hpp:179 */
+  NK_ERR_BETA = -24,            /* "precompute_factor: requires q < beta/4"                   modarith.hpp:180-181 */
+  NK_ERR_RANGE = -25,           /* "harvey_*_butterfly: inputs must be < 4q / < 2q"           ntt.hpp:144,161 */
   NK_ERR_CUDA = -100            /* CUDA runtime error; message has the CUDA error string */
 };
 
@@ -90,6 +95,17 @@ const char* nk_version(void);
 int nk_modulus(uint64_t q, uint32_t* bits, uint64_t* barrett_factor);
 /* Smallest primitive `order`-th root of unity mod q (order a power of two dividing q-1). */
 int nk_minimal_primitive_root(uint64_t order, uint64_t q, uint64_t* root);
+/* precompute_factor<bit_shift>(w, Modulus(q)).precon = floor(w 2^bit_shift / q)
+ * (modarith.hpp:176-183). Host-only. */
+int nk_precompute_factor(uint64_t w, uint64_t q, int bit_shift, uint64_t* precon);
+/* harvey_forward_butterfly / harvey_inverse_butterfly (ntt.hpp:137-166) on n
+ * host element pairs, run on the GPU in the reference's integer arithmetic:
+ * (x0, x1) -> (y0, y1) with the factor (w, precon) of width bit_shift. Inputs
+ * must be < 4q (forward) / < 2q (inverse), checked (the reference's checked
+ * build aborts, ntt.hpp:144,161). Blocking. */
+int nk_harvey_butterflies(int fwd, uint64_t q, int bit_shift, uint64_t w, uint64_t precon,
+                          const uint64_t* x0, const uint64_t* x1, uint64_t n, uint64_t* y0,
+                          uint64_t* y1, int device);
 /* Host precompute exactly as NttTables: root = NULL selects the minimal root (an explicit
  * *root is validated like std::optional<uint64_t> root, ntt.hpp:232-237), bit_shift = 0 selects
  * 52 iff 4q < 2^52. Any output pointer may be NULL; arrays hold n words. */

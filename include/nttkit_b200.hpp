@@ -9,6 +9,8 @@
 //   NttTables::inverse        ntt.hpp:289-306   NttTables::inverse (host spans)
 //   eltwise_mult_mod          eltwise.hpp:180   eltwise_mult_mod
 //   eltwise_mult_mod_int      eltwise.hpp:137   eltwise_mult_mod_int
+//   precompute_factor<B>      modarith.hpp:176  precompute_factor
+//   harvey_*_butterfly<B>     ntt.hpp:137,154   harvey_forward/inverse_butterfly
 //   eltwise_mult_mod_float    eltwise.hpp:158   eltwise_mult_mod_float
 //   eltwise_fma_mod           eltwise.hpp:263   eltwise_fma_mod (std::optional addend)
 //   poly_mult_mod             ring.hpp:28-43    poly_mult_mod
@@ -28,6 +30,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "nttkit_b200.h"
@@ -176,6 +179,40 @@ inline void eltwise_mult_mod(std::span<uint64_t> result, std::span<const uint64_
     throw std::invalid_argument("eltwise: operand lengths must match");
   check(nk_eltwise_mult_mod_host(result.data(), a.data(), b.data(), a.size(), m.value(),
                                  input_mod_factor, 0, nullptr));
+}
+
+/// precompute_factor<BitShift> (modarith.hpp:168-183)
+struct MultiplyFactor {
+  uint64_t operand;
+  uint64_t precon;
+  friend bool operator==(const MultiplyFactor&, const MultiplyFactor&) = default;
+};
+
+template <int BitShift>
+inline MultiplyFactor precompute_factor(uint64_t w, const Modulus& m) {
+  static_assert(BitShift == 52 || BitShift == 64, "accumulator width is 52 or 64");
+  uint64_t p = 0;
+  check(nk_precompute_factor(w, m.value(), BitShift, &p));
+  return {w, p};
+}
+
+/// harvey_forward_butterfly / harvey_inverse_butterfly (ntt.hpp:137-166), run
+/// on the GPU in the reference's integer arithmetic (a kernel launch per
+/// call: the scalar API exists for parity; batched work goes through the
+/// transforms).
+template <int BitShift>
+inline std::pair<uint64_t, uint64_t> harvey_forward_butterfly(uint64_t x0, uint64_t x1, const MultiplyFactor& w,
+                                                              const Modulus& m) {
+  uint64_t y0 = 0, y1 = 0;
+  check(nk_harvey_butterflies(1, m.value(), BitShift, w.operand, w.precon, &x0, &x1, 1, &y0, &y1, 0));
+  return {y0, y1};
+}
+template <int BitShift>
+inline std::pair<uint64_t, uint64_t> harvey_inverse_butterfly(uint64_t x0, uint64_t x1, const MultiplyFactor& w,
+                                                              const Modulus& m) {
+  uint64_t y0 = 0, y1 = 0;
+  check(nk_harvey_butterflies(0, m.value(), BitShift, w.operand, w.precon, &x0, &x1, 1, &y0, &y1, 0));
+  return {y0, y1};
 }
 
 inline void eltwise_mult_mod_int(std::span<uint64_t> result, std::span<const uint64_t> a,

@@ -59,6 +59,8 @@ _SIGS = {
     "nk_debug_butterflies": (C.c_int, [C.c_int, C.c_int, u64, u64, vp, vp, u64, vp, vp]),
     "nk_modulus": (C.c_int, [u64, C.POINTER(C.c_uint32), u64p]),
     "nk_minimal_primitive_root": (C.c_int, [u64, u64, u64p]),
+    "nk_precompute_factor": (C.c_int, [u64, u64, C.c_int, u64p]),
+    "nk_harvey_butterflies": (C.c_int, [C.c_int, u64, C.c_int, u64, u64, vp, vp, u64, vp, vp, C.c_int]),
     "nk_tables_host": (C.c_int, [u64, u64, u64p, C.c_int, u64p, u64p, u64p, u64p, u64p, u64p,
                                  u64p, C.POINTER(C.c_int)]),
     "nk_plan_create": (C.c_int, [C.POINTER(vp), C.c_int, u64, u64p, u64p, C.c_uint32, C.c_int]),
@@ -198,6 +200,44 @@ def minimal_primitive_root(order, m):
     r = u64()
     _check(lib().nk_minimal_primitive_root(int(order), q, C.byref(r)))
     return r.value
+
+
+class MultiplyFactor:
+    """precompute_factor<bit_shift>(w, m) (modarith.hpp:168-183)."""
+
+    def __init__(self, operand, m, bit_shift=64):
+        q = m.value() if isinstance(m, Modulus) else int(m)
+        p = u64()
+        _check(lib().nk_precompute_factor(int(operand), q, int(bit_shift), C.byref(p)))
+        self.operand, self.precon, self.bit_shift = int(operand), p.value, int(bit_shift)
+
+
+def precompute_factor(w, m, bit_shift=64):
+    return MultiplyFactor(w, m, bit_shift)
+
+
+def _harvey(fwd, x0, x1, w, m):
+    q = m.value() if isinstance(m, Modulus) else int(m)
+    scalar = np.isscalar(x0)
+    a = np.ascontiguousarray(np.atleast_1d(np.asarray(x0, dtype=np.uint64)))
+    b = np.ascontiguousarray(np.atleast_1d(np.asarray(x1, dtype=np.uint64)))
+    if a.size != b.size:
+        raise ValueError("eltwise: operand lengths must match")
+    y0, y1 = np.empty_like(a), np.empty_like(b)
+    _check(lib().nk_harvey_butterflies(int(fwd), q, w.bit_shift, w.operand, w.precon, _hp(a), _hp(b),
+                                       a.size, _hp(y0), _hp(y1), _device_of_default()))
+    return (int(y0[0]), int(y1[0])) if scalar else (y0, y1)
+
+
+def harvey_forward_butterfly(x0, x1, w, m):
+    """harvey_forward_butterfly<B> (ntt.hpp:137-149), computed on the GPU;
+    scalars or equal-length uint64 arrays; w a MultiplyFactor of width B."""
+    return _harvey(True, x0, x1, w, m)
+
+
+def harvey_inverse_butterfly(x0, x1, w, m):
+    """harvey_inverse_butterfly<B> (ntt.hpp:154-166), computed on the GPU."""
+    return _harvey(False, x0, x1, w, m)
 
 
 def tables_host(n, q, root=None, bit_shift=0):

@@ -777,6 +777,48 @@ int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint
   }
 }
 
+int nk_precompute_factor(uint64_t w, uint64_t q, int bit_shift, uint64_t* precon) {
+  nk::host::Modulus m;
+  if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
+  if (bit_shift != 52 && bit_shift != 64)
+    return fail(NK_ERR_BIT_SHIFT, "NttTables: accumulator width must be 52 or 64");
+  if (w >= q) return fail(NK_ERR_FACTOR_OPERAND, "precompute_factor: operand must be < q");
+  if (u128{q} * 4 > (u128{1} << bit_shift))
+    return fail(NK_ERR_BETA, "precompute_factor: requires q < beta/4");
+  if (precon) *precon = static_cast<uint64_t>((static_cast<u128>(w) << bit_shift) / q);
+  return 0;
+}
+
+int nk_harvey_butterflies(int fwd, uint64_t q, int bit_shift, uint64_t w, uint64_t precon, const uint64_t* x0,
+                          const uint64_t* x1, uint64_t n, uint64_t* y0, uint64_t* y1, int device) {
+  uint64_t wp = 0;
+  if (int rc = nk_precompute_factor(w, q, bit_shift, &wp)) return rc;
+  if (precon != wp) return fail(NK_ERR_FACTOR_OPERAND, "harvey butterfly: precon does not match the operand");
+  if (n == 0) return 0;
+  if (!x0 || !x1 || !y0 || !y1) return fail(NK_ERR_NULL, "harvey butterfly: NULL buffer");
+  const uint64_t bound = (fwd ? 4 : 2) * q;  // ntt.hpp:144 / 161
+  for (uint64_t i = 0; i < n; ++i)
+    if (x0[i] >= bound || x1[i] >= bound)
+      return fail(NK_ERR_RANGE, fwd ? "harvey_forward_butterfly: inputs must be < 4q"
+                                    : "harvey_inverse_butterfly: inputs must be < 2q");
+  if (int rc = ensure_device(device)) return rc;
+  uint64_t* d = nullptr;
+  NK_CUDA(cudaMalloc(&d, 4 * n * sizeof(uint64_t)));
+  int rc = 0;
+  cudaError_t e = cudaMemcpy(d, x0, n * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d + n, x1, n * 8, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpy(H2D)");
+  // the reference's exact integer arithmetic for the width (ArithInt<52/64>)
+  if (!rc) rc = nk_debug_butterflies(bit_shift == 52 ? 1 : 0, fwd, q, w, d, d + n, n, d + 2 * n, d + 3 * n);
+  if (!rc) {
+    e = cudaMemcpy(y0, d + 2 * n, n * 8, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(y1, d + 3 * n, n * 8, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpy(D2H)");
+  }
+  cudaFree(d);
+  return rc;
+}
+
 void nk_debug_block_kernel(int which) {
   g_no_lat = (which == 6);
   g_block_kernel = which == 6 ? -1 : which;

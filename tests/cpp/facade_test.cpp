@@ -45,6 +45,9 @@ int main(int argc, char** argv) {
   EXPECT(throws_invalid([] { nb::NttTables t(3, nb::Modulus(17)); }));
   EXPECT(throws_invalid([] { nb::NttTables t(4, nb::Modulus(17), std::nullopt, 48); }));
   EXPECT(throws_invalid([] { nb::NttTables t(4, nb::Modulus(17), uint64_t{3}); }));
+  // modarith.hpp:176-183 / test_modarith.cpp:195
+  EXPECT(nb::precompute_factor<64>(1, nb::Modulus(17)).precon == 1085102592571150095ull);
+  EXPECT(throws_invalid([] { nb::precompute_factor<64>(17, nb::Modulus(17)); }));
   if (cpu_only) {
     std::printf(failures ? "facade cpu checks FAILED\n" : "facade cpu checks ok\n");
     return failures ? 1 : 0;
@@ -83,6 +86,16 @@ int main(int argc, char** argv) {
   nb::poly_mult_mod(xc, xa, xb, t8);
   EXPECT(xc[0] == 96);
   for (int i = 1; i < 8; ++i) EXPECT(xc[i] == 0);
+  // test_ntt.cpp:264-275: the public butterflies
+  {
+    const nb::Modulus m17(17);
+    const auto f5 = nb::precompute_factor<64>(5, m17);
+    const auto [y0, y1] = nb::harvey_forward_butterfly<64>(0, 0, f5, m17);
+    EXPECT(y0 == 0 && y1 == 34);
+    const auto f3 = nb::precompute_factor<52>(3, m17);
+    const auto [z0, z1] = nb::harvey_inverse_butterfly<52>(7, 7, f3, m17);
+    EXPECT(z0 % 17 == 14 && z1 % 17 == 0);
+  }
   std::printf(failures ? "facade gpu checks FAILED\n" : "facade gpu checks ok\n");
   return failures ? 1 : 0;
 }

@@ -166,3 +166,21 @@ def test_cpp_facade_argument_checks():
     out = subprocess.run([exe, "--cpu"], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "facade cpu checks ok" in out.stdout
+
+
+def test_precompute_factor_and_butterfly_checks(nk):
+    """precompute_factor (modarith.hpp:176-183, test_modarith.cpp:195) and the
+    public butterflies' argument checks (ntt.hpp:142-144,159-161), before any
+    device work."""
+    assert nk.precompute_factor(1, 17, 64).precon == 1085102592571150095
+    assert nk.precompute_factor(3, 17, 52).precon == (3 << 52) // 17
+    with pytest.raises(ValueError, match="operand must be < q"):
+        nk.precompute_factor(17, 17, 64)
+    q52 = smallest_ntt_primes(52, 1, 1)[0]
+    with pytest.raises(ValueError, match=re.escape("requires q < beta/4")):
+        nk.precompute_factor(1, q52, 52)
+    w = nk.precompute_factor(5, 17, 64)
+    with pytest.raises(ValueError, match="inputs must be < 4q"):
+        nk.harvey_forward_butterfly(68, 0, w, 17)
+    with pytest.raises(ValueError, match="inputs must be < 2q"):
+        nk.harvey_inverse_butterfly(0, 34, w, 17)

@@ -125,3 +125,48 @@ def test_loose_policy_ranges(nk, fwd):
                 e0, e1 = (A + B) % q, (w * (A - B)) % q
             assert all(int(u) % q == v for u, v in zip(y0, e0)), (q, w)
             assert all(int(u) % q == v for u, v in zip(y1, e1)), (q, w)
+
+
+def test_public_harvey_butterflies(nk, oracle):
+    """The public scalar API (ntt.hpp:137-166) through nk_harvey_butterflies:
+    test_ntt.cpp's ZeroAndZeroMultiplier / SymmetryAndZero known answers and
+    the exhaustive q = 17 table, both widths, against the oracle."""
+    q = 17
+    for bs in (52, 64):
+        w5 = nk.precompute_factor(5, q, bs)
+        assert nk.harvey_forward_butterfly(0, 0, w5, q) == (0, 2 * q)  # test_ntt.cpp:264-275
+        w0 = nk.precompute_factor(0, q, bs)
+        for x0 in (0, 5, 40, 67):
+            z0, z1 = nk.harvey_forward_butterfly(x0, 9, w0, q)
+            assert z0 % q == x0 % q and z1 % q == x0 % q
+        w3 = nk.precompute_factor(3, q, bs)
+        for x in (0, 7, 30):  # test_ntt.cpp:301-313
+            y0, y1 = nk.harvey_inverse_butterfly(x, x, w3, q)
+            assert y1 % q == 0 and y0 % q == (2 * x) % q
+        for fwd, r in ((True, 4), (False, 2)):
+            a, b = np.meshgrid(np.arange(r * q, dtype=np.uint64), np.arange(r * q, dtype=np.uint64))
+            a, b = a.reshape(-1), b.reshape(-1)
+            for w in range(q):
+                f = nk.precompute_factor(w, q, bs)
+                fn = nk.harvey_forward_butterfly if fwd else nk.harvey_inverse_butterfly
+                y0, y1 = fn(a, b, f, q)
+                w0_, w1_ = oracle.butterflies(fwd, q, bs, w, a, b)
+                assert np.array_equal(y0, w0_) and np.array_equal(y1, w1_), (bs, fwd, w)
+
+
+def test_cpp_facade_on_device():
+    """tests/cpp/facade_test (the C++ drop-in facade: reference and HEXL names)
+    end to end on the GPU."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "tests", "cpp", "facade_test")
+    if not os.path.exists(exe):
+        import sys
+        sys.path.insert(0, root)
+        import __graft_entry__
+        __graft_entry__.build_facade_test()
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "facade gpu checks ok" in out.stdout
