@@ -27,8 +27,8 @@
  *                           and eltwise_fma_mod<B>                eltwise.hpp:231-259
  *                           (HEXL: EltwiseFMAMod, z == NULL is the vector-scalar
  *                            multiply                             PAPER.md:521,527-529)
- *   nk_eltwise_add_mod      eltwise_add_mod                       eltwise.hpp:47-57
- *   nk_eltwise_neg_mod      eltwise_neg_mod                       eltwise.hpp:60-70
+ *   nk_eltwise_add_mod[_host]  eltwise_add_mod                    eltwise.hpp:47-57
+ *   nk_eltwise_neg_mod[_host]  eltwise_neg_mod                    eltwise.hpp:60-70
  *   nk_poly_mult_mod[_host] poly_mult_mod(result, f, g, tables)   ring.hpp:28-43
  *   nk_modulus              Modulus(q)                            modarith.hpp:106-129
  *   nk_minimal_primitive_root  minimal_primitive_root             ntt.hpp:172-197
@@ -171,6 +171,10 @@ int nk_ntt_inverse_host(const nk_plan* plan, uint64_t* result, const uint64_t* o
 int nk_poly_mult_mod_host(const nk_plan* plan, uint64_t* result, const uint64_t* f,
                           const uint64_t* g, uint64_t length, uint32_t limb0, uint32_t nlimbs,
                           uint32_t npolys, void* stream);
+int nk_eltwise_add_mod_host(uint64_t* result, const uint64_t* a, const uint64_t* b, uint64_t n,
+                            uint64_t q, int device, void* stream);
+int nk_eltwise_neg_mod_host(uint64_t* result, const uint64_t* a, uint64_t n, uint64_t q, int device,
+                            void* stream);
 int nk_eltwise_mult_mod_host(uint64_t* result, const uint64_t* a, const uint64_t* b, uint64_t n,
                              uint64_t q, uint64_t input_mod_factor, int device, void* stream);
 int nk_eltwise_mult_mod_int_host(uint64_t* result, const uint64_t* a, const uint64_t* b, uint64_t n,

@@ -59,6 +59,23 @@ class Modulus {
   uint64_t barrett_ = 0;
 };
 
+/// Residue vector with its declared range bound (ntt.hpp:60-80): every element
+/// is promised to be below bound_factor * q (bookkeeping for the lazy
+/// contracts; checked by within_bound).
+struct CoeffVec {
+  std::vector<uint64_t> data;
+  uint64_t bound_factor = 1;
+  CoeffVec() = default;
+  explicit CoeffVec(std::vector<uint64_t> d, uint64_t factor = 1) : data(std::move(d)), bound_factor(factor) {}
+  uint64_t size() const noexcept { return data.size(); }
+  bool within_bound(const Modulus& m) const {
+    const unsigned __int128 bound = static_cast<unsigned __int128>(bound_factor) * m.value();
+    for (uint64_t x : data)
+      if (x >= bound) return false;
+    return true;
+  }
+};
+
 // Tables of many RNS limbs on one device; batched data is [npolys][nlimbs][n].
 class RnsNtt {
  public:
@@ -157,6 +174,21 @@ class NttTables : public RnsNtt {
       throw std::invalid_argument("transform: buffer length must equal n");
     host_call(false, result, operand, in, out);
   }
+  // CoeffVec overloads (ntt.hpp:308-320): the result carries output_mod_factor
+  CoeffVec forward(const CoeffVec& in, uint64_t input_mod_factor, uint64_t output_mod_factor) const {
+    if (in.bound_factor > input_mod_factor)
+      throw std::invalid_argument("forward: CoeffVec bound exceeds input_mod_factor");
+    CoeffVec out(std::vector<uint64_t>(in.data.size()), output_mod_factor);
+    forward(out.data, in.data, input_mod_factor, output_mod_factor);
+    return out;
+  }
+  CoeffVec inverse(const CoeffVec& in, uint64_t input_mod_factor, uint64_t output_mod_factor) const {
+    if (in.bound_factor > input_mod_factor)
+      throw std::invalid_argument("inverse: CoeffVec bound exceeds input_mod_factor");
+    CoeffVec out(std::vector<uint64_t>(in.data.size()), output_mod_factor);
+    inverse(out.data, in.data, input_mod_factor, output_mod_factor);
+    return out;
+  }
 
  private:
   static std::span<const uint64_t> one(const Modulus& m) {
@@ -248,6 +280,53 @@ inline void poly_mult_mod(std::span<uint64_t> result, std::span<const uint64_t> 
     throw std::invalid_argument("poly_mult_mod: operand lengths must equal n");
   check(nk_poly_mult_mod_host(tables.plan(), result.data(), f.data(), g.data(), f.size(), 0, 1, 1,
                               nullptr));
+}
+
+inline void eltwise_add_mod(std::span<uint64_t> result, std::span<const uint64_t> a,
+                            std::span<const uint64_t> b, const Modulus& m) {
+  if (result.size() != a.size() || a.size() != b.size())
+    throw std::invalid_argument("eltwise: operand lengths must match");
+  check(nk_eltwise_add_mod_host(result.data(), a.data(), b.data(), a.size(), m.value(), 0, nullptr));
+}
+
+inline void eltwise_neg_mod(std::span<uint64_t> result, std::span<const uint64_t> a, const Modulus& m) {
+  if (result.size() != a.size()) throw std::invalid_argument("eltwise: operand lengths must match");
+  check(nk_eltwise_neg_mod_host(result.data(), a.data(), a.size(), m.value(), 0, nullptr));
+}
+
+// CoeffVec conveniences (eltwise.hpp:273-303, ring.hpp:45-51); results are fully reduced
+inline CoeffVec eltwise_add_mod(const CoeffVec& a, const CoeffVec& b, const Modulus& m) {
+  CoeffVec out(std::vector<uint64_t>(a.size()), 1);
+  eltwise_add_mod(out.data, a.data, b.data, m);
+  return out;
+}
+inline CoeffVec eltwise_neg_mod(const CoeffVec& a, const Modulus& m) {
+  CoeffVec out(std::vector<uint64_t>(a.size()), 1);
+  eltwise_neg_mod(out.data, a.data, m);
+  return out;
+}
+inline CoeffVec eltwise_mult_mod(const CoeffVec& a, const CoeffVec& b, const Modulus& m,
+                                 uint64_t input_mod_factor) {
+  if (a.bound_factor > input_mod_factor || b.bound_factor > input_mod_factor)
+    throw std::invalid_argument("eltwise_mult_mod: CoeffVec bound exceeds input_mod_factor");
+  CoeffVec out(std::vector<uint64_t>(a.size()), 1);
+  eltwise_mult_mod(out.data, a.data, b.data, m, input_mod_factor);
+  return out;
+}
+inline CoeffVec eltwise_fma_mod(const CoeffVec& a, uint64_t y, const CoeffVec* z, const Modulus& m,
+                                uint64_t input_mod_factor) {
+  CoeffVec out(std::vector<uint64_t>(a.size()), 1);
+  std::optional<std::span<const uint64_t>> zs;
+  if (z != nullptr) zs = std::span<const uint64_t>(z->data);
+  eltwise_fma_mod(out.data, a.data, y, zs, m, input_mod_factor);
+  return out;
+}
+inline CoeffVec poly_mult_mod(const CoeffVec& f, const CoeffVec& g, const NttTables& tables) {
+  if (f.bound_factor != 1 || g.bound_factor != 1)
+    throw std::invalid_argument("poly_mult_mod: operands must be fully reduced");
+  CoeffVec out(std::vector<uint64_t>(f.size()), 1);
+  poly_mult_mod(out.data, f.data, g.data, tables);
+  return out;
 }
 
 // ---- Intel HEXL names ----

@@ -84,6 +84,8 @@ _SIGS = {
                                       u64, vp]),
     "nk_poly_mult_mod_host": (C.c_int, [vp, vp, vp, vp, u64, C.c_uint32, C.c_uint32, C.c_uint32,
                                         vp]),
+    "nk_eltwise_add_mod_host": (C.c_int, [vp, vp, vp, u64, u64, C.c_int, vp]),
+    "nk_eltwise_neg_mod_host": (C.c_int, [vp, vp, u64, u64, C.c_int, vp]),
     "nk_eltwise_mult_mod_host": (C.c_int, [vp, vp, vp, u64, u64, u64, C.c_int, vp]),
     "nk_eltwise_mult_mod_int_host": (C.c_int, [vp, vp, vp, u64, u64, u64, C.c_int, vp]),
     "nk_eltwise_mult_mod_float_host": (C.c_int, [vp, vp, vp, u64, u64, u64, C.c_int, vp]),
@@ -503,21 +505,39 @@ def eltwise_fma_mod(result, a, y, z, m, input_mod_factor=1, bit_shift=0, stream=
 
 
 def eltwise_add_mod(result, a, b, m, stream=None):
+    """result[i] = (a[i] + b[i]) mod q for canonical inputs (eltwise.hpp:47-57)."""
     q = _q_of(m)
-    if a.numel() != b.numel() or result.numel() != a.numel():
+    if _is_torch(a):
+        if a.numel() != b.numel() or result.numel() != a.numel():
+            raise ValueError("eltwise: operand lengths must match")
+        st = _stream_of(a) if stream is None else C.c_void_p(stream)
+        _check(lib().nk_eltwise_add_mod(_dev_ptr(result), _dev_ptr(a), _dev_ptr(b), a.numel(), q, st))
+        return result
+    aa, bb = _host_arr(a, "a"), _host_arr(b, "b")
+    out = np.empty_like(aa) if result is None else result
+    if not (aa.size == bb.size == out.size):
         raise ValueError("eltwise: operand lengths must match")
-    st = _stream_of(a) if stream is None else C.c_void_p(stream)
-    _check(lib().nk_eltwise_add_mod(_dev_ptr(result), _dev_ptr(a), _dev_ptr(b), a.numel(), q, st))
-    return result
+    _check(lib().nk_eltwise_add_mod_host(_hp(out), _hp(aa), _hp(bb), aa.size, q, _device_of_default(),
+                                         None if stream is None else C.c_void_p(stream)))
+    return out
 
 
 def eltwise_neg_mod(result, a, m, stream=None):
+    """result[i] = (q - a[i]) mod q for canonical inputs (eltwise.hpp:60-70)."""
     q = _q_of(m)
-    if result.numel() != a.numel():
+    if _is_torch(a):
+        if result.numel() != a.numel():
+            raise ValueError("eltwise: operand lengths must match")
+        st = _stream_of(a) if stream is None else C.c_void_p(stream)
+        _check(lib().nk_eltwise_neg_mod(_dev_ptr(result), _dev_ptr(a), a.numel(), q, st))
+        return result
+    aa = _host_arr(a, "a")
+    out = np.empty_like(aa) if result is None else result
+    if aa.size != out.size:
         raise ValueError("eltwise: operand lengths must match")
-    st = _stream_of(a) if stream is None else C.c_void_p(stream)
-    _check(lib().nk_eltwise_neg_mod(_dev_ptr(result), _dev_ptr(a), a.numel(), q, st))
-    return result
+    _check(lib().nk_eltwise_neg_mod_host(_hp(out), _hp(aa), aa.size, q, _device_of_default(),
+                                         None if stream is None else C.c_void_p(stream)))
+    return out
 
 
 def poly_mult_mod(result, f, g, tables):

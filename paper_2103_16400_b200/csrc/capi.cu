@@ -1420,6 +1420,32 @@ int eltwise_mult_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint6
 }
 }  // namespace
 
+int nk_eltwise_add_mod_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
+                            int device, void* stream) {
+  nk::host::Modulus m;
+  if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
+  if (n == 0) return 0;
+  if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_add_mod: NULL buffer");
+  if (int rc = ensure_device(device)) return rc;
+  return run_pipelined(device, S(stream), n, 1, {a, b}, res,
+                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
+                         return nk_eltwise_add_mod(d[0], d[0], d[1], nu, q, st);
+                       });
+}
+
+int nk_eltwise_neg_mod_host(uint64_t* res, const uint64_t* a, uint64_t n, uint64_t q, int device,
+                            void* stream) {
+  nk::host::Modulus m;
+  if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
+  if (n == 0) return 0;
+  if (!res || !a) return fail(NK_ERR_NULL, "eltwise_neg_mod: NULL buffer");
+  if (int rc = ensure_device(device)) return rc;
+  return run_pipelined(device, S(stream), n, 1, {a}, res,
+                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
+                         return nk_eltwise_neg_mod(d[0], d[0], nu, q, st);
+                       });
+}
+
 int nk_eltwise_mult_mod_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n,
                              uint64_t q, uint64_t fin, int device, void* stream) {
   return eltwise_mult_host(res, a, b, n, q, fin, kMultAuto, device, stream);

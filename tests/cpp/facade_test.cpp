@@ -86,6 +86,26 @@ int main(int argc, char** argv) {
   nb::poly_mult_mod(xc, xa, xb, t8);
   EXPECT(xc[0] == 96);
   for (int i = 1; i < 8; ++i) EXPECT(xc[i] == 0);
+  // CoeffVec overloads (ntt.hpp:308-320, eltwise.hpp:273-303, ring.hpp:45-51)
+  {
+    nb::CoeffVec cx(x, 1);
+    const nb::CoeffVec fx = ntt.GetDegree() == 4096 ? nb::NttTables(4096, nb::Modulus(q)).forward(cx, 1, 4)
+                                                    : nb::CoeffVec();
+    EXPECT(fx.bound_factor == 4 && fx.within_bound(nb::Modulus(q)));
+    const nb::CoeffVec back = nb::NttTables(4096, nb::Modulus(q)).inverse(
+        nb::NttTables(4096, nb::Modulus(q)).forward(cx, 1, 1), 1, 1);
+    EXPECT(back.data == x);
+    const nb::Modulus m97(97);
+    nb::CoeffVec a5(std::vector<uint64_t>{1, 96, 50, 0}, 1), b5(std::vector<uint64_t>{96, 96, 50, 0}, 1);
+    EXPECT((nb::eltwise_add_mod(a5, b5, m97).data == std::vector<uint64_t>{0, 95, 3, 0}));
+    EXPECT((nb::eltwise_neg_mod(a5, m97).data == std::vector<uint64_t>{96, 1, 47, 0}));
+    EXPECT((nb::eltwise_mult_mod(a5, b5, m97, 1).data == std::vector<uint64_t>{96, 1, 75, 0}));
+    EXPECT(throws_invalid([&] { nb::eltwise_mult_mod(nb::CoeffVec(a5.data, 2), b5, m97, 1); }));
+    nb::CoeffVec p1(std::vector<uint64_t>(8, 0), 1), p2(std::vector<uint64_t>(8, 0), 1);
+    p1.data[1] = 1;
+    p2.data[7] = 1;
+    EXPECT(nb::poly_mult_mod(p1, p2, t8).data[0] == 96);
+  }
   // test_ntt.cpp:264-275: the public butterflies
   {
     const nb::Modulus m17(17);

@@ -168,6 +168,18 @@ def test_add_neg(nk, oracle):
     assert np.array_equal(host(r), oracle.eltwise_neg_mod(a, q))
 
 
+def test_add_neg_host_buffers(nk, oracle):
+    """eltwise_add_mod / eltwise_neg_mod through the host-buffer entry points."""
+    q = primes_with_bits(60, 1)[0]
+    n = 70001
+    a = oracle.mt19937_64(61, n, q)
+    b = oracle.mt19937_64(62, n, q)
+    a[:3] = [0, q - 1, 1]
+    b[:3] = [0, q - 1, q - 1]
+    assert np.array_equal(nk.eltwise_add_mod(None, a, b, q), oracle.eltwise_add_mod(a, b, q))
+    assert np.array_equal(nk.eltwise_neg_mod(None, a, q), oracle.eltwise_neg_mod(a, q))
+
+
 def test_cfg2_full(nk, oracle):
     """BASELINE cfg2: 2^20 words, q = largest prime < 2^60, fin 1: vector-vector,
     vector-scalar (FMA without addend) and FMA."""
