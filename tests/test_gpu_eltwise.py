@@ -364,3 +364,40 @@ def test_host_pipeline_multi_chunk(nk, oracle):
     f = plan.forward(None, x, 1, 1)
     assert np.array_equal(f, oracle.forward(nn, moduli, x, 1, 1, threads=8))
     assert np.array_equal(plan.inverse(None, f, 1, 1), x)
+
+
+def test_eltwise_writes_stay_in_bounds(nk, oracle):
+    """Guard words around element-wise and poly-multiply results (see
+    test_gpu_ntt.test_writes_stay_in_bounds), odd lengths and offsets."""
+    sentinel = np.uint64(0x5A5A5A5A5A5A5A5A)
+    guard = 1024
+    for q in (primes_with_bits(60, 1)[0], primes_with_bits(49, 1)[0]):
+        for n in (1, 7, 4097, 70001):
+            a, b = oracle.mt19937_64(5, n, q), oracle.mt19937_64(6, n, q)
+            for name, run, want in (
+                ("mult", lambda o: nk.eltwise_mult_mod(o, dev(a), dev(b), q, 1), oracle.eltwise_mult_mod(a, b, q, 1)),
+                ("fma", lambda o: nk.eltwise_fma_mod(o, dev(a), 3, dev(b), q, 1), oracle.eltwise_fma_mod(a, 3, b, q, 1)),
+                ("vs", lambda o: nk.eltwise_fma_mod(o, dev(a), 3, None, q, 1), oracle.eltwise_fma_mod(a, 3, None, q, 1)),
+                ("add", lambda o: nk.eltwise_add_mod(o, dev(a), dev(b), q), oracle.eltwise_add_mod(a, b, q)),
+                ("neg", lambda o: nk.eltwise_neg_mod(o, dev(a), q), oracle.eltwise_neg_mod(a, q)),
+            ):
+                for off in (0, 1):
+                    buf = torch.full((n + 2 * guard + 1,), int(sentinel.view(np.int64)), dtype=torch.int64,
+                                     device="cuda")
+                    run(buf[guard + off:guard + off + n])
+                    h = host(buf)
+                    assert np.all(h[:guard + off] == sentinel), (name, n, off)
+                    assert np.all(h[guard + off + n:] == sentinel), (name, n, off)
+                    assert np.array_equal(h[guard + off:guard + off + n], want), (name, n, off)
+    # fused poly multiply (N = 16384) and the sequence path (N = 1024)
+    for n in (1024, 16384):
+        moduli = largest_ntt_primes(50, n, 2)
+        f = np.concatenate([oracle.mt19937_64(50 + r, n, moduli[r % 2]) for r in range(4)])
+        g = np.concatenate([oracle.mt19937_64(60 + r, n, moduli[r % 2]) for r in range(4)])
+        plan = nk.RnsNtt(n, moduli)
+        words = f.size
+        buf = torch.full((words + 2 * guard,), int(sentinel.view(np.int64)), dtype=torch.int64, device="cuda")
+        plan.poly_mult_mod(buf[guard:guard + words], dev(f), dev(g))
+        h = host(buf)
+        assert np.all(h[:guard] == sentinel) and np.all(h[guard + words:] == sentinel)
+        assert np.array_equal(h[guard:guard + words], oracle.poly_mult_mod(n, moduli, f, g))

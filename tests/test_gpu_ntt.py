@@ -331,3 +331,74 @@ def test_small_batch_plain_block_kernel(nk, oracle, logn, bits):
         check_dir(nk, oracle, n, moduli, 1, 950 + logn + bits)
     finally:
         nk.set_block_kernel(-1)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_limb_shards_on_one_gpu(nk, oracle, world):
+    """the multi-GPU partition simulated on one GPU. Each rank's
+    contiguous limb range (sharding.limb_shard) of a cfg3-shaped batch
+    (N = 16384, 8 limbs, 3 polys) is transformed by its own plan over its
+    limbs, as a rank would; the concatenated shards equal the whole-batch
+    transform (forward and inverse), and the same holds through the limb0/nlimbs
+    sub-range of one full plan."""
+    from paper_2103_16400_b200.sharding import limb_shard, shard_rows
+
+    n, nlimbs, npolys = 16384, 8, 3
+    moduli = largest_ntt_primes(50, n, nlimbs)
+    x = rows_of(oracle, moduli, n, npolys, 4242)
+    full_plan = nk.RnsNtt(n, moduli)
+    d = dev(x)
+    want_f = host(full_plan.forward(torch.empty_like(d), d, 1, 1))
+    want_i = host(full_plan.inverse(torch.empty_like(d), d, 1, 1))
+    got_f = np.empty((npolys, nlimbs, n), np.uint64)
+    got_i = np.empty((npolys, nlimbs, n), np.uint64)
+    for rank in range(world):
+        l0, cnt = limb_shard(nlimbs, world, rank)
+        if cnt == 0:
+            continue
+        plan = nk.RnsNtt(n, moduli[l0:l0 + cnt])
+        xs = dev(shard_rows(x, n, nlimbs, l0, cnt))
+        got_f[:, l0:l0 + cnt, :] = host(plan.forward(torch.empty_like(xs), xs, 1, 1)).reshape(npolys, cnt, n)
+        got_i[:, l0:l0 + cnt, :] = host(plan.inverse(torch.empty_like(xs), xs, 1, 1)).reshape(npolys, cnt, n)
+        # the same shard through the full plan's limb sub-range
+        sub = host(full_plan.forward(torch.empty_like(xs), xs, 1, 1, limb0=l0, nlimbs=cnt))
+        assert np.array_equal(sub.reshape(npolys, cnt, n), got_f[:, l0:l0 + cnt, :])
+    assert np.array_equal(got_f.reshape(-1), want_f)
+    assert np.array_equal(got_i.reshape(-1), want_i)
+    assert np.array_equal(want_f, oracle.forward(n, moduli, x, 1, 1, threads=8))
+
+
+SENTINEL = 0x5A5A5A5A5A5A5A5A
+
+
+@pytest.mark.parametrize("logn,bits,npolys", [(4, 30, 3), (10, 50, 2), (12, 50, 1), (13, 60, 200),
+                                              (14, 50, 3), (14, 60, 2), (15, 50, 1), (16, 60, 1)])
+def test_writes_stay_in_bounds(nk, oracle, logn, bits, npolys):
+    """compute-sanitizer is closed on this GPU pool, so out-of-bounds global
+    writes are caught with guard words instead: the result is a view into a
+    larger buffer whose words before and after it hold a sentinel, for every
+    kernel family (small, block, latency, pair, single-CTA, global pass) and
+    both directions, in place and out of place; results still match the
+    oracle."""
+    n = 1 << logn
+    moduli = largest_ntt_primes(bits, n, 2)
+    x = rows_of(oracle, moduli, n, npolys, 777 + logn)
+    words, guard = x.size, 4096
+    plan = nk.RnsNtt(n, moduli)
+    for fwd in (True, False):
+        buf = torch.full((words + 2 * guard,), SENTINEL, dtype=torch.int64, device="cuda")
+        out = buf[guard:guard + words]
+        d = dev(x)
+        (plan.forward if fwd else plan.inverse)(out, d, 1, 1)
+        h = host(buf)
+        assert np.all(h[:guard] == np.uint64(SENTINEL)) and np.all(h[guard + words:] == np.uint64(SENTINEL))
+        want = (oracle.forward if fwd else oracle.inverse)(n, moduli, x, 1, 1, threads=8)
+        assert np.array_equal(h[guard:guard + words], want)
+        # in place inside the guarded buffer
+        buf = torch.full((words + 2 * guard,), SENTINEL, dtype=torch.int64, device="cuda")
+        buf[guard:guard + words] = dev(x)
+        mid = buf[guard:guard + words]
+        (plan.forward if fwd else plan.inverse)(mid, mid, 1, 1)
+        h = host(buf)
+        assert np.all(h[:guard] == np.uint64(SENTINEL)) and np.all(h[guard + words:] == np.uint64(SENTINEL))
+        assert np.array_equal(h[guard:guard + words], want)
