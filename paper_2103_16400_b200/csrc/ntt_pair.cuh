@@ -402,7 +402,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
     }
 
     NK_TS(7);
-    pass14<A, FWD, P3, false>(v, tw, twl, a.n, xbase + jt3, cst);
+    // canonical inverse (Arith52S, whole rows): n^-1 folded into the last stage
+    // (bit 13, single twiddle), as in ntt_block14_tma
+    constexpr bool kFoldLast = !FWD && A::kSigned;
+    if constexpr (kFoldLast) {
+      pass14<A, FWD, P3, false, 1>(v, tw, twl, a.n, xbase + jt3, cst);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) A::inv_fold(v[r], v[r + 16], cst);
+    } else {
+      pass14<A, FWD, P3, false>(v, tw, twl, a.n, xbase + jt3, cst);
+    }
     NK_TS(8);
 
     if (FWD) {
@@ -455,7 +464,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
         __syncwarp();
       }
     } else {
-      if (lognb == 0) {
+      if (kFoldLast) {
+        // already canonical
+      } else if (lognb == 0) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = inv_out<A>(v[i], cst, a.fout);
       } else {
