@@ -138,7 +138,7 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_reference(moduli, rows, reps, threads, min_seconds=0.0):
+def cpu_reference(moduli, rows, reps, threads, min_seconds=0.0, warm_seconds=1.0):
     """The reference's NttTables::forward/inverse (oracle/_ref, the unmodified
     nttkit headers) on `rows` rows with `threads` host threads; returns the
     per-step times (at least `reps` steps and at least `min_seconds` total)."""
@@ -150,9 +150,16 @@ def cpu_reference(moduli, rows, reps, threads, min_seconds=0.0):
     npolys = max(1, rows // len(moduli))
     x = make_inputs(moduli, npolys, SEED)[: rows * N]
     out = np.empty_like(x)
+    out.fill(0)  # pre-fault: first-touch page faults are not the reference's cost
     mods = np.asarray(moduli, np.uint64)
     p = ref.lib.ref_plan_create(N, mods.ctypes.data_as(C.POINTER(C.c_uint64)), mods.size)
     ptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint64))  # noqa: E731
+    # steady state: the first steps on a fresh box run up to 2x slower (thread
+    # start-up, clock ramp), so at least warm_seconds of untimed steps first
+    t_w = time.perf_counter()
+    while time.perf_counter() - t_w < warm_seconds:
+        ref.lib.ref_plan_ntt(p, 0, ptr(out), ptr(x), rows, 1, 1, threads)
+        ref.lib.ref_plan_ntt(p, 1, ptr(out), ptr(out), rows, 1, 1, threads)
     times = []
     t_start = time.perf_counter()
     while len(times) < reps or time.perf_counter() - t_start < min_seconds:
@@ -176,8 +183,9 @@ def run_reference(args):
     moduli = cfg3_moduli()
     threads = os.cpu_count() or 1
     rows = NPOLYS * NLIMBS
-    cpu_reference(moduli, rows, max(1, args.warmup), threads)  # warm-up
-    times = cpu_reference(moduli, rows, args.steps, threads)
+    # warm-up: W steps and at least 1 s of steady state (inside cpu_reference)
+    times = cpu_reference(moduli, rows, args.steps, threads,
+                          warm_seconds=max(1.0, args.warmup * 0.1))
     t = statistics.median(times)
     v = 2 * rows * N / t / 1e6
     line = {
