@@ -54,23 +54,106 @@ def peaks():
         return 6650.0, 1965.0, "fallback"
 
 
-def cfg3_moduli():
-    from primes import largest_ntt_primes
+def _is_prime(n):
+    """Deterministic Miller-Rabin for n < 2^64 (the first 12 primes as bases)."""
+    if n < 2:
+        return False
+    small = (2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37)
+    for p in small:
+        if n % p == 0:
+            return n == p
+    d, r = n - 1, 0
+    while d % 2 == 0:
+        d //= 2
+        r += 1
+    for a in small:
+        x = pow(a, d, n)
+        if x in (1, n - 1):
+            continue
+        for _ in range(r - 1):
+            x = x * x % n
+            if x == n - 1:
+                break
+        else:
+            return False
+    return True
 
+
+def largest_ntt_primes(bits, n, count):
+    """Descending from 2^bits in steps of 2n: the primes q == 1 (mod 2n) below
+    2^bits (the BASELINE configs' moduli)."""
+    out, two_n = [], 2 * n
+    c = ((1 << bits) - 1) // two_n * two_n + 1
+    while len(out) < count and c > 2:
+        if c < (1 << bits) and _is_prime(c):
+            out.append(c)
+        c -= two_n
+    return out
+
+
+def cfg3_moduli():
+    """The 32 largest primes < 2^50 that are 1 mod 2N, descending
+    (tests/test_bench_inputs.py pins the list)."""
     return largest_ntt_primes(50, N, NLIMBS)
 
 
-def make_inputs(moduli, npolys, seed):
-    """[npolys][nlimbs][N] uniform in [0, q_l); the generator runs in parallel
-    per row (row r seeded seed + r) with numpy for speed."""
-    from oracle_lib import Oracle
+def cfg2_modulus():
+    """The largest prime below 2^60 (2^60 - 93)."""
+    c = (1 << 60) - 1
+    while not _is_prime(c):
+        c -= 2
+    return c
 
-    o = Oracle()
+
+_MT_NN, _MT_MM = 312, 156
+_MT_A, _MT_UM, _MT_LM = np.uint64(0xB5026F5AA96619E9), np.uint64(0xFFFFFFFF80000000), np.uint64(0x7FFFFFFF)
+
+
+def mt19937_64_rows(seeds, count):
+    """std::mt19937_64 streams, one per seed, vectorised over the seeds with
+    numpy: returns [len(seeds)][count] raw outputs (C++ [rand.eng.mers],
+    tests/test_bench_inputs.py checks it against the C generator)."""
+    u = np.uint64
+    rows = len(seeds)
+    mt = np.empty((rows, _MT_NN), np.uint64)
+    mt[:, 0] = np.asarray(seeds, np.uint64)
+    with np.errstate(over="ignore"):
+        for i in range(1, _MT_NN):
+            prev = mt[:, i - 1]
+            mt[:, i] = u(6364136223846793005) * (prev ^ (prev >> u(62))) + u(i)
+    out = np.empty((rows, count), np.uint64)
+    done = 0
+
+    def mix(a, b):
+        x = (a & _MT_UM) | (b & _MT_LM)
+        return (x >> u(1)) ^ np.where((x & u(1)) != 0, _MT_A, u(0))
+
+    while done < count:
+        # twist in three vectorised blocks (each block reads only finished words)
+        k = _MT_NN - _MT_MM
+        mt[:, :k] = mt[:, _MT_MM:] ^ mix(mt[:, :k], mt[:, 1:k + 1])
+        mt[:, k:_MT_NN - 1] = mt[:, :_MT_NN - 1 - k] ^ mix(mt[:, k:_MT_NN - 1], mt[:, k + 1:])
+        mt[:, _MT_NN - 1] = mt[:, _MT_MM - 1] ^ mix(mt[:, _MT_NN - 1], mt[:, 0])
+        y = mt.copy()
+        y ^= (y >> u(29)) & u(0x5555555555555555)
+        y ^= (y << u(17)) & u(0x71D67FFFEDA60000)
+        y ^= (y << u(37)) & u(0xFFF7EEE000000000)
+        y ^= y >> u(43)
+        take = min(_MT_NN, count - done)
+        out[:, done:done + take] = y[:, :take]
+        done += take
+    return out
+
+
+def make_inputs(moduli, npolys, seed):
+    """[npolys][nlimbs][N] uniform in [0, q_l): row r is std::mt19937_64(seed + r)
+    reduced mod its limb's q, the reference bench's eng() % q
+    (bench.hpp:126-131)."""
     L = len(moduli)
-    x = np.empty((npolys * L, N), np.uint64)
-    for r in range(npolys * L):
-        x[r] = o.mt19937_64(seed + r, N, moduli[r % L])
-    return x.reshape(-1)
+    rows = npolys * L
+    raw = mt19937_64_rows([seed + r for r in range(rows)], N)
+    q = np.asarray([moduli[r % L] for r in range(rows)], np.uint64)[:, None]
+    return (raw % q).reshape(-1)
 
 
 class ClockSampler:
@@ -138,7 +221,7 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_reference(moduli, rows, reps, threads, min_seconds=0.0, warm_seconds=1.0):
+def cpu_reference(moduli, rows, reps, threads, min_seconds=0.0, warm_seconds=1.0, check_forward=None):
     """The reference's NttTables::forward/inverse (oracle/_ref, the unmodified
     nttkit headers) on `rows` rows with `threads` host threads; returns the
     per-step times (at least `reps` steps and at least `min_seconds` total)."""
@@ -156,6 +239,9 @@ def cpu_reference(moduli, rows, reps, threads, min_seconds=0.0, warm_seconds=1.0
     ptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_uint64))  # noqa: E731
     # steady state: the first steps on a fresh box run up to 2x slower (thread
     # start-up, clock ramp), so at least warm_seconds of untimed steps first
+    if check_forward is not None:  # the GPU forward's words against the reference's
+        ref.lib.ref_plan_ntt(p, 0, ptr(out), ptr(x), rows, 1, 1, threads)
+        assert np.array_equal(out, check_forward[: out.size]), "GPU forward differs from the reference"
     t_w = time.perf_counter()
     while time.perf_counter() - t_w < warm_seconds:
         ref.lib.ref_plan_ntt(p, 0, ptr(out), ptr(x), rows, 1, 1, threads)
@@ -220,7 +306,6 @@ def modmul_bench(stream, reps=20):
     import torch
 
     import paper_2103_16400_b200 as nk
-    from primes import cfg2_modulus
 
     q = cfg2_modulus()
     n = 1 << 20
@@ -310,17 +395,13 @@ def run_gpu(args):
         plan.forward(d_f, d_in, 1, 1)
         plan.inverse(d_b, d_f, 1, 1)
 
-    # correctness gate before timing (bench.hpp:346-356 convention)
+    # correctness gate before timing (bench.hpp:346-356 convention): the round
+    # trip here; rank 0's cpu_baseline leg also checks the forward words
+    # against the reference's own (the only use of oracle/ in this arm)
     step()
     torch.cuda.synchronize()
     assert torch.equal(d_b, d_in), "round trip mismatch"
-    from oracle_lib import Oracle
-
-    o = Oracle()
-    rows_chk = NLIMBS
-    want = o.forward(N, moduli, x[: rows_chk * N], 1, 1, threads=os.cpu_count() or 1)
-    assert np.array_equal(d_f[: rows_chk * N].cpu().numpy().view(np.uint64), want), \
-        "forward mismatch vs oracle"
+    fwd_words = d_f.cpu().numpy().view(np.uint64) if (rank == 0 and not args.no_cpu_baseline) else None
 
     for _ in range(args.warmup):
         step()
@@ -398,7 +479,7 @@ def run_gpu(args):
         if not args.no_cpu_baseline:
             threads = os.cpu_count() or 1
             rows = NPOLYS * NLIMBS
-            times = cpu_reference(moduli, rows, 2, threads, min_seconds=10.0)
+            times = cpu_reference(moduli, rows, 2, threads, min_seconds=10.0, check_forward=fwd_words)
             tt = statistics.median(times)
             cpu = {"value": 2 * rows * N / tt / 1e6, "unit": "Mcoeff/s", "cores": threads,
                    "kind": "reference",

@@ -1,0 +1,29 @@
+"""bench.py's input generation and moduli are oracle-free (only its
+cpu_baseline leg may use oracle/); here they are checked against the oracle's
+C generator and prime search."""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from primes import cfg2_modulus, largest_ntt_primes  # noqa: E402
+
+
+def test_mt19937_64_rows_match_oracle(oracle):
+    seeds = [0, 1, 5489, 20260809, 2**63 + 12345, 2**64 - 1]
+    raw = bench.mt19937_64_rows(seeds, 1000)
+    for s, row in zip(seeds, raw):
+        assert np.array_equal(row, oracle.mt19937_64(s, 1000, 0)), s
+
+
+def test_make_inputs_and_moduli_match_oracle(oracle):
+    moduli = bench.cfg3_moduli()
+    assert moduli == largest_ntt_primes(50, bench.N, bench.NLIMBS)
+    assert bench.cfg2_modulus() == cfg2_modulus()
+    x = bench.make_inputs(moduli[:3], 2, 777).reshape(6, bench.N)
+    for r in range(6):
+        assert np.array_equal(x[r], oracle.mt19937_64(777 + r, bench.N, moduli[r % 3])), r

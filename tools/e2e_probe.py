@@ -43,7 +43,7 @@ def pcie():
 
 def e2e():
     import paper_2103_16400_b200 as nk
-    from primes import largest_ntt_primes
+    from bench import largest_ntt_primes
     n, limbs, polys = 16384, 32, 64
     m = largest_ntt_primes(50, n, limbs)
     plan = nk.RnsNtt(n, m)

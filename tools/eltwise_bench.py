@@ -3,7 +3,7 @@ import sys, os
 import torch
 sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
 import paper_2103_16400_b200 as nk
-from primes import cfg2_modulus
+from bench import cfg2_modulus
 q = cfg2_modulus(); n = 1 << 20; sets = 16; reps = 20
 g = torch.Generator(device="cuda").manual_seed(2)
 a = torch.randint(0, 1 << 59, (sets, n), dtype=torch.int64, device="cuda", generator=g)

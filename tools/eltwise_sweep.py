@@ -1,7 +1,7 @@
 import sys, torch
 sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
 import paper_2103_16400_b200 as nk
-from primes import cfg2_modulus
+from bench import cfg2_modulus
 q = cfg2_modulus()
 for logn in (18, 20, 22, 24, 26):
     n = 1 << logn; sets = max(2, (1 << 28) // (24 * n) + 1); reps = 10

@@ -9,7 +9,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
 import paper_2103_16400_b200 as nk  # noqa: E402
-from primes import cfg2_modulus  # noqa: E402
+from bench import cfg2_modulus  # noqa: E402
 
 q = cfg2_modulus()
 n = 1 << 20

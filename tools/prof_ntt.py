@@ -15,7 +15,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 import paper_2103_16400_b200 as nk  # noqa: E402
-from primes import largest_ntt_primes  # noqa: E402
+from bench import largest_ntt_primes  # noqa: E402
 
 
 def main():

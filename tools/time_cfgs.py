@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
 
 import paper_2103_16400_b200 as nk  # noqa: E402
-from primes import cfg2_modulus, largest_ntt_primes  # noqa: E402
+from bench import cfg2_modulus, largest_ntt_primes  # noqa: E402
 
 
 def timed(fn, reps=20, warm=3):

@@ -11,7 +11,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path[:0] = [ROOT, os.path.join(ROOT, "tests")]
 import paper_2103_16400_b200 as nk  # noqa: E402
-from primes import largest_ntt_primes  # noqa: E402
+from bench import largest_ntt_primes  # noqa: E402
 
 n = 16384
 moduli = largest_ntt_primes(50, n, 32)
