@@ -219,6 +219,8 @@ int launch_pair_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cud
   if (int rc = FWD ? make_superline_map(&map, a.in, buf_words) : make_row_map(&map, a.in, buf_words)) return rc;
   if (int rc = make_out_map(&omap, a.out, buf_words)) return rc;
   auto kern = nk::ntt_pair14<A, FWD, IL>;
+  if constexpr (FWD && std::is_same_v<A, nk::Arith52S>)
+    if (a.mulb) kern = nk::ntt_pair14<A, FWD, IL, true>;
   if (int rc = set_smem(kern, nk::kPairSmemBytes)) return rc;
   static int max_clusters[64] = {};
   int dev = 0;

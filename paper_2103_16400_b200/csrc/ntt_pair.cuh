@@ -164,7 +164,9 @@ __device__ __forceinline__ void bulk_wait_read() {
 
 // tout (forward): 3D view [words/32][2][16] of the result, boxes 16 x 1 x 32
 // with 128B swizzle = one warp's output round straight from its image.
-template <class A, bool FWD, bool ILTM0>
+// MULB: the fused poly_mult_mod forward (dyadic product in the store; a
+// separate instance so the plain transform carries none of its registers)
+template <class A, bool FWD, bool ILTM0, bool MULB = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
     ntt_pair14(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, NttArgs a,
                uint32_t nitems) {
@@ -416,13 +418,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
 
     if (FWD) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = fwd_out<A>(v[i], cst, a.fout);
       // 32 contiguous words per thread -> coalesced lines through the warp
       // image (32 rows of 16 words, 128B swizzle), one round per bit 4
       uint8_t* Wb = reinterpret_cast<uint8_t*>(W);
       uint64_t* wdst = dst + (w << 10) + (c << 13);
-      const uint64_t* mulb = a.mulb ? a.mulb + row * a.n + boff + (w << 10) + (c << 13) : nullptr;
-      if (!mulb) {
+      const uint64_t* mulb = MULB ? a.mulb + row * a.n + boff + (w << 10) + (c << 13) : nullptr;
+      // the fused product multiplies the signed words and canonicalises once
+      // (mulmod_signed_canon) in the store loop below
+      if constexpr (!(A::kSigned && MULB)) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = fwd_out<A>(v[i], cst, a.fout);
+      }
+      if constexpr (!MULB) {
         // the image rows are the TMA box rows: one bulk tensor store per round
         const int32_t srow = static_cast<int32_t>((row * a.n + boff + (w << 10) + (c << 13)) >> 5);
 #pragma unroll
@@ -452,11 +459,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
           const uint32_t rw = (l >> 3) + 4 * s2, cc = l & 7;
           ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Wb + (rw << 7) + ((cc ^ (rw & 7)) << 4));
           const uint32_t off = (rw << 5) + (h << 4) + (cc << 1);
-          if constexpr (A::kSigned) {
-            if (mulb) {  // fused dyadic product of poly_mult_mod (ring.hpp:39-41)
+          if constexpr (A::kSigned && MULB) {
+            {  // fused dyadic product of poly_mult_mod (ring.hpp:39-41)
               const ulonglong2 gb = __ldg(reinterpret_cast<const ulonglong2*>(mulb + off));
-              p.x = mulmod_canon(p.x, gb.x, cst);
-              p.y = mulmod_canon(p.y, gb.y, cst);
+              p.x = mulmod_signed_canon(p.x, gb.x, cst);
+              p.y = mulmod_signed_canon(p.y, gb.y, cst);
             }
           }
           *reinterpret_cast<ulonglong2*>(wdst + off) = p;
