@@ -187,6 +187,8 @@ int launch_tma_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cuda
   CUtensorMap map;
   if (int rc = make_row_map(&map, a.in, buf_words)) return rc;
   auto kern = nk::ntt_block14_tma<A, FWD, IL>;
+  if constexpr (!FWD)
+    if (a.logn > 14) kern = nk::ntt_block14_tma<A, FWD, IL, true>;
   if (int rc = set_smem(kern, nk::kTmaSmemBytes)) return rc;
   const uint64_t g = nitems < static_cast<uint64_t>(sm_count()) ? nitems : sm_count();
   kern<<<static_cast<unsigned>(g), 512, nk::kTmaSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));

@@ -502,7 +502,9 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __re
   }
 }
 
-template <class A, bool FWD, bool ILTM0>
+// LONG: the launch covers the low 14 bits of longer rows (an inverse then
+// stores intermediates only): a separate instance without the final-word code.
+template <class A, bool FWD, bool ILTM0, bool LONG = false>
 __global__ void __launch_bounds__(512, 1)
     ntt_block14_tma(const __grid_constant__ CUtensorMap tin, NttArgs a, uint32_t nitems) {
   using SC = Sched14<FWD>;
@@ -665,7 +667,10 @@ __global__ void __launch_bounds__(512, 1)
         __syncthreads();
       }
     } else {
-      if (kFoldLast) {
+      if constexpr (LONG) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = A::store(v[i]);  // intermediate of a long row
+      } else if constexpr (kFoldLast) {
         // already canonical
       } else if (lognb == 0) {
 #pragma unroll
