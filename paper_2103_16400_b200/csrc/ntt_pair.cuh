@@ -417,7 +417,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
     NK_TS(8);
 
     if (FWD) {
-#pragma unroll
       // 32 contiguous words per thread -> coalesced lines through the warp
       // image (32 rows of 16 words, 128B swizzle), one round per bit 4
       uint8_t* Wb = reinterpret_cast<uint8_t*>(W);
