@@ -11,8 +11,18 @@ import sys
 
 rep = sys.argv[1]
 kre = sys.argv[2] if len(sys.argv) > 2 else "ntt"
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
-                      "regex:" + kre], capture_output=True, text=True).stdout
+if rep.endswith(".csv") or rep.endswith(".csv.gz"):  # a --page source export (tools/gpu_check.sh)
+    import gzip
+    import re
+    opener = gzip.open if rep.endswith(".gz") else open
+    with opener(rep, "rt") as f:
+        text = f.read()
+    # keep the kernels whose name matches kre
+    parts = re.split(r'(?m)^(?="Kernel Name")', text)
+    out = "".join(p for p in parts if p.startswith('"Kernel Name"') and re.search(kre, p.splitlines()[0]))
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k",
+                          "regex:" + kre], capture_output=True, text=True).stdout
 lines = out.splitlines()
 # multiple kernels: blocks start with "Kernel Name"
 blocks, cur = [], None
