@@ -195,6 +195,7 @@ constexpr double kC52x15 = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer 
 
 template <int BS>
 struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)
+  static constexpr int kIltmFwd = 1;  // forward stages whose pre-reduction is skipped at fin = 1
   static constexpr bool kLoose = false;
   static constexpr bool kFP = false;
   __device__ static uint64_t load(uint64_t x) { return x; }
@@ -227,6 +228,7 @@ struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)
 };
 
 struct Arith52F {  // beta = 2^52 on the FP64 pipe (requires 4q < 2^52)
+  static constexpr int kIltmFwd = 1;  // forward stages whose pre-reduction is skipped at fin = 1
   static constexpr bool kLoose = false;
   static constexpr bool kFP = true;
   __device__ static uint64_t load(uint64_t x) { return x | kDBias; }
@@ -282,6 +284,7 @@ __device__ __forceinline__ double csubP(double y, double m) {
 }
 
 struct Arith52P {
+  static constexpr int kIltmFwd = 1;  // forward stages whose pre-reduction is skipped at fin = 1
   static constexpr bool kLoose = false;
   static constexpr bool kFP = true;
   __device__ static uint64_t load(uint64_t x) { return as_u(__dsub_rn(as_d(x | kDBias), kC52)); }
@@ -359,6 +362,12 @@ __device__ __forceinline__ double csubS(double y, double m) {
 }
 
 struct Arith52S {
+  // Forward stages without the conditional subtraction when the input is
+  // canonical (fin = 1): |x| < q in; after stage 1 |x| < q + q(1 + q/2^52)
+  // < 2.25q; stage 2's multiplicand is then < 2.25q < 4q (valid quotient) and
+  // its outputs are < 2.25q + q(1 + 2.25q/2^52) < 3.82q < 4q, the invariant
+  // the reducing stages start from (every bound uses q < 2^50).
+  static constexpr int kIltmFwd = 2;
   static constexpr bool kLoose = false;
   static constexpr bool kFP = true;
   static constexpr bool kSigned = true;
@@ -432,6 +441,7 @@ __device__ __forceinline__ uint64_t mul_loose(uint64_t x, uint64_t w, uint64_t w
 }
 
 struct ArithIntL {
+  static constexpr int kIltmFwd = 1;  // forward stages whose pre-reduction is skipped at fin = 1
   using Tw = ulonglong2;
   static constexpr bool kFP = false;
   static constexpr bool kSigned = false;
