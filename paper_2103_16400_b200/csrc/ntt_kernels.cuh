@@ -135,7 +135,7 @@ __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const ulonglon
           uint64_t& x0 = v[g * R + r0];
           uint64_t& x1 = v[g * R + r1];
           if (FWD) {
-            if (ILTM0 && s == 0) A::template fwd<true>(x0, x1, w, c);
+            if (ILTM0 && s < A::kIltmFwd) A::template fwd<true>(x0, x1, w, c);
             else A::template fwd<false>(x0, x1, w, c);
           } else {
             if (ILTM0 && s == 0) A::template inv<true>(x0, x1, w, c);
