@@ -1,9 +1,12 @@
 #!/usr/bin/env python
-"""Small invocations of every kernel family for compute-sanitizer
-(tools/sanitize.sh): each case runs once, checked against the oracle, so a
-sanitizer report can be tied to a kernel and a result.
+"""Small invocations of every kernel family for compute-sanitizer: each case
+runs once, checked against the oracle, so a sanitizer report can be tied to a
+kernel and a result. (compute-sanitizer is closed on this round's GPU pool;
+the guard-word tests in tests/ stand in for memcheck there.)
 
     python tools/sanitize_cases.py [case ...]     (no args: all cases)
+    compute-sanitizer --tool {memcheck,racecheck,synccheck,initcheck} \
+        python tools/sanitize_cases.py <case>
 """
 import os
 import sys
