@@ -458,6 +458,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
         for (int cc = 0; cc < 8; ++cc)
           *reinterpret_cast<ulonglong2*>(Wb + (l << 7) + ((cc ^ (l & 7)) << 4)) =
               make_ulonglong2(v[16 * h + 2 * cc], v[16 * h + 2 * cc + 1]);
+        // the round's multiplier words in flight across the image round trip,
+        // issued once the round's words left their registers (cfg5 736 -> 730 us)
+        ulonglong2 gbv[8];
+        if constexpr (A::kSigned && MULB) {
+#pragma unroll
+          for (int s2 = 0; s2 < 8; ++s2)
+            gbv[s2] = __ldg(reinterpret_cast<const ulonglong2*>(
+                mulb + ((((l >> 3) + 4 * s2) << 5) + (h << 4) + ((l & 7) << 1))));
+        }
         __syncwarp();
 #pragma unroll
         for (int s2 = 0; s2 < 8; ++s2) {  // 32 rows, 4 per warp instruction
@@ -466,7 +475,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
           const uint32_t off = (rw << 5) + (h << 4) + (cc << 1);
           if constexpr (A::kSigned && MULB) {
             {  // fused dyadic product of poly_mult_mod (ring.hpp:39-41)
-              const ulonglong2 gb = __ldg(reinterpret_cast<const ulonglong2*>(mulb + off));
+              const ulonglong2 gb = gbv[s2];
               p.x = mulmod_signed_canon(p.x, gb.x, cst);
               p.y = mulmod_signed_canon(p.y, gb.y, cst);
             }
