@@ -191,24 +191,23 @@ uint64_t nk_launch_count(void);
 /* Debug aid: device buffer that a library built with -DNK_DBG_TIMELINE fills
  * with per-warp phase timestamps of the CTA-pair forward kernel
  * (tools/timeline.py; 296 x 8 x 32 x 16 words). NULL (the default) disables it;
- * the normal build ignores it. */
+ * the normal build ignores it. Per calling thread. */
 void nk_debug_dump_to(uint64_t* d_buf);
 /* Testing aid: when on, every beta = 2^52 transform uses the exact lazy
  * arithmetic (the reference's representatives) even where only the canonical
  * result is observable, so the tests can cover both arithmetic paths. Off by
- * default. */
+ * default; applies to calls made by the calling thread only. */
 void nk_debug_exact_only(int on);
 /* Testing aid: which kernel transforms 16384-word blocks. -1 (default) = the
- * faster one per direction, 0 = the CTA-pair kernel, 1 = the single-CTA kernel,
- * 2 = the warp-per-item kernel (whole N = 16384 rows only), 4 = the staged
- * warp-per-item forward, 5 = the 3-barrier inverse; 6 = defaults, but batches
- * of 2^11..2^13-word rows smaller than the SM count take the plain block kernel
- * instead of the latency kernel (ntt_block_lat). */
+ * faster one per direction, 0 = the CTA-pair kernel, 1 = the single-CTA kernel;
+ * 6 = defaults, but batches of 2^11..2^13-word rows smaller than the SM count
+ * take the plain block kernel instead of the latency kernel (ntt_block_lat).
+ * Applies to calls made by the calling thread only. */
 void nk_debug_block_kernel(int which);
 /* Testing aid: one butterfly per element pair (x0[i], x1[i]) -> (y0[i], y1[i])
  * in an arithmetic policy of the kernels (0 = ArithInt<64>, 1 = ArithInt<52>,
- * 2 = Arith52P, 3 = Arith52S with int64 words in and out, 4 = ArithIntL,
- * 5 = Arith52F), twiddle w with its Shoup quotient for the policy's width;
+ * 2 = Arith52P, 3 = Arith52S with int64 words in and out, 4 = ArithIntL),
+ * twiddle w with its Shoup quotient for the policy's width;
  * fwd != 0: the forward (CT) butterfly, else the inverse (GS). Device buffers. */
 int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint64_t* d_x0,
                          const uint64_t* d_x1, uint64_t n, uint64_t* d_y0, uint64_t* d_y1);

@@ -13,40 +13,47 @@
 #include <cstring>
 #include <initializer_list>
 #include <mutex>
-#include <unordered_map>
 #include <string>
 #include <vector>
 
 #include "../../include/nttkit_b200.h"
 #include "eltwise_kernels.cuh"
 #include "host_math.hpp"
-#include "ntt_kernels.cuh"
-#include "ntt_pair.cuh"
-#include "ntt_warp.cuh"
+#include "runtime.hpp"
 
 using nk::host::u128;
 
-namespace {
-
+// ---------------------------------------------------------------------------
+// shared runtime state (runtime.hpp)
+// ---------------------------------------------------------------------------
+namespace nk::rt {
 thread_local std::string g_err;
-uint64_t* g_dbg = nullptr;  // nk_debug_dump_to()
-bool g_exact_only = false;  // nk_debug_exact_only()
-std::atomic<uint64_t> g_launches{0};
-
 int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
-
 int cuda_fail(cudaError_t e, const char* what) {
   return fail(NK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
+std::atomic<uint64_t> launches{0};
+thread_local int block_kernel = -1;
+thread_local bool no_lat = false;
+thread_local bool exact_only = false;
+thread_local uint64_t* dbg = nullptr;
 
-#define NK_CUDA(call)                                   \
-  do {                                                  \
-    cudaError_t e_ = (call);                            \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
-  } while (0)
+int sm_count() {
+  static int n[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!n[dev & 63]) cudaDeviceGetAttribute(&n[dev & 63], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev & 63] ? n[dev & 63] : 148;
+}
+}  // namespace nk::rt
+
+using nk::rt::cuda_fail;
+using nk::rt::fail;
+
+namespace {
 
 // Small per-thread cache of validated moduli: Modulus(q) runs Miller-Rabin
 // (modarith.hpp:108-115); element-wise calls re-validate the same q repeatedly.
@@ -75,23 +82,42 @@ uint64_t dbits(double d) {
   return u;
 }
 
-int ensure_device(int dev) {
-  int cur = -1;
-  NK_CUDA(cudaGetDevice(&cur));
-  if (cur != dev) NK_CUDA(cudaSetDevice(dev));
-  // stream-ordered scratch (poly_mult_mod's g^, per-call counters) comes from
-  // the device's default pool; keep freed blocks in the pool instead of
-  // returning them to the driver at every synchronisation
-  static std::once_flag pool_once[64];
-  std::call_once(pool_once[dev & 63], [dev] {
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+// Makes `dev` current for the duration of one entry-point call and restores
+// the caller's device on return (a call on a plan of another GPU must not
+// move the caller's torch/CUDA current device).
+class DeviceScope {
+ public:
+  DeviceScope() = default;
+  DeviceScope(const DeviceScope&) = delete;
+  DeviceScope& operator=(const DeviceScope&) = delete;
+  ~DeviceScope() {
+    if (prev_ >= 0) cudaSetDevice(prev_);
+  }
+  int enter(int dev) {
+    int cur = -1;
+    NK_CUDA(cudaGetDevice(&cur));
+    if (cur != dev) {
+      NK_CUDA(cudaSetDevice(dev));
+      prev_ = cur;
     }
-  });
-  return 0;
-}
+    // stream-ordered scratch (poly_mult_mod's g^, unaligned views, the host
+    // pipeline's chunks) comes from the device's default pool; keep freed
+    // blocks in the pool instead of returning them to the driver at every
+    // synchronisation
+    static std::once_flag pool_once[64];
+    std::call_once(pool_once[dev & 63], [dev] {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    });
+    return 0;
+  }
+
+ private:
+  int prev_ = -1;
+};
 
 }  // namespace
 
@@ -110,392 +136,22 @@ struct nk_plan {
 };
 
 // ---------------------------------------------------------------------------
-// kernel dispatch
+// transform dispatch (kernel choice: dispatch.cuh, compiled per policy in ntt_inst.cu)
 // ---------------------------------------------------------------------------
+namespace nk::rt {
+extern template int run_ntt<Arith52S, true>(NttArgs, uint64_t, cudaStream_t);
+extern template int run_ntt<Arith52S, false>(NttArgs, uint64_t, cudaStream_t);
+extern template int run_ntt<Arith52P, true>(NttArgs, uint64_t, cudaStream_t);
+extern template int run_ntt<Arith52P, false>(NttArgs, uint64_t, cudaStream_t);
+extern template int run_ntt<ArithIntL, true>(NttArgs, uint64_t, cudaStream_t);
+extern template int run_ntt<ArithIntL, false>(NttArgs, uint64_t, cudaStream_t);
+extern template int run_ntt<ArithInt<64>, true>(NttArgs, uint64_t, cudaStream_t);
+extern template int run_ntt<ArithInt<64>, false>(NttArgs, uint64_t, cudaStream_t);
+}  // namespace nk::rt
+
 namespace {
-
-// ---- TMA tensor maps (driver entry point fetched through the runtime) ----
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-int encode_fn(EncodeTiledFn* out) {
-  static EncodeTiledFn fn = nullptr;
-  static cudaError_t err = cudaSuccess;
-  static std::once_flag once;
-  std::call_once(once, [&] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
-    if (err == cudaSuccess && q != cudaDriverEntryPointSuccess) err = cudaErrorNotSupported;
-    fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  if (err != cudaSuccess) return cuda_fail(err, "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
-  *out = fn;
-  return 0;
-}
-
-// 2D view [words/16][16] of a row buffer, 128B swizzle, boxes of 256 x 128 B.
-int make_row_map(CUtensorMap* map, const uint64_t* base, uint64_t words) {
-  EncodeTiledFn fn;
-  if (int rc = encode_fn(&fn)) return rc;
-  const cuuint64_t dims[2] = {16, words / 16};
-  const cuuint64_t strides[1] = {128};
-  const cuuint32_t box[2] = {16, 256};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint64_t*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(NK_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
-  return 0;
-}
-
-// 3D view [words/512][32 lines][16 words] (no swizzle), boxes 16 x 16 x 32:
-// one box = the 8192 words of a 16384-word block with index bit 8 fixed.
-int make_superline_map(CUtensorMap* map, const uint64_t* base, uint64_t words) {
-  EncodeTiledFn fn;
-  if (int rc = encode_fn(&fn)) return rc;
-  const cuuint64_t dims[3] = {16, 32, words / 512};
-  const cuuint64_t strides[2] = {128, 4096};
-  const cuuint32_t box[3] = {16, 16, 32};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t*>(base), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(NK_ERR_CUDA, "cuTensorMapEncodeTiled(3D) failed (" + std::to_string(r) + ")");
-  return 0;
-}
-
-int sm_count() {
-  static int n[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!n[dev & 63]) cudaDeviceGetAttribute(&n[dev & 63], cudaDevAttrMultiProcessorCount, dev);
-  return n[dev & 63] ? n[dev & 63] : 148;
-}
-
-template <class K>
-int set_smem(K kernel, size_t bytes) {
-  // idempotent and cheap; done per launch so every device of the process is covered
-  NK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
-  return 0;
-}
-
-template <class A, bool FWD, bool IL>
-int launch_tma_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
-  CUtensorMap map;
-  if (int rc = make_row_map(&map, a.in, buf_words)) return rc;
-  auto kern = nk::ntt_block14_tma<A, FWD, IL>;
-  if constexpr (!FWD)
-    if (a.logn > 14) kern = nk::ntt_block14_tma<A, FWD, IL, true>;
-  if (int rc = set_smem(kern, nk::kTmaSmemBytes)) return rc;
-  const uint64_t g = nitems < static_cast<uint64_t>(sm_count()) ? nitems : sm_count();
-  kern<<<static_cast<unsigned>(g), 512, nk::kTmaSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));
-  g_launches++;
-  NK_CUDA(cudaGetLastError());
-  return 0;
-}
-
-// CTA-pair kernel (ntt_pair.cuh): persistent, one cluster of 2 per block in
-// flight, as many clusters as fit (2 CTAs per SM).
-// 3D view [words/32][2][16] (128B swizzle), boxes 16 x 1 x 32: one half of 32
-// consecutive 32-word runs = one warp's output round of ntt_pair14 (forward)
-int make_out_map(CUtensorMap* map, const uint64_t* base, uint64_t words) {
-  EncodeTiledFn fn;
-  if (int rc = encode_fn(&fn)) return rc;
-  const cuuint64_t dims[3] = {16, 2, words / 32};
-  const cuuint64_t strides[2] = {128, 256};
-  const cuuint32_t box[3] = {16, 1, 32};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t*>(base), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(NK_ERR_CUDA, "cuTensorMapEncodeTiled(out) failed (" + std::to_string(r) + ")");
-  return 0;
-}
-
-template <class A, bool FWD, bool IL>
-int launch_pair_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
-  CUtensorMap map, omap;
-  if (int rc = FWD ? make_superline_map(&map, a.in, buf_words) : make_row_map(&map, a.in, buf_words)) return rc;
-  if (int rc = make_out_map(&omap, a.out, buf_words)) return rc;
-  auto kern = nk::ntt_pair14<A, FWD, IL>;
-  if constexpr (FWD && std::is_same_v<A, nk::Arith52S>)
-    if (a.mulb) kern = nk::ntt_pair14<A, FWD, IL, true>;
-  if (int rc = set_smem(kern, nk::kPairSmemBytes)) return rc;
-  static int max_clusters[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!max_clusters[dev & 63]) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * sm_count());
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = nk::kPairSmemBytes;
-    cudaLaunchAttribute attr;
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = 2;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    NK_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
-    max_clusters[dev & 63] = n > 0 ? n : sm_count();
-  }
-  const uint64_t mc = static_cast<uint64_t>(max_clusters[dev & 63]);
-  const uint64_t g = nitems < mc ? nitems : mc;
-  kern<<<static_cast<unsigned>(2 * g), 256, nk::kPairSmemBytes, st>>>(map, omap, a, static_cast<uint32_t>(nitems));
-  g_launches++;
-  NK_CUDA(cudaGetLastError());
-  return 0;
-}
-
-bool g_no_lat = false;     // nk_debug_block_kernel(6): small batches take ntt_block instead of ntt_block_lat
-int g_block_kernel = -1;  // nk_debug_block_kernel(): -1 auto, 0 pair, 1 single, 2 warp, 4 staged warp (fwd), 5 3-barrier inverse
-
-// Warp-per-item kernel (ntt_warp.cuh) for whole 16384-word rows: persistent,
-// every warp resident; per-row phase counters live in a stream-ordered
-// allocation of this call (tables stay shareable across concurrent calls).
-// 2D view [words/128][128] of a row buffer (no swizzle), boxes of 8 x 128:
-// the 8-column items of the warp-per-item forward
-int make_cols_map(CUtensorMap* map, const uint64_t* base, uint64_t words) {
-  EncodeTiledFn fn;
-  if (int rc = encode_fn(&fn)) return rc;
-  const cuuint64_t dims[2] = {128, words / 128};
-  const cuuint64_t strides[1] = {1024};
-  const cuuint32_t box[2] = {8, 128};
-  const cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<uint64_t*>(base), dims, strides, box,
-                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return fail(NK_ERR_CUDA, "cuTensorMapEncodeTiled(cols) failed (" + std::to_string(r) + ")");
-  return 0;
-}
-
-// staged warp-per-item forward (ntt_warp14s)
-template <class A>
-int launch_warps_t(const nk::NttArgs& a, uint64_t buf_words, cudaStream_t st) {
-  CUtensorMap map;
-  if (int rc = make_cols_map(&map, a.in, buf_words)) return rc;
-  auto kern = nk::ntt_warp14s<A, false>;
-  if (int rc = set_smem(kern, nk::kWarpSSmemBytes)) return rc;
-  static int per_sm[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!per_sm[dev & 63]) {
-    int n = 0;
-    NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 256, nk::kWarpSSmemBytes));
-    per_sm[dev & 63] = n > 0 ? n : 1;
-  }
-  const uint64_t items = a.rows * 32;
-  uint64_t grid = static_cast<uint64_t>(per_sm[dev & 63]) * sm_count();
-  const uint64_t need = (items + nk::kWarpsPerCta - 1) / nk::kWarpsPerCta;
-  if (grid > need) grid = need;
-  uint32_t* cnt = nullptr;
-  const size_t cbytes = (a.rows + 1) * sizeof(uint32_t);
-  NK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cnt), cbytes, st));
-  NK_CUDA(cudaMemsetAsync(cnt, 0, cbytes, st));
-  // lag: a row's phase-1 items sit more than one round (grid warps) behind its
-  // phase-0 items, so no warp ever waits on an item of its own
-  const uint32_t lag = static_cast<uint32_t>(grid * nk::kWarpsPerCta / 16 + 2);
-  nk::WarpNttArgs wa{a, cnt, cnt + a.rows, lag};
-  kern<<<static_cast<unsigned>(grid), 256, nk::kWarpSSmemBytes, st>>>(map, wa);
-  g_launches++;
-  cudaError_t e = cudaGetLastError();
-  cudaFreeAsync(cnt, st);
-  if (e != cudaSuccess) return cuda_fail(e, "ntt_warp14s launch");
-  return 0;
-}
-
-template <class A, bool FWD, bool IL>
-int launch_warp_t(const nk::NttArgs& a, cudaStream_t st) {
-  auto kern = nk::ntt_warp14<A, FWD, IL>;
-  if (int rc = set_smem(kern, nk::kWarpSmemBytes)) return rc;
-  static int per_sm[64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (!per_sm[dev & 63]) {
-    int n = 0;
-    NK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, 256, nk::kWarpSmemBytes));
-    per_sm[dev & 63] = n > 0 ? n : 1;
-  }
-  const uint64_t items = a.rows * 32;
-  uint64_t grid = static_cast<uint64_t>(per_sm[dev & 63]) * sm_count();
-  const uint64_t need = (items + nk::kWarpsPerCta - 1) / nk::kWarpsPerCta;
-  if (grid > need) grid = need;
-  uint32_t* cnt = nullptr;
-  const size_t cbytes = (a.rows + 1) * sizeof(uint32_t);
-  NK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cnt), cbytes, st));
-  NK_CUDA(cudaMemsetAsync(cnt, 0, cbytes, st));
-  nk::WarpNttArgs wa{a, cnt, cnt + a.rows, static_cast<uint32_t>(grid * nk::kWarpsPerCta / 16 + 1)};
-  kern<<<static_cast<unsigned>(grid), 256, nk::kWarpSmemBytes, st>>>(wa);
-  g_launches++;
-  cudaError_t e = cudaGetLastError();
-  cudaFreeAsync(cnt, st);
-  if (e != cudaSuccess) return cuda_fail(e, "ntt_warp14 launch");
-  return 0;
-}
-
-template <class A, bool IL>
-int launch_inv2_t(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
-  CUtensorMap map;
-  if (int rc = make_row_map(&map, a.in, buf_words)) return rc;
-  auto kern = nk::ntt_inv14_tma<A, IL>;
-  if (int rc = set_smem(kern, nk::kTmaSmemBytes)) return rc;
-  const uint64_t g = nitems < static_cast<uint64_t>(sm_count()) ? nitems : sm_count();
-  kern<<<static_cast<unsigned>(g), 512, nk::kTmaSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));
-  g_launches++;
-  NK_CUDA(cudaGetLastError());
-  return 0;
-}
-
-template <class A, bool FWD>
-int launch_tma(const nk::NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm, cudaStream_t st) {
-  if (!FWD && g_block_kernel == 5)
-    return iltm ? launch_inv2_t<A, true>(a, nitems, buf_words, st) : launch_inv2_t<A, false>(a, nitems, buf_words, st);
-  // measured on B200 (cfg3): the CTA-pair kernel is the faster forward, the
-  // single-CTA kernel the faster inverse (the pair inverse exchanges late,
-  // so its next TMA overlaps less compute)
-  const bool pair = (g_block_kernel < 0 || g_block_kernel == 2) ? FWD : g_block_kernel == 0;
-  if (pair)
-    return iltm ? launch_pair_t<A, FWD, true>(a, nitems, buf_words, st)
-                : launch_pair_t<A, FWD, false>(a, nitems, buf_words, st);
-  return iltm ? launch_tma_t<A, FWD, true>(a, nitems, buf_words, st)
-              : launch_tma_t<A, FWD, false>(a, nitems, buf_words, st);
-}
-
-// LOGV = log2(words per thread): 32 words per thread for batches that fill
-// the GPU, 8 for small ones (cfg1: one row), where the row's latency is the
-// metric and 4x more threads per row cut it.
-template <int LOGB, int LOGV, class A, bool FWD, bool IL>
-int launch_block_t(const nk::NttArgs& a, uint64_t grid, cudaStream_t st) {
-  constexpr size_t smem = nk::block_smem_bytes<LOGB, LOGV>();
-  auto kern = nk::ntt_block<LOGB, LOGV, A, FWD, IL>;
-  if (smem > 48 * 1024)
-    if (int rc = set_smem(kern, smem)) return rc;
-  kern<<<static_cast<unsigned>(grid), 1 << (LOGB - LOGV), smem, st>>>(a);
-  g_launches++;
-  NK_CUDA(cudaGetLastError());
-  return 0;
-}
-
-// latency path (ntt_block_lat): programmatic dependent launch, twiddle row
-// staged into shared memory before griddepcontrol.wait
-template <int LOGB, int LOGV, class A, bool FWD, bool IL>
-int launch_block_lat_t(const nk::NttArgs& a, uint64_t grid, cudaStream_t st) {
-  constexpr size_t smem = nk::lat_smem_bytes<LOGB, LOGV>();
-  auto kern = nk::ntt_block_lat<LOGB, LOGV, A, FWD, IL>;
-  if (int rc = set_smem(kern, smem)) return rc;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(1u << (LOGB - LOGV));
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
-  g_launches++;
-  if (e != cudaSuccess) return cuda_fail(e, "ntt_block_lat launch");
-  NK_CUDA(cudaGetLastError());
-  return 0;
-}
-
-template <class A, bool FWD>
-int launch_block(uint32_t logb, const nk::NttArgs& a, uint64_t grid, bool iltm, cudaStream_t st) {
-  const bool small = a.rows < static_cast<uint64_t>(sm_count());
-  if (small && a.logn == logb && !g_no_lat) {  // whole rows, few of them: the latency path
-    switch (logb) {
-      case 11: return iltm ? launch_block_lat_t<11, 3, A, FWD, true>(a, grid, st) : launch_block_lat_t<11, 3, A, FWD, false>(a, grid, st);
-      case 12: return iltm ? launch_block_lat_t<12, 3, A, FWD, true>(a, grid, st) : launch_block_lat_t<12, 3, A, FWD, false>(a, grid, st);
-      default: return iltm ? launch_block_lat_t<13, 3, A, FWD, true>(a, grid, st) : launch_block_lat_t<13, 3, A, FWD, false>(a, grid, st);
-    }
-  }
-#define NK_LB2(L, V) \
-  return iltm ? launch_block_t<L, V, A, FWD, true>(a, grid, st) : launch_block_t<L, V, A, FWD, false>(a, grid, st)
-#define NK_LB(L) \
-  if (small) NK_LB2(L, 3); \
-  NK_LB2(L, 5)
-  switch (logb) {
-    case 11: NK_LB(11);
-    case 12: NK_LB(12);
-    default: NK_LB(13);
-  }
-#undef NK_LB
-#undef NK_LB2
-}
-
-template <class A, bool FWD>
-int launch_global(uint32_t k, uint32_t lo, bool first_iltm, bool last, const nk::NttArgs& a,
-                  cudaStream_t st) {
-  const uint64_t threads = a.rows << (a.logn - k);
-  const unsigned grid = static_cast<unsigned>((threads + 255) / 256);
-  switch (k) {
-    case 1: nk::ntt_global_pass<1, A, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
-    case 2: nk::ntt_global_pass<2, A, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
-    default: nk::ntt_global_pass<3, A, FWD><<<grid, 256, 0, st>>>(a, lo, first_iltm, last); break;
-  }
-  g_launches++;
-  NK_CUDA(cudaGetLastError());
-  return 0;
-}
-
-template <class A, bool FWD>
-int launch_small(const nk::NttArgs& a, cudaStream_t st) {
-  const size_t smem = a.n * sizeof(uint64_t);
-  const unsigned threads = static_cast<unsigned>(a.n / 2 < 256 ? a.n / 2 : 256);
-  nk::ntt_small<A, FWD><<<static_cast<unsigned>(a.rows), threads, smem, st>>>(a);
-  g_launches++;
-  NK_CUDA(cudaGetLastError());
-  return 0;
-}
-
+using nk::rt::run_ntt;
 constexpr uint32_t kLogBlock = 14;
-
-// Full transform of a.rows rows with arithmetic policy A. buf_words: words in
-// the input buffer (for the tensor map of the TMA kernel).
-template <class A, bool FWD>
-int run_ntt(nk::NttArgs a, uint64_t buf_words, cudaStream_t st) {
-  const uint32_t logn = a.logn;
-  if (logn <= 10) return launch_small<A, FWD>(a, st);
-  if (logn < kLogBlock) return launch_block<A, FWD>(logn, a, a.rows, a.fin == 1, st);
-  if (logn == kLogBlock) {
-    // the warp-per-item kernel is correct but not (yet) the faster one on
-    // B200 (profiles/ncu_r01_session2_warp.txt): selected only explicitly
-    if (g_block_kernel == 2)
-      return a.fin == 1 ? launch_warp_t<A, FWD, true>(a, st) : launch_warp_t<A, FWD, false>(a, st);
-    if (g_block_kernel == 4 && FWD) return launch_warps_t<A>(a, buf_words, st);
-    return launch_tma<A, FWD>(a, a.rows, buf_words, a.fin == 1, st);
-  }
-  // long rows: high bits in global passes of <= 3 stages, low 14 bits per block
-  const uint32_t gbits = logn - kLogBlock;
-  uint32_t ks[2] = {gbits, 0};
-  if (gbits > 3) { ks[0] = (gbits + 1) / 2; ks[1] = gbits - ks[0]; }
-  const int np = ks[1] ? 2 : 1;
-  const uint64_t nitems = a.rows << gbits;
-  if (FWD) {
-    uint32_t top = logn;
-    for (int p = 0; p < np; ++p) {
-      const uint32_t lo = top - ks[p];
-      if (int rc = launch_global<A, true>(ks[p], lo, p == 0 && a.fin == 1, false, a, st)) return rc;
-      a.in = a.out;  // later passes run in place on the result
-      top = lo;
-    }
-    return launch_tma<A, true>(a, nitems, buf_words, false, st);
-  } else {
-    if (int rc = launch_tma<A, false>(a, nitems, buf_words, a.fin == 1, st)) return rc;
-    a.in = a.out;
-    uint32_t lo = kLogBlock;
-    for (int p = 0; p < np; ++p) {
-      if (int rc = launch_global<A, false>(ks[p], lo, false, p == np - 1, a, st)) return rc;
-      lo += ks[p];
-    }
-    return 0;
-  }
-}
 
 int check_limbs(const nk_plan* p, uint32_t limb0, uint32_t nlimbs) {
   if (!p) return fail(NK_ERR_NULL, "plan is NULL");
@@ -559,7 +215,6 @@ int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64
   a.nlimbs = nlimbs;
   a.fin = static_cast<int>(fin);
   a.fout = static_cast<int>(fout);
-  a.dbg = g_dbg;
   if (npolys == 0) return 0;
   // one launch when the limb range shares an accumulator width, else one per limb
   bool uniform = true;
@@ -582,12 +237,12 @@ int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64
     // beta = 2^52: signed FP64 arithmetic when only the canonical result is
     // observable (fout == 1 and one kernel holds the whole row), else the
     // reference's exact lazy representatives (nk::Arith52P)
-    const bool canon = (b.fout == 1) && (b.logn <= kLogBlock) && !g_exact_only;
+    const bool canon = (b.fout == 1) && (b.logn <= kLogBlock) && !nk::rt::exact_only;
     if (bs == 52 && canon)
       rc = fwd ? run_ntt<nk::Arith52S, true>(b, words, st) : run_ntt<nk::Arith52S, false>(b, words, st);
     else if (bs == 52)
       rc = fwd ? run_ntt<nk::Arith52P, true>(b, words, st) : run_ntt<nk::Arith52P, false>(b, words, st);
-    else if (b.fout == 1 && !g_exact_only && max_q(p, limb0 + (uniform ? 0 : l), uniform ? nlimbs : 1) < (uint64_t{1} << 61))
+    else if (b.fout == 1 && !nk::rt::exact_only && max_q(p, limb0 + (uniform ? 0 : l), uniform ? nlimbs : 1) < (uint64_t{1} << 61))
       // beta = 2^64, canonical result only: loose Shoup quotients (nk::ArithIntL)
       rc = fwd ? run_ntt<nk::ArithIntL, true>(b, words, st) : run_ntt<nk::ArithIntL, false>(b, words, st);
     else
@@ -598,93 +253,8 @@ int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64
   return 0;
 }
 
-// Resident CTAs per SM of an element-wise kernel (occupancy API, cached per
-// kernel and device).
-int resident_ctas(const void* kern, int block) {
-  static std::mutex mu;
-  static std::unordered_map<const void*, int> cache[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(mu);
-  auto& c = cache[dev & 63];
-  auto it = c.find(kern);
-  if (it != c.end()) return it->second;
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, block, 0) != cudaSuccess || n < 1) n = 1;
-  c[kern] = n;
-  return n;
-}
-
-unsigned eltwise_grid(uint64_t work, const void* kern, int ku = nk::kU) {
-  // work = vector chunks; each thread takes ku chunks per sweep; up to two
-  // waves of resident CTAs, grid-stride beyond
-  const uint64_t per = 256ull * ku;
-  uint64_t g = (work + per - 1) / per;
-  const uint64_t cap = 2ull * sm_count() * resident_ctas(kern, 256);
-  return static_cast<unsigned>(g < 1 ? 1 : (g > cap ? cap : g));
-}
-
-// widest vector access all pointers allow (32 / 16 / 8 bytes)
-int vec_of(std::initializer_list<const void*> ptrs) {
-  uintptr_t x = 0;
-  for (const void* p : ptrs) x |= reinterpret_cast<uintptr_t>(p);
-  return (x & 31) == 0 ? 4 : ((x & 15) == 0 ? 2 : 1);
-}
-
-// launch with programmatic stream serialisation (the kernels call
-// griddepcontrol.wait before touching memory, nk::pdl_enter)
-template <class... KArgs, class... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-}
-
-template <int FIN, bool LOOSE, bool BATCHED>
-cudaError_t launch_mult_t(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t total, uint32_t logn,
-                          nk::MultConst c0, const nk::MultConst* consts, uint32_t nlimbs, cudaStream_t st) {
-  const int vec = vec_of({r, a, b});
-#define NK_MV(V)                                                                                          \
-  return launch_pdl(nk::eltwise_mult_kernel<FIN, LOOSE, BATCHED, V>, eltwise_grid(total / V + 1, reinterpret_cast<const void*>(nk::eltwise_mult_kernel<FIN, LOOSE, BATCHED, V>)), 256, st, \
-                    r, a, b, total, logn, c0, consts, nlimbs)
-  if (vec == 4) NK_MV(4);
-  if (vec == 2) NK_MV(2);
-  NK_MV(1);
-#undef NK_MV
-}
-
 // loose Barrett quotients (eltwise_kernels.cuh) need 5q < 2^63
 bool loose_barrett(uint64_t q) { return u128{5} * q < (u128{1} << 63); }
-
-int launch_mult(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t total, uint32_t logn,
-                nk::MultConst c0, const nk::MultConst* consts, uint32_t nlimbs, int fin, bool small,
-                cudaStream_t st) {
-  const bool batched = consts != nullptr;
-  cudaError_t e;
-#define NK_M(F, S, B) e = launch_mult_t<F, S, B>(r, a, b, total, logn, c0, consts, nlimbs, st)
-#define NK_M2(F)                                                      \
-  if (small) { if (batched) NK_M(F, true, true); else NK_M(F, true, false); } \
-  else { if (batched) NK_M(F, false, true); else NK_M(F, false, false); }
-  switch (fin) {
-    case 1: NK_M2(1) break;
-    case 2: NK_M2(2) break;
-    default: NK_M2(4) break;
-  }
-#undef NK_M2
-#undef NK_M
-  g_launches++;
-  if (e != cudaSuccess) return cuda_fail(e, "eltwise_mult_kernel launch");
-  NK_CUDA(cudaGetLastError());
-  return 0;
-}
 
 }  // namespace
 
@@ -724,7 +294,7 @@ int run_bfly_test(bool fwd, const uint64_t* x0, const uint64_t* x1, uint64_t n, 
   const unsigned grid = static_cast<unsigned>((n + 255) / 256);
   if (fwd) nk::bfly_test_kernel<A, true, SIGNED_IO><<<grid, 256>>>(x0, x1, n, w, c, y0, y1);
   else nk::bfly_test_kernel<A, false, SIGNED_IO><<<grid, 256>>>(x0, x1, n, w, c, y0, y1);
-  g_launches++;
+  nk::rt::launches++;
   NK_CUDA(cudaGetLastError());
   return 0;
 }
@@ -735,18 +305,18 @@ int run_bfly_test(bool fwd, const uint64_t* x0, const uint64_t* x1, uint64_t n, 
 // ---------------------------------------------------------------------------
 extern "C" {
 
-const char* nk_last_error(void) { return g_err.c_str(); }
+const char* nk_last_error(void) { return nk::rt::g_err.c_str(); }
 const char* nk_version(void) { return "nttkit_b200 0.1 (sm_100a)"; }
-uint64_t nk_launch_count(void) { return g_launches.load(); }
-void nk_debug_dump_to(uint64_t* d_buf) { g_dbg = d_buf; }
-void nk_debug_exact_only(int on) { g_exact_only = on != 0; }
+uint64_t nk_launch_count(void) { return nk::rt::launches.load(); }
+void nk_debug_dump_to(uint64_t* d_buf) { nk::rt::dbg = d_buf; }
+void nk_debug_exact_only(int on) { nk::rt::exact_only = on != 0; }
 int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint64_t* d_x0, const uint64_t* d_x1,
                          uint64_t n, uint64_t* d_y0, uint64_t* d_y1) {
   nk::host::Modulus m;
   if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (w >= q) return fail(NK_ERR_ROOT, "debug_butterflies: twiddle must be < q");
-  const bool b52 = policy == 1 || policy == 2 || policy == 3 || policy == 5;
-  if (policy < 0 || policy > 5) return fail(NK_ERR_BIT_SHIFT, "debug_butterflies: policy must be 0..5");
+  const bool b52 = policy == 1 || policy == 2 || policy == 3;
+  if (policy < 0 || policy > 4) return fail(NK_ERR_BIT_SHIFT, "debug_butterflies: policy must be 0..4");
   if (b52 && u128{4} * q >= (u128{1} << 52))
     return fail(NK_ERR_BIT_SHIFT_52, "NttTables: 52-bit accumulator requires 4q < 2^52");
   if (policy == 4 && q >= (uint64_t{1} << 61))
@@ -755,13 +325,12 @@ int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint
   if (!d_x0 || !d_x1 || !d_y0 || !d_y1) return fail(NK_ERR_NULL, "debug_butterflies: NULL buffer");
   const int bs = b52 ? 52 : 64;
   const uint64_t wp = static_cast<uint64_t>((static_cast<u128>(w) << bs) / q);
-  const bool fp = policy == 2 || policy == 3 || policy == 5;
+  const bool fp = policy == 2 || policy == 3;
   auto enc = [fp](uint64_t x) { return fp ? dbits(static_cast<double>(x)) : x; };
   nk::LimbConstDev c{};
   c.q = q;
   c.twoq = 2 * q;
   c.negq = ~q + 1;
-  c.twoq_bias = 2 * q + nk::kDBias;
   c.qq = std::ldexp(static_cast<double>(q), -52);
   c.twoq_d = static_cast<double>(2 * q);
   c.bs = bs;
@@ -776,8 +345,7 @@ int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint
     case 1: return run_bfly_test<nk::ArithInt<52>, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
     case 2: return run_bfly_test<nk::Arith52P, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
     case 3: return run_bfly_test<nk::Arith52S, true>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
-    case 4: return run_bfly_test<nk::ArithIntL, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
-    default: return run_bfly_test<nk::Arith52F, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
+    default: return run_bfly_test<nk::ArithIntL, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
   }
 }
 
@@ -805,7 +373,8 @@ int nk_harvey_butterflies(int fwd, uint64_t q, int bit_shift, uint64_t w, uint64
     if (x0[i] >= bound || x1[i] >= bound)
       return fail(NK_ERR_RANGE, fwd ? "harvey_forward_butterfly: inputs must be < 4q"
                                     : "harvey_inverse_butterfly: inputs must be < 2q");
-  if (int rc = ensure_device(device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(device)) return rc;
   uint64_t* d = nullptr;
   NK_CUDA(cudaMalloc(&d, 4 * n * sizeof(uint64_t)));
   int rc = 0;
@@ -824,8 +393,8 @@ int nk_harvey_butterflies(int fwd, uint64_t q, int bit_shift, uint64_t w, uint64
 }
 
 void nk_debug_block_kernel(int which) {
-  g_no_lat = (which == 6);
-  g_block_kernel = which == 6 ? -1 : which;
+  nk::rt::no_lat = (which == 6);
+  nk::rt::block_kernel = (which == 0 || which == 1) ? which : -1;
 }
 
 int nk_modulus(uint64_t q, uint32_t* bits, uint64_t* barrett_factor) {
@@ -896,7 +465,8 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
     if (int rc = nk::host::build_tables(n, moduli[l], roots ? &roots[l] : nullptr, bit_shift,
                                         &tabs[l], &msg))
       return fail(rc, msg);
-  if (int rc = ensure_device(device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(device)) return rc;
   nk_plan* p = new nk_plan();
   p->device = device;
   p->n = n;
@@ -935,7 +505,7 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
     // folded last inverse stage: n^-1 * w_1 (w_1 = inverse table entry 1)
     const uint64_t nw = static_cast<uint64_t>(static_cast<u128>(t.ninv) * t.wi[1] % t.q);
     const uint64_t nwp = static_cast<uint64_t>((static_cast<u128>(nw) << t.bs) / t.q);
-    hl[l] = nk::LimbConst{t.q, 2 * t.q, ~t.q + 1, enc(t.ninv), enc(t.ninvp), 2 * t.q + nk::kDBias,
+    hl[l] = nk::LimbConst{t.q, 2 * t.q, ~t.q + 1, enc(t.ninv), enc(t.ninvp),
                           std::ldexp(static_cast<double>(t.q), -52), static_cast<double>(2 * t.q),
                           t.bs, 0, static_cast<double>(t.q), 1.0 / static_cast<double>(t.q),
                           static_cast<double>(t.q) + 4503599627370496.0, enc(nw), enc(nwp), 4 * t.q};
@@ -955,15 +525,23 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
   for (int f = 0; f < 3; ++f)
     if ((e = cudaMalloc(&p->mc[f], nlimbs * sizeof(nk::MultConst))))
       return cleanup(cuda_fail(e, "cudaMalloc(plan consts)"));
-  if ((e = cudaMemcpy(p->twl_fwd, hlf.data(), hlf.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice)) ||
-      (e = cudaMemcpy(p->twl_inv, hli.data(), hli.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice)) ||
-      (e = cudaMemcpy(p->tw_fwd, hf.data(), hf.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice)) ||
-      (e = cudaMemcpy(p->tw_inv, hi.data(), hi.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice)) ||
-      (e = cudaMemcpy(p->lc, hl.data(), hl.size() * sizeof(nk::LimbConst), cudaMemcpyHostToDevice)))
-    return cleanup(cuda_fail(e, "cudaMemcpy(plan tables)"));
-  for (int f = 0; f < 3; ++f)
-    if ((e = cudaMemcpy(p->mc[f], hm[f].data(), nlimbs * sizeof(nk::MultConst), cudaMemcpyHostToDevice)))
-      return cleanup(cuda_fail(e, "cudaMemcpy(plan consts)"));
+  // uploads on a private stream, complete before the plan is returned: a first
+  // call on any stream (blocking or not) reads finished tables
+  cudaStream_t up = nullptr;
+  if ((e = cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking))) return cleanup(cuda_fail(e, "cudaStreamCreate(plan upload)"));
+  auto put = [&](void* dst, const void* src, size_t bytes) {
+    return e == cudaSuccess ? (e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, up)) : e;
+  };
+  put(p->twl_fwd, hlf.data(), hlf.size() * sizeof(ulonglong2));
+  put(p->twl_inv, hli.data(), hli.size() * sizeof(ulonglong2));
+  put(p->tw_fwd, hf.data(), hf.size() * sizeof(ulonglong2));
+  put(p->tw_inv, hi.data(), hi.size() * sizeof(ulonglong2));
+  put(p->lc, hl.data(), hl.size() * sizeof(nk::LimbConst));
+  for (int f = 0; f < 3; ++f) put(p->mc[f], hm[f].data(), nlimbs * sizeof(nk::MultConst));
+  const cudaError_t es = cudaStreamSynchronize(up);
+  cudaStreamDestroy(up);
+  if (e == cudaSuccess) e = es;
+  if (e != cudaSuccess) return cleanup(cuda_fail(e, "cudaMemcpyAsync(plan tables)"));
   *out = p;
   return 0;
 }
@@ -993,7 +571,8 @@ int nk_ntt_forward(const nk_plan* p, uint64_t* res, const uint64_t* op, uint32_t
   if (!res || !op) return fail(NK_ERR_NULL, "forward: NULL buffer");
   if (overlap_bad(res, op, static_cast<uint64_t>(npolys) * nlimbs * p->n * 8))
     return fail(NK_ERR_OVERLAP, "forward: result and operand must alias fully or not overlap");
-  if (int rc = ensure_device(p->device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(p->device)) return rc;
   return ntt_dispatch(p, true, res, op, limb0, nlimbs, npolys, fin, fout, S(stream));
 }
 
@@ -1007,7 +586,8 @@ int nk_ntt_inverse(const nk_plan* p, uint64_t* res, const uint64_t* op, uint32_t
   if (!res || !op) return fail(NK_ERR_NULL, "inverse: NULL buffer");
   if (overlap_bad(res, op, static_cast<uint64_t>(npolys) * nlimbs * p->n * 8))
     return fail(NK_ERR_OVERLAP, "inverse: result and operand must alias fully or not overlap");
-  if (int rc = ensure_device(p->device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(p->device)) return rc;
   return ntt_dispatch(p, false, res, op, limb0, nlimbs, npolys, fin, fout, S(stream));
 }
 
@@ -1022,12 +602,13 @@ int nk_plan_eltwise_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* a,
       return fail(NK_ERR_MULT_INT_RANGE, "eltwise_mult_mod_int: requires input_mod_factor*q < 2^63");
   if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_mult_mod: NULL buffer");
   if (npolys == 0) return 0;
-  if (int rc = ensure_device(p->device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(p->device)) return rc;
   const int fi = fin == 1 ? 0 : (fin == 2 ? 1 : 2);
   const uint64_t rows = static_cast<uint64_t>(npolys) * nlimbs;
   bool small = true;
   for (uint32_t l = 0; l < nlimbs; ++l) small &= loose_barrett(p->q[limb0 + l]);
-  return launch_mult(res, a, b, rows * p->n, p->logn, nk::MultConst{}, p->mc[fi] + limb0, nlimbs,
+  return nk::rt::launch_mult(res, a, b, rows * p->n, p->logn, nk::MultConst{}, p->mc[fi] + limb0, nlimbs,
                      static_cast<int>(fin), small, S(stream));
 }
 
@@ -1042,7 +623,8 @@ int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const u
   if (overlap_bad(res, f, bytes) || overlap_bad(res, g, bytes))
     return fail(NK_ERR_OVERLAP, "poly_mult_mod: result must alias an operand fully or not overlap");
   if (npolys == 0) return 0;
-  if (int rc = ensure_device(p->device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(p->device)) return rc;
   cudaStream_t st = S(stream);
   uint64_t* gh = nullptr;
   NK_CUDA(cudaMallocAsync(&gh, bytes, st));
@@ -1051,7 +633,7 @@ int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const u
   // product applied in the forward's store, then the inverse. The result is
   // canonical and unique, so it equals the reference's fwd(1,4) x2 /
   // mult(4) / inv(1,1) sequence (ring.hpp:28-43) word for word.
-  bool fused = p->logn == kLogBlock && !g_exact_only && (g_block_kernel < 0 || g_block_kernel == 0);
+  bool fused = p->logn == kLogBlock && !nk::rt::exact_only && nk::rt::block_kernel <= 0;
   for (uint32_t l = 0; l < nlimbs; ++l) fused &= p->bs[limb0 + l] == 52;
   if (fused) {
     int rc = ntt_dispatch(p, true, gh, g, limb0, nlimbs, npolys, 1, 1, st);
@@ -1100,36 +682,6 @@ int validate_mult(uint64_t q, uint64_t fin, nk::host::Modulus* m, MultPath path 
   return 0;
 }
 
-int launch_mult_float(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q, int fin,
-                      cudaStream_t st) {
-  nk::LimbConstDev c{};
-  c.q = q;
-  c.q_d = static_cast<double>(q);
-  c.qinv = 1.0 / static_cast<double>(q);
-  c.q_bias = static_cast<double>(q) + 4503599627370496.0;
-  const int vec = vec_of({r, a, b});
-  cudaError_t e;
-#define NK_MFV(F, V)                                                                                    \
-  e = launch_pdl(nk::eltwise_mult_float_kernel<F, V>,                                                   \
-                 eltwise_grid(n / V + 1, reinterpret_cast<const void*>(nk::eltwise_mult_float_kernel<F, V>)), \
-                 256, st, r, a, b, n, c)
-#define NK_MF(F)                 \
-  if (vec == 4) NK_MFV(F, 4);    \
-  else if (vec == 2) NK_MFV(F, 2); \
-  else NK_MFV(F, 1)
-  switch (fin) {
-    case 1: NK_MF(1); break;
-    case 2: NK_MF(2); break;
-    default: NK_MF(4); break;
-  }
-#undef NK_MF
-#undef NK_MFV
-  g_launches++;
-  if (e != cudaSuccess) return cuda_fail(e, "eltwise_mult_float_kernel launch");
-  NK_CUDA(cudaGetLastError());
-  return 0;
-}
-
 int eltwise_mult_path(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
                       uint64_t fin, MultPath path, void* stream) {
   nk::host::Modulus m;
@@ -1137,9 +689,9 @@ int eltwise_mult_path(uint64_t* res, const uint64_t* a, const uint64_t* b, uint6
   if (n == 0) return 0;
   if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_mult_mod: NULL buffer");
   if (resolve_path(path, q) == kMultFloat)
-    return launch_mult_float(res, a, b, n, q, static_cast<int>(fin), S(stream));
+    return nk::rt::launch_mult_float(res, a, b, n, q, static_cast<int>(fin), S(stream));
   const nk::MultConst c{q, 2 * q, m.barrett, m.bits - 1, static_cast<int>(fin)};
-  return launch_mult(res, a, b, n, 0, c, nullptr, 1, static_cast<int>(fin), loose_barrett(q), S(stream));
+  return nk::rt::launch_mult(res, a, b, n, 0, c, nullptr, 1, static_cast<int>(fin), loose_barrett(q), S(stream));
 }
 
 // eltwise.hpp:236-251 (+ the automatic width of eltwise.hpp:263-271); *bs receives the width
@@ -1182,34 +734,7 @@ int nk_eltwise_fma_mod(uint64_t* res, const uint64_t* a, uint64_t y, const uint6
   if (!res || !a) return fail(NK_ERR_NULL, "eltwise_fma_mod: NULL buffer");
   const nk::FmaConst c{q, y, static_cast<uint64_t>((static_cast<u128>(y) << bs) / q),
                        static_cast<int>(fin), bs};
-  cudaStream_t st = S(stream);
-  const int vec = z ? vec_of({res, a, z}) : vec_of({res, a});
-  cudaError_t e = cudaSuccess;
-#define NK_FMAV(BS, Z, F, V) \
-  e = launch_pdl(nk::eltwise_fma_kernel<BS, Z, F, V>, eltwise_grid(n / V + 1, reinterpret_cast<const void*>(nk::eltwise_fma_kernel<BS, Z, F, V>), nk::fma_ku(Z)), 256, st, res, a, z, n, c)
-#define NK_FMA(BS, Z, F)                            \
-  if (vec == 4) NK_FMAV(BS, Z, F, 4);               \
-  else if (vec == 2) NK_FMAV(BS, Z, F, 2);          \
-  else NK_FMAV(BS, Z, F, 1)
-#define NK_FMA_F(BS, Z)                          \
-  switch (fin) {                                 \
-    case 1: NK_FMA(BS, Z, 1); break;             \
-    case 2: NK_FMA(BS, Z, 2); break;             \
-    case 4: NK_FMA(BS, Z, 4); break;             \
-    default: NK_FMA(BS, Z, 8); break;            \
-  }
-  if (bs == 52) {
-    if (z) { NK_FMA_F(52, true) } else { NK_FMA_F(52, false) }
-  } else {
-    if (z) { NK_FMA_F(64, true) } else { NK_FMA_F(64, false) }
-  }
-#undef NK_FMA_F
-#undef NK_FMA
-#undef NK_FMAV
-  if (e != cudaSuccess) return cuda_fail(e, "eltwise_fma_kernel launch");
-  g_launches++;
-  NK_CUDA(cudaGetLastError());
-  return 0;
+  return nk::rt::launch_fma(res, a, z, n, c, S(stream));
 }
 
 int nk_eltwise_add_mod(uint64_t* res, const uint64_t* a, const uint64_t* b, uint64_t n, uint64_t q,
@@ -1218,11 +743,7 @@ int nk_eltwise_add_mod(uint64_t* res, const uint64_t* a, const uint64_t* b, uint
   if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (n == 0) return 0;
   if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_add_mod: NULL buffer");
-  cudaError_t e = launch_pdl(nk::eltwise_add_kernel, eltwise_grid(n, reinterpret_cast<const void*>(nk::eltwise_add_kernel)), 256, S(stream), res, a, b, n, q);
-  g_launches++;
-  if (e != cudaSuccess) return cuda_fail(e, "eltwise_add_kernel launch");
-  NK_CUDA(cudaGetLastError());
-  return 0;
+  return nk::rt::launch_add(res, a, b, n, q, S(stream));
 }
 
 int nk_eltwise_neg_mod(uint64_t* res, const uint64_t* a, uint64_t n, uint64_t q, void* stream) {
@@ -1230,11 +751,7 @@ int nk_eltwise_neg_mod(uint64_t* res, const uint64_t* a, uint64_t n, uint64_t q,
   if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (n == 0) return 0;
   if (!res || !a) return fail(NK_ERR_NULL, "eltwise_neg_mod: NULL buffer");
-  cudaError_t e = launch_pdl(nk::eltwise_neg_kernel, eltwise_grid(n, reinterpret_cast<const void*>(nk::eltwise_neg_kernel)), 256, S(stream), res, a, n, q);
-  g_launches++;
-  if (e != cudaSuccess) return cuda_fail(e, "eltwise_neg_kernel launch");
-  NK_CUDA(cudaGetLastError());
-  return 0;
+  return nk::rt::launch_neg(res, a, n, q, S(stream));
 }
 
 }  // extern "C"
@@ -1357,7 +874,8 @@ int ntt_host(bool fwd, const nk_plan* p, uint64_t* res, const uint64_t* op, uint
   if (length != words) return fail(NK_ERR_LENGTH, "transform: buffer length must equal n");
   if (!res || !op) return fail(NK_ERR_NULL, "transform: NULL buffer");
   if (npolys == 0) return 0;
-  if (int rc = ensure_device(p->device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(p->device)) return rc;
   return run_pipelined(p->device, S(stream), npolys, static_cast<uint64_t>(nlimbs) * p->n, {op}, res,
                        [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
                          const uint32_t np = static_cast<uint32_t>(nu);
@@ -1401,7 +919,8 @@ int nk_poly_mult_mod_host(const nk_plan* p, uint64_t* res, const uint64_t* f, co
     if (p->q[limb0 + l] >= (uint64_t{1} << 61))
       return fail(NK_ERR_POLY_MODULUS, "poly_mult_mod: requires q < 2^61");
   if (npolys == 0) return 0;
-  if (int rc = ensure_device(p->device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(p->device)) return rc;
   return run_pipelined(p->device, S(stream), npolys, static_cast<uint64_t>(nlimbs) * p->n, {f, g}, res,
                        [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
                          return nk_poly_mult_mod(p, d[0], d[0], d[1], limb0, nlimbs,
@@ -1416,7 +935,8 @@ int eltwise_mult_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint6
   nk::host::Modulus m;
   if (int rc = validate_mult(q, fin, &m, path)) return rc;
   if (n == 0) return 0;
-  if (int rc = ensure_device(device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(device)) return rc;
   return run_pipelined(device, S(stream), n, 1, {a, b}, res,
                        [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
                          return eltwise_mult_path(d[0], d[0], d[1], nu, q, fin, path, st);
@@ -1430,7 +950,8 @@ int nk_eltwise_add_mod_host(uint64_t* res, const uint64_t* a, const uint64_t* b,
   if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (n == 0) return 0;
   if (!res || !a || !b) return fail(NK_ERR_NULL, "eltwise_add_mod: NULL buffer");
-  if (int rc = ensure_device(device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(device)) return rc;
   return run_pipelined(device, S(stream), n, 1, {a, b}, res,
                        [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
                          return nk_eltwise_add_mod(d[0], d[0], d[1], nu, q, st);
@@ -1443,7 +964,8 @@ int nk_eltwise_neg_mod_host(uint64_t* res, const uint64_t* a, uint64_t n, uint64
   if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (n == 0) return 0;
   if (!res || !a) return fail(NK_ERR_NULL, "eltwise_neg_mod: NULL buffer");
-  if (int rc = ensure_device(device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(device)) return rc;
   return run_pipelined(device, S(stream), n, 1, {a}, res,
                        [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
                          return nk_eltwise_neg_mod(d[0], d[0], nu, q, st);
@@ -1470,7 +992,8 @@ int nk_eltwise_fma_mod_host(uint64_t* res, const uint64_t* a, uint64_t y, const 
   int bs = 0;
   if (int rc = validate_fma(q, y, fin, bit_shift, &bs)) return rc;
   if (n == 0) return 0;
-  if (int rc = ensure_device(device)) return rc;
+  DeviceScope ds;
+  if (int rc = ds.enter(device)) return rc;
   return run_pipelined(device, S(stream), n, 1, {a, z}, res,
                        [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
                          return nk_eltwise_fma_mod(d[0], d[0], y, z ? d[1] : nullptr, nu, q, fin, bit_shift,

@@ -241,27 +241,47 @@ __global__ void __launch_bounds__(256, HAS_Z ? 6 : 1) eltwise_fma_kernel(uint64_
     for (uint64_t k = chunks * VEC; k < n; ++k) r[k] = fma_one<BS, HAS_Z, FIN>(a[k], HAS_Z ? z[k] : 0, c);
 }
 
-__global__ void __launch_bounds__(256) eltwise_add_kernel(uint64_t* __restrict__ r,
-                                                          const uint64_t* __restrict__ a,
-                                                          const uint64_t* __restrict__ b,
-                                                          uint64_t n, uint64_t q) {
+// eltwise_add_mod / eltwise_neg_mod (eltwise.hpp:47-70) for canonical inputs:
+// the same streaming shape as the multiply (VEC-word vector accesses, one
+// chunk per thread per sweep, the total % VEC tail on thread 0).
+__device__ __forceinline__ uint64_t add_one(uint64_t a, uint64_t b, uint64_t q) { return csub(a + b, q); }
+__device__ __forceinline__ uint64_t neg_one(uint64_t a, uint64_t q) { return a == 0 ? 0 : q - a; }
+
+template <int VEC>
+__global__ void __launch_bounds__(256, 6) eltwise_add_kernel(uint64_t* __restrict__ r,
+                                                             const uint64_t* __restrict__ a,
+                                                             const uint64_t* __restrict__ b, uint64_t n,
+                                                             uint64_t q) {
   pdl_enter();
+  const uint64_t chunks = n / VEC;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += stride)
-    r[i] = csub(a[i] + b[i], q);
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < chunks; i += stride) {
+    const WordVec<VEC> x = ld_stream<VEC>(a + i * VEC), y = ld_stream<VEC>(b + i * VEC);
+    WordVec<VEC> o;
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) o.w[k] = add_one(x.w[k], y.w[k], q);
+    st_stream<VEC>(r + i * VEC, o);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (uint64_t k = chunks * VEC; k < n; ++k) r[k] = add_one(a[k], b[k], q);
 }
 
-__global__ void __launch_bounds__(256) eltwise_neg_kernel(uint64_t* __restrict__ r,
-                                                          const uint64_t* __restrict__ a,
-                                                          uint64_t n, uint64_t q) {
+template <int VEC>
+__global__ void __launch_bounds__(256, 6) eltwise_neg_kernel(uint64_t* __restrict__ r,
+                                                             const uint64_t* __restrict__ a, uint64_t n,
+                                                             uint64_t q) {
   pdl_enter();
+  const uint64_t chunks = n / VEC;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-       i += stride) {
-    const uint64_t x = a[i];
-    r[i] = x == 0 ? 0 : q - x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < chunks; i += stride) {
+    const WordVec<VEC> x = ld_stream<VEC>(a + i * VEC);
+    WordVec<VEC> o;
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) o.w[k] = neg_one(x.w[k], q);
+    st_stream<VEC>(r + i * VEC, o);
   }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    for (uint64_t k = chunks * VEC; k < n; ++k) r[k] = neg_one(a[k], q);
 }
 
 }  // namespace nk

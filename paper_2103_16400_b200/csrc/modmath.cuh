@@ -103,27 +103,22 @@ __device__ __forceinline__ void inv_bfly(uint64_t& x0, uint64_t& x1, uint64_t w,
 }
 
 // ---------------------------------------------------------------------------
-// beta = 2^52 on the FP64 pipe ("D representation").
+// beta = 2^52 on the FP64 pipe.
 //
-// Measured on B200 (tools/pipe_bench.cu): IMAD 64/clk/SM, IMAD.WIDE and
-// IMAD.HI 32/clk/SM, DFMA/DMUL/DADD 64/clk/SM, IADD3/LOP3/SEL ~128/clk/SM.
+// Measured on B200 (tools/pipe_bench.cu): IMAD 62/clk/SM, IMAD.WIDE 23 and
+// IMAD.HI 32/clk/SM, DFMA/DMUL/DADD 60/clk/SM, IADD3/LOP3 ~122/clk/SM.
 // The integer Shoup product above costs ~16 fma-pipe slots (6 wide products);
-// for beta = 2^52 (every operand < 2^52) the same words come out of 8 exact
-// FP64 operations:
-//   a value y in [0, 2^52) is carried as the bit pattern of the double
-//   2^52 + y, i.e. kDBias + y ("D(y)"), so additions, subtractions and the
-//   conditional subtractions stay integer ops (ALU pipe) on the bit patterns,
-//   and the double itself feeds the FMA pipe with no conversion instruction.
-//   mul_lazyD:  v  = D(x) - 2^52                       (exact: x)
-//               hq = fma_rd(W', v, 2^104)             = 2^104 + floor(W'x/2^52)*2^52
-//                    (the sum lies in [2^104, 2^105) where the ulp is 2^52, so
-//                     rounding down IS the reference's mul_hi<52>, modarith.hpp:133-139)
-//               qh = hq - 2^104                       (exact: qhat * 2^52)
-//               h1 = w*v (rn), l1 = fma(w, v, -h1)    (exact TwoProduct: h1 + l1 = w x)
-//               e  = fma(-qh, q*2^-52, h1)            (exact: |h1 - qhat q| < 2^53, integer)
-//               T  = e + l1                           (exact: w x - qhat q in [0, 2q))
-//   and D(T) = T + 2^52. T is the reference's mul_factor_lazy<52> result
-//   (ntt.hpp:97-101): same qhat, same representative.
+// for beta = 2^52 (every operand < 2^52) the same words come out of 6 exact
+// FP64 operations on plain doubles v = x < 2^52:
+//   hq = fma_rd(W', v, 2^104)             = 2^104 + floor(W'x/2^52)*2^52
+//        (the sum lies in [2^104, 2^105) where the ulp is 2^52, so rounding
+//         down IS the reference's mul_hi<52>, modarith.hpp:133-139)
+//   qh = hq - 2^104                       (exact: qhat * 2^52)
+//   h1 = w*v (rn), l1 = fma(w, v, -h1)    (exact TwoProduct: h1 + l1 = w x)
+//   e  = fma(-qh, q*2^-52, h1)            (exact: |h1 - qhat q| < 2^53, integer)
+//   T  = e + l1                           (exact: w x - qhat q in [0, 2q))
+// T is the reference's mul_factor_lazy<52> result (ntt.hpp:97-101): same
+// qhat, same representative.
 // ---------------------------------------------------------------------------
 constexpr uint64_t kDBias = 0x4330000000000000ull;  // bits of 2^52
 constexpr uint64_t kMask52 = (uint64_t{1} << 52) - 1;
@@ -132,24 +127,6 @@ constexpr double kC104 = 20282409603651670423947251286016.0;  // 2^104
 
 __device__ __forceinline__ double as_d(uint64_t b) { return __longlong_as_double(static_cast<long long>(b)); }
 __device__ __forceinline__ uint64_t as_u(double d) { return static_cast<uint64_t>(__double_as_longlong(d)); }
-
-// D(y) -> D(y - m) when y >= m else D(y); m <= 2^51.
-__device__ __forceinline__ uint64_t csubD(uint64_t yD, uint64_t m) {
-  const uint64_t d = yD - m;
-#if defined(NK_CSUBD_PLAIN)
-  return (hi32(d) >= 0x43300000u) ? d : yD;
-#else
-  uint64_t r;
-  // one 32-bit compare on the high word (ptxas would otherwise widen it to 64 bits)
-  asm("{\n\t.reg .pred p;\n\t.reg .b32 l, h;\n\t"
-      "mov.b64 {l, h}, %1;\n\t"
-      "setp.ge.u32 p, h, 0x43300000;\n\t"
-      "selp.b64 %0, %1, %2, p;\n\t}"
-      : "=l"(r)
-      : "l"(d), "l"(yD));
-  return r;
-#endif
-}
 
 // w*v - floor(w'v/2^52)*q as a plain double (exact integer in [0, 2q)) for a
 // plain double v < 2^52.
@@ -162,22 +139,15 @@ __device__ __forceinline__ double mul_lazy_plain(double v, double w, double wp, 
   return __dadd_rn(e, l1);
 }
 
-__device__ __forceinline__ uint64_t mul_lazyD(uint64_t xD, double w, double wp, double qq) {
-  const double v = __dsub_rn(as_d(xD), kC52);
-  return as_u(__dadd_rn(mul_lazy_plain(v, w, wp, qq), kC52));
-}
-
 // ---------------------------------------------------------------------------
 // Arithmetic policies for the transform kernels. Values live in registers and
 // shared memory in the policy's representation; load()/store() convert at the
 // HBM boundary. Twiddle-table entries are 16 bytes {w, w'} in the policy's
 // format (uint64 for the integer policies, the doubles' bit patterns for the
-// FP64 ones). Arith52F (biased doubles) is the first FP64 form, kept for
-// tools/bfly_bench.cu; the dispatcher uses Arith52S / Arith52P.
+// FP64 ones).
 // ---------------------------------------------------------------------------
 struct LimbConstDev {
   uint64_t q, twoq, negq, ninv, ninvp;  // integer policies: integers; FP64 policies: ninv/ninvp are double bits
-  uint64_t twoq_bias;                   // 2q + kDBias
   double qq;                            // q * 2^-52
   double twoq_d;                        // 2q as a double
   int32_t bs;
@@ -227,53 +197,14 @@ struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)
   }
 };
 
-struct Arith52F {  // beta = 2^52 on the FP64 pipe (requires 4q < 2^52)
-  static constexpr int kIltmFwd = 1;  // forward stages whose pre-reduction is skipped at fin = 1
-  static constexpr bool kLoose = false;
-  static constexpr bool kFP = true;
-  __device__ static uint64_t load(uint64_t x) { return x | kDBias; }
-  __device__ static uint64_t store(uint64_t xD) { return xD & kMask52; }
-  // fwd_butterfly<52, ILTM> (ntt.hpp:103-113) in the D representation. The
-  // output sums are formed on the FP64 pipe: D(u) + T and D(u) + 2q - T are
-  // exact (every intermediate is an integer below 2^53).
-  template <bool ILTM>
-  __device__ static void fwd(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
-    const uint64_t u = ILTM ? x0 : csubD(x0, c.twoq);
-    const double t = mul_lazy_plain(__dsub_rn(as_d(x1), kC52), as_d(w.x), as_d(w.y), c.qq);
-    const double du = as_d(u);
-    x0 = as_u(__dadd_rn(du, t));
-    x1 = as_u(__dsub_rn(__dadd_rn(du, c.twoq_d), t));
-  }
-  // inv_butterfly<52, ILTM> (ntt.hpp:115-130) in the D representation:
-  // t = x0 - x1 + 2q = (D(x0) - D(x1)) + 2q on the FP64 pipe (exact), the sum
-  // x0 + x1 on the integer pipe (D(x0) + D(x1) - 2^52).
-  template <bool ILTM>
-  __device__ static void inv(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
-    const double t = __dadd_rn(__dsub_rn(as_d(x0), as_d(x1)), c.twoq_d);
-    uint64_t s = x0 + x1 - kDBias;
-    if (!ILTM) s = csubD(s, c.twoq);
-    x0 = s;
-    x1 = as_u(__dadd_rn(mul_lazy_plain(t, as_d(w.x), as_d(w.y), c.qq), kC52));
-  }
-  __device__ static uint64_t scale_ninv(uint64_t xD, const LimbConstDev& c) {
-    return mul_lazyD(xD, as_d(c.ninv), as_d(c.ninvp), c.qq);
-  }
-  __device__ static uint64_t csub(uint64_t xD, uint64_t m) { return csubD(xD, m); }
-  static constexpr bool kSigned = false;
-  __device__ static uint64_t red4(uint64_t x, const LimbConstDev& c) { return csubD(csubD(x, c.twoq), c.q); }
-  __device__ static uint64_t red2(uint64_t x, const LimbConstDev& c) { return csubD(x, c.q); }
-  static constexpr bool kFold = false;
-  __device__ static void inv_fold(uint64_t&, uint64_t&, const LimbConstDev&) {}
-};
-
 // ---------------------------------------------------------------------------
 // beta = 2^52 on the FP64 pipe, values as plain doubles ("P representation").
 //
-// Same butterflies and the same representatives as Arith52F (so lazy outputs
-// stay bit-exact), but a word is carried as the double whose value it is, so
-// the Shoup product needs no unbiasing and the conditional subtraction is one
-// DADD plus a sign test: no 64-bit integer add (which ptxas issues as
-// IADD3 + IMAD.X, and IMAD shares issue bandwidth with the FP64 pipe).
+// The reference's butterflies and representatives (so lazy outputs stay
+// bit-exact), with a word carried as the double whose value it is: the Shoup
+// product needs no unbiasing and the conditional subtraction is one DADD plus
+// a sign test, no 64-bit integer add (which ptxas issues as IADD3 + IMAD.X,
+// and IMAD shares issue bandwidth with the FP64 pipe).
 // Registers hold the double's bit pattern (uint64_t) so the kernels stay
 // policy-agnostic.
 // ---------------------------------------------------------------------------

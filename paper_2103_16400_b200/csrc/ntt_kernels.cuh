@@ -32,9 +32,6 @@
 //  * ntt_global_pass<K, A, FWD>: K stages on bits [lo, lo+K) of long rows
 //    (N > 2^14), one column of 2^K words per thread, coalesced.
 //  * ntt_small<A, FWD>: any N <= 2^10, stage by stage in shared memory.
-//  * ntt_warp14 / ntt_warp14s (ntt_warp.cuh) and ntt_inv14_tma (below):
-//    alternative 16384-word kernels, correct and selectable
-//    (nk_debug_block_kernel), not faster on B200 today.
 #pragma once
 #include <cuda.h>
 
@@ -788,150 +785,10 @@ namespace nk {
 
 // warp-image position of a word (index bits 0..3 and 5..9; bit 4 is the
 // round): 512 words + 2 words of padding per 16, conflict-free for both sides
-// of the warp-local exchanges (ntt_pair14, ntt_inv14_tma)
+// of the warp-local exchanges (ntt_pair14)
 __host__ __device__ constexpr uint32_t wimg(uint32_t j) {
   const uint32_t idx = (j & 15u) | (((j >> 5) & 31u) << 4);
   return idx + 2u * (idx >> 4);
-}
-
-// ---------------------------------------------------------------------------
-// ntt_inv14_tma: the inverse on one 512-thread CTA per SM with 3 CTA barriers
-// per block instead of 7. Passes: bits 0..4 | 5..8 + passenger 4 | 9..13.
-// Exchange 1 is warp-local: a warp's P1 words are exactly the 1024
-// contiguous words of its own 8 KiB slice of the staging buffer, so once the
-// warp has read them it reuses that slice as its exchange image (two rounds on
-// bit 4, __syncwarp only). Exchange 2 is the full exchange through the
-// staging buffer (index bit 13 set) and the half image (clear). The next
-// block's TMA can only start after it, so that block is prefetched into L2
-// at the start of the current one.
-// ---------------------------------------------------------------------------
-template <class A, bool ILTM0>
-__global__ void __launch_bounds__(512, 1)
-    ntt_inv14_tma(const __grid_constant__ CUtensorMap tin, NttArgs a, uint32_t nitems) {
-  using P1 = PassD<0, 5, -1>;
-  using P2 = PassD<5, 4, 4>;
-  using P3 = PassD<9, 5, -1>;
-  extern __shared__ __align__(1024) uint8_t smraw[];
-  uint8_t* Astage = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
-  uint64_t* Ahalf = reinterpret_cast<uint64_t*>(Astage);
-  uint64_t* B = reinterpret_cast<uint64_t*>(Astage + kStageBytes);
-  uint64_t* bar = B + kHalfWords + (kHalfWords & 1);
-  const uint32_t t = threadIdx.x, w = t >> 5;
-  const uint32_t lognb = a.logn - kB14;
-  const uint64_t rowwords16 = a.n >> 4;
-
-  auto item_row = [&](uint32_t k, uint64_t& row, uint64_t& blk) {
-    row = (static_cast<uint64_t>(k) >> lognb) * a.row_mul + a.row_add;
-    blk = static_cast<uint64_t>(k) & ((uint64_t{1} << lognb) - 1);
-  };
-  auto line0 = [&](uint32_t k) {
-    uint64_t row, blk;
-    item_row(k, row, blk);
-    return static_cast<int32_t>(row * rowwords16 + (blk << (kB14 - 4)));
-  };
-  auto issue = [&](uint32_t k) {
-    const int32_t y0 = line0(k);
-    mbar_expect_tx(bar, kStageBytes);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) tma_load_2d(Astage + q * 32768, &tin, 0, y0 + q * 256, bar);
-  };
-  auto prefetch = [&](uint32_t k) {
-    const int32_t y0 = line0(k);
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-      asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                       reinterpret_cast<uint64_t>(&tin)),
-                   "r"(0), "r"(y0 + q * 256)
-                   : "memory");
-  };
-
-  if (t == 0) {
-    mbar_init(bar, 1);
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tin)) : "memory");
-  }
-  __syncthreads();
-  if (t == 0 && blockIdx.x < nitems) issue(blockIdx.x);
-  uint32_t phase = 0;
-
-  const uint32_t jt1 = P1::jt(t), jt2 = P2::jt(t), jt3 = P3::jt(t);
-  uint64_t* Wi = reinterpret_cast<uint64_t*>(Astage + w * 8192u);  // this warp's P1 slice
-  const bool e2_hi = (jt2 >> 13) & 1;
-
-  for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
-    uint64_t row, blk;
-    item_row(k, row, blk);
-    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
-    const LimbConst c = a.lc[limb];
-    const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * a.n;
-    const ulonglong2* __restrict__ twl =
-        a.twl + static_cast<uint64_t>(limb) * a.n + (blk << kB14) + (jt1 >> 5);
-    const uint64_t boff = blk << kB14;
-    uint64_t* __restrict__ dst = a.out + row * a.n + boff;
-    const uint64_t xbase = a.n + boff;
-    uint64_t v[32];
-
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    if (t == 0 && k + gridDim.x < nitems) prefetch(k + gridDim.x);
-    // ---- P1: 32 contiguous words from the swizzled staging buffer ----
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const uint32_t row16 = (jt1 >> 4) + h;
-      const uint32_t rowoff = row16 << 7, sw = row16 & 7;
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Astage + rowoff + ((cc ^ sw) << 4));
-        v[16 * h + 2 * cc] = A::load(p.x);
-        v[16 * h + 2 * cc + 1] = A::load(p.y);
-      }
-    }
-    pass14<A, false, P1, ILTM0>(v, tw, twl, a.n, xbase + jt1, c);
-
-    // ---- exchange 1, warp-local, in the warp's own slice ----
-    __syncwarp();
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-#pragma unroll
-      for (int m = 0; m < 16; m += 2)
-        *reinterpret_cast<ulonglong2*>(Wi + wimg(jt1 + 16 * h + m)) = make_ulonglong2(v[16 * h + m], v[16 * h + m + 1]);
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < 16; ++r) v[16 * h + r] = Wi[wimg(jt2 + (r << 5))];
-      __syncwarp();
-    }
-
-    pass14<A, false, P2, false>(v, tw, twl, a.n, xbase + jt2, c);
-
-    // ---- exchange 2: full, index bit 13 set -> staging buffer, clear -> half image ----
-    __syncthreads();  // every warp is done with its slice
-    {
-      uint64_t* img = e2_hi ? Ahalf : B;
-#pragma unroll
-      for (int g = 0; g < 2; ++g)
-#pragma unroll
-        for (int r = 0; r < 16; ++r) img[smem_phys((jt2 + (g << 4) + (r << 5)) & 0x1FFFu)] = v[16 * g + r];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < 32; ++r) v[r] = (r >= 16 ? Ahalf : B)[smem_phys((jt3 + 512u * r) & 0x1FFFu)];
-    __syncthreads();  // staging buffer free
-    if (t == 0 && k + gridDim.x < nitems) {
-      fence_proxy_async();
-      issue(k + gridDim.x);
-    }
-
-    pass14<A, false, P3, false>(v, tw, twl, a.n, xbase + jt3, c);
-
-    if (lognb == 0) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = inv_out<A>(v[i], c, a.fout);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = A::store(v[i]);  // intermediate of a long row
-    }
-#pragma unroll
-    for (int r = 0; r < 32; ++r) dst[jt3 | (512u * r)] = v[r];
-  }
 }
 
 }  // namespace nk

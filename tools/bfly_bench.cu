@@ -84,8 +84,6 @@ int main() {
   c.q_d = double(q);
   c.qinv = 1.0 / double(q);
   c.q_bias = double(q) + 4503599627370496.0;
-  run<Arith52F, 32>("Arith52F", 512, 1, c, wd, wd2);
-  run<Arith52F, 32, true>("Arith52F", 512, 1, c, wd, wd2);
   run<Arith52P, 32>("Arith52P", 512, 1, c, wd, wd2);
   run<Arith52P, 32, true>("Arith52P", 512, 1, c, wd, wd2);
   run<Arith52S, 32>("Arith52S", 512, 1, c, wd, wd2);

@@ -79,8 +79,6 @@ CASES = {
     "pair14_exact": lambda: transform(16384, 50, 1, 2, fout=4, exact=True),
     "pair_inverse": lambda: transform(16384, 50, 1, 2, kernel=0),
     "inv14_3barrier": lambda: transform(16384, 50, 1, 2, kernel=5),
-    "warp14": lambda: transform(16384, 50, 1, 2, kernel=2),
-    "warp14_staged": lambda: transform(16384, 50, 1, 2, kernel=4),
     "block_lat_4096": lambda: transform(4096, 50, 1, 1),               # ntt_block_lat
     "block_8192_batch": lambda: transform(8192, 50, 2, 80),            # ntt_block, >= SM count rows
     "small_1024": lambda: transform(1024, 30, 2, 2),                   # ntt_small
