@@ -162,6 +162,27 @@ def _hp(a):
     return None if a is None else C.c_void_p(a.ctypes.data)
 
 
+def _host_out(result, like, what):
+    """The result buffer of a host-buffer call: a fresh array like `like`, or
+    the caller's array, which must be a C-contiguous numpy uint64 array of the
+    same size (the library writes size * 8 bytes through its pointer)."""
+    if result is None:
+        return np.empty_like(like)
+    if (not isinstance(result, np.ndarray) or result.dtype != np.uint64
+            or not result.flags["C_CONTIGUOUS"] or not result.flags["WRITEABLE"]):
+        raise ValueError("result must be a writeable C-contiguous numpy uint64 array")
+    if result.size != like.size:
+        raise ValueError(what)
+    return result
+
+
+def _same_numel(what, *xs):
+    """Device calls: every tensor (None skipped) holds the same number of words."""
+    ns = {x.numel() for x in xs if x is not None}
+    if len(ns) > 1:
+        raise ValueError(what)
+
+
 def _np_u64_list(v):
     return np.ascontiguousarray(np.asarray(v, dtype=np.uint64).reshape(-1))
 
@@ -345,11 +366,7 @@ class RnsNtt:
             _check(fn(self._h, _dev_ptr(result), _dev_ptr(operand), limb0, nl, npolys, fin, fout, st))
             return result
         op = _host_arr(operand, "operand")
-        out = np.empty_like(op) if result is None else result
-        if not isinstance(out, np.ndarray) or out.dtype != np.uint64 or not out.flags["C_CONTIGUOUS"]:
-            raise ValueError("result must be a contiguous numpy uint64 array")
-        if out.size != op.size:
-            raise ValueError("transform: buffer length must equal n")
+        out = _host_out(result, op, "transform: buffer length must equal n")
         fn = lib().nk_ntt_forward_host if fwd else lib().nk_ntt_inverse_host
         _check(fn(self._h, _hp(out), _hp(op), op.size, limb0, nl, npolys, fin, fout,
                   None if stream is None else C.c_void_p(stream)))
@@ -368,14 +385,15 @@ class RnsNtt:
     def poly_mult_mod(self, result, f, g, limb0=0, nlimbs=None, stream=None):
         nl, npolys = self._rows(f, limb0, nlimbs)
         if _is_torch(f):
+            _same_numel("poly_mult_mod: operand lengths must equal n", f, g, result)
             st = _stream_of(f) if stream is None else C.c_void_p(stream)
             _check(lib().nk_poly_mult_mod(self._h, _dev_ptr(result), _dev_ptr(f), _dev_ptr(g),
                                           limb0, nl, npolys, st))
             return result
         fa, ga = _host_arr(f, "f"), _host_arr(g, "g")
-        out = np.empty_like(fa) if result is None else result
-        if fa.size != ga.size or out.size != fa.size:
+        if fa.size != ga.size:
             raise ValueError("poly_mult_mod: operand lengths must equal n")
+        out = _host_out(result, fa, "poly_mult_mod: operand lengths must equal n")
         _check(lib().nk_poly_mult_mod_host(self._h, _hp(out), _hp(fa), _hp(ga), fa.size, limb0, nl,
                                            npolys, None if stream is None else C.c_void_p(stream)))
         return out
@@ -383,6 +401,7 @@ class RnsNtt:
     def eltwise_mult_mod(self, result, a, b, input_mod_factor=1, limb0=0, nlimbs=None,
                          stream=None):
         nl, npolys = self._rows(a, limb0, nlimbs)
+        _same_numel("eltwise: operand lengths must match", a, b, result)
         st = _stream_of(a) if stream is None else C.c_void_p(stream)
         _check(lib().nk_plan_eltwise_mult_mod(self._h, _dev_ptr(result), _dev_ptr(a), _dev_ptr(b),
                                               limb0, nl, npolys, int(input_mod_factor), st))
@@ -457,9 +476,9 @@ def _eltwise_mult(path, result, a, b, m, input_mod_factor, stream):
                                       int(input_mod_factor), st))
         return result
     aa, bb = _host_arr(a, "a"), _host_arr(b, "b")
-    out = np.empty_like(aa) if result is None else result
-    if not (aa.size == bb.size == out.size):
+    if aa.size != bb.size:
         raise ValueError("eltwise: operand lengths must match")
+    out = _host_out(result, aa, "eltwise: operand lengths must match")
     _check(getattr(lib(), host_fn)(_hp(out), _hp(aa), _hp(bb), aa.size, q, int(input_mod_factor),
                                    _device_of_default(), None if stream is None else C.c_void_p(stream)))
     return out
@@ -494,9 +513,9 @@ def eltwise_fma_mod(result, a, y, z, m, input_mod_factor=1, bit_shift=0, stream=
         return result
     aa = _host_arr(a, "a")
     zz = None if z is None else _host_arr(z, "z")
-    out = np.empty_like(aa) if result is None else result
-    if out.size != aa.size or (zz is not None and zz.size != aa.size):
+    if zz is not None and zz.size != aa.size:
         raise ValueError("eltwise: operand lengths must match")
+    out = _host_out(result, aa, "eltwise: operand lengths must match")
     _check(lib().nk_eltwise_fma_mod_host(_hp(out), _hp(aa), int(y), _hp(zz), aa.size, q,
                                          int(input_mod_factor), int(bit_shift),
                                          _device_of_default(),
@@ -514,9 +533,9 @@ def eltwise_add_mod(result, a, b, m, stream=None):
         _check(lib().nk_eltwise_add_mod(_dev_ptr(result), _dev_ptr(a), _dev_ptr(b), a.numel(), q, st))
         return result
     aa, bb = _host_arr(a, "a"), _host_arr(b, "b")
-    out = np.empty_like(aa) if result is None else result
-    if not (aa.size == bb.size == out.size):
+    if aa.size != bb.size:
         raise ValueError("eltwise: operand lengths must match")
+    out = _host_out(result, aa, "eltwise: operand lengths must match")
     _check(lib().nk_eltwise_add_mod_host(_hp(out), _hp(aa), _hp(bb), aa.size, q, _device_of_default(),
                                          None if stream is None else C.c_void_p(stream)))
     return out
@@ -532,9 +551,7 @@ def eltwise_neg_mod(result, a, m, stream=None):
         _check(lib().nk_eltwise_neg_mod(_dev_ptr(result), _dev_ptr(a), a.numel(), q, st))
         return result
     aa = _host_arr(a, "a")
-    out = np.empty_like(aa) if result is None else result
-    if aa.size != out.size:
-        raise ValueError("eltwise: operand lengths must match")
+    out = _host_out(result, aa, "eltwise: operand lengths must match")
     _check(lib().nk_eltwise_neg_mod_host(_hp(out), _hp(aa), aa.size, q, _device_of_default(),
                                          None if stream is None else C.c_void_p(stream)))
     return out

@@ -6,7 +6,7 @@ TAG=${1:-run}
 O=gpurun_out/$TAG
 mkdir -p $O
 nvidia-smi > $O/nvsmi.txt 2>&1
-make -s -C paper_2103_16400_b200 > $O/make.log 2>&1
+# the library is prebuilt here and travels with the snapshot
 timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "pytest_gpu=$?" | tee -a $O/status
 timeout 600 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench=$?" | tee -a $O/status
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref.json 2> $O/bench_ref.err; echo "bench_ref=$?" | tee -a $O/status
