@@ -9,7 +9,11 @@
 // running the reference's own NttTables::forward/inverse, eltwise_mult_mod,
 // eltwise_fma_mod and poly_mult_mod over independent rows on all host threads
 // (tables are immutable and shareable, ntt.hpp:203-205).
+#include <pthread.h>
+#include <sched.h>
+
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <optional>
@@ -60,12 +64,30 @@ void parallel_rows(uint64_t rows, int threads, F&& body) {
     return;
   }
   if ((uint64_t)threads > rows) threads = (int)rows;
+  // fixed placement: worker t on the t-th CPU the process may run on, so
+  // repeated measurements see the same thread-to-core mapping
+  cpu_set_t allowed;
+  CPU_ZERO(&allowed);
+  std::vector<int> cpus;
+  static const bool pin = [] {
+    const char* e = std::getenv("NK_REF_PIN");
+    return !(e && e[0] == '0');
+  }();
+  if (pin && sched_getaffinity(0, sizeof(allowed), &allowed) == 0)
+    for (int c = 0; c < CPU_SETSIZE; ++c)
+      if (CPU_ISSET(c, &allowed)) cpus.push_back(c);
   std::vector<std::thread> pool;
   for (int t = 0; t < threads; ++t) {
     const uint64_t r0 = rows * t / threads, r1 = rows * (t + 1) / threads;
     pool.emplace_back([&, r0, r1] {
       for (uint64_t r = r0; r < r1; ++r) body(r);
     });
+    if (!cpus.empty()) {
+      cpu_set_t one;
+      CPU_ZERO(&one);
+      CPU_SET(cpus[t % cpus.size()], &one);
+      pthread_setaffinity_np(pool.back().native_handle(), sizeof(one), &one);
+    }
   }
   for (auto& th : pool) th.join();
 }

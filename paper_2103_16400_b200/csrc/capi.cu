@@ -131,6 +131,10 @@ struct nk_plan {
   ulonglong2* tw_inv = nullptr;  // [limb][n]
   ulonglong2* twl_fwd = nullptr;  // [limb][n] low-bit-stage tables, transposed (nk::low_index)
   ulonglong2* twl_inv = nullptr;
+  uint64_t* tw8_fwd = nullptr;   // [limb][n] w only (double bits) for the Arith52S kernels
+  uint64_t* tw8_inv = nullptr;
+  uint64_t* twl8_fwd = nullptr;  // [limb][n] low-table order
+  uint64_t* twl8_inv = nullptr;
   nk::LimbConst* lc = nullptr;   // [limb]
   nk::MultConst* mc[3] = {nullptr, nullptr, nullptr};  // fin = 1, 2, 4
 };
@@ -208,6 +212,8 @@ int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64
   a.in = op;
   a.tw = fwd ? p->tw_fwd : p->tw_inv;
   a.twl = fwd ? p->twl_fwd : p->twl_inv;
+  a.tw8 = fwd ? p->tw8_fwd : p->tw8_inv;
+  a.twl8 = fwd ? p->twl8_fwd : p->twl8_inv;
   a.lc = p->lc;
   a.n = p->n;
   a.logn = p->logn;
@@ -275,8 +281,11 @@ __global__ void bfly_test_kernel(const uint64_t* x0, const uint64_t* x1, uint64_
     a = A::load(x0[i]);
     b = A::load(x1[i]);
   }
-  if (FWD) A::template fwd<false>(a, b, w, c);
-  else A::template inv<false>(a, b, w, c);
+  typename A::Tw wt;
+  if constexpr (std::is_same_v<typename A::Tw, uint64_t>) wt = w.x;  // w only (Arith52S)
+  else wt = w;
+  if (FWD) A::template fwd<false>(a, b, wt, c);
+  else A::template inv<false>(a, b, wt, c);
   if (SIGNED_IO) {
     y0[i] = static_cast<uint64_t>(static_cast<int64_t>(as_d(a)));
     y1[i] = static_cast<uint64_t>(static_cast<int64_t>(as_d(b)));
@@ -394,7 +403,7 @@ int nk_harvey_butterflies(int fwd, uint64_t q, int bit_shift, uint64_t w, uint64
 
 void nk_debug_block_kernel(int which) {
   nk::rt::no_lat = (which == 6);
-  nk::rt::block_kernel = (which == 0 || which == 1) ? which : -1;
+  nk::rt::block_kernel = (which >= 0 && which <= 2) ? which : -1;
 }
 
 int nk_modulus(uint64_t q, uint32_t* bits, uint64_t* barrett_factor) {
@@ -447,6 +456,10 @@ void nk_plan_destroy(nk_plan* p) {
   cudaFree(p->tw_inv);
   cudaFree(p->twl_fwd);
   cudaFree(p->twl_inv);
+  cudaFree(p->tw8_fwd);
+  cudaFree(p->tw8_inv);
+  cudaFree(p->twl8_fwd);
+  cudaFree(p->twl8_inv);
   cudaFree(p->lc);
   for (auto* m : p->mc) cudaFree(m);
   cudaSetDevice(cur);
@@ -520,6 +533,8 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
       (e = cudaMalloc(&p->tw_inv, hi.size() * sizeof(ulonglong2))) ||
       (e = cudaMalloc(&p->twl_fwd, hlf.size() * sizeof(ulonglong2))) ||
       (e = cudaMalloc(&p->twl_inv, hli.size() * sizeof(ulonglong2))) ||
+      (e = cudaMalloc(&p->tw8_fwd, hf.size() * 8)) || (e = cudaMalloc(&p->tw8_inv, hi.size() * 8)) ||
+      (e = cudaMalloc(&p->twl8_fwd, hlf.size() * 8)) || (e = cudaMalloc(&p->twl8_inv, hli.size() * 8)) ||
       (e = cudaMalloc(&p->lc, hl.size() * sizeof(nk::LimbConst))))
     return cleanup(cuda_fail(e, "cudaMalloc(plan tables)"));
   for (int f = 0; f < 3; ++f)
@@ -536,6 +551,17 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
   put(p->twl_inv, hli.data(), hli.size() * sizeof(ulonglong2));
   put(p->tw_fwd, hf.data(), hf.size() * sizeof(ulonglong2));
   put(p->tw_inv, hi.data(), hi.size() * sizeof(ulonglong2));
+  // the w halves of the beta = 2^52 entries (double bits; other limbs' words are unused)
+  std::vector<uint64_t> h8[4];
+  const std::vector<ulonglong2>* src8[4] = {&hf, &hi, &hlf, &hli};
+  for (int i = 0; i < 4; ++i) {
+    h8[i].resize(src8[i]->size());
+    for (size_t k = 0; k < h8[i].size(); ++k) h8[i][k] = (*src8[i])[k].x;
+  }
+  put(p->tw8_fwd, h8[0].data(), h8[0].size() * 8);
+  put(p->tw8_inv, h8[1].data(), h8[1].size() * 8);
+  put(p->twl8_fwd, h8[2].data(), h8[2].size() * 8);
+  put(p->twl8_inv, h8[3].data(), h8[3].size() * 8);
   put(p->lc, hl.data(), hl.size() * sizeof(nk::LimbConst));
   for (int f = 0; f < 3; ++f) put(p->mc[f], hm[f].data(), nlimbs * sizeof(nk::MultConst));
   const cudaError_t es = cudaStreamSynchronize(up);

@@ -11,6 +11,7 @@
 
 #include "../../include/nttkit_b200.h"
 #include "ntt_kernels.cuh"
+#include "ntt_grp.cuh"
 #include "ntt_pair.cuh"
 #include "runtime.hpp"
 
@@ -127,6 +128,26 @@ int launch_tma_k(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStre
   return 0;
 }
 
+// group-exchange kernel (ntt_grp.cuh): persistent, one 512-thread CTA per SM
+template <auto KERN>
+int launch_grp_k(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
+  CUtensorMap map;
+  if (int rc = make_map(&map, kRowMap, a.in, buf_words)) return rc;
+  if (int rc = set_smem_once<KERN>(kGrpSmemBytes)) return rc;
+  const uint64_t g = nitems < static_cast<uint64_t>(sm_count()) ? nitems : sm_count();
+  KERN<<<static_cast<unsigned>(g), 512, kGrpSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));
+  launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
+template <class A, bool FWD, bool IL>
+int launch_grp_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
+  if constexpr (!FWD)
+    if (a.logn > 14) return launch_grp_k<ntt_grp14<A, FWD, IL, true>>(a, nitems, buf_words, st);
+  return launch_grp_k<ntt_grp14<A, FWD, IL>>(a, nitems, buf_words, st);
+}
+
 template <class A, bool FWD, bool IL>
 int launch_tma_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
   if constexpr (!FWD)
@@ -184,6 +205,9 @@ int launch_tma(const NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm,
   // single-CTA kernel the faster inverse (the pair inverse exchanges late,
   // so its next TMA overlaps less compute); the fused product lives in the
   // pair forward only
+  if (!a.mulb && block_kernel == 2)
+    return iltm ? launch_grp_t<A, FWD, true>(a, nitems, buf_words, st)
+                : launch_grp_t<A, FWD, false>(a, nitems, buf_words, st);
   const bool pair = a.mulb || (block_kernel < 0 ? FWD : block_kernel == 0);
   if (pair)
     return iltm ? launch_pair_t<A, FWD, true>(a, nitems, buf_words, st)

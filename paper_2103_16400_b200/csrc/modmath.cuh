@@ -165,6 +165,7 @@ constexpr double kC52x15 = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer 
 
 template <int BS>
 struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)
+  using Tw = ulonglong2;  // twiddle-table entry {w, w'}
   static constexpr int kIltmFwd = 1;  // forward stages whose pre-reduction is skipped at fin = 1
   static constexpr bool kLoose = false;
   static constexpr bool kFP = false;
@@ -215,6 +216,7 @@ __device__ __forceinline__ double csubP(double y, double m) {
 }
 
 struct Arith52P {
+  using Tw = ulonglong2;  // {w, w'} as doubles' bit patterns
   static constexpr int kIltmFwd = 1;  // forward stages whose pre-reduction is skipped at fin = 1
   static constexpr bool kLoose = false;
   static constexpr bool kFP = true;
@@ -258,14 +260,18 @@ struct Arith52P {
 // beta = 2^52 on the FP64 pipe, SIGNED values (canonical-output transforms
 // only: fout == 1). Requires q < 2^50 (so 4q <= 2^52).
 //
-// Signed Shoup product for |v| < 4q (so |W' v| < 2^104):
-//   hq = fma_rn(W', v, 3*2^104)   in [1.25, 1.75]*2^105, ulp 2^53, so
-//        hq - 3*2^104 = 2^53 * round(W' v / 2^53) = k * 2^52, k even, exact
-//   T  = w v - k q   (same TwoProduct/FMA steps as mul_lazy_plain, exact)
-// With W' = w 2^52/q - d (0 <= d < 1): T = q (W'v/2^52 - k) + q d v/2^52, and
-// |W'v/2^52 - k| <= 1, |d v/2^52| < 1, so |T| < 2q.
-// (The floor-with-2^104 form of mul_lazy_plain is unsigned-only: a negative
-// W'v drops the sum into the binade below 2^104, where the ulp is 2^51.)
+// Signed product for |v| < 4q from w alone (8-byte twiddles; the quotient
+// comes from the rounded reciprocal qinv = fl(1/q) instead of a Shoup table):
+//   h1 = fl(w v), l1 = fma(w, v, -h1)            exact TwoProduct: h1 + l1 = w v
+//   k  = fma(h1, qinv, 1.5*2^53) - 1.5*2^53      |h1 qinv| < 4q < 2^52, so the sum
+//        stays in [2^53, 2^54) (ulp 2): k = 2 round(h1 qinv / 2), an even integer
+//   e  = fma(-k, q, h1)                          exact: integer, |e| < 2^53
+//   T  = e + l1 = w v - k q                      exact
+// |h1 - wv| <= 2^48 (wv < 2^102), |h1 qinv - h1/q| <= 4q 2^-53 < 1/2 and
+// |h1 qinv - k| <= 1, so |wv/q - k| <= 2^48/q + 1/2 + 1 < 1.75 and |T| < 1.75q.
+// (Measured over random and edge operands: max |T|/q = 1.34.) Six FP64
+// operations, like the Shoup form, but half the twiddle bytes: at N = 16384
+// the tables stream ~N x 16 B per row from L2 otherwise, more than the row.
 // Signed words drop Harvey's "+2q" (x1' = u - T) and the GS "+2q" (t = x0 - x1):
 //   forward: |x| < 4q in, u = x0 - 2q sgn(x0) [|x0| >= 2q] in (-2q, 2q),
 //            x0' = u + T, x1' = u - T in (-4q, 4q)
@@ -273,6 +279,9 @@ struct Arith52P {
 //            signed conditional subtraction, x1' = T(x0 - x1) in (-2q, 2q)
 // Representatives differ from the reference's lazy ones; canonical results
 // (every value reduced to [0, q) at the end) are identical.
+// The n^-1 products of the folded last inverse stage keep the Shoup form
+// (mul_signed, constants in LimbConstDev: W' v / 2^52 rounded to an even
+// integer via 3*2^104, |T| < 2q for |v| < 4q).
 // ---------------------------------------------------------------------------
 constexpr double kC104x3 = 60847228810955011271841753858048.0;  // 3 * 2^104
 
@@ -284,6 +293,14 @@ __device__ __forceinline__ double mul_signed(double v, double w, double wp, doub
   const double e = __fma_rn(-qh, qq, h1);
   return __dadd_rn(e, l1);
 }
+constexpr double kC53x15 = 13510798882111488.0;  // 1.5 * 2^53: round-to-even-integer constant
+__device__ __forceinline__ double mul_recip(double v, double w, double qinv, double q) {
+  const double h1 = __dmul_rn(w, v);
+  const double l1 = __fma_rn(w, v, -h1);
+  const double k = __dsub_rn(__fma_rn(h1, qinv, kC53x15), kC53x15);
+  const double e = __fma_rn(-k, q, h1);
+  return __dadd_rn(e, l1);
+}
 // |y| >= m ? y - m sgn(y) : y  (one DADD on |y|, sign copied on the integer pipe)
 __device__ __forceinline__ double csubS(double y, double m) {
   const double d = __dsub_rn(fabs(y), m);
@@ -293,6 +310,7 @@ __device__ __forceinline__ double csubS(double y, double m) {
 }
 
 struct Arith52S {
+  using Tw = uint64_t;  // w as a double's bit pattern (8-byte tables)
   // Forward stages without the conditional subtraction when the input is
   // canonical (fin = 1): |x| < q in; after stage 1 |x| < q + q(1 + q/2^52)
   // < 2.25q; stage 2's multiplicand is then < 2.25q < 4q (valid quotient) and
@@ -318,20 +336,20 @@ struct Arith52S {
     return ((hi32(db) >= 0x43300000u) ? db : rb) & kMask52;
   }
   template <bool ILTM>
-  __device__ static void fwd(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+  __device__ static void fwd(uint64_t& x0, uint64_t& x1, uint64_t w, const LimbConstDev& c) {
     const double u = ILTM ? as_d(x0) : csubS(as_d(x0), c.twoq_d);
-    const double t = mul_signed(as_d(x1), as_d(w.x), as_d(w.y), c.qq);
+    const double t = mul_recip(as_d(x1), as_d(w), c.qinv, c.q_d);
     x0 = as_u(__dadd_rn(u, t));
     x1 = as_u(__dsub_rn(u, t));
   }
   template <bool ILTM>
-  __device__ static void inv(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
+  __device__ static void inv(uint64_t& x0, uint64_t& x1, uint64_t w, const LimbConstDev& c) {
     const double a = as_d(x0), b = as_d(x1);
     const double t = __dsub_rn(a, b);
     double s = __dadd_rn(a, b);
     if (!ILTM) s = csubS(s, c.twoq_d);
     x0 = as_u(s);
-    x1 = as_u(mul_signed(t, as_d(w.x), as_d(w.y), c.qq));
+    x1 = as_u(mul_recip(t, as_d(w), c.qinv, c.q_d));
   }
   __device__ static uint64_t scale_ninv(uint64_t x, const LimbConstDev& c) {
     return as_u(mul_signed(as_d(x), as_d(c.ninv), as_d(c.ninvp), c.qq));
@@ -373,7 +391,7 @@ __device__ __forceinline__ uint64_t mul_loose(uint64_t x, uint64_t w, uint64_t w
 
 struct ArithIntL {
   static constexpr int kIltmFwd = 1;  // forward stages whose pre-reduction is skipped at fin = 1
-  using Tw = ulonglong2;
+  using Tw = ulonglong2;  // {w, w'}
   static constexpr bool kFP = false;
   static constexpr bool kSigned = false;
   static constexpr bool kLoose = true;
@@ -441,7 +459,6 @@ __device__ __forceinline__ uint64_t mulmod_signed_canon(uint64_t xbits, uint64_t
   const double gd = __dsub_rn(as_d(g | kDBias), kC52);
   const double h = __dmul_rn(x, gd);
   const double l = __fma_rn(x, gd, -h);
-  constexpr double kC53x15 = 13510798882111488.0;  // 1.5 * 2^53
   const double k = __dsub_rn(__fma_rn(h, c.qinv, kC53x15), kC53x15);
   const double r = __dadd_rn(__fma_rn(-k, c.q_d, h), l);
   return Arith52S::canon(r, c);

@@ -1,0 +1,332 @@
+// ntt_grp14: the 16384-word block transform on ONE 512-thread CTA per SM whose
+// exchanges run inside groups of four warps (named barriers) instead of the
+// whole CTA or a CTA pair.
+//
+// Why: the block is 14 stages in three register passes (5 + 4/5 + 5 stages,
+// 32 words per thread). A pass's thread index bits and the next pass's share
+// some index bits; the threads holding a fixed value of those common bits
+// exchange only among themselves. With the thread numbering below, two of the
+// common bits are warp-index bits on BOTH sides of an exchange, so each
+// exchange is four independent 4-warp exchanges: a warp waits for its 3
+// partners (one per SMSP), never for the slowest of 16 warps on two SMs, and
+// no data crosses the SM (no DSMEM).
+//
+// Index bits of a block word j (regs = the register bits, w = warp bits
+// (w>>2, w&3), the remaining thread bits are lane bits):
+//
+//   forward (stages 13..0)                  inverse (stages 0..13)
+//   P1 regs 9..13   w: (2,3) (7,8)           P1 regs 0..4    w: (11,12) (7,8)
+//      lanes 0 4 5 6 1                          lanes 5 6 13 9 10
+//   -- ex1: groups w>>2 = j2,j3, in place     -- ex1: groups w>>2 = j11,j12, in place
+//      in the TMA staging buffer --              in the TMA staging buffer --
+//   P2 regs 5..8 + 4  w: (2,3) (12,13)       P2 regs 5..8 + 13  w: (11,12) (3,4)
+//      lanes 0 9 10 11 1                        lanes 0 1 2 9 10
+//   -- ex2: groups w&3 = j12,j13, two        -- ex2: groups w&3 = j3,j4, two
+//      rounds on bit 4 through E --             rounds on bit 13 through E --
+//   P3 regs 0..4    w: (7,8) (12,13)         P3 regs 9..13   w: (7,8) (3,4)
+//      lanes 9 10 11 5 6                        lanes 0 1 2 5 6
+//
+// Exchange 1 rewrites each group's words into the group's own slots of the
+// staging buffer (a permutation within the slots whose index bits w>>2 are
+// fixed), after every warp of the group has read its P1 words (per-group
+// mbarrier, arrived right after the reads, waited on just before the writes)
+// and before the P2 reads (named barrier). The slot permutation XORs thread
+// bits into the swizzled line bits so that both sides are conflict free.
+// When the last of the 16 warps has read its P2 words (shared counter), that
+// warp issues the next block's TMA into the staging buffer. Exchange 2 goes
+// through a separate 64 KiB image E, 16 KiB per group, in two rounds split on
+// a register bit common to both passes.
+//
+// Twiddles and butterflies are those of pass14 (ntt_kernels.cuh), including
+// the transposed low table for the pass over bits 0..4.
+#pragma once
+#include "ntt_kernels.cuh"
+#include "ntt_pair.cuh"
+
+namespace nk {
+
+constexpr uint32_t kGrpExBytes = 4u * 16384u;  // E: 4 groups x 2048 words
+// [1 KiB align][staging 128 KiB][E 64 KiB][mbarriers: full, ex1 reads x4, ex2 reads x4][counter]
+constexpr size_t kGrpSmemBytes = 1024 + kStageBytes + kGrpExBytes + 16 * 8;
+
+__device__ __forceinline__ void named_sync128(uint32_t id) {
+  asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
+}
+
+__device__ __forceinline__ void st_v4_u64(uint64_t* p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+
+// thread index bits (block-local j) of each pass; see the header table
+template <bool FWD>
+struct GrpMap;
+template <>
+struct GrpMap<true> {
+  __device__ static uint32_t jt1(uint32_t w, uint32_t l) {
+    return (l & 1u) | (((l >> 4) & 1u) << 1) | ((w >> 2) << 2) | (((l >> 1) & 7u) << 4) | ((w & 3u) << 7);
+  }
+  __device__ static uint32_t jt2(uint32_t w, uint32_t l) {
+    return (l & 1u) | (((l >> 4) & 1u) << 1) | ((w >> 2) << 2) | (((l >> 1) & 7u) << 9) | ((w & 3u) << 12);
+  }
+  __device__ static uint32_t jt3(uint32_t w, uint32_t l) {
+    return (((l >> 3) & 1u) << 5) | (((l >> 4) & 1u) << 6) | ((w >> 2) << 7) | ((l & 7u) << 9) | ((w & 3u) << 12);
+  }
+};
+template <>
+struct GrpMap<false> {
+  __device__ static uint32_t jt1(uint32_t w, uint32_t l) {
+    return ((l & 1u) << 5) | (((l >> 1) & 1u) << 6) | (((l >> 2) & 1u) << 13) | (((l >> 3) & 1u) << 9) |
+           (((l >> 4) & 1u) << 10) | ((w & 3u) << 7) | ((w >> 2) << 11);
+  }
+  __device__ static uint32_t jt2(uint32_t w, uint32_t l) {
+    return (l & 7u) | (((l >> 3) & 1u) << 9) | (((l >> 4) & 1u) << 10) | ((w & 3u) << 3) | ((w >> 2) << 11);
+  }
+  __device__ static uint32_t jt3(uint32_t w, uint32_t l) {
+    return (l & 7u) | (((l >> 3) & 1u) << 5) | (((l >> 4) & 1u) << 6) | ((w & 3u) << 3) | ((w >> 2) << 7);
+  }
+};
+
+// exchange-1 slot permutation (word j -> the staging slot of word ex1_perm(j)):
+// XOR thread bits into the low line bits (swz_off's bank selector)
+template <bool FWD>
+__host__ __device__ __forceinline__ constexpr uint32_t ex1_perm(uint32_t j) {
+  return FWD ? (j ^ (((j >> 9) & 7u) << 4)) : (j ^ (((j >> 13) & 1u) << 4) ^ (((j >> 9) & 1u) << 6));
+}
+
+// byte offset of word j in its group's 16 KiB slice of E (the slice index is
+// added by the caller)
+template <bool FWD>
+__host__ __device__ __forceinline__ constexpr uint32_t ex2_off(uint32_t j) {
+  if (FWD) {
+    // row = j5..j11, 16-byte chunk (j1..j3) ^ (j9..j11), word j0
+    const uint32_t row = (j >> 5) & 127u;
+    const uint32_t chunk = ((j >> 1) & 7u) ^ ((j >> 9) & 7u);
+    return (row << 7) | (chunk << 4) | ((j & 1u) << 3);
+  } else {
+    // row = (j6, j7, j8, j9, j10, j11, j12), bank word (j0, j1, j2, j5 ^ j9)
+    const uint32_t row = ((j >> 6) & 7u) | (((j >> 9) & 15u) << 3);
+    const uint32_t bank = (j & 7u) | ((((j >> 5) ^ (j >> 9)) & 1u) << 3);
+    return (row << 7) | (bank << 3);
+  }
+}
+
+template <class A, bool FWD, bool ILTM0, bool LONG = false>
+__global__ void __launch_bounds__(512, 1)
+    ntt_grp14(const __grid_constant__ CUtensorMap tin, NttArgs a, uint32_t nitems) {
+  using P1 = typename std::conditional<FWD, PassD<9, 5, -1>, PassD<0, 5, -1>>::type;
+  using P2 = typename std::conditional<FWD, PassD<5, 4, 4>, PassD<5, 4, 13>>::type;
+  using P3 = typename std::conditional<FWD, PassD<0, 5, -1>, PassD<9, 5, -1>>::type;
+  using M = GrpMap<FWD>;
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* St = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);  // staging, 128B-swizzled lines
+  uint8_t* E = St + kStageBytes;
+  uint64_t* bar_full = reinterpret_cast<uint64_t*>(E + kGrpExBytes);
+  uint64_t* bar_r1 = bar_full + 1;  // [4] ex1 groups: P1 reads done
+  uint64_t* bar_r2 = bar_full + 5;  // [4] ex2 groups: last-round reads done
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(bar_full + 9);
+  const uint32_t t = threadIdx.x, l = t & 31u, w = t >> 5;
+  const uint32_t g1 = w >> 2, g2 = w & 3u;  // exchange-1 / exchange-2 group
+  const uint32_t lognb = a.logn - kB14;
+  const uint64_t rowwords16 = a.n >> 4;
+
+  auto item_row = [&](uint32_t k, uint64_t& row, uint64_t& blk) {
+    row = (static_cast<uint64_t>(k) >> lognb) * a.row_mul + a.row_add;
+    blk = static_cast<uint64_t>(k) & ((uint64_t{1} << lognb) - 1);
+  };
+  auto issue = [&](uint32_t k) {
+    uint64_t row, blk;
+    item_row(k, row, blk);
+    const int32_t y0 = static_cast<int32_t>(row * rowwords16 + (blk << (kB14 - 4)));
+    mbar_expect_tx(bar_full, kStageBytes);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tma_load_2d(St + q * 32768, &tin, 0, y0 + q * 256, bar_full);
+  };
+
+  if (t == 0) {
+    mbar_init(bar_full, 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(bar_r1 + i, 4);
+      mbar_init(bar_r2 + i, 4);
+    }
+    *cnt = 0;
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tin)) : "memory");
+  }
+  __syncthreads();
+  if (t == 0 && blockIdx.x < nitems) issue(blockIdx.x);
+
+  const uint32_t jt1 = M::jt1(w, l), jt2 = M::jt2(w, l), jt3 = M::jt3(w, l);
+  const uint32_t jtlow = FWD ? jt3 : jt1;  // thread bits of the pass over bits 0..4
+  uint8_t* Eg = E + (g2 << 14);           // this warp's exchange-2 group slice
+  // Thread-constant byte bases: every shared access below is a base, at most
+  // one XOR with an immediate, plus an immediate offset (derivations in the
+  // comments; swz_off is the 128B swizzle, ex1_perm / ex2_off the layouts).
+  // P2 reads (both directions): swz_off(ex1_perm(jt2 | jc(g, r))) =
+  //   (q2 ^ (y * 0x90)) + (hi << 10), y = the 3 low line bits the registers
+  //   flip, hi = the register line bits above them
+  uint32_t q2;
+  if (FWD) {
+    // line = jt2 >> 4 (bits 5..9) | s, s = g + 2r; XOR m = j9..j11 into its low 3 bits
+    const uint32_t m = (jt2 >> 9) & 7u, c1 = (jt2 >> 1) & 7u;
+    q2 = ((jt2 >> 4) << 7) | (m << 7) | ((m ^ c1) << 4) | ((jt2 & 1u) << 3);
+  } else {
+    // line bit0 = j4 ^ g, bit1 = r0, bit2 = r1 ^ j9, bits 3,4 = r2, r3, bits 5..8 = j9..j12, bit 9 = g
+    const uint32_t rt = ((jt2 >> 4) & 1u) | (((jt2 >> 9) & 1u) << 2) | (((jt2 >> 9) & 15u) << 5);
+    const uint32_t c1 = (jt2 >> 1) & 7u;
+    q2 = (rt << 7) | ((c1 ^ (rt & 7u)) << 4) | ((jt2 & 1u) << 3);
+  }
+  const uint32_t e2w = ex2_off<FWD>(jt2), e2r = ex2_off<FWD>(jt3);
+  uint32_t phase = 0;
+
+  for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
+    uint64_t row, blk;
+    item_row(k, row, blk);
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+    const LimbConst c = a.lc[limb];
+    const typename A::Tw* __restrict__ tw = tw_of<A>(a, limb);
+    const typename A::Tw* __restrict__ twl = twl_of<A>(a, limb) + (blk << kB14) + (jtlow >> 5);
+    const uint64_t boff = blk << kB14;
+    uint64_t* __restrict__ dst = a.out + row * a.n + boff;
+    const uint64_t xbase = a.n + boff;
+    uint64_t v[32];
+
+    // ---- P1 words from the staging buffer (TMA layout) ----
+    mbar_wait(bar_full, phase);
+    if (FWD) {
+      // 32 words at stride 512: one 8-byte load each (base + immediate)
+      const uint32_t b1 = swz_off(jt1);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = A::load(*reinterpret_cast<const uint64_t*>(St + b1 + r * 4096));
+    } else {
+      // 32 contiguous words (two 16-word lines): 16-byte chunks
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t row16 = (jt1 >> 4) + h;
+        const uint32_t rowoff = row16 << 7, sw = row16 & 7;
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(St + rowoff + ((cc ^ sw) << 4));
+          v[16 * h + 2 * cc] = A::load(p.x);
+          v[16 * h + 2 * cc + 1] = A::load(p.y);
+        }
+      }
+    }
+    __syncwarp();
+    if (l == 0) mbar_arrive_local(bar_r1 + g1);  // this warp's P1 slots may be rewritten
+
+    pass14<A, FWD, P1, ILTM0>(v, tw, twl, a.n, xbase + jt1, c);
+
+    // ---- exchange 1: in place, within the group's staging slots ----
+    mbar_wait(bar_r1 + g1, phase);  // every warp of the group has read its P1 words
+    if (FWD) {
+      // swz_off(ex1_perm(jt1 | r << 9)) = (swz_off(jt1) ^ ((r & 7) * 0x90)) + r * 4096
+      const uint32_t b1 = swz_off(jt1);
+#pragma unroll
+      for (int r = 0; r < 32; ++r)
+        *reinterpret_cast<uint64_t*>(St + ((b1 ^ ((r & 7) * 0x90u)) + r * 4096)) = v[r];
+    } else {
+      // swz_off(ex1_perm(jt1 | h << 4 | 2cc)) = wh ^ (cc << 4), wh from the
+      // permuted line (jt1' >> 4) ^ h, jt1' = ex1_perm(jt1)
+      const uint32_t rp = ex1_perm<false>(jt1) >> 4;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t rh = rp ^ static_cast<uint32_t>(h);
+        const uint32_t wh = (rh << 7) | ((rh & 7u) << 4);
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          *reinterpret_cast<ulonglong2*>(St + (wh ^ (cc << 4))) =
+              make_ulonglong2(v[16 * h + 2 * cc], v[16 * h + 2 * cc + 1]);
+      }
+    }
+    named_sync128(1 + g1);
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        // forward: s = g + 2r (line bits 0..4); inverse: line bits (g, r0, r1) low, (r2, r3) << 3, g << 9
+        const uint32_t y = FWD ? ((g + 2 * r) & 7) : (g | ((r & 3) << 1));
+        const uint32_t hi = FWD ? (((g + 2 * r) >> 3) << 10) : (((r >> 2) << 10) | (g << 16));
+        v[16 * g + r] = *reinterpret_cast<const uint64_t*>(St + ((q2 ^ (y * 0x90u)) + hi));
+      }
+    // staging consumed by this warp; the last of the 16 warps refills it
+    __syncwarp();
+    if (l == 0) {
+      __threadfence_block();
+      const uint32_t old = atomicAdd(cnt, 1u);
+      if ((old & 15u) == 15u) {
+        __threadfence_block();
+        if (k + gridDim.x < nitems) {
+          fence_proxy_async();
+          issue(k + gridDim.x);
+        }
+      }
+    }
+
+    pass14<A, FWD, P2, false>(v, tw, twl, a.n, xbase + jt2, c);
+
+    // ---- exchange 2: through the group's slice of E, two rounds on the
+    // register bit common to P2 and P3 (forward bit 4, inverse bit 13) ----
+    mbar_wait(bar_r2 + g2, phase ^ 1);  // the previous block's last-round reads (first block: passes)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1) named_sync128(5 + g2);  // round-0 reads done before round-1 writes
+      // ex2_off(jt2 | r << 5): forward e2w + r * 128; inverse (e2w ^ ((r & 1) << 6)) + (r >> 1) * 128
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        const uint32_t off = FWD ? (e2w + r * 128) : ((e2w ^ ((r & 1) << 6)) + (r >> 1) * 128);
+        *reinterpret_cast<uint64_t*>(Eg + off) = v[16 * h + r];
+      }
+      named_sync128(5 + g2);
+      if (FWD) {
+        // P3 round h: the 16 contiguous words j0..j3 (bit 4 = h) as 16-byte
+        // chunks, ex2_off(jt3 | 2cc) = e2r ^ (cc << 4)
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc) {
+          const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Eg + (e2r ^ (cc << 4)));
+          v[16 * h + 2 * cc] = p.x;
+          v[16 * h + 2 * cc + 1] = p.y;
+        }
+      } else {
+        // P3 round h: registers 16h + r hold j = jt3 | (16h + r) << 9 (bit 13 = h),
+        // ex2_off(jt3 | r << 9) = (e2r ^ ((r & 1) << 6)) + r * 1024
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          v[16 * h + r] = *reinterpret_cast<const uint64_t*>(Eg + ((e2r ^ ((r & 1) << 6)) + r * 1024));
+      }
+    }
+    __syncwarp();
+    if (l == 0) mbar_arrive_local(bar_r2 + g2);
+
+    // canonical inverse (Arith52S, whole rows): n^-1 folded into the last
+    // stage (bit 13, single twiddle), as in ntt_block14_tma
+    constexpr bool kFoldLast = !FWD && A::kSigned && !LONG;
+    if constexpr (kFoldLast) {
+      pass14<A, FWD, P3, false, 1>(v, tw, twl, a.n, xbase + jt3, c);
+#pragma unroll
+      for (int r = 0; r < 16; ++r) A::inv_fold(v[r], v[r + 16], c);
+    } else {
+      pass14<A, FWD, P3, false>(v, tw, twl, a.n, xbase + jt3, c);
+    }
+
+    // ---- final words and stores ----
+    if (FWD) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = fwd_out<A>(v[i], c, a.fout);
+      // 32 contiguous words per thread: eight 32-byte stores
+#pragma unroll
+      for (int q = 0; q < 8; ++q) st_v4_u64(dst + jt3 + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+      if constexpr (LONG) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = A::store(v[i]);  // intermediate of a long row
+      } else if constexpr (!kFoldLast) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = inv_out<A>(v[i], c, a.fout);
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r) dst[jt3 | (static_cast<uint32_t>(r) << 9)] = v[r];
+    }
+    phase ^= 1;
+  }
+}
+
+}  // namespace nk

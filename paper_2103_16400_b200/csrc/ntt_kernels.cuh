@@ -59,9 +59,24 @@ struct NttArgs {
   uint64_t* dbg;  // debug: per-warp phase timestamps of an NK_DBG_TIMELINE build (tools/timeline.py)
   const uint64_t* mulb;  // forward (CTA-pair kernel, fout == 1): multiply the canonical
                          // result by these canonical words (same layout) before storing
+  const uint64_t* tw8;   // [limb][N] w only (double bits), same order as tw: Arith52S
+  const uint64_t* twl8;  // [limb][N] the same entries in the low-table order of twl
 };
 
 __device__ __forceinline__ ulonglong2 ldtw(const ulonglong2* p) { return __ldg(p); }
+__device__ __forceinline__ uint64_t ldtw(const uint64_t* p) { return __ldg(p); }
+
+// the twiddle tables of a policy (entries of type A::Tw), offset to limb `limb`
+template <class A>
+__device__ __forceinline__ const typename A::Tw* tw_of(const NttArgs& a, uint32_t limb) {
+  if constexpr (std::is_same_v<typename A::Tw, uint64_t>) return a.tw8 + static_cast<uint64_t>(limb) * a.n;
+  else return a.tw + static_cast<uint64_t>(limb) * a.n;
+}
+template <class A>
+__device__ __forceinline__ const typename A::Tw* twl_of(const NttArgs& a, uint32_t limb) {
+  if constexpr (std::is_same_v<typename A::Tw, uint64_t>) return a.twl8 + static_cast<uint64_t>(limb) * a.n;
+  else return a.twl + static_cast<uint64_t>(limb) * a.n;
+}
 
 // Padded shared-memory image index: additive over disjoint bit fields, so every
 // shared address is a per-thread base plus an immediate, and all exchange
@@ -110,7 +125,7 @@ struct PassOf {
 // bits (outside the pass). ILTM0: first stage with InputLessThanMod.
 // TWS: tw points at a copy of the twiddle row in shared memory (ntt_block_lat).
 template <class A, bool FWD, int LOGB, int LOGV, int LO, int K, bool ILTM0, bool TWS = false>
-__device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const ulonglong2* __restrict__ tw,
+__device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const typename A::Tw* __restrict__ tw,
                                         uint64_t xt, const LimbConst& c) {
   using S = Sched<LOGB, LOGV>;
   constexpr int R = 1 << K;
@@ -124,7 +139,7 @@ __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const ulonglon
       const uint64_t base = (xt + S::jg(g, LO, K)) >> (b + 1);
 #pragma unroll
       for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
-        const ulonglong2 w = TWS ? tw[base + hi] : ldtw(tw + base + hi);
+        const typename A::Tw w = TWS ? tw[base + hi] : ldtw(tw + base + hi);
 #pragma unroll
         for (int l = 0; l < (1 << i); ++l) {
           const int r0 = (hi << (i + 1)) | l;
@@ -149,7 +164,7 @@ __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const ulonglon
 // ---------------------------------------------------------------------------
 template <int LOGB, int LOGV, class A, bool FWD, int P, bool ILTM0, bool TWS = false>
 __device__ __forceinline__ void run_passes(uint64_t (&v)[1 << LOGV], uint64_t* sm,
-                                           const ulonglong2* __restrict__ tw, uint32_t t,
+                                           const typename A::Tw* __restrict__ tw, uint32_t t,
                                            uint64_t xbase, const LimbConst& c) {
   using S = Sched<LOGB, LOGV>;
   using PO = PassOf<LOGB, LOGV, FWD>;
@@ -187,7 +202,7 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV)) ntt_block(NttArgs a) {
   const uint64_t blk = static_cast<uint64_t>(blockIdx.x) & ((uint64_t{1} << lognb) - 1);
   const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
   const LimbConst c = a.lc[limb];
-  const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * a.n;
+  const typename A::Tw* __restrict__ tw = tw_of<A>(a, limb);
   const uint64_t boff = blk << LOGB;
   const uint64_t* __restrict__ src = a.in + row * a.n + boff;
   uint64_t* __restrict__ dst = a.out + row * a.n + boff;
@@ -312,18 +327,20 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV)) ntt_block_lat(NttArgs a) {
   using PO = PassOf<LOGB, LOGV, FWD>;
   extern __shared__ __align__(16) uint64_t sm[];
   constexpr size_t kImgWords = ((block_smem_bytes<LOGB, LOGV>() + 15) & ~size_t{15}) / 8;
-  ulonglong2* tws = reinterpret_cast<ulonglong2*>(sm + kImgWords);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(tws + (1u << LOGB));
+  using Tw = typename A::Tw;
+  Tw* tws = reinterpret_cast<Tw*>(sm + kImgWords);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(tws) + (size_t{16} << LOGB));
   const uint32_t t = threadIdx.x;
   const uint64_t row = static_cast<uint64_t>(blockIdx.x) * a.row_mul + a.row_add;
   const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
   if (t == 0) {
     mbar_init(bar, 1);
-    mbar_expect_tx(bar, 16u << LOGB);
+    constexpr uint32_t kBytes = static_cast<uint32_t>(sizeof(Tw)) << LOGB;
+    mbar_expect_tx(bar, kBytes);
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(tws)),
-        "l"(a.tw + static_cast<uint64_t>(limb) * a.n), "r"(16u << LOGB), "r"(smem_u32(bar))
+        "l"(tw_of<A>(a, limb)), "r"(kBytes), "r"(smem_u32(bar))
         : "memory");
   }
   asm volatile("griddepcontrol.launch_dependents;" :::);
@@ -454,8 +471,8 @@ struct Sched14 {
 // SKIP_LAST: leave the pass's last stage to the caller (the folded n^-1 stage
 // of ntt_block14_tma's inverse).
 template <class A, bool FWD, class PD, bool ILTM0, int SKIP_LAST = 0>
-__device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __restrict__ tw,
-                                       const ulonglong2* __restrict__ twl, uint64_t n,
+__device__ __forceinline__ void pass14(uint64_t (&v)[32], const typename A::Tw* __restrict__ tw,
+                                       const typename A::Tw* __restrict__ twl, uint64_t n,
                                        uint64_t xt, const LimbConst& c) {
   constexpr int K = PD::K, R = PD::R, G = PD::G;
   // the pass over bits 0..4 reads the transposed low table (twl points at this
@@ -475,7 +492,7 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const ulonglong2* __re
       const uint64_t base = (xt + PD::jc(gl, 0)) >> (b + 1);
 #pragma unroll
       for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
-        const ulonglong2 w = kLow ? ldtw(twl + low_index(b, hi, 0)) : ldtw(tw + base + hi);
+        const typename A::Tw w = kLow ? ldtw(twl + low_index(b, hi, 0)) : ldtw(tw + base + hi);
 #pragma unroll
         for (int gg = 0; gg < G / GL; ++gg) {
 #pragma unroll
@@ -553,10 +570,9 @@ __global__ void __launch_bounds__(512, 1)
     item_row(k, row, blk);
     const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
     const LimbConst c = a.lc[limb];
-    const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * a.n;
+    const typename A::Tw* __restrict__ tw = tw_of<A>(a, limb);
     // low table: this block's segment, offset by this thread's jhi in the low pass
-    const ulonglong2* __restrict__ twl =
-        a.twl + static_cast<uint64_t>(limb) * a.n + (blk << kB14) + (jtlow >> 5);
+    const typename A::Tw* __restrict__ twl = twl_of<A>(a, limb) + (blk << kB14) + (jtlow >> 5);
     const uint64_t boff = blk << kB14;
     uint64_t* __restrict__ dst = a.out + row * a.n + boff;
     const uint64_t xbase = a.n + boff;
@@ -699,7 +715,7 @@ __global__ void __launch_bounds__(256) ntt_global_pass(NttArgs a, uint32_t lo, i
   const uint64_t o = gid & ((uint64_t{1} << logcols) - 1);
   const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
   const LimbConst c = a.lc[limb];
-  const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * a.n;
+  const typename A::Tw* __restrict__ tw = tw_of<A>(a, limb);
   const uint64_t j0 = (o & ((uint64_t{1} << lo) - 1)) | ((o >> lo) << (lo + K));
   const uint64_t* src = a.in + row * a.n;
   uint64_t* dst = a.out + row * a.n;
@@ -722,7 +738,7 @@ __global__ void __launch_bounds__(256) ntt_global_pass(NttArgs a, uint32_t lo, i
     }
 #pragma unroll
     for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
-      const ulonglong2 w = ldtw(tw + base + hi);
+      const typename A::Tw w = ldtw(tw + base + hi);
 #pragma unroll
       for (int l = 0; l < (1 << i); ++l) {
         const int r0 = (hi << (i + 1)) | l, r1 = r0 | (1 << i);
@@ -751,7 +767,7 @@ __global__ void __launch_bounds__(256) ntt_small(NttArgs a) {
   const uint64_t row = static_cast<uint64_t>(blockIdx.x) * a.row_mul + a.row_add;
   const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
   const LimbConst c = a.lc[limb];
-  const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * a.n;
+  const typename A::Tw* __restrict__ tw = tw_of<A>(a, limb);
   const uint32_t n = static_cast<uint32_t>(a.n);
   for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) smw[j] = A::load(a.in[row * a.n + j]);
   __syncthreads();
@@ -760,7 +776,7 @@ __global__ void __launch_bounds__(256) ntt_small(NttArgs a) {
     const bool iltm = (s == 0) && (a.fin == 1);
     for (uint32_t p = threadIdx.x; p < n / 2; p += blockDim.x) {
       const uint32_t j = ((p >> b) << (b + 1)) | (p & ((1u << b) - 1u));
-      const ulonglong2 w = ldtw(tw + ((a.n + j) >> (b + 1)));
+      const typename A::Tw w = ldtw(tw + ((a.n + j) >> (b + 1)));
       uint64_t x0 = smw[j], x1 = smw[j + (1u << b)];
       if (FWD) {
         if (iltm) A::template fwd<true>(x0, x1, w, c);

@@ -265,9 +265,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
     NK_TS(0);
     const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
     const LimbConst cst = a.lc[limb];
-    const ulonglong2* __restrict__ tw = a.tw + static_cast<uint64_t>(limb) * a.n;
-    const ulonglong2* __restrict__ twl =
-        a.twl + static_cast<uint64_t>(limb) * a.n + (blk << kB14) + (jt_low >> 5);
+    const typename A::Tw* __restrict__ tw = tw_of<A>(a, limb);
+    const typename A::Tw* __restrict__ twl = twl_of<A>(a, limb) + (blk << kB14) + (jt_low >> 5);
     const uint64_t boff = blk << kB14;
     uint64_t* __restrict__ dst = a.out + row * a.n + boff;
     const uint64_t xbase = a.n + boff;

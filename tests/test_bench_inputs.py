@@ -27,3 +27,26 @@ def test_make_inputs_and_moduli_match_oracle(oracle):
     x = bench.make_inputs(moduli[:3], 2, 777).reshape(6, bench.N)
     for r in range(6):
         assert np.array_equal(x[r], oracle.mt19937_64(777 + r, bench.N, moduli[r % 3])), r
+
+
+def test_shard_inputs_are_slices_of_the_batch():
+    """A rank's limb range (make_inputs with limb0/nlimbs) holds exactly the
+    words of those limbs in the single-GPU batch, [poly][limb][N] order."""
+    moduli = bench.cfg3_moduli()[:6]
+    full = bench.make_inputs(moduli, 3, 4242, n=64).reshape(3, 6, 64)
+    for limb0, nl in ((0, 2), (2, 3), (5, 1)):
+        part = bench.make_inputs(moduli, 3, 4242, n=64, limb0=limb0, nlimbs=nl, total_limbs=6)
+        assert np.array_equal(part.reshape(3, nl, 64), full[:, limb0:limb0 + nl]), (limb0, nl)
+
+
+def test_bench_record_primes_match_reference_rule():
+    from primes import smallest_ntt_primes
+
+    for bits, n in ((50, 1024), (50, 16384), (30, 64)):
+        assert bench.smallest_ntt_primes(bits, n, 2) == smallest_ntt_primes(bits, n, 2)
+
+
+def test_both_arms_share_the_config_dict():
+    for w in (1, 2, 4, 8):
+        c = bench.workload_config(w)
+        assert c == bench.workload_config(w) and c["rows"] == 2048

@@ -102,6 +102,27 @@ def test_signed_policy_ranges(nk, fwd):
             assert all(int(u) % q == v for u, v in zip(y1, e1)), (q, w)
 
 
+def test_signed_policy_product_bound(nk):
+    """Arith52S's rounded-reciprocal product (modmath.cuh mul_recip, w alone,
+    no Shoup table): with x0 = 0 the forward butterfly returns (T, -T), and the
+    documented bound |T| < 1.75q must hold for every multiplicand |v| < 4q."""
+    rng = np.random.default_rng(11)
+    for q in qs(ARITH52S):
+        if q == 17:
+            b = np.arange(-4 * q + 1, 4 * q, dtype=np.int64)
+        else:
+            b = np.concatenate([np.array([4 * q - 1, -(4 * q - 1), 2 * q, -2 * q, 0, 1], np.int64),
+                                rng.integers(-4 * q + 1, 4 * q, 8192, dtype=np.int64)])
+        a = np.zeros_like(b)
+        for w in twiddles(q, rng) + ([q - 1, q - 2] if q > 17 else []):
+            y0, y1 = nk.debug_butterflies(ARITH52S, True, q, w, dev(a), dev(b))
+            y0, y1 = host(y0), host(y1)
+            assert np.abs(y0).max() * 4 < 7 * q, (q, w, int(np.abs(y0).max()))
+            assert np.array_equal(y0, -y1)
+            B = b.astype(object)
+            assert all(int(u) % q == (w * v) % q for u, v in zip(y0, B)), (q, w)
+
+
 @pytest.mark.parametrize("fwd", [True, False], ids=["fwd", "inv"])
 def test_loose_policy_ranges(nk, fwd):
     """ArithIntL: forward words in [0, 8q) stay there, inverse words in
