@@ -4,7 +4,14 @@
 //
 //   reference (nttkit::)                        this facade (nttkit_b200::)
 //   Modulus(q)                modarith.hpp:106  Modulus(q)
+//   bit_reverse(i, log2n)     ntt.hpp:37-46     bit_reverse (host)
+//   bit_reverse_permute(v)    ntt.hpp:49-58     bit_reverse_permute (host)
+//   minimal_primitive_root    ntt.hpp:172-197   minimal_primitive_root (host)
 //   NttTables(n, m[, root])   ntt.hpp:210-217   NttTables(n, m[, root][, bit_shift])
+//   NttTables accessors       ntt.hpp:249-261   size, log2_size, modulus, root, inv_root,
+//                                               bit_shift, inv_size, root_powers_rev,
+//                                               root_precons_rev, inv_root_powers_rev,
+//                                               inv_root_precons_rev (host copies)
 //   NttTables::forward        ntt.hpp:268-285   NttTables::forward (host spans)
 //   NttTables::inverse        ntt.hpp:289-306   NttTables::inverse (host spans)
 //   eltwise_mult_mod          eltwise.hpp:180   eltwise_mult_mod
@@ -76,6 +83,49 @@ struct CoeffVec {
   }
 };
 
+/// precompute_factor<BitShift> (modarith.hpp:168-183)
+struct MultiplyFactor {
+  uint64_t operand;
+  uint64_t precon;
+  friend bool operator==(const MultiplyFactor&, const MultiplyFactor&) = default;
+};
+
+/// Reverse the low log2n bits of i (ntt.hpp:37-46). The reference checks the
+/// contract in checked builds; here a violation throws std::invalid_argument.
+constexpr uint64_t bit_reverse(uint64_t i, unsigned log2n) {
+  if (!(log2n < 64 && (log2n == 0 ? i == 0 : i >> log2n == 0)))
+    throw std::invalid_argument("bit_reverse: index must have log2n bits");
+  uint64_t r = 0;
+  for (unsigned b = 0; b < log2n; ++b) {
+    r = (r << 1) | (i & 1);
+    i >>= 1;
+  }
+  return r;
+}
+
+/// In-place bit-reversal permutation of a power-of-two-length span (an
+/// involution; ntt.hpp:49-58).
+template <typename T>
+void bit_reverse_permute(std::span<T> v) {
+  const uint64_t n = v.size();
+  if (n == 0 || (n & (n - 1)) != 0)
+    throw std::invalid_argument("bit_reverse_permute: length must be a power of two");
+  unsigned log2n = 0;
+  while ((uint64_t{1} << log2n) < n) ++log2n;
+  for (uint64_t i = 0; i < n; ++i) {
+    const uint64_t j = bit_reverse(i, log2n);
+    if (i < j) std::swap(v[i], v[j]);
+  }
+}
+
+/// Smallest primitive `order`'th root of unity mod q (ntt.hpp:172-197), the
+/// root NttTables uses when none is supplied.
+inline uint64_t minimal_primitive_root(uint64_t order, const Modulus& m) {
+  uint64_t r = 0;
+  check(nk_minimal_primitive_root(order, m.value(), &r));
+  return r;
+}
+
 // Tables of many RNS limbs on one device; batched data is [npolys][nlimbs][n].
 class RnsNtt {
  public:
@@ -139,9 +189,11 @@ class RnsNtt {
 // NttTables(n, Modulus[, root][, bit_shift]) — one limb, reference semantics.
 class NttTables : public RnsNtt {
  public:
-  NttTables(uint64_t n, const Modulus& m) : RnsNtt(n, one(m)), m_(m) {}
+  NttTables(uint64_t n, const Modulus& m) : RnsNtt(n, one(m)), m_(m) { build_host(); }
   NttTables(uint64_t n, const Modulus& m, uint64_t root)
-      : RnsNtt(n, one(m), 0, 0, std::span<const uint64_t>(&root_holder(root), 1)), m_(m) {}
+      : RnsNtt(n, one(m), 0, 0, std::span<const uint64_t>(&root_holder(root), 1)), m_(m) {
+    build_host();
+  }
   NttTables(uint64_t n, const Modulus& m, std::optional<uint64_t> root, int bit_shift)
       : RnsNtt(n, one(m), 0, bit_shift,
                root ? std::optional<std::span<const uint64_t>>(
@@ -150,18 +202,27 @@ class NttTables : public RnsNtt {
         m_(m) {
     // the reference validates the width before it looks at a root (ntt.hpp:226-231);
     // nk_plan_create applies the same order.
+    build_host();
   }
   const Modulus& modulus() const noexcept { return m_; }
-  uint64_t root() const {
-    uint64_t psi = 0;
-    check(nk_plan_info(plan(), 0, nullptr, nullptr, &psi, nullptr, nullptr));
-    return psi;
+  unsigned log2_size() const noexcept {
+    unsigned l = 0;
+    while ((uint64_t{1} << l) < size()) ++l;
+    return l;
   }
-  int bit_shift() const {
-    int bs = 0;
-    check(nk_plan_info(plan(), 0, nullptr, nullptr, nullptr, &bs, nullptr));
-    return bs;
-  }
+  uint64_t root() const { return host().psi; }
+  /// psi^-1: the inverse table holds psi^-i at bit_reverse(i), so psi^-1 sits at n/2
+  uint64_t inv_root() const { return host().wi[size() / 2]; }
+  int bit_shift() const { return host().bs; }
+  /// n^-1 mod q with its precon for the table width (ntt.hpp:259)
+  MultiplyFactor inv_size() const { return {host().ninv, host().ninvp}; }
+  /// psi^i at index bit_reverse(i), with the matching precon array (ntt.hpp:256-261);
+  /// copies of the tables the device plan was built from, bit for bit the
+  /// reference's build_tables (ntt.hpp:343-361)
+  std::span<const uint64_t> root_powers_rev() const { return host().w; }
+  std::span<const uint64_t> root_precons_rev() const { return host().wp; }
+  std::span<const uint64_t> inv_root_powers_rev() const { return host().wi; }
+  std::span<const uint64_t> inv_root_precons_rev() const { return host().wip; }
   void forward(std::span<uint64_t> result, std::span<const uint64_t> operand, uint64_t in,
                uint64_t out) const {
     if (result.size() != size() || operand.size() != size())
@@ -201,7 +262,32 @@ class NttTables : public RnsNtt {
     v = r;
     return v;
   }
+  struct HostTables {
+    uint64_t psi = 0, ninv = 0, ninvp = 0;
+    int bs = 0;
+    std::vector<uint64_t> w, wp, wi, wip;
+  };
+  // built once at construction from the plan's own (n, q, root, width), host
+  // side only; immutable afterwards (concurrent const calls are safe, ntt.hpp:203-205)
+  const HostTables& host() const { return *host_; }
+  void build_host() {
+    {
+      auto h = std::make_shared<HostTables>();
+      const uint64_t n = size();
+      h->w.resize(n);
+      h->wp.resize(n);
+      h->wi.resize(n);
+      h->wip.resize(n);
+      uint64_t psi = 0;
+      int bs = 0;
+      check(nk_plan_info(plan(), 0, nullptr, nullptr, &psi, &bs, nullptr));
+      check(nk_tables_host(n, m_.value(), &psi, bs, &h->psi, h->w.data(), h->wp.data(), h->wi.data(),
+                           h->wip.data(), &h->ninv, &h->ninvp, &h->bs));
+      host_ = std::move(h);
+    }
+  }
   Modulus m_;
+  std::shared_ptr<const HostTables> host_;
 };
 
 inline void eltwise_mult_mod(std::span<uint64_t> result, std::span<const uint64_t> a,
@@ -213,12 +299,6 @@ inline void eltwise_mult_mod(std::span<uint64_t> result, std::span<const uint64_
                                  input_mod_factor, 0, nullptr));
 }
 
-/// precompute_factor<BitShift> (modarith.hpp:168-183)
-struct MultiplyFactor {
-  uint64_t operand;
-  uint64_t precon;
-  friend bool operator==(const MultiplyFactor&, const MultiplyFactor&) = default;
-};
 
 template <int BitShift>
 inline MultiplyFactor precompute_factor(uint64_t w, const Modulus& m) {

@@ -218,6 +218,27 @@ class Modulus:
         return f"Modulus({self._q})"
 
 
+def bit_reverse(i, log2n):
+    """Reverse the low log2n bits of i (ntt.hpp:37-46)."""
+    i, log2n = int(i), int(log2n)
+    if not (0 <= log2n < 64 and (i == 0 if log2n == 0 else i >> log2n == 0)):
+        raise ValueError("bit_reverse: index must have log2n bits")
+    return int(format(i, f"0{log2n}b")[::-1], 2) if log2n else 0
+
+
+def bit_reverse_permute(v):
+    """In-place bit-reversal permutation of a power-of-two-length array (ntt.hpp:49-58)."""
+    n = len(v)
+    if n == 0 or n & (n - 1):
+        raise ValueError("bit_reverse_permute: length must be a power of two")
+    log2n = n.bit_length() - 1
+    for i in range(n):
+        j = bit_reverse(i, log2n)
+        if i < j:
+            v[i], v[j] = v[j], v[i]
+    return v
+
+
 def minimal_primitive_root(order, m):
     q = m.value() if isinstance(m, Modulus) else int(m)
     r = u64()
@@ -431,6 +452,38 @@ class NttTables(RnsNtt):
     def bit_shift(self):
         return self.info()["bit_shift"]
 
+    # ntt.hpp:249-261 accessors: host copies of the tables the plan was built
+    # from (nk_tables_host, bit for bit the reference's build_tables)
+    def _host_tables(self):
+        if getattr(self, "_ht", None) is None:
+            info = self.info()
+            self._ht = tables_host(self.n, self._m.value(), info["psi"], info["bit_shift"])
+        return self._ht
+
+    def log2_size(self):
+        return self.n.bit_length() - 1
+
+    def inv_root(self):
+        return int(self._host_tables()["wi"][self.n // 2])  # psi^-1 at bit_reverse(1)
+
+    def inv_size(self):
+        t = self._host_tables()
+        f = MultiplyFactor.__new__(MultiplyFactor)
+        f.operand, f.precon, f.bit_shift = t["ninv"], t["ninvp"], t["bit_shift"]
+        return f
+
+    def root_powers_rev(self):
+        return self._host_tables()["w"]
+
+    def root_precons_rev(self):
+        return self._host_tables()["wp"]
+
+    def inv_root_powers_rev(self):
+        return self._host_tables()["wi"]
+
+    def inv_root_precons_rev(self):
+        return self._host_tables()["wip"]
+
     def forward(self, result, operand, input_mod_factor, output_mod_factor, stream=None):
         self._check_len(result, operand)
         return super().forward(result, operand, input_mod_factor, output_mod_factor, stream=stream)
@@ -593,5 +646,6 @@ def EltwiseFMAMod(result, arg1, arg2, arg3, n, modulus, input_mod_factor):
 __all__ = [
     "Modulus", "NttTables", "RnsNtt", "NTT", "eltwise_mult_mod", "eltwise_fma_mod",
     "eltwise_add_mod", "eltwise_neg_mod", "poly_mult_mod", "EltwiseMultMod", "EltwiseFMAMod",
-    "minimal_primitive_root", "tables_host", "launch_count", "lib", "CudaError",
+    "minimal_primitive_root", "tables_host", "launch_count", "lib", "CudaError", "bit_reverse",
+    "bit_reverse_permute",
 ]

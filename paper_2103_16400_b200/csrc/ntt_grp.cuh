@@ -46,8 +46,9 @@
 namespace nk {
 
 constexpr uint32_t kGrpExBytes = 4u * 16384u;  // E: 4 groups x 2048 words
-// [1 KiB align][staging 128 KiB][E 64 KiB][mbarriers: full, ex1 reads x4, ex2 reads x4][counter]
-constexpr size_t kGrpSmemBytes = 1024 + kStageBytes + kGrpExBytes + 16 * 8;
+constexpr uint32_t kGrpOutBytes = 16u * 2048u;  // forward output images: 2 KiB per warp
+// [1 KiB align][staging 128 KiB][E 64 KiB][O 32 KiB][mbarriers: full, ex1 reads x4, ex2 reads x4][counter]
+constexpr size_t kGrpSmemBytes = 1024 + kStageBytes + kGrpExBytes + kGrpOutBytes + 16 * 8;
 
 __device__ __forceinline__ void named_sync128(uint32_t id) {
   asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
@@ -120,7 +121,8 @@ __global__ void __launch_bounds__(512, 1)
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* St = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);  // staging, 128B-swizzled lines
   uint8_t* E = St + kStageBytes;
-  uint64_t* bar_full = reinterpret_cast<uint64_t*>(E + kGrpExBytes);
+  uint8_t* O = E + kGrpExBytes;
+  uint64_t* bar_full = reinterpret_cast<uint64_t*>(O + kGrpOutBytes);
   uint64_t* bar_r1 = bar_full + 1;  // [4] ex1 groups: P1 reads done
   uint64_t* bar_r2 = bar_full + 5;  // [4] ex2 groups: last-round reads done
   uint32_t* cnt = reinterpret_cast<uint32_t*>(bar_full + 9);
@@ -216,6 +218,7 @@ __global__ void __launch_bounds__(512, 1)
     pass14<A, FWD, P1, ILTM0>(v, tw, twl, a.n, xbase + jt1, c);
 
     // ---- exchange 1: in place, within the group's staging slots ----
+#if !defined(NK_EXP_NO_EX)  // perf experiment only: exchanges skipped (wrong results)
     mbar_wait(bar_r1 + g1, phase);  // every warp of the group has read its P1 words
     if (FWD) {
       // swz_off(ex1_perm(jt1 | r << 9)) = (swz_off(jt1) ^ ((r & 7) * 0x90)) + r * 4096
@@ -247,6 +250,7 @@ __global__ void __launch_bounds__(512, 1)
         const uint32_t hi = FWD ? (((g + 2 * r) >> 3) << 10) : (((r >> 2) << 10) | (g << 16));
         v[16 * g + r] = *reinterpret_cast<const uint64_t*>(St + ((q2 ^ (y * 0x90u)) + hi));
       }
+#endif
     // staging consumed by this warp; the last of the 16 warps refills it
     __syncwarp();
     if (l == 0) {
@@ -265,6 +269,7 @@ __global__ void __launch_bounds__(512, 1)
 
     // ---- exchange 2: through the group's slice of E, two rounds on the
     // register bit common to P2 and P3 (forward bit 4, inverse bit 13) ----
+#if !defined(NK_EXP_NO_EX)
     mbar_wait(bar_r2 + g2, phase ^ 1);  // the previous block's last-round reads (first block: passes)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -295,6 +300,7 @@ __global__ void __launch_bounds__(512, 1)
     }
     __syncwarp();
     if (l == 0) mbar_arrive_local(bar_r2 + g2);
+#endif
 
     // canonical inverse (Arith52S, whole rows): n^-1 folded into the last
     // stage (bit 13, single twiddle), as in ntt_block14_tma
@@ -311,9 +317,28 @@ __global__ void __launch_bounds__(512, 1)
     if (FWD) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = fwd_out<A>(v[i], c, a.fout);
-      // 32 contiguous words per thread: eight 32-byte stores
+      // 32 contiguous words per thread (a 256-byte run per lane) -> four
+      // rounds through the warp's 2 KiB image: each lane writes 64 bytes of
+      // its run as row l, then every STG.128 stores 8 rows x 64 bytes (16-byte
+      // chunks XOR-swizzled by (row >> 1) & 3: both sides conflict free)
+      uint8_t* Ow = O + (w << 11);
+      const uint32_t wrow = ((l >> 1) << 7) | ((l & 1u) << 6), wsw = (l >> 1) & 3u;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) st_v4_u64(dst + jt3 + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      for (int q = 0; q < 4; ++q) {
+        if (q) __syncwarp();  // the previous round's rows have been read
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+          *reinterpret_cast<ulonglong2*>(Ow + wrow + ((cc ^ wsw) << 4)) =
+              make_ulonglong2(v[8 * q + 2 * cc], v[8 * q + 2 * cc + 1]);
+        __syncwarp();
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {
+          const uint32_t rw = (l >> 2) + 8 * s2, cc = l & 3u;
+          const ulonglong2 p =
+              *reinterpret_cast<const ulonglong2*>(Ow + ((rw >> 1) << 7) + ((rw & 1u) << 6) + ((cc ^ ((rw >> 1) & 3u)) << 4));
+          *reinterpret_cast<ulonglong2*>(dst + M::jt3(w, rw) + 8 * q + 2 * cc) = p;
+        }
+      }
     } else {
       if constexpr (LONG) {
 #pragma unroll

@@ -48,9 +48,49 @@ int main(int argc, char** argv) {
   // modarith.hpp:176-183 / test_modarith.cpp:195
   EXPECT(nb::precompute_factor<64>(1, nb::Modulus(17)).precon == 1085102592571150095ull);
   EXPECT(throws_invalid([] { nb::precompute_factor<64>(17, nb::Modulus(17)); }));
+  // ntt.hpp:37-58 / test_ntt.cpp: bit reversal and its permutation (host only)
+  EXPECT(nb::bit_reverse(1, 3) == 4 && nb::bit_reverse(6, 3) == 3 && nb::bit_reverse(0, 0) == 0);
+  EXPECT(throws_invalid([] { (void)nb::bit_reverse(8, 3); }));
+  {
+    std::vector<uint64_t> p{0, 1, 2, 3, 4, 5, 6, 7};
+    nb::bit_reverse_permute(std::span<uint64_t>(p));
+    EXPECT((p == std::vector<uint64_t>{0, 4, 2, 6, 1, 5, 3, 7}));
+    nb::bit_reverse_permute(std::span<uint64_t>(p));
+    EXPECT((p == std::vector<uint64_t>{0, 1, 2, 3, 4, 5, 6, 7}));
+    std::vector<uint64_t> bad(6);
+    EXPECT(throws_invalid([&] { nb::bit_reverse_permute(std::span<uint64_t>(bad)); }));
+  }
+  // test_ntt.cpp:37-43: minimal primitive roots
+  EXPECT(nb::minimal_primitive_root(4, nb::Modulus(17)) == 4);
+  EXPECT(nb::minimal_primitive_root(2, nb::Modulus(5)) == 4);
+  EXPECT(nb::minimal_primitive_root(8, nb::Modulus(17)) == 2);  // NttTables(4, 17).root()
+  EXPECT(nb::minimal_primitive_root(4, nb::Modulus(5)) == 2);   // NttTables(2, 5).root()
+  EXPECT(throws_invalid([] { (void)nb::minimal_primitive_root(3, nb::Modulus(17)); }));
   if (cpu_only) {
     std::printf(failures ? "facade cpu checks FAILED\n" : "facade cpu checks ok\n");
     return failures ? 1 : 0;
+  }
+  // test_ntt.cpp:44-55 (TableLayout): accessors of NttTables(4, 17), psi = 2
+  {
+    const nb::Modulus m(17);
+    const nb::NttTables t(4, m);
+    EXPECT(t.log2_size() == 2 && t.size() == 4 && t.root() == 2 && t.bit_shift() == 52);  // 4q < 2^52
+    EXPECT(t.inv_root() == 9);  // 2 * 9 = 18 == 1 (mod 17)
+    uint64_t p = 1;
+    for (uint64_t i = 0; i < 4; ++i) {
+      EXPECT(t.root_powers_rev()[nb::bit_reverse(i, 2)] == p);
+      const unsigned __int128 pre = (static_cast<unsigned __int128>(p) << 52) / 17;
+      EXPECT(t.root_precons_rev()[nb::bit_reverse(i, 2)] == static_cast<uint64_t>(pre));
+      p = p * 2 % 17;
+    }
+    uint64_t pi = 1;
+    for (uint64_t i = 0; i < 4; ++i) {
+      EXPECT(t.inv_root_powers_rev()[nb::bit_reverse(i, 2)] == pi);
+      pi = pi * 9 % 17;
+    }
+    EXPECT(t.inv_root_precons_rev().size() == 4);
+    EXPECT(t.inv_size().operand * 4 % 17 == 1);
+    EXPECT(t.inv_size() == nb::precompute_factor<52>(t.inv_size().operand, m));
   }
   // test_ntt.cpp:94-114: n=2, q=5
   nb::NttTables t2(2, nb::Modulus(5));

@@ -184,3 +184,16 @@ def test_precompute_factor_and_butterfly_checks(nk):
         nk.harvey_forward_butterfly(68, 0, w, 17)
     with pytest.raises(ValueError, match="inputs must be < 2q"):
         nk.harvey_inverse_butterfly(0, 34, w, 17)
+
+
+def test_bit_reverse_helpers(nk):
+    """ntt.hpp:37-58 (test_ntt.cpp BitReverse): the mirror's host helpers."""
+    assert nk.bit_reverse(1, 3) == 4 and nk.bit_reverse(6, 3) == 3 and nk.bit_reverse(0, 0) == 0
+    with pytest.raises(ValueError):
+        nk.bit_reverse(8, 3)
+    v = list(range(8))
+    assert nk.bit_reverse_permute(v) == [0, 4, 2, 6, 1, 5, 3, 7]
+    assert nk.bit_reverse_permute(v) == list(range(8))
+    with pytest.raises(ValueError):
+        nk.bit_reverse_permute([0] * 6)
+    assert nk.minimal_primitive_root(8, 17) == 2 and nk.minimal_primitive_root(4, 5) == 2
