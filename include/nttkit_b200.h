@@ -199,7 +199,7 @@ void nk_debug_dump_to(uint64_t* d_buf);
  * default; applies to calls made by the calling thread only. */
 void nk_debug_exact_only(int on);
 /* Testing aid: which kernel transforms 16384-word blocks. -1 (default) = the
- * faster one per direction, 0 = the CTA-pair kernel, 1 = the single-CTA kernel;
+ * faster one per direction, 0 = the CTA-pair kernel, 1 = the group-exchange kernel;
  * 6 = defaults, but batches of 2^11..2^13-word rows smaller than the SM count
  * take the plain block kernel instead of the latency kernel (ntt_block_lat).
  * Applies to calls made by the calling thread only. */

@@ -116,18 +116,6 @@ int set_smem_once(size_t bytes) {
   return 0;
 }
 
-template <auto KERN>
-int launch_tma_k(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
-  CUtensorMap map;
-  if (int rc = make_map(&map, kRowMap, a.in, buf_words)) return rc;
-  if (int rc = set_smem_once<KERN>(kTmaSmemBytes)) return rc;
-  const uint64_t g = nitems < static_cast<uint64_t>(sm_count()) ? nitems : sm_count();
-  KERN<<<static_cast<unsigned>(g), 512, kTmaSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));
-  launches++;
-  NK_CUDA(cudaGetLastError());
-  return 0;
-}
-
 // group-exchange kernel (ntt_grp.cuh): persistent, one 512-thread CTA per SM
 template <auto KERN>
 int launch_grp_k(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
@@ -146,13 +134,6 @@ int launch_grp_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStre
   if constexpr (!FWD)
     if (a.logn > 14) return launch_grp_k<ntt_grp14<A, FWD, IL, true>>(a, nitems, buf_words, st);
   return launch_grp_k<ntt_grp14<A, FWD, IL>>(a, nitems, buf_words, st);
-}
-
-template <class A, bool FWD, bool IL>
-int launch_tma_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
-  if constexpr (!FWD)
-    if (a.logn > 14) return launch_tma_k<ntt_block14_tma<A, FWD, IL, true>>(a, nitems, buf_words, st);
-  return launch_tma_k<ntt_block14_tma<A, FWD, IL>>(a, nitems, buf_words, st);
 }
 
 // CTA-pair kernel (ntt_pair.cuh): persistent, one cluster of 2 per block in
@@ -201,19 +182,17 @@ int launch_pair_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStr
 
 template <class A, bool FWD>
 int launch_tma(const NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm, cudaStream_t st) {
-  // measured on B200 (cfg3): the CTA-pair kernel is the faster forward, the
-  // single-CTA kernel the faster inverse (the pair inverse exchanges late,
-  // so its next TMA overlaps less compute); the fused product lives in the
-  // pair forward only
-  if (!a.mulb && block_kernel == 2)
-    return iltm ? launch_grp_t<A, FWD, true>(a, nitems, buf_words, st)
-                : launch_grp_t<A, FWD, false>(a, nitems, buf_words, st);
+  // measured on B200 (cfg3 / cfg4): the CTA-pair kernel is the faster forward
+  // (228 / 359 us; the group kernel 228 / 396), the group-exchange kernel the
+  // faster inverse (227 / 346 us; the pair inverse 227 / 398: it exchanges
+  // late, so its next TMA overlaps less compute); the fused product lives in
+  // the pair forward only
   const bool pair = a.mulb || (block_kernel < 0 ? FWD : block_kernel == 0);
   if (pair)
     return iltm ? launch_pair_t<A, FWD, true>(a, nitems, buf_words, st)
                 : launch_pair_t<A, FWD, false>(a, nitems, buf_words, st);
-  return iltm ? launch_tma_t<A, FWD, true>(a, nitems, buf_words, st)
-              : launch_tma_t<A, FWD, false>(a, nitems, buf_words, st);
+  return iltm ? launch_grp_t<A, FWD, true>(a, nitems, buf_words, st)
+              : launch_grp_t<A, FWD, false>(a, nitems, buf_words, st);
 }
 
 // LOGV = log2(words per thread): 32 words per thread for batches that fill

@@ -161,7 +161,6 @@ struct LimbConstDev {
   uint64_t nw, nwp;
   uint64_t fourq;  // 4q (ArithIntL)
 };
-constexpr double kC52x15 = 6755399441055744.0;  // 1.5 * 2^52: round-to-integer constant
 
 template <int BS>
 struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)
@@ -294,10 +293,23 @@ __device__ __forceinline__ double mul_signed(double v, double w, double wp, doub
   return __dadd_rn(e, l1);
 }
 constexpr double kC53x15 = 13510798882111488.0;  // 1.5 * 2^53: round-to-even-integer constant
+constexpr double kC52x15 = 6755399441055744.0;   // 1.5 * 2^52: round-to-integer constant
 __device__ __forceinline__ double mul_recip(double v, double w, double qinv, double q) {
   const double h1 = __dmul_rn(w, v);
   const double l1 = __fma_rn(w, v, -h1);
   const double k = __dsub_rn(__fma_rn(h1, qinv, kC53x15), kC53x15);
+  const double e = __fma_rn(-k, q, h1);
+  return __dadd_rn(e, l1);
+}
+// The same product with the integer-grid constant 1.5*2^52 for |v| < 2q:
+// |h1 qinv| < 2q < 2^51 keeps the sum in [2^52, 2^53) (ulp 1), so k is the
+// nearest integer to h1 qinv and |wv/q - k| <= 1/2 + 2^47/q + 2q 2^-53 < 7/8:
+// |T| < 0.875q (used where a canonical result follows: one fix-up instead of
+// a full canonicalisation).
+__device__ __forceinline__ double mul_recip_fine(double v, double w, double qinv, double q) {
+  const double h1 = __dmul_rn(w, v);
+  const double l1 = __fma_rn(w, v, -h1);
+  const double k = __dsub_rn(__fma_rn(h1, qinv, kC52x15), kC52x15);
   const double e = __fma_rn(-k, q, h1);
   return __dadd_rn(e, l1);
 }
@@ -330,7 +342,11 @@ struct Arith52S {
   // when that stays >= 2^52), so no signed-zero case can arise.
   __device__ static uint64_t canon(double x, const LimbConstDev& c) {
     const double k = __dsub_rn(__fma_rn(x, c.qinv, kC52x15), kC52x15);
-    const double r = __fma_rn(-k, c.q_d, x);
+    return canon_small(__fma_rn(-k, c.q_d, x), c);
+  }
+  // canonical integer of an integer-valued double |r| < q (+1): r + q, minus q
+  // when that stays >= q, in the biased domain (2^52 + r + q)
+  __device__ static uint64_t canon_small(double r, const LimbConstDev& c) {
     const uint64_t rb = as_u(__dadd_rn(r, c.q_bias));  // 2^52 + r + q
     const uint64_t db = as_u(__dsub_rn(as_d(rb), c.q_d));
     return ((hi32(db) >= 0x43300000u) ? db : rb) & kMask52;
@@ -356,10 +372,13 @@ struct Arith52S {
   }
   // see ArithInt::inv_fold; signed doubles |x| < 2q in, canonical words out
   static constexpr bool kFold = true;
+  // (|a +- b| < 4q reduced to < 2q, then the fine product: |T| < 0.875q, one
+  // fix-up to [0, q): 10 FP64 operations per word instead of 12)
   __device__ static void inv_fold(uint64_t& x0, uint64_t& x1, const LimbConstDev& c) {
     const double a = as_d(x0), b = as_d(x1);
-    x0 = canon(mul_signed(__dadd_rn(a, b), as_d(c.ninv), as_d(c.ninvp), c.qq), c);
-    x1 = canon(mul_signed(__dsub_rn(a, b), as_d(c.nw), as_d(c.nwp), c.qq), c);
+    const double s = csubS(__dadd_rn(a, b), c.twoq_d), t = csubS(__dsub_rn(a, b), c.twoq_d);
+    x0 = canon_small(mul_recip_fine(s, as_d(c.ninv), c.qinv, c.q_d), c);
+    x1 = canon_small(mul_recip_fine(t, as_d(c.nw), c.qinv, c.q_d), c);
   }
 };
 
@@ -450,18 +469,15 @@ __device__ __forceinline__ uint64_t mulmod_canon(uint64_t a, uint64_t b, const L
 
 // (x * g) mod q as a canonical word, for a signed Arith52S word |x| < 4q (a
 // forward transform's output before canonicalisation) and a canonical g < q:
-// TwoProduct h + l = x g, k = 2 round(h / 2q) through the rounded reciprocal
-// (ulp 2: |h / q| < 4q <= 2^52), r = (h - k q) + l exact with |r| < 2q, then
-// Arith52S::canon. 12 FP64 operations per word instead of canon + mulmod_canon
-// (15): the fused poly_mult_mod forward multiplies before canonicalising.
+// x reduced to |x| < 2q (csubS), the fine rounded-reciprocal product
+// (mul_recip_fine, |T| < 0.875q), then one fix-up to [0, q)
+// (Arith52S::canon_small): 10 FP64 operations per word instead of canon +
+// mulmod_canon (15): the fused poly_mult_mod forward multiplies before
+// canonicalising.
 __device__ __forceinline__ uint64_t mulmod_signed_canon(uint64_t xbits, uint64_t g, const LimbConstDev& c) {
-  const double x = as_d(xbits);
+  const double x = csubS(as_d(xbits), c.twoq_d);
   const double gd = __dsub_rn(as_d(g | kDBias), kC52);
-  const double h = __dmul_rn(x, gd);
-  const double l = __fma_rn(x, gd, -h);
-  const double k = __dsub_rn(__fma_rn(h, c.qinv, kC53x15), kC53x15);
-  const double r = __dadd_rn(__fma_rn(-k, c.q_d, h), l);
-  return Arith52S::canon(r, c);
+  return Arith52S::canon_small(mul_recip_fine(x, gd, c.qinv, c.q_d), c);
 }
 
 // Final word of a forward transform (small_mod(x, q, 4) when fout == 1,

@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(512, 1)
 #endif
 
     // canonical inverse (Arith52S, whole rows): n^-1 folded into the last
-    // stage (bit 13, single twiddle), as in ntt_block14_tma
+    // stage (bit 13, single twiddle), as in ntt_pair14 / ntt_grp14
     constexpr bool kFoldLast = !FWD && A::kSigned && !LONG;
     if constexpr (kFoldLast) {
       pass14<A, FWD, P3, false, 1>(v, tw, twl, a.n, xbase + jt3, c);

@@ -17,14 +17,12 @@
 // beta = 2^64; capi.cu: ntt_dispatch_aligned picks one per call):
 //  * ntt_pair14<A, FWD, ILTM0> (ntt_pair.cuh): the forward's 16384-word block
 //    kernel, one block per CTA pair (cluster of 2), two pairs per SM.
-//  * ntt_block14_tma<A, FWD, ILTM0>: the inverse's. Persistent, one 512-thread
-//    CTA per SM, walks 16384-word blocks (a whole row at N = 16384, or the low
-//    14 bits of a longer row). Each block arrives by TMA (cp.async.bulk.tensor,
-//    128B swizzle) into a shared staging buffer while the previous block is
-//    still being transformed; the block is transformed in registers (32 words
-//    per thread, three register passes of 5/5/4 stages) with two exchanges
-//    through a padded half-size shared buffer; results leave with coalesced
-//    stores.
+//  * ntt_grp14<A, FWD, ILTM0> (ntt_grp.cuh): the inverse's. Persistent, one
+//    512-thread CTA per SM, walks 16384-word blocks (a whole row at N = 16384,
+//    or the low 14 bits of a longer row); each block arrives by TMA
+//    (cp.async.bulk.tensor, 128B swizzle) into a staging buffer while the
+//    previous block is still being transformed; three register passes of
+//    5/4(+1)/5 stages with exchanges inside 4-warp groups.
 //  * ntt_block<LOGB, LOGV, A, FWD, ILTM0>: same register passes for
 //    2^11..2^14-word blocks, loads straight from global; ntt_block_lat: the
 //    same for batches smaller than the SM count, twiddle row staged in shared
@@ -394,25 +392,13 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV)) ntt_block_lat(NttArgs a) {
   }
 }
 
-// ---------------------------------------------------------------------------
-// ntt_block14_tma: the hot kernel (see the header comment).
-//
-// Pass schedule (each thread holds 32 words; a pass with K = 4 butterfly bits
-// also holds one extra index bit X in registers, as value-index bit 4):
-//   forward: P1 bits 13..9 | P2 bits 8..5 + X = 4  | P3 bits 4..0
-//   inverse: P1 bits 4..0  | P2 bits 8..5 + X = 13 | P3 bits 13..9
-// Exchange 1 (P1 -> P2) is a full exchange: words with index bit 13 clear go
-// to the padded half image B, the others to the staging buffer A (already
-// consumed), so no thread holds pending values while it reads. Only then is
-// the next block's TMA issued into A. Exchange 2 (P2 -> P3) uses B alone in
-// two rounds split on X, which is value-index bit 4 in both passes: a thread
-// writes v[16h..16h+15] and reads back into exactly those registers.
-// Shared: [A: 128 KiB, TMA staging / half image][B: padded half image][mbarrier]
+// 16384-word blocks (the transforms' block kernels: ntt_pair14 in
+// ntt_pair.cuh, ntt_grp14 in ntt_grp.cuh): one register pass = 4 or 5
+// butterfly bits over 32 words per thread; PassD below describes a pass, pass14
+// runs it.
 // ---------------------------------------------------------------------------
 constexpr int kB14 = 14;
-constexpr uint32_t kStageBytes = (1u << kB14) * 8;  // 128 KiB
-constexpr uint32_t kHalfWords = smem_phys((1u << (kB14 - 1)) - 1) + 1;
-constexpr size_t kTmaSmemBytes = 1024 /*align*/ + kStageBytes + kHalfWords * 8 + 16;
+constexpr uint32_t kStageBytes = (1u << kB14) * 8;  // 128 KiB: one block
 
 // deposit the low bits of t into the set bits of MASK (ascending), like PDEP
 template <uint32_t MASK>
@@ -459,17 +445,10 @@ struct PassD {
   }
 };
 
-template <bool FWD>
-struct Sched14 {
-  using P1 = typename std::conditional<FWD, PassD<9, 5, -1>, PassD<0, 5, -1>>::type;
-  using P2 = typename std::conditional<FWD, PassD<5, 4, 4>, PassD<5, 4, 13>>::type;
-  using P3 = typename std::conditional<FWD, PassD<0, 5, -1>, PassD<9, 5, -1>>::type;
-  static constexpr int X = FWD ? 4 : 13;  // split bit of exchange 2
-};
 
 // One register pass over the bits of PD (stage order by direction).
 // SKIP_LAST: leave the pass's last stage to the caller (the folded n^-1 stage
-// of ntt_block14_tma's inverse).
+// of the canonical inverses).
 template <class A, bool FWD, class PD, bool ILTM0, int SKIP_LAST = 0>
 __device__ __forceinline__ void pass14(uint64_t (&v)[32], const typename A::Tw* __restrict__ tw,
                                        const typename A::Tw* __restrict__ twl, uint64_t n,
@@ -512,189 +491,6 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const typename A::Tw* 
           }
         }
       }
-    }
-  }
-}
-
-// LONG: the launch covers the low 14 bits of longer rows (an inverse then
-// stores intermediates only): a separate instance without the final-word code.
-template <class A, bool FWD, bool ILTM0, bool LONG = false>
-__global__ void __launch_bounds__(512, 1)
-    ntt_block14_tma(const __grid_constant__ CUtensorMap tin, NttArgs a, uint32_t nitems) {
-  using SC = Sched14<FWD>;
-  using P1 = typename SC::P1;
-  using P2 = typename SC::P2;
-  using P3 = typename SC::P3;
-  constexpr int X = SC::X;
-  extern __shared__ __align__(1024) uint8_t smraw[];
-  // 1024-byte alignment for the 128B-swizzle atoms, kept as shared-space pointer arithmetic
-  uint8_t* Astage = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
-  uint64_t* Ahalf = reinterpret_cast<uint64_t*>(Astage);
-  uint64_t* B = reinterpret_cast<uint64_t*>(Astage + kStageBytes);
-  uint64_t* bar = B + kHalfWords + (kHalfWords & 1);
-  const uint32_t t = threadIdx.x;
-  const uint32_t lognb = a.logn - kB14;
-  const uint64_t rowwords16 = a.n >> 4;  // tensor rows (of 16 words) per data row
-
-  auto item_row = [&](uint32_t k, uint64_t& row, uint64_t& blk) {
-    row = (static_cast<uint64_t>(k) >> lognb) * a.row_mul + a.row_add;
-    blk = static_cast<uint64_t>(k) & ((uint64_t{1} << lognb) - 1);
-  };
-  auto issue = [&](uint32_t k) {
-    uint64_t row, blk;
-    item_row(k, row, blk);
-    const int32_t y0 = static_cast<int32_t>(row * rowwords16 + (blk << (kB14 - 4)));
-    mbar_expect_tx(bar, kStageBytes);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) tma_load_2d(Astage + q * 32768, &tin, 0, y0 + q * 256, bar);
-  };
-
-  if (t == 0) {
-    mbar_init(bar, 1);
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tin)) : "memory");
-  }
-  __syncthreads();
-  if (t == 0 && blockIdx.x < nitems) issue(blockIdx.x);
-  uint32_t phase = 0;
-
-  const uint32_t jt1 = P1::jt(t), jt2 = P2::jt(t), jt3 = P3::jt(t);
-  const uint32_t jtlow = FWD ? jt3 : jt1;  // thread index bits of the pass over bits 0..4
-  // per-thread shared-memory bases (index bits of t and of the registers are
-  // disjoint, so every access below is base + immediate)
-  const uint32_t e1w = smem_phys(jt1 & 0x1FFFu), e1r = smem_phys(jt2 & 0x1FFFu);
-  const bool e1w_hi = (jt1 >> 13) & 1, e1r_hi = (jt2 >> 13) & 1;
-  const uint32_t e2w = smem_phys(squeeze<X>(jt2)), e2r = smem_phys(squeeze<X>(jt3));
-
-  for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
-    uint64_t row, blk;
-    item_row(k, row, blk);
-    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
-    const LimbConst c = a.lc[limb];
-    const typename A::Tw* __restrict__ tw = tw_of<A>(a, limb);
-    // low table: this block's segment, offset by this thread's jhi in the low pass
-    const typename A::Tw* __restrict__ twl = twl_of<A>(a, limb) + (blk << kB14) + (jtlow >> 5);
-    const uint64_t boff = blk << kB14;
-    uint64_t* __restrict__ dst = a.out + row * a.n + boff;
-    const uint64_t xbase = a.n + boff;
-    uint64_t v[32];
-
-    // ---- P1 words from the swizzled staging buffer ----
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    if constexpr (P1::LO == 0) {
-      // 32 contiguous words (two tensor rows): 16-byte chunks
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t row16 = (jt1 >> 4) + h;
-        const uint32_t rowoff = row16 << 7, sw = row16 & 7;
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-          const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Astage + rowoff + ((cc ^ sw) << 4));
-          v[16 * h + 2 * cc] = A::load(p.x);
-          v[16 * h + 2 * cc + 1] = A::load(p.y);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < 32; ++r)
-        v[r] = A::load(*reinterpret_cast<const uint64_t*>(Astage + swz_off(jt1 | P1::jc(0, r))));
-    }
-    __syncthreads();  // staging consumed (A is reused as a half image below)
-
-    pass14<A, FWD, P1, ILTM0>(v, tw, twl, a.n, xbase + jt1, c);
-
-    // ---- exchange 1: full, through A (index bit 13 set) and B (clear) ----
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const uint32_t jc = P1::jc(0, r);
-      uint64_t* img = (((jc >> 13) & 1) | e1w_hi) ? Ahalf : B;
-      img[e1w + smem_phys(jc & 0x1FFFu)] = v[r];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int g = 0; g < P2::G; ++g)
-#pragma unroll
-      for (int r = 0; r < P2::R; ++r) {
-        const uint32_t jc = P2::jc(g, r);
-        const uint64_t* img = (((jc >> 13) & 1) | e1r_hi) ? Ahalf : B;
-        v[g * P2::R + r] = img[e1r + smem_phys(jc & 0x1FFFu)];
-      }
-    __syncthreads();  // A free: prefetch the next block while P2/P3 compute
-    if (t == 0 && k + gridDim.x < nitems) {
-      fence_proxy_async();
-      issue(k + gridDim.x);
-    }
-
-    pass14<A, FWD, P2, false>(v, tw, twl, a.n, xbase + jt2, c);
-
-    // ---- exchange 2: B only, two rounds split on bit X (value-index bit 4) ----
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-#pragma unroll
-      for (int r = 0; r < 16; ++r) B[e2w + smem_phys(squeeze<X>(P2::jc(h, r)))] = v[16 * h + r];
-      __syncthreads();
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const int i = 16 * h + r;  // P3 value index with bit 4 == h
-        v[i] = B[e2r + smem_phys(squeeze<X>(P3::jc(0, i)))];
-      }
-      __syncthreads();
-    }
-
-    // Canonical inverse (Arith52S, whole 16384-word rows by dispatch): the
-    // last stage (bit 13, the single twiddle w_1) takes the n^-1 factor and
-    // produces canonical words (A::inv_fold): two products per butterfly
-    // instead of three, 3.5 fewer FP64 operations per word.
-    constexpr bool kFoldLast = !FWD && A::kSigned;
-    if constexpr (kFoldLast) {
-      pass14<A, FWD, P3, false, 1>(v, tw, twl, a.n, xbase + jt3, c);
-#pragma unroll
-      for (int r = 0; r < 16; ++r) A::inv_fold(v[r], v[r + 16], c);
-    } else {
-      pass14<A, FWD, P3, false>(v, tw, twl, a.n, xbase + jt3, c);
-    }
-
-    // ---- fix-ups and store ----
-    if (FWD) {
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = fwd_out<A>(v[i], c, a.fout);
-      // P3 holds 32 contiguous words per thread; transpose each half (bit 4)
-      // through B so the global stores are lane-contiguous: B holds the half as
-      // 512 rows of 16 words (row = t) in the 128B-swizzled arrangement, so
-      // both the 16-byte writes (8 lanes, 8 rows) and the row reads (8 lanes,
-      // one row) are conflict free.
-      uint8_t* Bb = reinterpret_cast<uint8_t*>(B);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc)
-          *reinterpret_cast<ulonglong2*>(Bb + (t << 7) + ((cc ^ (t & 7)) << 4)) =
-              make_ulonglong2(v[16 * h + 2 * cc], v[16 * h + 2 * cc + 1]);
-        __syncthreads();
-#pragma unroll
-        for (int s2 = 0; s2 < 8; ++s2) {
-          const uint32_t rowi = (t >> 3) + (s2 << 6), cc = t & 7;  // squeezed row, chunk
-          const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Bb + (rowi << 7) + ((cc ^ (rowi & 7)) << 4));
-          *reinterpret_cast<ulonglong2*>(dst + (rowi << 5) + (h << 4) + (cc << 1)) = p;
-        }
-        __syncthreads();
-      }
-    } else {
-      if constexpr (LONG) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = A::store(v[i]);  // intermediate of a long row
-      } else if constexpr (kFoldLast) {
-        // already canonical
-      } else if (lognb == 0) {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = inv_out<A>(v[i], c, a.fout);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = A::store(v[i]);  // intermediate of a long row
-      }
-      // P3 holds j = t + 512 r: coalesced already
-#pragma unroll
-      for (int r = 0; r < 32; ++r) dst[jt3 | P3::jc(0, r)] = v[r];
     }
   }
 }

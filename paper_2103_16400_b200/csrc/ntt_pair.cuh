@@ -28,7 +28,7 @@
 // The warp-local exchange uses a per-warp 4.5 KiB image (two rounds split on
 // bit 4, which is a register bit on both sides) under __syncwarp only.
 // Butterfly arithmetic, twiddle addressing and the low (lane-contiguous)
-// twiddle table are those of ntt_block14_tma (ntt_kernels.cuh: pass14).
+// twiddle table are those of pass14 (ntt_kernels.cuh).
 #pragma once
 #include "ntt_kernels.cuh"
 
@@ -404,7 +404,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
 
     NK_TS(7);
     // canonical inverse (Arith52S, whole rows): n^-1 folded into the last stage
-    // (bit 13, single twiddle), as in ntt_block14_tma
+    // (bit 13, single twiddle), as in ntt_pair14 / ntt_grp14
     constexpr bool kFoldLast = !FWD && A::kSigned;
     if constexpr (kFoldLast) {
       pass14<A, FWD, P3, false, 1>(v, tw, twl, a.n, xbase + jt3, cst);

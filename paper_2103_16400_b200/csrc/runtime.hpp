@@ -35,7 +35,7 @@ extern std::atomic<uint64_t> launches;
 // Testing aids, per calling thread (nk_debug_block_kernel / nk_debug_exact_only /
 // nk_debug_dump_to): they change dispatch only for calls made by the thread
 // that set them.
-extern thread_local int block_kernel;  // -1 auto, 0 CTA pair, 1 single CTA (16384-word blocks)
+extern thread_local int block_kernel;  // -1 auto, 0 CTA pair, 1 group exchange (16384-word blocks)
 extern thread_local bool no_lat;       // small batches take ntt_block instead of ntt_block_lat
 extern thread_local bool exact_only;   // beta = 2^52 transforms always take the lazy-exact policy
 extern thread_local uint64_t* dbg;     // NK_DBG_TIMELINE builds: per-warp phase stamps

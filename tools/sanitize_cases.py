@@ -74,11 +74,11 @@ def poly():
 
 
 CASES = {
-    "pair14_and_block14": lambda: transform(16384, 50, 1, 3),          # ntt_pair14 fwd, ntt_block14_tma inv
-    "pair14_int": lambda: transform(16384, 60, 1, 2, fin=4),           # integer (ArithIntL) pair / block
+    "pair14_and_grp14": lambda: transform(16384, 50, 1, 3),            # ntt_pair14 fwd, ntt_grp14 inv
+    "pair14_int": lambda: transform(16384, 60, 1, 2, fin=4),           # integer (ArithIntL) pair / grp
     "pair14_exact": lambda: transform(16384, 50, 1, 2, fout=4, exact=True),
     "pair_inverse": lambda: transform(16384, 50, 1, 2, kernel=0),
-    "inv14_3barrier": lambda: transform(16384, 50, 1, 2, kernel=5),
+    "grp_forward": lambda: transform(16384, 50, 1, 2, kernel=1),
     "block_lat_4096": lambda: transform(4096, 50, 1, 1),               # ntt_block_lat
     "block_8192_batch": lambda: transform(8192, 50, 2, 80),            # ntt_block, >= SM count rows
     "small_1024": lambda: transform(1024, 30, 2, 2),                   # ntt_small
