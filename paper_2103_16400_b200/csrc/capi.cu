@@ -6,8 +6,11 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -816,14 +819,121 @@ int host_depth() {
   return v;
 }
 
-// One pipeline (streams + ordering event) per device. Host-buffer calls from
-// several threads (the reference allows concurrent calls on shared tables,
-// ntt.hpp:203-205, test_ntt.cpp:349-375) take turns on it: they are
-// PCIe-bound, so serialising them costs no throughput, and the ordering event
-// is never re-recorded by one call while another waits on it.
+// Parallel host memcpy for pageable buffers: a small persistent pool (the
+// caller takes a share too). One copy at a time; each splits into equal parts.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
+  }
+  void copy(void* dst, const void* src, size_t bytes) {
+    if (bytes < (size_t{1} << 20) || workers_.empty()) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    std::lock_guard<std::mutex> one(call_mu_);
+    const int parts = static_cast<int>(workers_.size()) + 1;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      bytes_ = bytes;
+      parts_ = parts;
+      next_ = 0;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    run_parts();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ == parts_; });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    const unsigned n = hw >= 4 ? std::min(8u, hw / 2) : 0;
+    for (unsigned i = 1; i < n; ++i) workers_.emplace_back([this] { work(); });
+  }
+  void run_parts() {
+    for (;;) {
+      int part;
+      char* d;
+      const char* sp;
+      size_t bytes;
+      int parts;
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (next_ >= parts_) return;
+        part = next_++;
+        d = dst_;
+        sp = src_;
+        bytes = bytes_;
+        parts = parts_;
+      }
+      const size_t b0 = bytes * part / parts, b1 = bytes * (part + 1) / parts;
+      std::memcpy(d + b0, sp + b0, b1 - b0);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (++done_ == parts_) done_cv_.notify_all();
+    }
+  }
+  void work() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      run_parts();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0;
+  int parts_ = 0, next_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+// host memory the DMA engines can read directly (pinned / registered), as
+// opposed to pageable memory the driver would stage through its own buffer
+bool is_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type != cudaMemoryTypeUnregistered;
+}
+
+// One pipeline (streams, events, pinned staging buffers for pageable
+// callers) per device. Host-buffer calls from several threads (the reference
+// allows concurrent calls on shared tables, ntt.hpp:203-205,
+// test_ntt.cpp:349-375) take turns on it: they are PCIe-bound, so
+// serialising them costs no throughput, and the ordering event is never
+// re-recorded by one call while another waits on it.
 struct HostPipe {
   cudaStream_t s[kMaxDepth] = {};
   cudaEvent_t start = nullptr;
+  cudaEvent_t up[kMaxDepth] = {};    // slot's uploads done (its input staging may be refilled)
+  cudaEvent_t down[kMaxDepth] = {};  // slot's download done (its output staging may be read)
+  uint64_t* stage[kMaxDepth][3] = {};  // pinned staging: inputs 0..1, output 2
+  uint64_t stage_bytes = 0;
   std::mutex mu;
 };
 
@@ -837,6 +947,10 @@ int host_pipe(int dev, HostPipe** out) {
     for (auto& st : hp.s)
       if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp.start, cudaEventDisableTiming);
+    for (int k = 0; k < kMaxDepth && e == cudaSuccess; ++k) {
+      e = cudaEventCreateWithFlags(&hp.up[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp.down[k], cudaEventDisableTiming);
+    }
     err[dev & 63] = e;
   });
   if (err[dev & 63] != cudaSuccess) return cuda_fail(err[dev & 63], "host pipeline streams");
@@ -844,8 +958,26 @@ int host_pipe(int dev, HostPipe** out) {
   return 0;
 }
 
+// pinned staging of at least `bytes` per slot and buffer (kept for later calls)
+int stage_reserve(HostPipe* hp, uint64_t bytes) {
+  if (hp->stage_bytes >= bytes) return 0;
+  for (auto& slot : hp->stage)
+    for (auto*& b : slot) {
+      if (b) cudaFreeHost(b);
+      b = nullptr;
+    }
+  hp->stage_bytes = 0;
+  for (auto& slot : hp->stage)
+    for (auto*& b : slot) NK_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&b), bytes, cudaHostAllocDefault));
+  hp->stage_bytes = bytes;
+  return 0;
+}
+
 // fn(device buffers of the chunk (inputs; the first is also the output),
 //    first unit, units in chunk, stream) -> int
+// Pageable host buffers go through pinned staging: the host copies chunk c's
+// inputs in (and chunk c - depth's result out) with CopyPool while the DMA
+// engines move the pinned chunks, instead of the driver's serial staging.
 template <class Fn>
 int run_pipelined(int dev, cudaStream_t user, uint64_t units, uint64_t unit_words,
                   std::initializer_list<const uint64_t*> hin, uint64_t* hout, Fn&& fn) {
@@ -853,11 +985,25 @@ int run_pipelined(int dev, cudaStream_t user, uint64_t units, uint64_t unit_word
   if (int rc = host_pipe(dev, &hp)) return rc;
   std::lock_guard<std::mutex> lock(hp->mu);
   const int nin = static_cast<int>(hin.size());
+  const uint64_t* in[2] = {nullptr, nullptr};
+  bool in_staged[2] = {false, false};
+  {
+    int j = 0;
+    for (const uint64_t* h : hin) {
+      in[j] = h;
+      in_staged[j] = !is_pinned(h);
+      ++j;
+    }
+  }
+  const bool out_staged = !is_pinned(hout);
   const uint64_t unit_bytes = unit_words * 8;
   uint64_t per = host_chunk_bytes() / unit_bytes;
   if (per < 1) per = 1;
   if (per > units) per = units;
   const uint64_t nchunks = (units + per - 1) / per;
+  const bool any_staged = out_staged || in_staged[0] || in_staged[1];
+  if (any_staged)
+    if (int rc = stage_reserve(hp, per * unit_bytes)) return rc;
   NK_CUDA(cudaEventRecord(hp->start, user));
   uint64_t* buf[kMaxDepth][2] = {};
   int rc = 0;
@@ -868,21 +1014,54 @@ int run_pipelined(int dev, cudaStream_t user, uint64_t units, uint64_t unit_word
       e = cudaMallocAsync(&buf[k][j], per * unit_bytes, hp->s[k]);
     if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline buffers");
   }
+  auto chunk_of = [&](uint64_t c, uint64_t& off, uint64_t& bytes, uint64_t& u0, uint64_t& nu) {
+    u0 = c * per;
+    nu = (u0 + per <= units) ? per : units - u0;
+    off = u0 * unit_words;
+    bytes = nu * unit_bytes;
+  };
+  // copy chunk c's result from its slot's output staging to the caller's buffer
+  auto drain = [&](uint64_t c) -> int {
+    if (!out_staged) return 0;
+    const int k = static_cast<int>(c % nst);
+    uint64_t off, bytes, u0, nu;
+    chunk_of(c, off, bytes, u0, nu);
+    NK_CUDA(cudaEventSynchronize(hp->down[k]));
+    CopyPool::get().copy(hout + off, hp->stage[k][2], bytes);
+    return 0;
+  };
   for (uint64_t c = 0; c < nchunks && !rc; ++c) {
     const int k = static_cast<int>(c % nst);
-    const uint64_t u0 = c * per, nu = (u0 + per <= units) ? per : units - u0;
-    const uint64_t off = u0 * unit_words, bytes = nu * unit_bytes;
-    cudaError_t e = cudaSuccess;
-    int j = 0;
-    for (const uint64_t* h : hin) {
-      if (e == cudaSuccess && h) e = cudaMemcpyAsync(buf[k][j], h + off, bytes, cudaMemcpyHostToDevice, hp->s[k]);
-      ++j;
+    uint64_t off, bytes, u0, nu;
+    chunk_of(c, off, bytes, u0, nu);
+    if (c >= static_cast<uint64_t>(nst)) {
+      if ((rc = drain(c - nst))) break;  // the slot's previous result is out of its staging
+      if (in_staged[0] || in_staged[1]) {
+        const cudaError_t e = cudaEventSynchronize(hp->up[k]);  // its previous uploads are done
+        if (e != cudaSuccess) { rc = cuda_fail(e, "cudaEventSynchronize(host pipeline)"); break; }
+      }
     }
+    cudaError_t e = cudaSuccess;
+    for (int j = 0; j < nin && e == cudaSuccess; ++j) {
+      if (!in[j]) continue;
+      const uint64_t* src = in[j] + off;
+      if (in_staged[j]) {
+        CopyPool::get().copy(hp->stage[k][j], src, bytes);
+        src = hp->stage[k][j];
+      }
+      e = cudaMemcpyAsync(buf[k][j], src, bytes, cudaMemcpyHostToDevice, hp->s[k]);
+    }
+    if (e == cudaSuccess) e = cudaEventRecord(hp->up[k], hp->s[k]);
     if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMemcpyAsync(H2D)"); break; }
     if ((rc = fn(buf[k], u0, nu, hp->s[k]))) break;
-    e = cudaMemcpyAsync(hout + off, buf[k][0], bytes, cudaMemcpyDeviceToHost, hp->s[k]);
+    e = cudaMemcpyAsync(out_staged ? hp->stage[k][2] : hout + off, buf[k][0], bytes, cudaMemcpyDeviceToHost,
+                        hp->s[k]);
+    if (e == cudaSuccess) e = cudaEventRecord(hp->down[k], hp->s[k]);
     if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync(D2H)");
   }
+  if (!rc)
+    for (uint64_t c = nchunks > static_cast<uint64_t>(nst) ? nchunks - nst : 0; c < nchunks && !rc; ++c)
+      rc = drain(c);
   for (int k = 0; k < nst; ++k) {
     for (int j = 0; j < nin; ++j)
       if (buf[k][j]) cudaFreeAsync(buf[k][j], hp->s[k]);

@@ -238,6 +238,7 @@ int launch_block(uint32_t logb, const NttArgs& a, uint64_t grid, bool iltm, cuda
   const bool small = a.rows < static_cast<uint64_t>(sm_count());
   if (small && a.logn == logb && !no_lat) {  // whole rows, few of them: the latency path
     switch (logb) {
+      case 10: return iltm ? launch_block_lat_t<10, 3, A, FWD, true>(a, grid, st) : launch_block_lat_t<10, 3, A, FWD, false>(a, grid, st);
       case 11: return iltm ? launch_block_lat_t<11, 3, A, FWD, true>(a, grid, st) : launch_block_lat_t<11, 3, A, FWD, false>(a, grid, st);
       case 12: return iltm ? launch_block_lat_t<12, 3, A, FWD, true>(a, grid, st) : launch_block_lat_t<12, 3, A, FWD, false>(a, grid, st);
       default: return iltm ? launch_block_lat_t<13, 3, A, FWD, true>(a, grid, st) : launch_block_lat_t<13, 3, A, FWD, false>(a, grid, st);
@@ -249,6 +250,7 @@ int launch_block(uint32_t logb, const NttArgs& a, uint64_t grid, bool iltm, cuda
   if (small) NK_LB2(L, 3); \
   NK_LB2(L, 5)
   switch (logb) {
+    case 10: NK_LB(10);
     case 11: NK_LB(11);
     case 12: NK_LB(12);
     default: NK_LB(13);
@@ -289,7 +291,7 @@ template <class A, bool FWD>
 int run_ntt(NttArgs a, uint64_t buf_words, cudaStream_t st) {
   a.dbg = dbg;
   const uint32_t logn = a.logn;
-  if (logn <= 10) return launch_small<A, FWD>(a, st);
+  if (logn < 10) return launch_small<A, FWD>(a, st);
   if (logn < kLogBlock) return launch_block<A, FWD>(logn, a, a.rows, a.fin == 1, st);
   if (logn == kLogBlock) return launch_tma<A, FWD>(a, a.rows, buf_words, a.fin == 1, st);
   // long rows: high bits in global passes of <= 3 stages, low 14 bits per block

@@ -24,12 +24,12 @@
 //    previous block is still being transformed; three register passes of
 //    5/4(+1)/5 stages with exchanges inside 4-warp groups.
 //  * ntt_block<LOGB, LOGV, A, FWD, ILTM0>: same register passes for
-//    2^11..2^14-word blocks, loads straight from global; ntt_block_lat: the
+//    2^10..2^13-word rows, loads straight from global; ntt_block_lat: the
 //    same for batches smaller than the SM count, twiddle row staged in shared
 //    memory before griddepcontrol.wait (programmatic dependent launch).
 //  * ntt_global_pass<K, A, FWD>: K stages on bits [lo, lo+K) of long rows
 //    (N > 2^14), one column of 2^K words per thread, coalesced.
-//  * ntt_small<A, FWD>: any N <= 2^10, stage by stage in shared memory.
+//  * ntt_small<A, FWD>: any N <= 2^9, stage by stage in shared memory.
 #pragma once
 #include <cuda.h>
 
@@ -158,7 +158,7 @@ __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const typename
 }
 
 // ---------------------------------------------------------------------------
-// ntt_block: register passes with full padded shared exchanges (2^11..2^14)
+// ntt_block: register passes with full padded shared exchanges (2^10..2^13)
 // ---------------------------------------------------------------------------
 template <int LOGB, int LOGV, class A, bool FWD, int P, bool ILTM0, bool TWS = false>
 __device__ __forceinline__ void run_passes(uint64_t (&v)[1 << LOGV], uint64_t* sm,
@@ -302,7 +302,7 @@ __device__ __forceinline__ uint32_t swz_off(uint32_t j) {
 }
 
 // ---------------------------------------------------------------------------
-// ntt_block_lat: whole rows of 2^11..2^13 words for batches smaller than the
+// ntt_block_lat: whole rows of 2^10..2^13 words for batches smaller than the
 // SM count (cfg1: one row), where a transform's latency is the metric. Same
 // passes as ntt_block, plus:
 //  * the row's twiddle table (plan data, read-only since plan creation) is
@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(256) ntt_global_pass(NttArgs a, uint32_t lo, i
 }
 
 // ---------------------------------------------------------------------------
-// Any N <= 2^10: one CTA per row, whole row in shared memory, one stage at a
+// Any N <= 2^9: one CTA per row, whole row in shared memory, one stage at a
 // time. Used for the small sizes of the reference's tests.
 // ---------------------------------------------------------------------------
 template <class A, bool FWD>

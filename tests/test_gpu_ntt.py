@@ -252,7 +252,7 @@ def test_block_kernels_match_oracle(nk, oracle, kernel, logn, bits, npolys, arit
         nk.set_block_kernel(-1)
 
 
-@pytest.mark.parametrize("logn", [11, 12, 13])
+@pytest.mark.parametrize("logn", [10, 11, 12, 13])
 def test_block_sizes_large_batches(nk, oracle, logn, arith):
     """Batches of >= #SMs rows take the 32-words-per-thread block kernels (small
     batches take the 8-words-per-thread ones, test_block_sizes_match_oracle)."""
@@ -318,7 +318,7 @@ def test_shared_tables_across_threads(nk, oracle):
         assert np.array_equal(dev_out[i], expected[i])
 
 
-@pytest.mark.parametrize("logn", [11, 12, 13])
+@pytest.mark.parametrize("logn", [10, 11, 12, 13])
 @pytest.mark.parametrize("bits", [50, 60])
 def test_small_batch_plain_block_kernel(nk, oracle, logn, bits):
     """Small batches of 2^11..2^13-word rows normally take the latency kernel
@@ -402,3 +402,29 @@ def test_writes_stay_in_bounds(nk, oracle, logn, bits, npolys):
         h = host(buf)
         assert np.all(h[:guard] == np.uint64(SENTINEL)) and np.all(h[guard + words:] == np.uint64(SENTINEL))
         assert np.array_equal(h[guard:guard + words], want)
+
+
+@pytest.mark.parametrize("pinned", [False, True], ids=["pageable", "pinned"])
+def test_host_pipeline_multi_chunk_in_place(nk, oracle, pinned):
+    """Host-buffer transforms spanning several 16 MiB pipeline chunks, result
+    aliasing the operand (ntt.hpp:267-268), from pageable numpy memory (pinned
+    staging + parallel host copies) and from pinned memory (direct DMA)."""
+    n = 16384
+    moduli = largest_ntt_primes(50, n, 3)
+    npolys = 100  # 300 rows = 37.5 MiB: three chunks
+    plan = nk.RnsNtt(n, moduli)
+    x = rows_of(oracle, moduli, n, npolys, 4242)
+    want = host(plan.forward(torch.empty_like(dev(x)), dev(x), 1, 1))
+    if pinned:
+        buf = torch.from_numpy(x.view(np.int64)).pin_memory().numpy().view(np.uint64)
+    else:
+        buf = x.copy()
+    plan.forward(buf, buf, 1, 1)
+    assert np.array_equal(buf, want)
+    plan.inverse(buf, buf, 1, 1)
+    assert np.array_equal(buf, x)
+    # element-wise host calls through the same pipeline (two staged inputs)
+    q = moduli[0]
+    a, b = x[:2_400_000] % np.uint64(q), x[2_400_000:4_800_000] % np.uint64(q)  # two chunks each
+    r = nk.eltwise_mult_mod(None, a, b, q, 1)
+    assert np.array_equal(r, oracle.eltwise_mult_mod(a, b, q, 1))

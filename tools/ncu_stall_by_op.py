@@ -3,8 +3,15 @@
 import collections, csv, subprocess, sys
 rep, kre = sys.argv[1], sys.argv[2]
 which = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", "regex:" + kre],
-                     capture_output=True, text=True).stdout
+if rep.endswith(".csv.gz") or rep.endswith(".csv"):  # a --page source export (tools/gpu_check.sh)
+    import gzip, re
+    txt = (gzip.open(rep, "rt") if rep.endswith(".gz") else open(rep)).read()
+    # keep the blocks of kernels matching kre
+    parts = txt.split('"Kernel Name"')
+    out = "".join('"Kernel Name"' + p for p in parts[1:] if re.search(kre, p.splitlines()[0]))
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", "regex:" + kre],
+                         capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 blocks, cur = [], None
 for r in rows:

@@ -1,6 +1,14 @@
 #!/usr/bin/env python
-"""cfg2 element-wise kernels for ncu: EltwiseMultMod vv, FMA and vs-mult on
-2^20 x 60-bit words (each launched a few times)."""
+"""cfg2 element-wise kernels for ncu: EltwiseMultMod vv, FMA and vs-mult with
+a 60-bit modulus (each launched a few times).
+
+    python tools/prof_eltwise.py            2^20 words (cfg2's size; L2-resident)
+    python tools/prof_eltwise.py --big      2^26 words per operand (512 MiB, far
+                                            larger than L2): one launch streams
+                                            from HBM in steady state, so ncu's
+                                            dram__bytes and duration measure the
+                                            kernel's sustained bandwidth
+"""
 import os
 import sys
 
@@ -12,7 +20,7 @@ import paper_2103_16400_b200 as nk  # noqa: E402
 from bench import cfg2_modulus  # noqa: E402
 
 q = cfg2_modulus()
-n = 1 << 20
+n = 1 << (26 if "--big" in sys.argv else 20)
 g = torch.Generator(device="cuda").manual_seed(3)
 a = torch.randint(0, q, (n,), dtype=torch.int64, device="cuda", generator=g)
 b = torch.randint(0, q, (n,), dtype=torch.int64, device="cuda", generator=g)
@@ -22,4 +30,4 @@ for _ in range(3):
     nk.eltwise_fma_mod(r, a, 12345, b, q, 1)
     nk.eltwise_fma_mod(r, a, 12345, None, q, 1)
 torch.cuda.synchronize()
-print("ok")
+print("ok", n)
