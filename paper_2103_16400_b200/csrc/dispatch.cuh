@@ -303,7 +303,7 @@ int run_ntt(NttArgs a, uint64_t buf_words, cudaStream_t st) {
   }
   const int np = ks[1] ? 2 : 1;
   const uint64_t nitems = a.rows << gbits;
-  if (FWD) {
+  if constexpr (FWD) {
     uint32_t top = logn;
     for (int p = 0; p < np; ++p) {
       const uint32_t lo = top - ks[p];
