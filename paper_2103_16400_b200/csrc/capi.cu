@@ -190,18 +190,21 @@ int ntt_dispatch(const nk_plan* p, bool fwd, uint64_t* res, const uint64_t* op, 
     return ntt_dispatch_aligned(p, fwd, res, op, limb0, nlimbs, npolys, fin, fout, st, mulb);
   const size_t bytes = static_cast<size_t>(npolys) * nlimbs * p->n * 8;
   uint64_t *t = nullptr, *tm = nullptr;
-  NK_CUDA(cudaMallocAsync(&t, bytes, st));
-  NK_CUDA(cudaMemcpyAsync(t, op, bytes, cudaMemcpyDeviceToDevice, st));
-  if (mulb) {
-    NK_CUDA(cudaMallocAsync(&tm, bytes, st));
-    NK_CUDA(cudaMemcpyAsync(tm, mulb, bytes, cudaMemcpyDeviceToDevice, st));
+  int rc = 0;
+  cudaError_t e = cudaMallocAsync(&t, bytes, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(t, op, bytes, cudaMemcpyDeviceToDevice, st);
+  if (e == cudaSuccess && mulb) {
+    e = cudaMallocAsync(&tm, bytes, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(tm, mulb, bytes, cudaMemcpyDeviceToDevice, st);
   }
-  int rc = ntt_dispatch_aligned(p, fwd, t, t, limb0, nlimbs, npolys, fin, fout, st, mulb ? tm : nullptr);
+  if (e != cudaSuccess) rc = cuda_fail(e, "unaligned view: aligned copy");
+  if (!rc) rc = ntt_dispatch_aligned(p, fwd, t, t, limb0, nlimbs, npolys, fin, fout, st, mulb ? tm : nullptr);
   if (!rc) {
-    cudaError_t e = cudaMemcpyAsync(res, t, bytes, cudaMemcpyDeviceToDevice, st);
+    e = cudaMemcpyAsync(res, t, bytes, cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync(unaligned result)");
   }
-  cudaFreeAsync(t, st);
+  // the scratch goes back to the pool on every path
+  if (t) cudaFreeAsync(t, st);
   if (tm) cudaFreeAsync(tm, st);
   return rc;
 }
