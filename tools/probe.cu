@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <type_traits>
 
 #include "modmath.cuh"
 
@@ -33,13 +34,19 @@ __global__ void __launch_bounds__(256) dfma_loop(double* out, int iters) {
 
 // butterflies over V register words, three stages per iteration (spans 1, 2,
 // 4), two twiddles: the transforms' inner loop without memory or exchanges
+template <class Tw>
+__device__ __forceinline__ Tw as_tw(ulonglong2 w) {
+  if constexpr (std::is_same_v<Tw, uint64_t>) return w.x;  // w only (Arith52S's 8-byte tables)
+  else return w;
+}
+
 template <class A, int V, bool INV>
 __global__ void __launch_bounds__(512, 1) bfly_loop(uint64_t* out, LimbConstDev c, ulonglong2 w0, ulonglong2 w1,
                                                     int iters) {
   uint64_t v[V];
 #pragma unroll
   for (int i = 0; i < V; ++i) v[i] = A::load((threadIdx.x * 977u + i * 131u) % 1000003u);
-  const ulonglong2 w[2] = {w0, w1};
+  const typename A::Tw w[2] = {as_tw<typename A::Tw>(w0), as_tw<typename A::Tw>(w1)};
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int s = 0; s < 3; ++s) {
