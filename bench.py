@@ -502,7 +502,7 @@ def run_configs(rates, hbm, threads):
 
     # ---- cfg1: N = 4096, one 50-bit limb, forward(1,1) + inverse(1,1) latency ----
     n1 = 4096
-    q1 = largest_ntt_primes(50, 2 * n1, 1)[0]
+    q1 = largest_ntt_primes(50, n1, 1)[0]  # q == 1 mod 2N (1125899906826241)
     x1 = make_inputs([q1], 1, 1 ^ BASE_SEED, n=n1)
     p1 = nk.RnsNtt(n1, [q1])
     rp = RefPlan(n1, [q1])

@@ -50,3 +50,13 @@ def test_both_arms_share_the_config_dict():
     for w in (1, 2, 4, 8):
         c = bench.workload_config(w)
         assert c == bench.workload_config(w) and c["rows"] == 2048
+
+
+def test_config_moduli_match_survey_appendix_a():
+    """bench.py's moduli for cfg1, cfg2, cfg4 and the ends of cfg3."""
+    assert bench.largest_ntt_primes(50, 4096, 1) == [1125899906826241]
+    assert bench.cfg2_modulus() == 1152921504606846883
+    m3 = bench.cfg3_moduli()
+    assert (m3[0], m3[15], m3[31]) == (1125899904679937, 1125899893964801, 1125899884036097)
+    m4 = bench.largest_ntt_primes(60, 65536, 24)
+    assert (m4[0], m4[23]) == (1152921504606584833, 1152921504559267841)

@@ -55,7 +55,7 @@ def main():
     out = []
     # cfg1
     n = 4096
-    q1 = largest_ntt_primes(50, 2 * n, 1)[0]
+    q1 = largest_ntt_primes(50, n, 1)[0]  # cfg1: q == 1 mod 2N
     p1 = nk.RnsNtt(n, [q1])
     x = rnd(n, q1, gen)
     f, b = torch.empty_like(x), torch.empty_like(x)
