@@ -186,6 +186,29 @@ def make_inputs(moduli, npolys, seed, n=N, limb0=0, nlimbs=None, total_limbs=Non
     return (raw % q).reshape(-1)
 
 
+def rank_inputs(world, rank, n=N, npolys=NPOLYS):
+    """Rank `rank`'s share of the cfg3 batch: (first limb, limb count, its rows
+    [npolys][count][n] — the batch's own words for those limbs)."""
+    from paper_2103_16400_b200.sharding import limb_shard
+
+    moduli = cfg3_moduli()
+    limb0, nl = limb_shard(NLIMBS, world, rank)
+    x = make_inputs(moduli, npolys, SEED, n=n, limb0=limb0, nlimbs=nl, total_limbs=NLIMBS)
+    return limb0, nl, x
+
+
+def reduce_over_ranks(v, op, world, backend):
+    """max / sum of a float over the ranks (the bench's max-over-ranks timing)."""
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def workload_config(world):
     """The `config` dict of both arms (identical by construction)."""
     return {"workload": "cfg3: N=16384, 32 limbs x 64 polys, fwd(1,1)+inv(1,1)",
@@ -723,7 +746,6 @@ def run_gpu(args):
     import torch.distributed as dist
 
     import paper_2103_16400_b200 as nk
-    from paper_2103_16400_b200.sharding import limb_shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -738,31 +760,20 @@ def run_gpu(args):
             dist.init_process_group("gloo")
 
     def max_over_ranks(v):
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64,
-                         device="cuda" if args.dist_backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_over_ranks(v, "max", world, args.dist_backend)
 
     def sum_over_ranks(v):
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64,
-                         device="cuda" if args.dist_backend == "nccl" else "cpu")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+        return reduce_over_ranks(v, "sum", world, args.dist_backend)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
     moduli = cfg3_moduli()
-    limb0, nl = limb_shard(NLIMBS, world, rank)
+    limb0, nl, x = rank_inputs(world, rank)
     plan = nk.RnsNtt(N, moduli[limb0:limb0 + nl], device=device)
     words = NPOLYS * nl * N
     total_words = NPOLYS * NLIMBS * N
-    x = make_inputs(moduli, NPOLYS, SEED, limb0=limb0, nlimbs=nl, total_limbs=NLIMBS)
     d_in = torch.from_numpy(x.view(np.int64)).cuda()
     d_f = torch.empty_like(d_in)
     d_b = torch.empty_like(d_in)

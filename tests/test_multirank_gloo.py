@@ -82,3 +82,48 @@ def test_limb_shard_balanced(nlimbs, world):
     for a, c in parts:
         assert a == pos
         pos += c
+
+
+def _bench_worker(rank, world, port, q):
+    """bench.py's own multi-GPU helpers on CPU: each rank's share of the cfg3
+    batch (rank_inputs, reduced N) and the max/sum-over-ranks reductions."""
+    import sys
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+
+        n, npolys = 64, 3
+        limb0, nl, x = bench.rank_inputs(world, rank, n=n, npolys=npolys)
+        parts = [None] * world
+        dist.all_gather_object(parts, (limb0, nl, x))
+        full = bench.make_inputs(bench.cfg3_moduli(), npolys, bench.SEED, n=n).reshape(npolys, bench.NLIMBS, n)
+        rebuilt = np.empty_like(full)
+        for a, c, part in parts:
+            rebuilt[:, a:a + c, :] = part.reshape(npolys, c, n)
+        ok = np.array_equal(rebuilt, full)
+        mx = bench.reduce_over_ranks(10.0 * (rank + 1), "max", world, "gloo")
+        sm = bench.reduce_over_ranks(1.0 + rank, "sum", world, "gloo")
+        cfgs = [None] * world
+        dist.all_gather_object(cfgs, bench.workload_config(world))
+        q.put((rank, ok, mx, sm, all(c == cfgs[0] for c in cfgs)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_multirank_helpers_two_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bench_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    results = sorted(q.get(timeout=5) for _ in range(world))
+    assert all(p.exitcode == 0 for p in procs)
+    assert all(ok and same for _, ok, _, _, same in results), results
+    assert all(mx == 20.0 and sm == 3.0 for _, _, mx, sm, _ in results), results
