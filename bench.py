@@ -643,6 +643,9 @@ def run_configs(rates, hbm, threads):
     buf5 = np.empty_like(f5)
     rp5.poly(buf5, f5, g5, rows5, threads)
     assert np.array_equal(host(r5), buf5), "cfg5 mismatch"
+    l0 = nk.launch_count()
+    p5.poly_mult_mod(r5, df5, dg5)
+    launches5 = nk.launch_count() - l0
     us5 = 1e3 * dev_time_ms(lambda: p5.poly_mult_mod(r5, df5, dg5), 10)
     bfly5 = 3 * (N // 2) * 14 * rows5
     sample5 = 16
@@ -653,9 +656,12 @@ def run_configs(rates, hbm, threads):
     out["cfg5"] = {
         "op": "poly_mult_mod, N=16384, 16 x 50-bit limbs x 128 pairs (2048 row pairs)",
         "bound": "fp64 pipe (3 transforms x 9 FP64 ops/butterfly vs the live DFMA rate)",
+        "kernel": "poly_mul14 (both forwards, product, inverse on chip; g^ held in TMEM)",
+        "launches_per_call": launches5,
         "us": us5, "Gcoeff_s": N * rows5 / us5 / 1e3, "fp64_floor_us": floor5,
         "roofline_frac": floor5 / us5 if floor5 else None,
-        "hbm_floor_us_fused": 24 * N * rows5 / (hbm * 1e9) * 1e6,
+        "hbm_floor_us": 24 * N * rows5 / (hbm * 1e9) * 1e6,
+        "hbm_bytes_per_coeff": 24,
         "cpu_ref_us_1thread": c15 * 1e6 * rows5 / sample5,
         "cpu_ref_1thread_sample": f"{sample5} of {rows5} row pairs, scaled",
         "cpu_ref_us_all_cores": ca5 * 1e6, "speedup_vs_cpu_all_cores": ca5 * 1e6 / us5}

@@ -111,6 +111,172 @@ __host__ __device__ __forceinline__ constexpr uint32_t ex2_off(uint32_t j) {
   }
 }
 
+namespace grp {
+
+// P2-read base (both directions): swz_off(ex1_perm(jt2 | jc(g, r))) =
+//   (q2 ^ (y * 0x90)) + (hi << 10), y = the 3 low line bits the registers
+//   flip, hi = the register line bits above them (see ex1 below)
+template <bool FWD>
+__device__ __forceinline__ uint32_t q2_of(uint32_t jt2) {
+  if (FWD) {
+    // line = jt2 >> 4 (bits 5..9) | s, s = g + 2r; XOR m = j9..j11 into its low 3 bits
+    const uint32_t m = (jt2 >> 9) & 7u, c1 = (jt2 >> 1) & 7u;
+    return ((jt2 >> 4) << 7) | (m << 7) | ((m ^ c1) << 4) | ((jt2 & 1u) << 3);
+  } else {
+    // line bit0 = j4 ^ g, bit1 = r0, bit2 = r1 ^ j9, bits 3,4 = r2, r3, bits 5..8 = j9..j12, bit 9 = g
+    const uint32_t rt = ((jt2 >> 4) & 1u) | (((jt2 >> 9) & 1u) << 2) | (((jt2 >> 9) & 15u) << 5);
+    const uint32_t c1 = (jt2 >> 1) & 7u;
+    return (rt << 7) | ((c1 ^ (rt & 7u)) << 4) | ((jt2 & 1u) << 3);
+  }
+}
+
+// P1 words from the staging buffer. Forward: 32 words at stride 512, one
+// 8-byte load each (base + immediate). Inverse: 32 contiguous words (two
+// 16-word lines) as 16-byte chunks; `key` is XORed into the chunk swizzle
+// (0 for the TMA layout; poly_mul14's product image uses j9..j11). RAW: the
+// buffer already holds the policy's representation (no A::load).
+template <class A, bool FWD, bool RAW = false>
+__device__ __forceinline__ void p1_read(uint64_t (&v)[32], const uint8_t* St, uint32_t jt1, uint32_t key = 0) {
+  if (FWD) {
+    const uint32_t b1 = swz_off(jt1);
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      const uint64_t x = *reinterpret_cast<const uint64_t*>(St + b1 + r * 4096);
+      v[r] = RAW ? x : A::load(x);
+    }
+  } else {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t row16 = (jt1 >> 4) + h;
+      const uint32_t rowoff = row16 << 7, sw = (row16 & 7) ^ key;
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(St + rowoff + ((cc ^ sw) << 4));
+        v[16 * h + 2 * cc] = RAW ? p.x : A::load(p.x);
+        v[16 * h + 2 * cc + 1] = RAW ? p.y : A::load(p.y);
+      }
+    }
+  }
+}
+
+// Exchange 1: in place, within the group's staging slots. Waits (bar_r1g,
+// `parity`) until every warp of the group has read its P1 words, writes this
+// thread's words to their exchange slots, syncs the group, reads the P2 words.
+template <bool FWD>
+__device__ __forceinline__ void ex1(uint64_t (&v)[32], uint8_t* St, uint32_t jt1, uint32_t q2, uint64_t* bar_r1g,
+                                    uint32_t parity, uint32_t g1) {
+  mbar_wait(bar_r1g, parity);
+  if (FWD) {
+    // swz_off(ex1_perm(jt1 | r << 9)) = (swz_off(jt1) ^ ((r & 7) * 0x90)) + r * 4096
+    const uint32_t b1 = swz_off(jt1);
+#pragma unroll
+    for (int r = 0; r < 32; ++r) *reinterpret_cast<uint64_t*>(St + ((b1 ^ ((r & 7) * 0x90u)) + r * 4096)) = v[r];
+  } else {
+    // swz_off(ex1_perm(jt1 | h << 4 | 2cc)) = wh ^ (cc << 4), wh from the
+    // permuted line (jt1' >> 4) ^ h, jt1' = ex1_perm(jt1)
+    const uint32_t rp = ex1_perm<false>(jt1) >> 4;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t rh = rp ^ static_cast<uint32_t>(h);
+      const uint32_t wh = (rh << 7) | ((rh & 7u) << 4);
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc)
+        *reinterpret_cast<ulonglong2*>(St + (wh ^ (cc << 4))) = make_ulonglong2(v[16 * h + 2 * cc], v[16 * h + 2 * cc + 1]);
+    }
+  }
+  named_sync128(1 + g1);
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      // forward: s = g + 2r (line bits 0..4); inverse: line bits (g, r0, r1) low, (r2, r3) << 3, g << 9
+      const uint32_t y = FWD ? ((g + 2 * r) & 7) : (g | ((r & 3) << 1));
+      const uint32_t hi = FWD ? (((g + 2 * r) >> 3) << 10) : (((r >> 2) << 10) | (g << 16));
+      v[16 * g + r] = *reinterpret_cast<const uint64_t*>(St + ((q2 ^ (y * 0x90u)) + hi));
+    }
+}
+
+// This warp has consumed the staging buffer; the last of the 16 warps (shared
+// counter) runs `refill` (e.g. issues the next TMA into the buffer).
+template <class F>
+__device__ __forceinline__ void staging_consumed(uint32_t* cnt, uint32_t l, F&& refill) {
+  __syncwarp();
+  if (l == 0) {
+    __threadfence_block();
+    const uint32_t old = atomicAdd(cnt, 1u);
+    if ((old & 15u) == 15u) {
+      __threadfence_block();
+      refill();
+    }
+  }
+}
+
+// Exchange 2: through the group's slice Eg of E, two rounds on the register
+// bit common to P2 and P3 (forward bit 4, inverse bit 13). Waits (bar_r2g,
+// `parity`) for the previous exchange's last-round reads; arrives when this
+// warp's last-round reads are done.
+template <bool FWD>
+__device__ __forceinline__ void ex2(uint64_t (&v)[32], uint8_t* Eg, uint32_t e2w, uint32_t e2r, uint64_t* bar_r2g,
+                                    uint32_t parity, uint32_t g2, uint32_t l) {
+  mbar_wait(bar_r2g, parity);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    if (h == 1) named_sync128(5 + g2);  // round-0 reads done before round-1 writes
+    // ex2_off(jt2 | r << 5): forward e2w + r * 128; inverse (e2w ^ ((r & 1) << 6)) + (r >> 1) * 128
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const uint32_t off = FWD ? (e2w + r * 128) : ((e2w ^ ((r & 1) << 6)) + (r >> 1) * 128);
+      *reinterpret_cast<uint64_t*>(Eg + off) = v[16 * h + r];
+    }
+    named_sync128(5 + g2);
+    if (FWD) {
+      // P3 round h: the 16 contiguous words j0..j3 (bit 4 = h) as 16-byte
+      // chunks, ex2_off(jt3 | 2cc) = e2r ^ (cc << 4)
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Eg + (e2r ^ (cc << 4)));
+        v[16 * h + 2 * cc] = p.x;
+        v[16 * h + 2 * cc + 1] = p.y;
+      }
+    } else {
+      // P3 round h: registers 16h + r hold j = jt3 | (16h + r) << 9 (bit 13 = h),
+      // ex2_off(jt3 | r << 9) = (e2r ^ ((r & 1) << 6)) + r * 1024
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        v[16 * h + r] = *reinterpret_cast<const uint64_t*>(Eg + ((e2r ^ ((r & 1) << 6)) + r * 1024));
+    }
+  }
+  __syncwarp();
+  if (l == 0) mbar_arrive_local(bar_r2g);
+}
+
+// Forward result words (32 contiguous per thread, a 256-byte run per lane) to
+// global memory in four rounds through the warp's 2 KiB image Ow: each lane
+// writes 64 bytes of its run as row l, then every STG.128 stores 8 rows x 64
+// bytes (16-byte chunks XOR-swizzled by (row >> 1) & 3: both sides conflict
+// free).
+__device__ __forceinline__ void fwd_store(const uint64_t (&v)[32], uint8_t* Ow, uint32_t w, uint32_t l,
+                                          uint64_t* __restrict__ dst) {
+  const uint32_t wrow = ((l >> 1) << 7) | ((l & 1u) << 6), wsw = (l >> 1) & 3u;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (q) __syncwarp();  // the previous round's rows have been read
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc)
+      *reinterpret_cast<ulonglong2*>(Ow + wrow + ((cc ^ wsw) << 4)) = make_ulonglong2(v[8 * q + 2 * cc], v[8 * q + 2 * cc + 1]);
+    __syncwarp();
+#pragma unroll
+    for (int s2 = 0; s2 < 4; ++s2) {
+      const uint32_t rw = (l >> 2) + 8 * s2, cc = l & 3u;
+      const ulonglong2 p =
+          *reinterpret_cast<const ulonglong2*>(Ow + ((rw >> 1) << 7) + ((rw & 1u) << 6) + ((cc ^ ((rw >> 1) & 3u)) << 4));
+      *reinterpret_cast<ulonglong2*>(dst + GrpMap<true>::jt3(w, rw) + 8 * q + 2 * cc) = p;
+    }
+  }
+}
+
+}  // namespace grp
+
 template <class A, bool FWD, bool ILTM0, bool LONG = false>
 __global__ void __launch_bounds__(512, 1)
     ntt_grp14(const __grid_constant__ CUtensorMap tin, NttArgs a, uint32_t nitems) {
@@ -161,21 +327,8 @@ __global__ void __launch_bounds__(512, 1)
   uint8_t* Eg = E + (g2 << 14);           // this warp's exchange-2 group slice
   // Thread-constant byte bases: every shared access below is a base, at most
   // one XOR with an immediate, plus an immediate offset (derivations in the
-  // comments; swz_off is the 128B swizzle, ex1_perm / ex2_off the layouts).
-  // P2 reads (both directions): swz_off(ex1_perm(jt2 | jc(g, r))) =
-  //   (q2 ^ (y * 0x90)) + (hi << 10), y = the 3 low line bits the registers
-  //   flip, hi = the register line bits above them
-  uint32_t q2;
-  if (FWD) {
-    // line = jt2 >> 4 (bits 5..9) | s, s = g + 2r; XOR m = j9..j11 into its low 3 bits
-    const uint32_t m = (jt2 >> 9) & 7u, c1 = (jt2 >> 1) & 7u;
-    q2 = ((jt2 >> 4) << 7) | (m << 7) | ((m ^ c1) << 4) | ((jt2 & 1u) << 3);
-  } else {
-    // line bit0 = j4 ^ g, bit1 = r0, bit2 = r1 ^ j9, bits 3,4 = r2, r3, bits 5..8 = j9..j12, bit 9 = g
-    const uint32_t rt = ((jt2 >> 4) & 1u) | (((jt2 >> 9) & 1u) << 2) | (((jt2 >> 9) & 15u) << 5);
-    const uint32_t c1 = (jt2 >> 1) & 7u;
-    q2 = (rt << 7) | ((c1 ^ (rt & 7u)) << 4) | ((jt2 & 1u) << 3);
-  }
+  // helpers; swz_off is the 128B swizzle, ex1_perm / ex2_off the layouts).
+  const uint32_t q2 = grp::q2_of<FWD>(jt2);
   const uint32_t e2w = ex2_off<FWD>(jt2), e2r = ex2_off<FWD>(jt3);
   uint32_t phase = 0;
 
@@ -193,114 +346,26 @@ __global__ void __launch_bounds__(512, 1)
 
     // ---- P1 words from the staging buffer (TMA layout) ----
     mbar_wait(bar_full, phase);
-    if (FWD) {
-      // 32 words at stride 512: one 8-byte load each (base + immediate)
-      const uint32_t b1 = swz_off(jt1);
-#pragma unroll
-      for (int r = 0; r < 32; ++r) v[r] = A::load(*reinterpret_cast<const uint64_t*>(St + b1 + r * 4096));
-    } else {
-      // 32 contiguous words (two 16-word lines): 16-byte chunks
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t row16 = (jt1 >> 4) + h;
-        const uint32_t rowoff = row16 << 7, sw = row16 & 7;
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-          const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(St + rowoff + ((cc ^ sw) << 4));
-          v[16 * h + 2 * cc] = A::load(p.x);
-          v[16 * h + 2 * cc + 1] = A::load(p.y);
-        }
-      }
-    }
+    grp::p1_read<A, FWD>(v, St, jt1);
     __syncwarp();
     if (l == 0) mbar_arrive_local(bar_r1 + g1);  // this warp's P1 slots may be rewritten
 
     pass14<A, FWD, P1, ILTM0>(v, tw, twl, a.n, xbase + jt1, c);
 
     // ---- exchange 1: in place, within the group's staging slots ----
-#if !defined(NK_EXP_NO_EX)  // perf experiment only: exchanges skipped (wrong results)
-    mbar_wait(bar_r1 + g1, phase);  // every warp of the group has read its P1 words
-    if (FWD) {
-      // swz_off(ex1_perm(jt1 | r << 9)) = (swz_off(jt1) ^ ((r & 7) * 0x90)) + r * 4096
-      const uint32_t b1 = swz_off(jt1);
-#pragma unroll
-      for (int r = 0; r < 32; ++r)
-        *reinterpret_cast<uint64_t*>(St + ((b1 ^ ((r & 7) * 0x90u)) + r * 4096)) = v[r];
-    } else {
-      // swz_off(ex1_perm(jt1 | h << 4 | 2cc)) = wh ^ (cc << 4), wh from the
-      // permuted line (jt1' >> 4) ^ h, jt1' = ex1_perm(jt1)
-      const uint32_t rp = ex1_perm<false>(jt1) >> 4;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t rh = rp ^ static_cast<uint32_t>(h);
-        const uint32_t wh = (rh << 7) | ((rh & 7u) << 4);
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc)
-          *reinterpret_cast<ulonglong2*>(St + (wh ^ (cc << 4))) =
-              make_ulonglong2(v[16 * h + 2 * cc], v[16 * h + 2 * cc + 1]);
-      }
-    }
-    named_sync128(1 + g1);
-#pragma unroll
-    for (int g = 0; g < 2; ++g)
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        // forward: s = g + 2r (line bits 0..4); inverse: line bits (g, r0, r1) low, (r2, r3) << 3, g << 9
-        const uint32_t y = FWD ? ((g + 2 * r) & 7) : (g | ((r & 3) << 1));
-        const uint32_t hi = FWD ? (((g + 2 * r) >> 3) << 10) : (((r >> 2) << 10) | (g << 16));
-        v[16 * g + r] = *reinterpret_cast<const uint64_t*>(St + ((q2 ^ (y * 0x90u)) + hi));
-      }
-#endif
+    grp::ex1<FWD>(v, St, jt1, q2, bar_r1 + g1, phase, g1);
     // staging consumed by this warp; the last of the 16 warps refills it
-    __syncwarp();
-    if (l == 0) {
-      __threadfence_block();
-      const uint32_t old = atomicAdd(cnt, 1u);
-      if ((old & 15u) == 15u) {
-        __threadfence_block();
-        if (k + gridDim.x < nitems) {
-          fence_proxy_async();
-          issue(k + gridDim.x);
-        }
+    grp::staging_consumed(cnt, l, [&] {
+      if (k + gridDim.x < nitems) {
+        fence_proxy_async();
+        issue(k + gridDim.x);
       }
-    }
+    });
 
     pass14<A, FWD, P2, false>(v, tw, twl, a.n, xbase + jt2, c);
 
-    // ---- exchange 2: through the group's slice of E, two rounds on the
-    // register bit common to P2 and P3 (forward bit 4, inverse bit 13) ----
-#if !defined(NK_EXP_NO_EX)
-    mbar_wait(bar_r2 + g2, phase ^ 1);  // the previous block's last-round reads (first block: passes)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (h == 1) named_sync128(5 + g2);  // round-0 reads done before round-1 writes
-      // ex2_off(jt2 | r << 5): forward e2w + r * 128; inverse (e2w ^ ((r & 1) << 6)) + (r >> 1) * 128
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        const uint32_t off = FWD ? (e2w + r * 128) : ((e2w ^ ((r & 1) << 6)) + (r >> 1) * 128);
-        *reinterpret_cast<uint64_t*>(Eg + off) = v[16 * h + r];
-      }
-      named_sync128(5 + g2);
-      if (FWD) {
-        // P3 round h: the 16 contiguous words j0..j3 (bit 4 = h) as 16-byte
-        // chunks, ex2_off(jt3 | 2cc) = e2r ^ (cc << 4)
-#pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-          const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Eg + (e2r ^ (cc << 4)));
-          v[16 * h + 2 * cc] = p.x;
-          v[16 * h + 2 * cc + 1] = p.y;
-        }
-      } else {
-        // P3 round h: registers 16h + r hold j = jt3 | (16h + r) << 9 (bit 13 = h),
-        // ex2_off(jt3 | r << 9) = (e2r ^ ((r & 1) << 6)) + r * 1024
-#pragma unroll
-        for (int r = 0; r < 16; ++r)
-          v[16 * h + r] = *reinterpret_cast<const uint64_t*>(Eg + ((e2r ^ ((r & 1) << 6)) + r * 1024));
-      }
-    }
-    __syncwarp();
-    if (l == 0) mbar_arrive_local(bar_r2 + g2);
-#endif
+    // ---- exchange 2: the previous block's last-round reads (first block: passes) ----
+    grp::ex2<FWD>(v, Eg, e2w, e2r, bar_r2 + g2, phase ^ 1, g2, l);
 
     // canonical inverse (Arith52S, whole rows): n^-1 folded into the last
     // stage (bit 13, single twiddle), as in ntt_pair14 / ntt_grp14
@@ -317,28 +382,7 @@ __global__ void __launch_bounds__(512, 1)
     if (FWD) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = fwd_out<A>(v[i], c, a.fout);
-      // 32 contiguous words per thread (a 256-byte run per lane) -> four
-      // rounds through the warp's 2 KiB image: each lane writes 64 bytes of
-      // its run as row l, then every STG.128 stores 8 rows x 64 bytes (16-byte
-      // chunks XOR-swizzled by (row >> 1) & 3: both sides conflict free)
-      uint8_t* Ow = O + (w << 11);
-      const uint32_t wrow = ((l >> 1) << 7) | ((l & 1u) << 6), wsw = (l >> 1) & 3u;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        if (q) __syncwarp();  // the previous round's rows have been read
-#pragma unroll
-        for (int cc = 0; cc < 4; ++cc)
-          *reinterpret_cast<ulonglong2*>(Ow + wrow + ((cc ^ wsw) << 4)) =
-              make_ulonglong2(v[8 * q + 2 * cc], v[8 * q + 2 * cc + 1]);
-        __syncwarp();
-#pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) {
-          const uint32_t rw = (l >> 2) + 8 * s2, cc = l & 3u;
-          const ulonglong2 p =
-              *reinterpret_cast<const ulonglong2*>(Ow + ((rw >> 1) << 7) + ((rw & 1u) << 6) + ((cc ^ ((rw >> 1) & 3u)) << 4));
-          *reinterpret_cast<ulonglong2*>(dst + M::jt3(w, rw) + 8 * q + 2 * cc) = p;
-        }
-      }
+      grp::fwd_store(v, O + (w << 11), w, l, dst);
     } else {
       if constexpr (LONG) {
 #pragma unroll

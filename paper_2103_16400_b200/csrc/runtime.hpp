@@ -15,6 +15,7 @@
 namespace nk {
 struct MultConst;
 struct FmaConst;
+struct PolyArgs;
 }  // namespace nk
 
 namespace nk::rt {
@@ -35,7 +36,7 @@ extern std::atomic<uint64_t> launches;
 // Testing aids, per calling thread (nk_debug_block_kernel / nk_debug_exact_only /
 // nk_debug_dump_to): they change dispatch only for calls made by the thread
 // that set them.
-extern thread_local int block_kernel;  // -1 auto, 0 CTA pair, 1 group exchange (16384-word blocks)
+extern thread_local int block_kernel;  // -1 auto, 0 CTA pair, 1 group exchange (16384-word blocks; poly_mult_mod: see capi.cu)
 extern thread_local bool no_lat;       // small batches take ntt_block instead of ntt_block_lat
 extern thread_local bool exact_only;   // beta = 2^52 transforms always take the lazy-exact policy
 extern thread_local uint64_t* dbg;     // NK_DBG_TIMELINE builds: per-warp phase stamps
@@ -47,6 +48,10 @@ int sm_count();  // of the current device
 // the input buffer (for the TMA tensor maps).
 template <class A, bool FWD>
 int run_ntt(NttArgs a, uint64_t buf_words, cudaStream_t st);
+
+// poly_mult_mod of N = 16384 rows in one kernel (poly.cu, ntt_poly.cuh):
+// signed FP64 policy, canonical f and g with 16-byte aligned rows.
+int run_poly_mul14(const PolyArgs& pa, const uint64_t* f, const uint64_t* g, cudaStream_t st);
 
 // element-wise launchers (eltwise.cu)
 int launch_mult(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t total, uint32_t logn,

@@ -276,24 +276,30 @@ def test_cfg5_sample(nk, oracle):
         assert np.array_equal(got[r], want), r
 
 
-@pytest.mark.parametrize("exact", [False, True], ids=["fused", "unfused"])
-def test_poly_16384_paths_and_aliasing(nk, oracle, exact):
-    """N = 16384 with 50-bit limbs runs the fused sequence (forward g, forward f
-    with the dyadic product in its store, inverse); exact_only forces the
-    reference's fwd(1,4)/mult(4)/inv(1,1) sequence. Both must equal the
-    oracle, also when the result aliases f or g and for all-(q-1) inputs."""
+@pytest.mark.parametrize("path", ["single", "pair3", "reference"])
+def test_poly_16384_paths_and_aliasing(nk, oracle, path):
+    """N = 16384 with 50-bit limbs: the single on-chip kernel (default:
+    forward g to TMEM, forward f, product, inverse), the three-launch sequence
+    (nk_debug_block_kernel(0): forward g, forward f with the dyadic product in
+    its store, inverse) and the reference's fwd(1,4)/mult(4)/inv(1,1) sequence
+    (exact_only). All must equal the oracle, also when the result aliases f or
+    g and for all-(q-1) and all-zero rows."""
     from primes import largest_ntt_primes
 
     n = 16384
     moduli = largest_ntt_primes(50, n, 3)
     plan = nk.RnsNtt(n, moduli)
-    nk.set_exact_only(exact)
+    nk.set_exact_only(path == "reference")
+    nk.set_block_kernel(0 if path == "pair3" else -1)
     try:
         npolys = 2
         rows = npolys * len(moduli)
         f = np.stack([oracle.mt19937_64(70 + r, n, moduli[r % 3]) for r in range(rows)]).reshape(-1)
         g = np.stack([oracle.mt19937_64(170 + r, n, moduli[r % 3]) for r in range(rows)]).reshape(-1)
-        g[:n] = moduli[0] - 1  # extreme row
+        g[:n] = moduli[0] - 1  # extreme rows
+        f[n:2 * n] = moduli[1] - 1
+        g[n:2 * n] = moduli[1] - 1
+        f[2 * n:3 * n] = 0
         want = np.concatenate([oracle.poly_mult_mod(n, [moduli[r % 3]], f[r * n:(r + 1) * n],
                                                     g[r * n:(r + 1) * n]) for r in range(rows)])
         df, dg = dev(f), dev(g)
@@ -307,6 +313,56 @@ def test_poly_16384_paths_and_aliasing(nk, oracle, exact):
         assert np.array_equal(host(dg), want)
     finally:
         nk.set_exact_only(False)
+        nk.set_block_kernel(-1)
+
+
+@pytest.mark.parametrize("rows_per_limb", [1, 100, 149])
+def test_poly_16384_single_kernel_shapes(nk, oracle, rows_per_limb):
+    """The single-kernel poly_mult_mod over a limb sub-range (limb0 = 1 of 4
+    limbs) with fewer rows than SMs, about one per SM, and more than SMs (CTAs
+    looping over rows); one kernel launch per call."""
+    from primes import largest_ntt_primes
+
+    n = 16384
+    moduli = largest_ntt_primes(50, n, 4)
+    plan = nk.RnsNtt(n, moduli)
+    sub = moduli[1:3]
+    rows = rows_per_limb * len(sub)
+    f = np.stack([oracle.mt19937_64(900 + r, n, sub[r % 2]) for r in range(rows)])
+    g = np.stack([oracle.mt19937_64(5900 + r, n, sub[r % 2]) for r in range(rows)])
+    df, dg = dev(f.reshape(-1)), dev(g.reshape(-1))
+    out = torch.empty_like(df)
+    before = nk.launch_count()
+    plan.poly_mult_mod(out, df, dg, limb0=1, nlimbs=2)
+    torch.cuda.synchronize()
+    assert nk.launch_count() - before == 1
+    got = host(out).reshape(rows, n)
+    for r in sorted({0, 1, rows // 2, rows - 2, rows - 1}):
+        want = oracle.poly_mult_mod(n, [sub[r % 2]], f[r], g[r])
+        assert np.array_equal(got[r], want), r
+
+
+def test_poly_16384_unaligned_operands_fall_back(nk, oracle):
+    """The single kernel loads f and g with TMA (16-byte aligned rows); 8-byte
+    aligned views take the multi-launch sequence instead, same result."""
+    from primes import largest_ntt_primes
+
+    n = 16384
+    moduli = largest_ntt_primes(50, n, 2)
+    rows = 4
+    f = np.concatenate([oracle.mt19937_64(80 + r, n, moduli[r % 2]) for r in range(rows)])
+    g = np.concatenate([oracle.mt19937_64(90 + r, n, moduli[r % 2]) for r in range(rows)])
+    want = oracle.poly_mult_mod(n, moduli, f, g)
+    plan = nk.RnsNtt(n, moduli)
+    words = f.size
+    fb = torch.zeros(words + 1, dtype=torch.int64, device="cuda")
+    fb[1:] = dev(f)
+    out = torch.empty(words, dtype=torch.int64, device="cuda")
+    before = nk.launch_count()
+    plan.poly_mult_mod(out, fb[1:], dev(g))
+    torch.cuda.synchronize()
+    assert nk.launch_count() - before > 1
+    assert np.array_equal(host(out), want)
 
 
 @pytest.mark.parametrize("offset", [0, 1, 2, 3])

@@ -63,13 +63,17 @@ def eltwise():
     assert np.array_equal(host(r), o.eltwise_mult_mod(a5, b5, q50, 1))
 
 
-def poly():
+def poly(kernel=-1):
     n = 16384
     moduli = largest_ntt_primes(50, n, 2)
     f = np.concatenate([o.mt19937_64(21 + r, n, moduli[r % 2]) for r in range(4)])
     g = np.concatenate([o.mt19937_64(31 + r, n, moduli[r % 2]) for r in range(4)])
     plan = nk.RnsNtt(n, moduli)
-    got = host(plan.poly_mult_mod(torch.empty(f.size, dtype=torch.int64, device="cuda"), dev(f), dev(g)))
+    nk.set_block_kernel(kernel)
+    try:
+        got = host(plan.poly_mult_mod(torch.empty(f.size, dtype=torch.int64, device="cuda"), dev(f), dev(g)))
+    finally:
+        nk.set_block_kernel(-1)
     assert np.array_equal(got, o.poly_mult_mod(n, moduli, f, g))
 
 
@@ -84,7 +88,8 @@ CASES = {
     "small_1024": lambda: transform(1024, 30, 2, 2),                   # ntt_small
     "global_pass_65536": lambda: transform(65536, 60, 1, 1, fin=4),    # ntt_global_pass + block
     "eltwise": eltwise,
-    "poly_fused": poly,
+    "poly_single": poly,                                               # poly_mul14 (TMEM)
+    "poly_three_launch": lambda: poly(kernel=0),                       # pair14 with the fused product
 }
 
 if __name__ == "__main__":

@@ -130,6 +130,11 @@ def main():
     t5 = timed(lambda: p5.poly_mult_mod(o, fx, gx), 10, 2)
     out.append({"cfg": 5, "op": "poly_mult_mod (2048 row pairs)", "us": 1e3 * t5,
                 "Gcoeff_s": words / t5 / 1e6, "hbm_floor_us": 24 * words / 6455.6e3})
+    nk.set_block_kernel(0)  # the three-launch sequence, for comparison
+    t5b = timed(lambda: p5.poly_mult_mod(o, fx, gx), 10, 2)
+    nk.set_block_kernel(-1)
+    out.append({"cfg": 5, "op": "poly_mult_mod, three launches", "us": 1e3 * t5b,
+                "Gcoeff_s": words / t5b / 1e6})
     for line in out:
         print(json.dumps(line), flush=True)
 
