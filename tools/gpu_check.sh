@@ -1,7 +1,8 @@
 #!/bin/bash
 # One gpurun call: GPU parity tests, bench line, reference arm, launch lists,
-# ncu --set full captures of the cfg3 transforms and of the element-wise
-# kernels at steady state, all-config device times.
+# ncu --set full captures of the cfg3 transforms, of the element-wise
+# kernels at steady state and of the single-kernel poly_mult_mod, all-config
+# device times.
 #   gpurun --timeout 2400 -- bash tools/gpu_check.sh [tag]
 TAG=${1:-run}
 O=gpurun_out/$TAG
@@ -31,6 +32,9 @@ if [ "${SKIP_NCU:-0}" = "0" ]; then
   timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
       --log-file $O/launches_cfg5.csv python tools/prof_ntt.py --n 16384 --limbs 16 --polys 128 --op poly --iters 1 > $O/ncu_cfg5.log 2>&1
   echo "ncu_cfg45=$?" | tee -a $O/status
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:poly_mul14 -s 1 -c 1 \
+      -o $O/prof_poly python tools/prof_ntt.py --n 16384 --limbs 16 --polys 128 --op poly --iters 2 > $O/ncu_poly.log 2>&1
+  echo "ncu_poly=$?" | tee -a $O/status
 fi
 cat $O/status
 tail -3 $O/pytest_gpu.log
