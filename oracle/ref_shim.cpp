@@ -57,6 +57,24 @@ std::vector<std::unique_ptr<NttTables>> make_tables(uint64_t n, const uint64_t* 
   return t;
 }
 
+// CPUs the workers are placed on: the process's affinity mask when the shim
+// is first used (captured once, so nothing that later narrows the calling
+// thread's mask can collapse the placement)
+const std::vector<int>& worker_cpus() {
+  static const std::vector<int> cpus = [] {
+    std::vector<int> v;
+    const char* e = std::getenv("NK_REF_PIN");
+    if (e && e[0] == '0') return v;
+    cpu_set_t allowed;
+    CPU_ZERO(&allowed);
+    if (sched_getaffinity(0, sizeof(allowed), &allowed) == 0)
+      for (int c = 0; c < CPU_SETSIZE; ++c)
+        if (CPU_ISSET(c, &allowed)) v.push_back(c);
+    return v;
+  }();
+  return cpus;
+}
+
 template <class F>
 void parallel_rows(uint64_t rows, int threads, F&& body) {
   if (threads <= 1 || rows <= 1) {
@@ -64,30 +82,26 @@ void parallel_rows(uint64_t rows, int threads, F&& body) {
     return;
   }
   if ((uint64_t)threads > rows) threads = (int)rows;
-  // fixed placement: worker t on the t-th CPU the process may run on, so
-  // repeated measurements see the same thread-to-core mapping
-  cpu_set_t allowed;
-  CPU_ZERO(&allowed);
-  std::vector<int> cpus;
-  static const bool pin = [] {
-    const char* e = std::getenv("NK_REF_PIN");
-    return !(e && e[0] == '0');
-  }();
-  if (pin && sched_getaffinity(0, sizeof(allowed), &allowed) == 0)
-    for (int c = 0; c < CPU_SETSIZE; ++c)
-      if (CPU_ISSET(c, &allowed)) cpus.push_back(c);
+  // fixed placement: worker t on the t-th allowed CPU, so repeated
+  // measurements see the same thread-to-core mapping. Each worker pins
+  // itself: pinning it from here through its handle races with its exit
+  // (an exited thread's handle resolves to the caller, which would pin the
+  // calling thread instead).
+  const std::vector<int>& cpus = worker_cpus();
   std::vector<std::thread> pool;
+  pool.reserve(threads);
   for (int t = 0; t < threads; ++t) {
     const uint64_t r0 = rows * t / threads, r1 = rows * (t + 1) / threads;
-    pool.emplace_back([&, r0, r1] {
+    const int cpu = cpus.empty() ? -1 : cpus[t % cpus.size()];
+    pool.emplace_back([&body, r0, r1, cpu] {
+      if (cpu >= 0) {
+        cpu_set_t one;
+        CPU_ZERO(&one);
+        CPU_SET(cpu, &one);
+        pthread_setaffinity_np(pthread_self(), sizeof(one), &one);
+      }
       for (uint64_t r = r0; r < r1; ++r) body(r);
     });
-    if (!cpus.empty()) {
-      cpu_set_t one;
-      CPU_ZERO(&one);
-      CPU_SET(cpus[t % cpus.size()], &one);
-      pthread_setaffinity_np(pool.back().native_handle(), sizeof(one), &one);
-    }
   }
   for (auto& th : pool) th.join();
 }
