@@ -823,11 +823,14 @@ namespace {
 
 // Pipelined host-buffer execution. The work is cut into chunks of whole
 // units (polynomials for transforms, words for element-wise ops) of about
-// kChunkBytes; chunk i is uploaded, computed and downloaded on internal stream
-// i % 2, so the upload of one chunk, the kernels of another and the download of
-// a third overlap (PCIe is full duplex and the kernels are ~50x faster than
-// the copies). Blocking: returns when the results are in host memory. Work
-// previously queued on the caller's stream is ordered before the chunks.
+// kChunkBytes. Uploads, kernels and downloads run on three internal streams
+// linked by per-slot events, with separate input and output buffers per slot:
+// an upload waits only for the kernel that read its slot's inputs, a kernel
+// for its upload and for the download that emptied its slot's output, so the
+// two DMA directions stream back to back (PCIe is full duplex and the kernels
+// are ~50x faster than the copies). Blocking: returns when the results are in
+// host memory. Work previously queued on the caller's stream is ordered
+// before the chunks.
 constexpr uint64_t kChunkBytes = 16ull << 20;
 constexpr int kMaxDepth = 4;
 
@@ -845,7 +848,7 @@ int host_depth() {
   static const int v = [] {
     const char* e = getenv("NK_HOST_DEPTH");
     const int d = e ? atoi(e) : 0;
-    return d >= 1 && d <= kMaxDepth ? d : 2;
+    return d >= 2 && d <= kMaxDepth ? d : 3;
   }();
   return v;
 }
@@ -959,10 +962,11 @@ bool is_pinned(const void* p) {
 // serialising them costs no throughput, and the ordering event is never
 // re-recorded by one call while another waits on it.
 struct HostPipe {
-  cudaStream_t s[kMaxDepth] = {};
+  cudaStream_t s[3] = {};  // uploads, kernels, downloads
   cudaEvent_t start = nullptr;
   cudaEvent_t up[kMaxDepth] = {};    // slot's uploads done (its input staging may be refilled)
-  cudaEvent_t down[kMaxDepth] = {};  // slot's download done (its output staging may be read)
+  cudaEvent_t kern[kMaxDepth] = {};  // slot's kernels done (its device inputs may be refilled)
+  cudaEvent_t down[kMaxDepth] = {};  // slot's download done (its output buffer / staging may be reused)
   uint64_t* stage[kMaxDepth][3] = {};  // pinned staging: inputs 0..1, output 2
   uint64_t stage_bytes = 0;
   std::mutex mu;
@@ -980,6 +984,7 @@ int host_pipe(int dev, HostPipe** out) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp.start, cudaEventDisableTiming);
     for (int k = 0; k < kMaxDepth && e == cudaSuccess; ++k) {
       e = cudaEventCreateWithFlags(&hp.up[k], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp.kern[k], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&hp.down[k], cudaEventDisableTiming);
     }
     err[dev & 63] = e;
@@ -1004,8 +1009,8 @@ int stage_reserve(HostPipe* hp, uint64_t bytes) {
   return 0;
 }
 
-// fn(device buffers of the chunk (inputs; the first is also the output),
-//    first unit, units in chunk, stream) -> int
+// fn(device input buffers of the chunk, device output buffer, first unit,
+//    units in chunk, stream) -> int
 // Pageable host buffers go through pinned staging: the host copies chunk c's
 // inputs in (and chunk c - depth's result out) with CopyPool while the DMA
 // engines move the pinned chunks, instead of the driver's serial staging.
@@ -1031,23 +1036,56 @@ int run_pipelined(int dev, cudaStream_t user, uint64_t units, uint64_t unit_word
   uint64_t per = host_chunk_bytes() / unit_bytes;
   if (per < 1) per = 1;
   if (per > units) per = units;
-  const uint64_t nchunks = (units + per - 1) / per;
+  // Chunk schedule: full chunks, except that long runs start and end with a
+  // quarter and a half chunk. The first upload and the last download are not
+  // overlapped with anything, so they should be short; every chunk also costs
+  // a fixed ~20-30 us (copy / kernel hand-offs), so the middle stays large.
+  std::vector<uint64_t> first;  // first unit of chunk c, plus a final entry = units
+  {
+    std::vector<uint64_t> sizes;
+    if (per >= 4 && units >= 4 * per) {
+      const uint64_t q4 = per / 4, q2 = per / 2;
+      sizes = {q4, q2};
+      for (uint64_t mid = units - 2 * (q4 + q2); mid;) {
+        const uint64_t c = mid < per ? mid : per;
+        sizes.push_back(c);
+        mid -= c;
+      }
+      sizes.push_back(q2);
+      sizes.push_back(q4);
+    } else {
+      for (uint64_t u = 0; u < units; u += per) sizes.push_back(units - u < per ? units - u : per);
+    }
+    first.push_back(0);
+    for (uint64_t c : sizes) first.push_back(first.back() + c);
+  }
+  const uint64_t nchunks = first.size() - 1;
   const bool any_staged = out_staged || in_staged[0] || in_staged[1];
   if (any_staged)
     if (int rc = stage_reserve(hp, per * unit_bytes)) return rc;
   NK_CUDA(cudaEventRecord(hp->start, user));
+  cudaStream_t su = hp->s[0], sk = hp->s[1], sd = hp->s[2];
   uint64_t* buf[kMaxDepth][2] = {};
+  uint64_t* obuf[kMaxDepth] = {};
   int rc = 0;
   const int nst = static_cast<int>(nchunks < static_cast<uint64_t>(host_depth()) ? nchunks : host_depth());
-  for (int k = 0; k < nst && !rc; ++k) {
-    cudaError_t e = cudaStreamWaitEvent(hp->s[k], hp->start, 0);
-    for (int j = 0; j < nin && e == cudaSuccess; ++j)
-      e = cudaMallocAsync(&buf[k][j], per * unit_bytes, hp->s[k]);
+  {
+    cudaError_t e = cudaSuccess;
+    for (cudaStream_t st : {su, sk, sd})
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st, hp->start, 0);
+    for (int k = 0; k < nst && e == cudaSuccess; ++k) {
+      for (int j = 0; j < nin && e == cudaSuccess; ++j) e = cudaMallocAsync(&buf[k][j], per * unit_bytes, su);
+      if (e == cudaSuccess) e = cudaMallocAsync(&obuf[k], per * unit_bytes, su);
+    }
+    // the kernel and download streams use the buffers after su allocated them
+    if (e == cudaSuccess) e = cudaEventRecord(hp->up[0], su);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sk, hp->up[0], 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, hp->up[0], 0);
     if (e != cudaSuccess) rc = cuda_fail(e, "host pipeline buffers");
   }
   auto chunk_of = [&](uint64_t c, uint64_t& off, uint64_t& bytes, uint64_t& u0, uint64_t& nu) {
-    u0 = c * per;
-    nu = (u0 + per <= units) ? per : units - u0;
+    u0 = first[c];
+    nu = first[c + 1] - u0;
     off = u0 * unit_words;
     bytes = nu * unit_bytes;
   };
@@ -1063,16 +1101,18 @@ int run_pipelined(int dev, cudaStream_t user, uint64_t units, uint64_t unit_word
   };
   for (uint64_t c = 0; c < nchunks && !rc; ++c) {
     const int k = static_cast<int>(c % nst);
+    const bool reuse = c >= static_cast<uint64_t>(nst);  // slot k held chunk c - nst
     uint64_t off, bytes, u0, nu;
     chunk_of(c, off, bytes, u0, nu);
-    if (c >= static_cast<uint64_t>(nst)) {
+    if (reuse) {
       if ((rc = drain(c - nst))) break;  // the slot's previous result is out of its staging
       if (in_staged[0] || in_staged[1]) {
         const cudaError_t e = cudaEventSynchronize(hp->up[k]);  // its previous uploads are done
         if (e != cudaSuccess) { rc = cuda_fail(e, "cudaEventSynchronize(host pipeline)"); break; }
       }
     }
-    cudaError_t e = cudaSuccess;
+    // uploads: after the kernels that read the slot's previous inputs
+    cudaError_t e = reuse ? cudaStreamWaitEvent(su, hp->kern[k], 0) : cudaSuccess;
     for (int j = 0; j < nin && e == cudaSuccess; ++j) {
       if (!in[j]) continue;
       const uint64_t* src = in[j] + off;
@@ -1080,23 +1120,42 @@ int run_pipelined(int dev, cudaStream_t user, uint64_t units, uint64_t unit_word
         CopyPool::get().copy(hp->stage[k][j], src, bytes);
         src = hp->stage[k][j];
       }
-      e = cudaMemcpyAsync(buf[k][j], src, bytes, cudaMemcpyHostToDevice, hp->s[k]);
+      e = cudaMemcpyAsync(buf[k][j], src, bytes, cudaMemcpyHostToDevice, su);
     }
-    if (e == cudaSuccess) e = cudaEventRecord(hp->up[k], hp->s[k]);
+    if (e == cudaSuccess) e = cudaEventRecord(hp->up[k], su);
     if (e != cudaSuccess) { rc = cuda_fail(e, "cudaMemcpyAsync(H2D)"); break; }
-    if ((rc = fn(buf[k], u0, nu, hp->s[k]))) break;
-    e = cudaMemcpyAsync(out_staged ? hp->stage[k][2] : hout + off, buf[k][0], bytes, cudaMemcpyDeviceToHost,
-                        hp->s[k]);
-    if (e == cudaSuccess) e = cudaEventRecord(hp->down[k], hp->s[k]);
+    // kernels: after the uploads, and after the download that emptied the slot's output
+    e = cudaStreamWaitEvent(sk, hp->up[k], 0);
+    if (e == cudaSuccess && reuse) e = cudaStreamWaitEvent(sk, hp->down[k], 0);
+    if (e != cudaSuccess) { rc = cuda_fail(e, "cudaStreamWaitEvent(host pipeline)"); break; }
+    if ((rc = fn(buf[k], obuf[k], u0, nu, sk))) break;
+    e = cudaEventRecord(hp->kern[k], sk);
+    // download: after the kernels
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, hp->kern[k], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out_staged ? hp->stage[k][2] : hout + off, obuf[k], bytes, cudaMemcpyDeviceToHost, sd);
+    if (e == cudaSuccess) e = cudaEventRecord(hp->down[k], sd);
     if (e != cudaSuccess) rc = cuda_fail(e, "cudaMemcpyAsync(D2H)");
   }
   if (!rc)
     for (uint64_t c = nchunks > static_cast<uint64_t>(nst) ? nchunks - nst : 0; c < nchunks && !rc; ++c)
       rc = drain(c);
-  for (int k = 0; k < nst; ++k) {
-    for (int j = 0; j < nin; ++j)
-      if (buf[k][j]) cudaFreeAsync(buf[k][j], hp->s[k]);
-    cudaError_t e = cudaStreamSynchronize(hp->s[k]);
+  // every use of the buffers precedes the last download in sd's order only
+  // through events; join the other streams into sd before freeing
+  {
+    cudaError_t e = cudaEventRecord(hp->up[0], su);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, hp->up[0], 0);
+    if (e == cudaSuccess) e = cudaEventRecord(hp->kern[0], sk);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sd, hp->kern[0], 0);
+    for (int k = 0; k < nst; ++k) {
+      for (int j = 0; j < nin; ++j)
+        if (buf[k][j]) cudaFreeAsync(buf[k][j], sd);
+      if (obuf[k]) cudaFreeAsync(obuf[k], sd);
+    }
+    for (cudaStream_t st : {su, sk, sd}) {
+      const cudaError_t e2 = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) e = e2;
+    }
     if (!rc && e != cudaSuccess) rc = cuda_fail(e, "cudaStreamSynchronize(host pipeline)");
   }
   return rc;
@@ -1113,10 +1172,10 @@ int ntt_host(bool fwd, const nk_plan* p, uint64_t* res, const uint64_t* op, uint
   DeviceScope ds;
   if (int rc = ds.enter(p->device)) return rc;
   return run_pipelined(p->device, S(stream), npolys, static_cast<uint64_t>(nlimbs) * p->n, {op}, res,
-                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
+                       [&](uint64_t* const* d, uint64_t* o, uint64_t, uint64_t nu, cudaStream_t st) {
                          const uint32_t np = static_cast<uint32_t>(nu);
-                         return fwd ? nk_ntt_forward(p, d[0], d[0], limb0, nlimbs, np, fin, fout, st)
-                                    : nk_ntt_inverse(p, d[0], d[0], limb0, nlimbs, np, fin, fout, st);
+                         return fwd ? nk_ntt_forward(p, o, d[0], limb0, nlimbs, np, fin, fout, st)
+                                    : nk_ntt_inverse(p, o, d[0], limb0, nlimbs, np, fin, fout, st);
                        });
 }
 
@@ -1158,9 +1217,9 @@ int nk_poly_mult_mod_host(const nk_plan* p, uint64_t* res, const uint64_t* f, co
   DeviceScope ds;
   if (int rc = ds.enter(p->device)) return rc;
   return run_pipelined(p->device, S(stream), npolys, static_cast<uint64_t>(nlimbs) * p->n, {f, g}, res,
-                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
-                         return nk_poly_mult_mod(p, d[0], d[0], d[1], limb0, nlimbs,
-                                                 static_cast<uint32_t>(nu), st);
+                       [&](uint64_t* const* d, uint64_t* o, uint64_t, uint64_t nu, cudaStream_t st) {
+                         return nk_poly_mult_mod(p, o, d[0], d[1], limb0, nlimbs, static_cast<uint32_t>(nu),
+                                                 st);
                        });
 }
 
@@ -1174,8 +1233,8 @@ int eltwise_mult_host(uint64_t* res, const uint64_t* a, const uint64_t* b, uint6
   DeviceScope ds;
   if (int rc = ds.enter(device)) return rc;
   return run_pipelined(device, S(stream), n, 1, {a, b}, res,
-                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
-                         return eltwise_mult_path(d[0], d[0], d[1], nu, q, fin, path, st);
+                       [&](uint64_t* const* d, uint64_t* o, uint64_t, uint64_t nu, cudaStream_t st) {
+                         return eltwise_mult_path(o, d[0], d[1], nu, q, fin, path, st);
                        });
 }
 }  // namespace
@@ -1189,8 +1248,8 @@ int nk_eltwise_add_mod_host(uint64_t* res, const uint64_t* a, const uint64_t* b,
   DeviceScope ds;
   if (int rc = ds.enter(device)) return rc;
   return run_pipelined(device, S(stream), n, 1, {a, b}, res,
-                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
-                         return nk_eltwise_add_mod(d[0], d[0], d[1], nu, q, st);
+                       [&](uint64_t* const* d, uint64_t* o, uint64_t, uint64_t nu, cudaStream_t st) {
+                         return nk_eltwise_add_mod(o, d[0], d[1], nu, q, st);
                        });
 }
 
@@ -1203,8 +1262,8 @@ int nk_eltwise_neg_mod_host(uint64_t* res, const uint64_t* a, uint64_t n, uint64
   DeviceScope ds;
   if (int rc = ds.enter(device)) return rc;
   return run_pipelined(device, S(stream), n, 1, {a}, res,
-                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
-                         return nk_eltwise_neg_mod(d[0], d[0], nu, q, st);
+                       [&](uint64_t* const* d, uint64_t* o, uint64_t, uint64_t nu, cudaStream_t st) {
+                         return nk_eltwise_neg_mod(o, d[0], nu, q, st);
                        });
 }
 
@@ -1231,9 +1290,8 @@ int nk_eltwise_fma_mod_host(uint64_t* res, const uint64_t* a, uint64_t y, const 
   DeviceScope ds;
   if (int rc = ds.enter(device)) return rc;
   return run_pipelined(device, S(stream), n, 1, {a, z}, res,
-                       [&](uint64_t* const* d, uint64_t, uint64_t nu, cudaStream_t st) {
-                         return nk_eltwise_fma_mod(d[0], d[0], y, z ? d[1] : nullptr, nu, q, fin, bit_shift,
-                                                   st);
+                       [&](uint64_t* const* d, uint64_t* o, uint64_t, uint64_t nu, cudaStream_t st) {
+                         return nk_eltwise_fma_mod(o, d[0], y, z ? d[1] : nullptr, nu, q, fin, bit_shift, st);
                        });
 }
 

@@ -422,6 +422,27 @@ def test_host_pipeline_multi_chunk(nk, oracle):
     assert np.array_equal(plan.inverse(None, f, 1, 1), x)
 
 
+def test_host_pipeline_ramped_chunks(nk, oracle):
+    """Long host-buffer runs (at least four full chunks) start and end with a
+    quarter and a half chunk: results must match, for words and for whole
+    polynomials, with an odd remainder in the middle."""
+    from primes import cfg2_modulus, largest_ntt_primes
+
+    q = cfg2_modulus()
+    n = 9 * (1 << 21) + 4321  # 4.5 full 16 MiB chunks of words
+    a = oracle.mt19937_64(311, n, q)
+    b = oracle.mt19937_64(312, n, q)
+    assert np.array_equal(nk.eltwise_mult_mod(None, a, b, q, 1), oracle.eltwise_mult_mod(a, b, q, 1))
+    nn = 16384
+    moduli = largest_ntt_primes(50, nn, 8)  # 1 MiB polynomials: 16 per full chunk
+    plan = nk.RnsNtt(nn, moduli)
+    npolys = 71
+    x = np.concatenate([oracle.mt19937_64(500 + r, nn, moduli[r % 8]) for r in range(8 * npolys)])
+    f = plan.forward(None, x, 1, 1)
+    assert np.array_equal(f, oracle.forward(nn, moduli, x, 1, 1, threads=8))
+    assert np.array_equal(plan.inverse(None, f, 1, 1), x)
+
+
 def test_eltwise_writes_stay_in_bounds(nk, oracle):
     """Guard words around element-wise and poly-multiply results (see
     test_gpu_ntt.test_writes_stay_in_bounds), odd lengths and offsets."""
