@@ -48,7 +48,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 METRIC = "fwd/inv NTT Mcoeff/s (N=16384, batched limbs)"
-FWD_KERNEL = "ntt_pair14<Arith52S,fwd>"  # the forward's only launch at cfg3
+FWD_KERNEL = "ntt_grp14<Arith52S,fwd>"  # the forward's only launch at cfg3
 # FP64 operations per butterfly of the signed canonical arithmetic
 # (modmath.cuh Arith52S: 6 for the Shoup product, 2 output adds, 1 for the
 # conditional subtraction), the floor the transform kernels are bound by

@@ -139,6 +139,11 @@ struct nk_plan {
   uint64_t* tw8_inv = nullptr;
   uint64_t* twl8_fwd = nullptr;  // [limb][n] low-table order
   uint64_t* twl8_inv = nullptr;
+  // the low tables in the group-exchange kernels' thread order (NttArgs::twg)
+  ulonglong2* twg_fwd = nullptr;
+  ulonglong2* twg_inv = nullptr;
+  uint64_t* twg8_fwd = nullptr;
+  uint64_t* twg8_inv = nullptr;
   nk::LimbConst* lc = nullptr;   // [limb]
   nk::MultConst* mc[3] = {nullptr, nullptr, nullptr};  // fin = 1, 2, 4
 };
@@ -221,6 +226,8 @@ int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64
   a.twl = fwd ? p->twl_fwd : p->twl_inv;
   a.tw8 = fwd ? p->tw8_fwd : p->tw8_inv;
   a.twl8 = fwd ? p->twl8_fwd : p->twl8_inv;
+  a.twg = fwd ? p->twg_fwd : p->twg_inv;
+  a.twg8 = fwd ? p->twg8_fwd : p->twg8_inv;
   a.lc = p->lc;
   a.n = p->n;
   a.logn = p->logn;
@@ -467,6 +474,10 @@ void nk_plan_destroy(nk_plan* p) {
   cudaFree(p->tw8_inv);
   cudaFree(p->twl8_fwd);
   cudaFree(p->twl8_inv);
+  cudaFree(p->twg_fwd);
+  cudaFree(p->twg_inv);
+  cudaFree(p->twg8_fwd);
+  cudaFree(p->twg8_inv);
   cudaFree(p->lc);
   for (auto* m : p->mc) cudaFree(m);
   cudaSetDevice(cur);
@@ -493,6 +504,8 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
   p->logn = tabs[0].logn;
   p->nlimbs = nlimbs;
   std::vector<ulonglong2> hf(n * nlimbs), hi(n * nlimbs), hlf(n * nlimbs), hli(n * nlimbs);
+  const bool blocks = n >= (uint64_t{1} << 14);
+  std::vector<ulonglong2> hgf(blocks ? n * nlimbs : 0), hgi(blocks ? n * nlimbs : 0);
   std::vector<nk::LimbConst> hl(nlimbs);
   std::vector<nk::MultConst> hm[3];
   for (auto& v : hm) v.resize(nlimbs);
@@ -519,6 +532,17 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
               hlf[l * n + dst] = hf[l * n + src];
               hli[l * n + dst] = hi[l * n + src];
             }
+      // thread order of the group-exchange kernels' low pass (forward P3, inverse P1)
+      for (uint64_t blk = 0; blk < (n >> 14); ++blk)
+        for (int b = 0; b < 5; ++b)
+          for (int d = 0; d < (1 << (4 - b)); ++d)
+            for (uint32_t t = 0; t < 512; ++t) {
+              const uint64_t dst = l * n + (blk << 14) + nk::low_index(b, d, t);
+              const uint32_t jf = nk::GrpMap<true>::jt3(t >> 5, t & 31u) >> 5;
+              const uint32_t ji = nk::GrpMap<false>::jt1(t >> 5, t & 31u) >> 5;
+              hgf[dst] = hlf[l * n + (blk << 14) + nk::low_index(b, d, jf)];
+              hgi[dst] = hli[l * n + (blk << 14) + nk::low_index(b, d, ji)];
+            }
     }
     // -q modulo 2^64 (the 52-bit negated modulus of ntt.hpp:85-92 agrees modulo 2^52,
     // see modmath.cuh)
@@ -542,6 +566,9 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
       (e = cudaMalloc(&p->twl_inv, hli.size() * sizeof(ulonglong2))) ||
       (e = cudaMalloc(&p->tw8_fwd, hf.size() * 8)) || (e = cudaMalloc(&p->tw8_inv, hi.size() * 8)) ||
       (e = cudaMalloc(&p->twl8_fwd, hlf.size() * 8)) || (e = cudaMalloc(&p->twl8_inv, hli.size() * 8)) ||
+      (blocks && ((e = cudaMalloc(&p->twg_fwd, hgf.size() * sizeof(ulonglong2))) ||
+                  (e = cudaMalloc(&p->twg_inv, hgi.size() * sizeof(ulonglong2))) ||
+                  (e = cudaMalloc(&p->twg8_fwd, hgf.size() * 8)) || (e = cudaMalloc(&p->twg8_inv, hgi.size() * 8)))) ||
       (e = cudaMalloc(&p->lc, hl.size() * sizeof(nk::LimbConst))))
     return cleanup(cuda_fail(e, "cudaMalloc(plan tables)"));
   for (int f = 0; f < 3; ++f)
@@ -559,9 +586,9 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
   put(p->tw_fwd, hf.data(), hf.size() * sizeof(ulonglong2));
   put(p->tw_inv, hi.data(), hi.size() * sizeof(ulonglong2));
   // the w halves of the beta = 2^52 entries (double bits; other limbs' words are unused)
-  std::vector<uint64_t> h8[4];
-  const std::vector<ulonglong2>* src8[4] = {&hf, &hi, &hlf, &hli};
-  for (int i = 0; i < 4; ++i) {
+  std::vector<uint64_t> h8[6];
+  const std::vector<ulonglong2>* src8[6] = {&hf, &hi, &hlf, &hli, &hgf, &hgi};
+  for (int i = 0; i < 6; ++i) {
     h8[i].resize(src8[i]->size());
     for (size_t k = 0; k < h8[i].size(); ++k) h8[i][k] = (*src8[i])[k].x;
   }
@@ -569,6 +596,12 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
   put(p->tw8_inv, h8[1].data(), h8[1].size() * 8);
   put(p->twl8_fwd, h8[2].data(), h8[2].size() * 8);
   put(p->twl8_inv, h8[3].data(), h8[3].size() * 8);
+  if (blocks) {
+    put(p->twg_fwd, hgf.data(), hgf.size() * sizeof(ulonglong2));
+    put(p->twg_inv, hgi.data(), hgi.size() * sizeof(ulonglong2));
+    put(p->twg8_fwd, h8[4].data(), h8[4].size() * 8);
+    put(p->twg8_inv, h8[5].data(), h8[5].size() * 8);
+  }
   put(p->lc, hl.data(), hl.size() * sizeof(nk::LimbConst));
   for (int f = 0; f < 3; ++f) put(p->mc[f], hm[f].data(), nlimbs * sizeof(nk::MultConst));
   const cudaError_t es = cudaStreamSynchronize(up);
@@ -679,7 +712,7 @@ int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const u
     pa.a.out = res;
     pa.a.in = f;
     pa.a.tw8 = p->tw8_fwd;
-    pa.a.twl8 = p->twl8_fwd;
+    pa.a.twg8 = p->twg8_fwd;
     pa.a.lc = p->lc;
     pa.a.n = p->n;
     pa.a.logn = p->logn;
@@ -690,7 +723,7 @@ int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const u
     pa.a.fin = 1;
     pa.a.fout = 1;
     pa.itw8 = p->tw8_inv;
-    pa.itwl8 = p->twl8_inv;
+    pa.itwg8 = p->twg8_inv;
     return nk::rt::run_poly_mul14(pa, f, g, st);
   }
   uint64_t* gh = nullptr;

@@ -39,7 +39,7 @@ int encode_fn(EncodeTiledFn* out) {
   return 0;
 }
 
-enum MapKind { kRowMap = 0, kSuperlineMap = 1, kOutMap = 2 };
+enum MapKind { kRowMap = 0, kSuperlineMap = 1, kOutMap = 2, kGrpOutMap = 3 };
 
 // A tensor map is a pure function of (kind, base, words): the last few are
 // cached per thread, so repeated calls on the same buffers (a serving loop,
@@ -80,6 +80,16 @@ int make_map(CUtensorMap* map, MapKind kind, const uint64_t* base, uint64_t word
     const cuuint32_t estr[3] = {1, 1, 1};
     r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (kind == kGrpOutMap) {
+    // 5D view [words/512][4 (j7, j8)][4 (j5, j6)][2 halves][16 words] (128B swizzle),
+    // boxes 16 x 1 x 1 x 1 x 8: one half of the runs j5j6 of 8 consecutive
+    // 512-word pieces = 8 rows of a warp's output image in ntt_grp14
+    const cuuint64_t dims[5] = {16, 2, 4, 4, words / 512};
+    const cuuint64_t strides[4] = {128, 256, 1024, 4096};
+    const cuuint32_t box[5] = {16, 1, 1, 1, 8};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else {
     // 3D view [words/32][2][16] (128B swizzle), boxes 16 x 1 x 32: one half of
     // 32 consecutive 32-word runs = one warp's output round of ntt_pair14
@@ -117,13 +127,15 @@ int set_smem_once(size_t bytes) {
 }
 
 // group-exchange kernel (ntt_grp.cuh): persistent, one 512-thread CTA per SM
-template <auto KERN>
+template <auto KERN, bool FWD>
 int launch_grp_k(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
-  CUtensorMap map;
+  CUtensorMap map, omap;
   if (int rc = make_map(&map, kRowMap, a.in, buf_words)) return rc;
+  // the forward stores its result by TMA (the inverse with plain stores: omap unused)
+  if (int rc = FWD ? make_map(&omap, kGrpOutMap, a.out, buf_words) : (omap = map, 0)) return rc;
   if (int rc = set_smem_once<KERN>(kGrpSmemBytes)) return rc;
   const uint64_t g = nitems < static_cast<uint64_t>(sm_count()) ? nitems : sm_count();
-  KERN<<<static_cast<unsigned>(g), 512, kGrpSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));
+  KERN<<<static_cast<unsigned>(g), 512, kGrpSmemBytes, st>>>(map, omap, a, static_cast<uint32_t>(nitems));
   launches++;
   NK_CUDA(cudaGetLastError());
   return 0;
@@ -132,8 +144,8 @@ int launch_grp_k(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStre
 template <class A, bool FWD, bool IL>
 int launch_grp_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
   if constexpr (!FWD)
-    if (a.logn > 14) return launch_grp_k<ntt_grp14<A, FWD, IL, true>>(a, nitems, buf_words, st);
-  return launch_grp_k<ntt_grp14<A, FWD, IL>>(a, nitems, buf_words, st);
+    if (a.logn > 14) return launch_grp_k<ntt_grp14<A, FWD, IL, true>, FWD>(a, nitems, buf_words, st);
+  return launch_grp_k<ntt_grp14<A, FWD, IL>, FWD>(a, nitems, buf_words, st);
 }
 
 // CTA-pair kernel (ntt_pair.cuh): persistent, one cluster of 2 per block in
@@ -182,12 +194,12 @@ int launch_pair_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStr
 
 template <class A, bool FWD>
 int launch_tma(const NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm, cudaStream_t st) {
-  // measured on B200 (cfg3 / cfg4): the CTA-pair kernel is the faster forward
-  // (228 / 359 us; the group kernel 228 / 396), the group-exchange kernel the
-  // faster inverse (227 / 346 us; the pair inverse 227 / 398: it exchanges
-  // late, so its next TMA overlaps less compute); the fused product lives in
-  // the pair forward only
-  const bool pair = a.mulb || (block_kernel < 0 ? FWD : block_kernel == 0);
+  // measured on B200 (cfg3 / cfg4, forward / inverse): with the low tables in
+  // thread order the group-exchange kernel is the faster one in both
+  // directions (220 / 217 us against the CTA-pair kernel's 228 / 229 us on
+  // cfg3; 363 / 348 us against 363 / 384 us on cfg4); the three-launch
+  // poly_mult_mod's fused product lives in the pair forward only
+  const bool pair = a.mulb || block_kernel == 0;
   if (pair)
     return iltm ? launch_pair_t<A, FWD, true>(a, nitems, buf_words, st)
                 : launch_pair_t<A, FWD, false>(a, nitems, buf_words, st);

@@ -160,7 +160,9 @@ struct LimbConstDev {
   // folded last stage of canonical inverses (inv_fold)
   uint64_t nw, nwp;
   uint64_t fourq;  // 4q (ArithIntL)
+  uint64_t pad2[2];  // 128 bytes: one bulk copy into shared memory (ntt_grp14)
 };
+static_assert(sizeof(LimbConstDev) == 128, "LimbConstDev is copied as one 128-byte bulk transfer");
 
 template <int BS>
 struct ArithInt {  // integer Shoup products, beta = 2^BS (52 or 64)

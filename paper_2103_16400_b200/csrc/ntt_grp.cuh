@@ -47,8 +47,9 @@ namespace nk {
 
 constexpr uint32_t kGrpExBytes = 4u * 16384u;  // E: 4 groups x 2048 words
 constexpr uint32_t kGrpOutBytes = 16u * 2048u;  // forward output images: 2 KiB per warp
-// [1 KiB align][staging 128 KiB][E 64 KiB][O 32 KiB][mbarriers: full, ex1 reads x4, ex2 reads x4][counter]
-constexpr size_t kGrpSmemBytes = 1024 + kStageBytes + kGrpExBytes + kGrpOutBytes + 16 * 8;
+// [1 KiB align][staging 128 KiB][E 64 KiB][O 32 KiB][limb constants x2]
+// [mbarriers: full, ex1 reads x4, ex2 reads x4][counter][output images read x4]
+constexpr size_t kGrpSmemBytes = 1024 + kStageBytes + kGrpExBytes + kGrpOutBytes + 2 * sizeof(LimbConst) + 16 * 8;
 
 __device__ __forceinline__ void named_sync128(uint32_t id) {
   asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory");
@@ -63,26 +64,26 @@ template <bool FWD>
 struct GrpMap;
 template <>
 struct GrpMap<true> {
-  __device__ static uint32_t jt1(uint32_t w, uint32_t l) {
+  __host__ __device__ static constexpr uint32_t jt1(uint32_t w, uint32_t l) {
     return (l & 1u) | (((l >> 4) & 1u) << 1) | ((w >> 2) << 2) | (((l >> 1) & 7u) << 4) | ((w & 3u) << 7);
   }
-  __device__ static uint32_t jt2(uint32_t w, uint32_t l) {
+  __host__ __device__ static constexpr uint32_t jt2(uint32_t w, uint32_t l) {
     return (l & 1u) | (((l >> 4) & 1u) << 1) | ((w >> 2) << 2) | (((l >> 1) & 7u) << 9) | ((w & 3u) << 12);
   }
-  __device__ static uint32_t jt3(uint32_t w, uint32_t l) {
+  __host__ __device__ static constexpr uint32_t jt3(uint32_t w, uint32_t l) {
     return (((l >> 3) & 1u) << 5) | (((l >> 4) & 1u) << 6) | ((w >> 2) << 7) | ((l & 7u) << 9) | ((w & 3u) << 12);
   }
 };
 template <>
 struct GrpMap<false> {
-  __device__ static uint32_t jt1(uint32_t w, uint32_t l) {
+  __host__ __device__ static constexpr uint32_t jt1(uint32_t w, uint32_t l) {
     return ((l & 1u) << 5) | (((l >> 1) & 1u) << 6) | (((l >> 2) & 1u) << 13) | (((l >> 3) & 1u) << 9) |
            (((l >> 4) & 1u) << 10) | ((w & 3u) << 7) | ((w >> 2) << 11);
   }
-  __device__ static uint32_t jt2(uint32_t w, uint32_t l) {
+  __host__ __device__ static constexpr uint32_t jt2(uint32_t w, uint32_t l) {
     return (l & 7u) | (((l >> 3) & 1u) << 9) | (((l >> 4) & 1u) << 10) | ((w & 3u) << 3) | ((w >> 2) << 11);
   }
-  __device__ static uint32_t jt3(uint32_t w, uint32_t l) {
+  __host__ __device__ static constexpr uint32_t jt3(uint32_t w, uint32_t l) {
     return (l & 7u) | (((l >> 3) & 1u) << 5) | (((l >> 4) & 1u) << 6) | ((w & 3u) << 3) | ((w >> 2) << 7);
   }
 };
@@ -159,13 +160,12 @@ __device__ __forceinline__ void p1_read(uint64_t (&v)[32], const uint8_t* St, ui
   }
 }
 
-// Exchange 1: in place, within the group's staging slots. Waits (bar_r1g,
-// `parity`) until every warp of the group has read its P1 words, writes this
-// thread's words to their exchange slots, syncs the group, reads the P2 words.
+// Exchange 1: in place, within the group's staging slots: wait (bar_r1g,
+// `parity`) until every warp of the group has read its P1 words, write this
+// thread's words to their exchange slots (ex1_write), sync the group, read the
+// P2 words (ex1_read). The kernels interleave the pieces with arithmetic.
 template <bool FWD>
-__device__ __forceinline__ void ex1(uint64_t (&v)[32], uint8_t* St, uint32_t jt1, uint32_t q2, uint64_t* bar_r1g,
-                                    uint32_t parity, uint32_t g1) {
-  mbar_wait(bar_r1g, parity);
+__device__ __forceinline__ void ex1_write(const uint64_t (&v)[32], uint8_t* St, uint32_t jt1) {
   if (FWD) {
     // swz_off(ex1_perm(jt1 | r << 9)) = (swz_off(jt1) ^ ((r & 7) * 0x90)) + r * 4096
     const uint32_t b1 = swz_off(jt1);
@@ -184,7 +184,9 @@ __device__ __forceinline__ void ex1(uint64_t (&v)[32], uint8_t* St, uint32_t jt1
         *reinterpret_cast<ulonglong2*>(St + (wh ^ (cc << 4))) = make_ulonglong2(v[16 * h + 2 * cc], v[16 * h + 2 * cc + 1]);
     }
   }
-  named_sync128(1 + g1);
+}
+template <bool FWD>
+__device__ __forceinline__ void ex1_read(uint64_t (&v)[32], const uint8_t* St, uint32_t q2) {
 #pragma unroll
   for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -194,6 +196,14 @@ __device__ __forceinline__ void ex1(uint64_t (&v)[32], uint8_t* St, uint32_t jt1
       const uint32_t hi = FWD ? (((g + 2 * r) >> 3) << 10) : (((r >> 2) << 10) | (g << 16));
       v[16 * g + r] = *reinterpret_cast<const uint64_t*>(St + ((q2 ^ (y * 0x90u)) + hi));
     }
+}
+template <bool FWD>
+__device__ __forceinline__ void ex1(uint64_t (&v)[32], uint8_t* St, uint32_t jt1, uint32_t q2, uint64_t* bar_r1g,
+                                    uint32_t parity, uint32_t g1) {
+  mbar_wait(bar_r1g, parity);
+  ex1_write<FWD>(v, St, jt1);
+  named_sync128(1 + g1);
+  ex1_read<FWD>(v, St, q2);
 }
 
 // This warp has consumed the staging buffer; the last of the 16 warps (shared
@@ -212,9 +222,39 @@ __device__ __forceinline__ void staging_consumed(uint32_t* cnt, uint32_t l, F&& 
 }
 
 // Exchange 2: through the group's slice Eg of E, two rounds on the register
-// bit common to P2 and P3 (forward bit 4, inverse bit 13). Waits (bar_r2g,
-// `parity`) for the previous exchange's last-round reads; arrives when this
-// warp's last-round reads are done.
+// bit common to P2 and P3 (forward bit 4, inverse bit 13): round h moves
+// registers 16h .. 16h + 15 (ex2_write, group sync, ex2_read; the round-0
+// reads of every warp of the group precede the round-1 writes). Waits
+// (bar_r2g, `parity`) for the previous exchange's last-round reads; arrives
+// when this warp's last-round reads are done.
+template <bool FWD>
+__device__ __forceinline__ void ex2_write(const uint64_t (&v)[32], uint8_t* Eg, uint32_t e2w, int h) {
+  // ex2_off(jt2 | r << 5): forward e2w + r * 128; inverse (e2w ^ ((r & 1) << 6)) + (r >> 1) * 128
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const uint32_t off = FWD ? (e2w + r * 128) : ((e2w ^ ((r & 1) << 6)) + (r >> 1) * 128);
+    *reinterpret_cast<uint64_t*>(Eg + off) = v[16 * h + r];
+  }
+}
+template <bool FWD>
+__device__ __forceinline__ void ex2_read(uint64_t (&v)[32], const uint8_t* Eg, uint32_t e2r, int h) {
+  if (FWD) {
+    // P3 round h: the 16 contiguous words j0..j3 (bit 4 = h) as 16-byte
+    // chunks, ex2_off(jt3 | 2cc) = e2r ^ (cc << 4)
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Eg + (e2r ^ (cc << 4)));
+      v[16 * h + 2 * cc] = p.x;
+      v[16 * h + 2 * cc + 1] = p.y;
+    }
+  } else {
+    // P3 round h: registers 16h + r hold j = jt3 | (16h + r) << 9 (bit 13 = h),
+    // ex2_off(jt3 | r << 9) = (e2r ^ ((r & 1) << 6)) + r * 1024
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      v[16 * h + r] = *reinterpret_cast<const uint64_t*>(Eg + ((e2r ^ ((r & 1) << 6)) + r * 1024));
+  }
+}
 template <bool FWD>
 __device__ __forceinline__ void ex2(uint64_t (&v)[32], uint8_t* Eg, uint32_t e2w, uint32_t e2r, uint64_t* bar_r2g,
                                     uint32_t parity, uint32_t g2, uint32_t l) {
@@ -222,29 +262,9 @@ __device__ __forceinline__ void ex2(uint64_t (&v)[32], uint8_t* Eg, uint32_t e2w
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     if (h == 1) named_sync128(5 + g2);  // round-0 reads done before round-1 writes
-    // ex2_off(jt2 | r << 5): forward e2w + r * 128; inverse (e2w ^ ((r & 1) << 6)) + (r >> 1) * 128
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      const uint32_t off = FWD ? (e2w + r * 128) : ((e2w ^ ((r & 1) << 6)) + (r >> 1) * 128);
-      *reinterpret_cast<uint64_t*>(Eg + off) = v[16 * h + r];
-    }
+    ex2_write<FWD>(v, Eg, e2w, h);
     named_sync128(5 + g2);
-    if (FWD) {
-      // P3 round h: the 16 contiguous words j0..j3 (bit 4 = h) as 16-byte
-      // chunks, ex2_off(jt3 | 2cc) = e2r ^ (cc << 4)
-#pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(Eg + (e2r ^ (cc << 4)));
-        v[16 * h + 2 * cc] = p.x;
-        v[16 * h + 2 * cc + 1] = p.y;
-      }
-    } else {
-      // P3 round h: registers 16h + r hold j = jt3 | (16h + r) << 9 (bit 13 = h),
-      // ex2_off(jt3 | r << 9) = (e2r ^ ((r & 1) << 6)) + r * 1024
-#pragma unroll
-      for (int r = 0; r < 16; ++r)
-        v[16 * h + r] = *reinterpret_cast<const uint64_t*>(Eg + ((e2r ^ ((r & 1) << 6)) + r * 1024));
-    }
+    ex2_read<FWD>(v, Eg, e2r, h);
   }
   __syncwarp();
   if (l == 0) mbar_arrive_local(bar_r2g);
@@ -277,9 +297,24 @@ __device__ __forceinline__ void fwd_store(const uint64_t (&v)[32], uint8_t* Ow, 
 
 }  // namespace grp
 
+#ifndef NK_GRP_PIPE
+#define NK_GRP_PIPE 1
+#endif
+
+#if defined(NK_DBG_TIMELINE)  // perf experiment: per-warp phase timestamps into a.dbg (tools/timeline.py --grp)
+#define NK_GTS(id)                                                                             \
+  do {                                                                                         \
+    if (a.dbg && l == 0 && it_ < 16)                                                           \
+      a.dbg[((static_cast<uint64_t>(blockIdx.x) * 16 + w) * 16 + it_) * 16 + (id)] = clock64(); \
+  } while (0)
+#else
+#define NK_GTS(id) ((void)0)
+#endif
+
 template <class A, bool FWD, bool ILTM0, bool LONG = false>
 __global__ void __launch_bounds__(512, 1)
-    ntt_grp14(const __grid_constant__ CUtensorMap tin, NttArgs a, uint32_t nitems) {
+    ntt_grp14(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, NttArgs a,
+              uint32_t nitems) {
   using P1 = typename std::conditional<FWD, PassD<9, 5, -1>, PassD<0, 5, -1>>::type;
   using P2 = typename std::conditional<FWD, PassD<5, 4, 4>, PassD<5, 4, 13>>::type;
   using P3 = typename std::conditional<FWD, PassD<0, 5, -1>, PassD<9, 5, -1>>::type;
@@ -288,10 +323,15 @@ __global__ void __launch_bounds__(512, 1)
   uint8_t* St = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);  // staging, 128B-swizzled lines
   uint8_t* E = St + kStageBytes;
   uint8_t* O = E + kGrpExBytes;
-  uint64_t* bar_full = reinterpret_cast<uint64_t*>(O + kGrpOutBytes);
+  // the block's limb constants arrive with its words (one more bulk copy on
+  // bar_full), alternating between two slots: no global-load latency at the
+  // start of a block, and the fields are read from shared memory where used
+  const LimbConst* Cs = reinterpret_cast<const LimbConst*>(O + kGrpOutBytes);
+  uint64_t* bar_full = reinterpret_cast<uint64_t*>(O + kGrpOutBytes + 2 * sizeof(LimbConst));
   uint64_t* bar_r1 = bar_full + 1;  // [4] ex1 groups: P1 reads done
   uint64_t* bar_r2 = bar_full + 5;  // [4] ex2 groups: last-round reads done
   uint32_t* cnt = reinterpret_cast<uint32_t*>(bar_full + 9);
+  uint64_t* bar_o = bar_full + 10;  // [4] ex2 groups (forward): the output images in E have been read by their stores
   const uint32_t t = threadIdx.x, l = t & 31u, w = t >> 5;
   const uint32_t g1 = w >> 2, g2 = w & 3u;  // exchange-1 / exchange-2 group
   const uint32_t lognb = a.logn - kB14;
@@ -301,13 +341,19 @@ __global__ void __launch_bounds__(512, 1)
     row = (static_cast<uint64_t>(k) >> lognb) * a.row_mul + a.row_add;
     blk = static_cast<uint64_t>(k) & ((uint64_t{1} << lognb) - 1);
   };
-  auto issue = [&](uint32_t k) {
+  // slot: parity of the block's position in this CTA's sequence
+  auto issue = [&](uint32_t k, uint32_t slot) {
     uint64_t row, blk;
     item_row(k, row, blk);
     const int32_t y0 = static_cast<int32_t>(row * rowwords16 + (blk << (kB14 - 4)));
-    mbar_expect_tx(bar_full, kStageBytes);
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+    mbar_expect_tx(bar_full, kStageBytes + static_cast<uint32_t>(sizeof(LimbConst)));
 #pragma unroll
     for (int q = 0; q < 4; ++q) tma_load_2d(St + q * 32768, &tin, 0, y0 + q * 256, bar_full);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(Cs + slot)),
+                 "l"(a.lc + limb), "r"(static_cast<uint32_t>(sizeof(LimbConst))), "r"(smem_u32(bar_full))
+                 : "memory");
   };
 
   if (t == 0) {
@@ -315,15 +361,16 @@ __global__ void __launch_bounds__(512, 1)
     for (int i = 0; i < 4; ++i) {
       mbar_init(bar_r1 + i, 4);
       mbar_init(bar_r2 + i, 4);
+      mbar_init(bar_o + i, 4);
     }
     *cnt = 0;
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tin)) : "memory");
+    if (FWD) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tout)) : "memory");
   }
   __syncthreads();
-  if (t == 0 && blockIdx.x < nitems) issue(blockIdx.x);
+  if (t == 0 && blockIdx.x < nitems) issue(blockIdx.x, 0);
 
   const uint32_t jt1 = M::jt1(w, l), jt2 = M::jt2(w, l), jt3 = M::jt3(w, l);
-  const uint32_t jtlow = FWD ? jt3 : jt1;  // thread bits of the pass over bits 0..4
   uint8_t* Eg = E + (g2 << 14);           // this warp's exchange-2 group slice
   // Thread-constant byte bases: every shared access below is a base, at most
   // one XOR with an immediate, plus an immediate offset (derivations in the
@@ -331,14 +378,17 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t q2 = grp::q2_of<FWD>(jt2);
   const uint32_t e2w = ex2_off<FWD>(jt2), e2r = ex2_off<FWD>(jt3);
   uint32_t phase = 0;
+  uint32_t it_ = 0;
+  (void)it_;
 
   for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
     uint64_t row, blk;
     item_row(k, row, blk);
+    NK_GTS(0);
     const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
-    const LimbConst c = a.lc[limb];
     const typename A::Tw* __restrict__ tw = tw_of<A>(a, limb);
-    const typename A::Tw* __restrict__ twl = twl_of<A>(a, limb) + (blk << kB14) + (jtlow >> 5);
+    // low pass: the thread-order table (a warp's loads are 32 consecutive entries)
+    const typename A::Tw* __restrict__ twl = twg_of<A>(a, limb) + (blk << kB14) + t;
     const uint64_t boff = blk << kB14;
     uint64_t* __restrict__ dst = a.out + row * a.n + boff;
     const uint64_t xbase = a.n + boff;
@@ -346,11 +396,69 @@ __global__ void __launch_bounds__(512, 1)
 
     // ---- P1 words from the staging buffer (TMA layout) ----
     mbar_wait(bar_full, phase);
+    // (register allocation: the inverse is spill-free with the fields copied to
+    // registers here, the forward with the fields read where they are used)
+    typename std::conditional<FWD, const LimbConst&, const LimbConst>::type c = Cs[phase];
+    NK_GTS(1);
     grp::p1_read<A, FWD>(v, St, jt1);
     __syncwarp();
     if (l == 0) mbar_arrive_local(bar_r1 + g1);  // this warp's P1 slots may be rewritten
+    NK_GTS(2);
 
+    // Inverse, pipelined (kPipe): the exchanges' shared-memory traffic is
+    // issued between arithmetic that does not depend on it. P1's last stage
+    // (bit 4) runs after the wait for the group's P1 reads, so its results go
+    // to their exchange slots as they are formed; P2 runs one half (bit 13)
+    // at a time with the round-0 writes of exchange 2 between the halves;
+    // P3's stages below bit 13 run per half, around the round-1 traffic.
+    constexpr bool kPipe = !FWD && NK_GRP_PIPE;
+    constexpr bool kFoldLast = !FWD && A::kSigned && !LONG;
+    if constexpr (kPipe) {
+      stages14<A, FWD, P1, ILTM0, 0, 4>(v, tw, twl, a.n, xbase + jt1, c);
+      mbar_wait(bar_r1 + g1, phase);
+      stages14<A, FWD, P1, ILTM0, 4, 5>(v, tw, twl, a.n, xbase + jt1, c);
+      NK_GTS(3);
+      grp::ex1_write<FWD>(v, St, jt1);
+      named_sync128(1 + g1);
+      grp::ex1_read<FWD>(v, St, q2);
+      grp::staging_consumed(cnt, l, [&] {
+        if (k + gridDim.x < nitems) {
+          fence_proxy_async();
+          issue(k + gridDim.x, phase ^ 1);
+        }
+      });
+      NK_GTS(4);
+      stages14<A, FWD, P2, false, 0, 4, 0>(v, tw, twl, a.n, xbase + jt2, c);
+      mbar_wait(bar_r2 + g2, phase ^ 1);
+      grp::ex2_write<FWD>(v, Eg, e2w, 0);
+      stages14<A, FWD, P2, false, 0, 4, 1>(v, tw, twl, a.n, xbase + jt2, c);
+      NK_GTS(5);
+      named_sync128(5 + g2);
+      grp::ex2_read<FWD>(v, Eg, e2r, 0);
+      stages14<A, FWD, P3, false, 0, 1, 0>(v, tw, twl, a.n, xbase + jt3, c);
+      named_sync128(5 + g2);  // round-0 reads done before round-1 writes
+      grp::ex2_write<FWD>(v, Eg, e2w, 1);
+      stages14<A, FWD, P3, false, 1, 3, 0>(v, tw, twl, a.n, xbase + jt3, c);
+      named_sync128(5 + g2);
+      grp::ex2_read<FWD>(v, Eg, e2r, 1);
+      __syncwarp();
+      if (l == 0) mbar_arrive_local(bar_r2 + g2);
+      NK_GTS(6);
+      stages14<A, FWD, P3, false, 3, 4, 0>(v, tw, twl, a.n, xbase + jt3, c);
+      stages14<A, FWD, P3, false, 0, 4, 1>(v, tw, twl, a.n, xbase + jt3, c);
+      if constexpr (kFoldLast) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) A::inv_fold(v[r], v[r + 16], c);
+      } else {
+        stages14<A, FWD, P3, false, 4, 5>(v, tw, twl, a.n, xbase + jt3, c);
+      }
+    } else {
     pass14<A, FWD, P1, ILTM0>(v, tw, twl, a.n, xbase + jt1, c);
+    NK_GTS(3);
+    if (FWD && l == 0) {  // the previous block's output stores have read this warp's images
+      bulk_wait_read();
+      mbar_arrive_local(bar_o + g2);
+    }
 
     // ---- exchange 1: in place, within the group's staging slots ----
     grp::ex1<FWD>(v, St, jt1, q2, bar_r1 + g1, phase, g1);
@@ -358,18 +466,21 @@ __global__ void __launch_bounds__(512, 1)
     grp::staging_consumed(cnt, l, [&] {
       if (k + gridDim.x < nitems) {
         fence_proxy_async();
-        issue(k + gridDim.x);
+        issue(k + gridDim.x, phase ^ 1);
       }
     });
 
+    NK_GTS(4);
     pass14<A, FWD, P2, false>(v, tw, twl, a.n, xbase + jt2, c);
+    NK_GTS(5);
 
     // ---- exchange 2: the previous block's last-round reads (first block: passes) ----
+    if (FWD) mbar_wait(bar_o + g2, phase);  // ... and its output images have left the slice
     grp::ex2<FWD>(v, Eg, e2w, e2r, bar_r2 + g2, phase ^ 1, g2, l);
+    NK_GTS(6);
 
     // canonical inverse (Arith52S, whole rows): n^-1 folded into the last
     // stage (bit 13, single twiddle), as in ntt_pair14 / ntt_grp14
-    constexpr bool kFoldLast = !FWD && A::kSigned && !LONG;
     if constexpr (kFoldLast) {
       pass14<A, FWD, P3, false, 1>(v, tw, twl, a.n, xbase + jt3, c);
 #pragma unroll
@@ -377,12 +488,47 @@ __global__ void __launch_bounds__(512, 1)
     } else {
       pass14<A, FWD, P3, false>(v, tw, twl, a.n, xbase + jt3, c);
     }
+    }
 
+    NK_GTS(7);
     // ---- final words and stores ----
     if (FWD) {
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = fwd_out<A>(v[i], c, a.fout);
-      grp::fwd_store(v, O + (w << 11), w, l, dst);
+      // Each thread holds a 256-byte run; a warp's 32 runs are 8 pieces (j9..j11)
+      // of 4 consecutive runs (j5, j6). Two rounds (the run's halves): the warp
+      // writes its 32 half-runs as the rows of a 4 KiB image (row = lane, 128B
+      // swizzle: conflict free) in its quarter of the exchange-2 slice, then four
+      // bulk tensor stores (one per j5j6: 8 rows, the box of the 5-D map) move it
+      // out. The slice is free once the group's exchange-2 reads are done
+      // (bar_r2), and taken again by the next block's exchange 2 after every
+      // warp's stores have read their images (bar_o, arrived in the next block).
+      uint8_t* Wb = Eg + ((w >> 2) << 12);
+      mbar_wait(bar_r2 + g2, phase);
+      const int32_t c4 = static_cast<int32_t>(((row * a.n + boff) >> 9) + 8u * (w & 3u));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        if (h == 1) {
+          if (l == 0) bulk_wait_read();
+          __syncwarp();
+        }
+#pragma unroll
+        for (int cc = 0; cc < 8; ++cc)
+          *reinterpret_cast<ulonglong2*>(Wb + (l << 7) + ((cc ^ (l & 7)) << 4)) =
+              make_ulonglong2(v[16 * h + 2 * cc], v[16 * h + 2 * cc + 1]);
+        fence_proxy_async();
+        __syncwarp();
+        if (l == 0) {
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2)
+            asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4, %5}], [%6];" ::"l"(
+                             reinterpret_cast<uint64_t>(&tout)),
+                         "r"(0), "r"(h), "r"(s2), "r"(static_cast<int32_t>(w >> 2)), "r"(c4),
+                         "r"(smem_u32(Wb + (s2 << 10)))
+                         : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
     } else {
       if constexpr (LONG) {
 #pragma unroll
@@ -394,8 +540,11 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
       for (int r = 0; r < 32; ++r) dst[jt3 | (static_cast<uint32_t>(r) << 9)] = v[r];
     }
+    NK_GTS(8);
     phase ^= 1;
+    ++it_;
   }
+  if (FWD && l == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace nk

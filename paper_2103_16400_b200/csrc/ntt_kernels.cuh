@@ -59,6 +59,11 @@ struct NttArgs {
                          // result by these canonical words (same layout) before storing
   const uint64_t* tw8;   // [limb][N] w only (double bits), same order as tw: Arith52S
   const uint64_t* twl8;  // [limb][N] the same entries in the low-table order of twl
+  // the low tables in the group-exchange kernels' thread order (entry (b, d, t)
+  // = low-table entry (b, d, jhi of thread t's low pass), GrpMap in ntt_grp.cuh):
+  // a warp's 32 loads of one (stage, d) are 32 consecutive entries
+  const ulonglong2* twg;
+  const uint64_t* twg8;
 };
 
 __device__ __forceinline__ ulonglong2 ldtw(const ulonglong2* p) { return __ldg(p); }
@@ -74,6 +79,12 @@ template <class A>
 __device__ __forceinline__ const typename A::Tw* twl_of(const NttArgs& a, uint32_t limb) {
   if constexpr (std::is_same_v<typename A::Tw, uint64_t>) return a.twl8 + static_cast<uint64_t>(limb) * a.n;
   else return a.twl + static_cast<uint64_t>(limb) * a.n;
+}
+
+template <class A>
+__device__ __forceinline__ const typename A::Tw* twg_of(const NttArgs& a, uint32_t limb) {
+  if constexpr (std::is_same_v<typename A::Tw, uint64_t>) return a.twg8 + static_cast<uint64_t>(limb) * a.n;
+  else return a.twg + static_cast<uint64_t>(limb) * a.n;
 }
 
 // Padded shared-memory image index: additive over disjoint bit fields, so every
@@ -446,16 +457,19 @@ struct PassD {
 };
 
 
-// One register pass over the bits of PD (stage order by direction).
-// SKIP_LAST: leave the pass's last stage to the caller (the folded n^-1 stage
-// of the canonical inverses).
-template <class A, bool FWD, class PD, bool ILTM0, int SKIP_LAST = 0>
-__device__ __forceinline__ void pass14(uint64_t (&v)[32], const typename A::Tw* __restrict__ tw,
-                                       const typename A::Tw* __restrict__ twl, uint64_t n,
-                                       uint64_t xt, const LimbConst& c) {
+// Stages [S0, S1) (processing order) of the register pass PD, on all 32 words
+// or on one half of them (HALF = 0 / 1: registers 16 HALF .. 16 HALF + 15;
+// only for stages whose butterflies stay inside a half: every stage of a
+// K = 4 pass, whose halves are its two groups, and the stages below register
+// bit 4 of a K = 5 pass). The kernels use the halves to overlap an exchange
+// round of one half with the arithmetic of the other.
+template <class A, bool FWD, class PD, bool ILTM0, int S0, int S1, int HALF = -1>
+__device__ __forceinline__ void stages14(uint64_t (&v)[32], const typename A::Tw* __restrict__ tw,
+                                         const typename A::Tw* __restrict__ twl, uint64_t n,
+                                         uint64_t xt, const LimbConst& c) {
   constexpr int K = PD::K, R = PD::R, G = PD::G;
   // the pass over bits 0..4 reads the transposed low table (twl points at this
-  // block's segment plus this thread's jhi): loads of one (stage, d) are
+  // block's segment plus this thread's position): loads of one (stage, d) are
   // lane-contiguous and their offsets are immediates
   constexpr bool kLow = (PD::LO == 0 && PD::K == 5);
   // a passenger bit below the pass's bits does not reach the twiddle index
@@ -463,17 +477,20 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const typename A::Tw* 
   constexpr bool kShared = (G == 2) && (PD::X >= 0) && (PD::X < PD::LO);
   constexpr int GL = kShared ? 1 : G;  // groups with their own twiddles
 #pragma unroll
-  for (int s = 0; s < K - SKIP_LAST; ++s) {
+  for (int s = S0; s < S1; ++s) {
     const int i = FWD ? (K - 1 - s) : s;
     const int b = PD::LO + i;
 #pragma unroll
     for (int gl = 0; gl < GL; ++gl) {
+      if (HALF >= 0 && G == 2 && !kShared && gl != HALF) continue;
       const uint64_t base = (xt + PD::jc(gl, 0)) >> (b + 1);
 #pragma unroll
       for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
+        if (HALF >= 0 && G == 1 && (((hi << (i + 1)) >> 4) & 1) != HALF) continue;
         const typename A::Tw w = kLow ? ldtw(twl + low_index(b, hi, 0)) : ldtw(tw + base + hi);
 #pragma unroll
         for (int gg = 0; gg < G / GL; ++gg) {
+          if (HALF >= 0 && kShared && gg != HALF) continue;
 #pragma unroll
           for (int l = 0; l < (1 << i); ++l) {
             const int g = kShared ? gg : gl;
@@ -493,6 +510,16 @@ __device__ __forceinline__ void pass14(uint64_t (&v)[32], const typename A::Tw* 
       }
     }
   }
+}
+
+// One register pass over the bits of PD (stage order by direction).
+// SKIP_LAST: leave the pass's last stage to the caller (the folded n^-1 stage
+// of the canonical inverses).
+template <class A, bool FWD, class PD, bool ILTM0, int SKIP_LAST = 0>
+__device__ __forceinline__ void pass14(uint64_t (&v)[32], const typename A::Tw* __restrict__ tw,
+                                       const typename A::Tw* __restrict__ twl, uint64_t n,
+                                       uint64_t xt, const LimbConst& c) {
+  stages14<A, FWD, PD, ILTM0, 0, PD::K - SKIP_LAST>(v, tw, twl, n, xt, c);
 }
 
 // ---------------------------------------------------------------------------

@@ -23,7 +23,8 @@
 // signed inverse's |x| < 2q input range.
 //
 // Product image (the inverse's P1 input): word j at line j >> 4, 16-byte chunk
-// ((j >> 1) & 7) ^ (line & 7) ^ ((j >> 9) & 7). Against the TMA layout the
+// ((j >> 1) & 7) ^ (line & 7) ^ ((j >> 9) & 7) ^ (j >> 13) (the last term makes the
+// inverse's P1 reads conflict free: its eight lanes of a phase differ in j5, j6, j13). Against the TMA layout the
 // extra XOR (j9..j11) permutes chunks inside a line only, so every exchange-1
 // group keeps its slot set (exchange 1 is in place); it makes the writes
 // conflict free (the forward's P3 threads of one 8-lane phase differ exactly
@@ -35,9 +36,9 @@
 namespace nk {
 
 struct PolyArgs {
-  NttArgs a;             // out, forward tables (tw8 / twl8), lc, n, rows, limbs
+  NttArgs a;             // out, forward tables (tw8 / twg8), lc, n, rows, limbs
   const uint64_t* itw8;  // inverse tables of the plan, same layouts
-  const uint64_t* itwl8;
+  const uint64_t* itwg8;
 };
 
 // [grp layout][bar_free][TMEM base address]
@@ -91,7 +92,7 @@ __device__ __forceinline__ void poly_forward(uint64_t (&v)[32], uint8_t* St, uin
   const LimbConst c = a.lc[limb];
   const uint64_t n = a.n;
   const uint64_t* __restrict__ tw = a.tw8 + static_cast<uint64_t>(limb) * n;
-  const uint64_t* __restrict__ twl = a.twl8 + static_cast<uint64_t>(limb) * n + (jt3 >> 5);
+  const uint64_t* __restrict__ twl = a.twg8 + static_cast<uint64_t>(limb) * n + t;
   mbar_wait(bar_full, fph);
   grp::p1_read<A, true>(v, St, jt1);
   __syncwarp();
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(512, 1)
     mbar_wait(bar_free, it & 1u);  // every warp has read f's staging words
     {
       const uint32_t to = tid_opaque(), jf3 = MF::jt3(to >> 5, to & 31u);
-      const uint32_t key = (jf3 >> 9) & 7u;
+      const uint32_t key = ((jf3 >> 9) & 7u) ^ ((jf3 >> 13) & 1u);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const uint32_t line = (jf3 >> 4) | static_cast<uint32_t>(h);
@@ -227,8 +228,8 @@ __global__ void __launch_bounds__(512, 1)
       const uint32_t ji1 = MI::jt1(wo, lo), ji2 = MI::jt2(wo, lo), ji3 = MI::jt3(wo, lo);
       const LimbConst c = a.lc[limb];
       const uint64_t* __restrict__ itw = pa.itw8 + static_cast<uint64_t>(limb) * a.n;
-      const uint64_t* __restrict__ itwl = pa.itwl8 + static_cast<uint64_t>(limb) * a.n + (ji1 >> 5);
-      grp::p1_read<A, false, true>(v, St, ji1, (ji1 >> 9) & 7u);
+      const uint64_t* __restrict__ itwl = pa.itwg8 + static_cast<uint64_t>(limb) * a.n + tid_opaque();
+      grp::p1_read<A, false, true>(v, St, ji1, ((ji1 >> 9) & 7u) ^ ((ji1 >> 13) & 1u));
       __syncwarp();
       if (l == 0) mbar_arrive_local(bar_r1 + g1);
       pass14<A, false, I1, false>(v, itw, itwl, a.n, a.n + ji1, c);

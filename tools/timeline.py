@@ -16,6 +16,7 @@ from bench import largest_ntt_primes  # noqa: E402
 n = 16384
 moduli = largest_ntt_primes(50, n, 32)
 plan = nk.RnsNtt(n, moduli)
+nk.set_block_kernel(0)  # the CTA-pair kernel
 x = torch.randint(0, 1 << 49, (64 * 32 * n,), dtype=torch.int64, device="cuda")
 o = torch.empty_like(x)
 plan.forward(o, x, 1, 1)
