@@ -13,6 +13,7 @@
 #include "ntt_kernels.cuh"
 #include "ntt_grp.cuh"
 #include "ntt_pair.cuh"
+#include "ntt_str.cuh"
 #include "runtime.hpp"
 
 namespace nk::rt {
@@ -39,7 +40,7 @@ int encode_fn(EncodeTiledFn* out) {
   return 0;
 }
 
-enum MapKind { kRowMap = 0, kSuperlineMap = 1, kOutMap = 2, kGrpOutMap = 3 };
+enum MapKind { kRowMap = 0, kSuperlineMap = 1, kOutMap = 2, kGrpOutMap = 3, kStrOutMap = 4 };
 
 // A tensor map is a pure function of (kind, base, words): the last few are
 // cached per thread, so repeated calls on the same buffers (a serving loop,
@@ -80,6 +81,15 @@ int make_map(CUtensorMap* map, MapKind kind, const uint64_t* base, uint64_t word
     const cuuint32_t estr[3] = {1, 1, 1};
     r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (kind == kStrOutMap) {
+    // 2D view [words/16][16] (128B swizzle), boxes of 32 x 128 B: the 512 consecutive
+    // words of one warp's stream output in ntt_str14
+    const cuuint64_t dims[2] = {16, words / 16};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {16, 32};
+    const cuuint32_t estr[2] = {1, 1};
+    r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else if (kind == kGrpOutMap) {
     // 5D view [words/512][4 (j7, j8)][4 (j5, j6)][2 halves][16 words] (128B swizzle),
     // boxes 16 x 1 x 1 x 1 x 8: one half of the runs j5j6 of 8 consecutive
@@ -148,6 +158,21 @@ int launch_grp_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStre
   return launch_grp_k<ntt_grp14<A, FWD, IL>, FWD>(a, nitems, buf_words, st);
 }
 
+// two-stream forward (ntt_str.cuh): persistent, one 512-thread CTA per SM
+template <class A, bool IL>
+int launch_str_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
+  constexpr auto kern = ntt_str14<A, IL>;
+  CUtensorMap map, omap;
+  if (int rc = make_map(&map, kRowMap, a.in, buf_words)) return rc;
+  if (int rc = make_map(&omap, kStrOutMap, a.out, buf_words)) return rc;
+  if (int rc = set_smem_once<kern>(kStrSmemBytes)) return rc;
+  const uint64_t g = nitems < static_cast<uint64_t>(sm_count()) ? nitems : sm_count();
+  kern<<<static_cast<unsigned>(g), 512, kStrSmemBytes, st>>>(map, omap, a, static_cast<uint32_t>(nitems));
+  launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+
 // CTA-pair kernel (ntt_pair.cuh): persistent, one cluster of 2 per block in
 // flight, as many clusters as fit (2 CTAs per SM).
 template <auto KERN, bool FWD>
@@ -200,6 +225,9 @@ int launch_tma(const NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm,
   // cfg3; 363 / 348 us against 363 / 384 us on cfg4); the three-launch
   // poly_mult_mod's fused product lives in the pair forward only
   const bool pair = a.mulb || block_kernel == 0;
+  if constexpr (FWD)
+    if (!a.mulb && block_kernel == 2)
+      return iltm ? launch_str_t<A, true>(a, nitems, buf_words, st) : launch_str_t<A, false>(a, nitems, buf_words, st);
   if (pair)
     return iltm ? launch_pair_t<A, FWD, true>(a, nitems, buf_words, st)
                 : launch_pair_t<A, FWD, false>(a, nitems, buf_words, st);

@@ -64,6 +64,9 @@ struct NttArgs {
   // a warp's 32 loads of one (stage, d) are 32 consecutive entries
   const ulonglong2* twg;
   const uint64_t* twg8;
+  // the two-stream forward's low-stage twiddles in (stream, entry, thread) order (ntt_str.cuh)
+  const ulonglong2* twq;
+  const uint64_t* twq8;
 };
 
 __device__ __forceinline__ ulonglong2 ldtw(const ulonglong2* p) { return __ldg(p); }

@@ -1,0 +1,302 @@
+// ntt_str14: the forward 16384-word block transform as TWO STREAMS per thread.
+//
+// Why: in ntt_grp14 the 16 warps of the CTA move through
+// the block in lockstep, so while they exchange words through shared memory
+// (about 30% of a block) nobody computes, although the hardware overlaps the
+// FP64 pipe and the shared-memory path perfectly. After the forward's first
+// stage (index bit 13) the block is two independent 8192-word transforms, A
+// (bit 13 clear) and B. Here every thread carries 16 words of each and
+// alternates between them: while one stream's words are in flight through
+// shared memory the thread runs the other stream's stages, so the data
+// movement hides behind arithmetic of the same warp and no barrier is waited
+// on with nothing to do.
+//
+// Passes (block-local index j, S = j13 the stream; t = 32 w + l):
+//   P1  bits 13..9 on 32 words, as ntt_grp14 (thread bits j0..j8: jt1): stage
+//       13 on all 16 pairs, then stages 12..9 per stream
+//   e1  CTA-wide exchange of each stream, in place in its half of the staging
+//       buffer (after every warp has read its P1 words): P1's register bits
+//       j9..j12 become warp bits, thread bits j5..j8 become registers
+//   Q2  bits 8..5 on 16 words per stream; lanes j0..j4, warps j9..j12 (the
+//       twiddles are warp-uniform)
+//   e2  warp-local exchange (warp bits unchanged: only __syncwarp) through the
+//       warp's 4 KiB of E: registers j5..j8 <-> lane bits, j1..j4 become registers
+//   Q3  bits 4..1; lanes (j0, j5..j8), warps j9..j12
+//   sh  lane pairs (l, l ^ 1) swap half their words by shuffle: j0 becomes a
+//       register bit, j1 the lane bit
+//   Q4  bit 0; then the canonical words of the stream go out: the warp's 512
+//       words are contiguous in memory, written as a 4 KiB 128B-swizzled image
+//       (the same 4 KiB of E) and stored by one bulk tensor store
+// Both exchanges use 8-byte accesses with the 16-byte-chunk XOR swizzles
+// derived below (conflict free on both sides; tests/test_str_layout.py).
+//
+// Twiddles: P1 and Q2 read the reference-order table (broadcast loads), Q3 and
+// Q4 a table in (stream, entry, thread) order: entry 0 = stage bit 4, 1..2 =
+// bit 3, 3..6 = bit 2, 7..14 = bit 1, 15..22 = bit 0 (kStrEntries = 23), so a
+// warp's 32 loads are 32 consecutive entries. The butterflies, their order
+// and the twiddles are the reference's (ntt.hpp:363-394): every arithmetic
+// policy keeps its exactness argument.
+#pragma once
+#include "ntt_grp.cuh"
+
+namespace nk {
+
+constexpr int kStrEntries = 23;
+constexpr uint32_t kStrTableWords = 2u * kStrEntries * 512u;  // per limb (and 16384-word block)
+
+// thread index bits of each pass (block-local j without the stream bit)
+struct StrMap {
+  __host__ __device__ static constexpr uint32_t jt1(uint32_t w, uint32_t l) { return GrpMap<true>::jt1(w, l); }
+  __host__ __device__ static constexpr uint32_t jt2(uint32_t w, uint32_t l) { return l | (w << 9); }
+  __host__ __device__ static constexpr uint32_t jt3(uint32_t w, uint32_t l) {
+    return (l & 1u) | ((l >> 1) << 5) | (w << 9);
+  }
+};
+
+// table index (reference order, relative to the limb's table) of entry e of
+// thread t in stream S, for a block at offset boff of a row of length n
+__host__ __device__ constexpr uint64_t str_tw_index(uint64_t n, uint64_t boff, uint32_t S, int e, uint32_t t) {
+  const uint32_t w = t >> 5, l = t & 31u;
+  const uint64_t jb = boff + (static_cast<uint64_t>(S) << 13);
+  if (e < 15) {
+    // Q3 stage bit b, hi = the register bits above b
+    const int b = e == 0 ? 4 : (e < 3 ? 3 : (e < 7 ? 2 : 1));
+    const int hi = e == 0 ? 0 : (e < 3 ? e - 1 : (e < 7 ? e - 3 : e - 7));
+    const uint64_t j = jb + StrMap::jt3(w, l) + (static_cast<uint64_t>(hi) << (b + 1));
+    return (n + j) >> (b + 1);
+  }
+  // Q4: bit 0; registers (j2, j3, j4) = hi, lane bit 0 = j1
+  const int hi = e - 15;
+  const uint64_t j = jb + (StrMap::jt3(w, l) & ~1u) + ((l & 1u) << 1) + (static_cast<uint64_t>(hi) << 2);
+  return (n + j) >> 1;
+}
+
+template <class A>
+__device__ __forceinline__ const typename A::Tw* twq_of(const NttArgs& a, uint32_t limb) {
+  const uint64_t per_limb = (a.n >> kB14) * kStrTableWords;
+  if constexpr (std::is_same_v<typename A::Tw, uint64_t>) return a.twq8 + limb * per_limb;
+  else return a.twq + limb * per_limb;
+}
+
+// [1 KiB align][staging 128 KiB][E 64 KiB][limb constants x2][mbarriers: full, P1 reads, e1 A, e1 B][counter]
+constexpr size_t kStrSmemBytes = 1024 + kStageBytes + kGrpExBytes + 2 * sizeof(LimbConst) + 8 * 8;
+
+namespace str {
+
+// K stages (forward order: bit LO + K - 1 first) on the 16 registers x[0..15]
+// whose index bits are j_LO .. j_{LO+3}; the twiddle of stage bit b, position
+// hi (the register bits above b) comes from `twf(i, hi)`, i = b - LO.
+template <class A, int NST, bool ILTM, class F>
+__device__ __forceinline__ void pass16(uint64_t* x, const LimbConst& c, F&& twf) {
+#pragma unroll
+  for (int s = 0; s < NST; ++s) {
+    const int i = 3 - s;
+#pragma unroll
+    for (int hi = 0; hi < (16 >> (i + 1)); ++hi) {
+      const typename A::Tw w = twf(i, hi);
+#pragma unroll
+      for (int lo = 0; lo < (1 << i); ++lo) {
+        const int r0 = (hi << (i + 1)) | lo, r1 = r0 | (1 << i);
+        A::template fwd<false>(x[r0], x[r1], w, c);
+      }
+    }
+  }
+}
+
+}  // namespace str
+
+template <class A, bool ILTM0>
+__global__ void __launch_bounds__(512, 1)
+    ntt_str14(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, NttArgs a,
+              uint32_t nitems) {
+  using P1 = PassD<9, 5, -1>;
+  using Tw = typename A::Tw;
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* St = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);  // staging (TMA, 128B-swizzled), then e1
+  uint8_t* E = St + kStageBytes;                                         // per warp 4 KiB: e2, then the output image
+  const LimbConst* Cs = reinterpret_cast<const LimbConst*>(E + kGrpExBytes);
+  uint64_t* bar_full = reinterpret_cast<uint64_t*>(E + kGrpExBytes + 2 * sizeof(LimbConst));
+  uint64_t* bar_rd = bar_full + 1;  // every warp has read its P1 words
+  uint64_t* bar_w = bar_full + 2;   // [2] every warp has written its e1 words of stream S
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(bar_full + 4);
+  const uint32_t t = threadIdx.x, l = t & 31u, w = t >> 5;
+  const uint32_t lognb = a.logn - kB14;
+  const uint64_t rowwords16 = a.n >> 4;
+
+  auto item_row = [&](uint32_t k, uint64_t& row, uint64_t& blk) {
+    row = (static_cast<uint64_t>(k) >> lognb) * a.row_mul + a.row_add;
+    blk = static_cast<uint64_t>(k) & ((uint64_t{1} << lognb) - 1);
+  };
+  auto issue = [&](uint32_t k, uint32_t slot) {
+    uint64_t row, blk;
+    item_row(k, row, blk);
+    const int32_t y0 = static_cast<int32_t>(row * rowwords16 + (blk << (kB14 - 4)));
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+    mbar_expect_tx(bar_full, kStageBytes + static_cast<uint32_t>(sizeof(LimbConst)));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tma_load_2d(St + q * 32768, &tin, 0, y0 + q * 256, bar_full);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(Cs + slot)),
+                 "l"(a.lc + limb), "r"(static_cast<uint32_t>(sizeof(LimbConst))), "r"(smem_u32(bar_full))
+                 : "memory");
+  };
+
+  if (t == 0) {
+    mbar_init(bar_full, 1);
+    mbar_init(bar_rd, 16);
+    mbar_init(bar_w, 16);
+    mbar_init(bar_w + 1, 16);
+    *cnt = 0;
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tin)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tout)) : "memory");
+  }
+  __syncthreads();
+  if (t == 0 && blockIdx.x < nitems) issue(blockIdx.x, 0);
+
+  // ---- thread-constant byte offsets (derivations: header and section comments) ----
+  const uint32_t jt1 = StrMap::jt1(w, l);
+  // e1, write side: stream word j' = jt1 | r << 9 at chunk-swizzled position
+  //   phys(j') = j' ^ (((j' >> 4) & 7) << 1): the half-warp's lanes (j0, j4, j5, j6) hit 16 distinct 8-byte slots
+  const uint32_t e1w = (jt1 ^ (((jt1 >> 4) & 7u) << 1)) << 3;  // + r * 4096 + S * 65536
+  // e1, read side: j' = l | r << 5 | w << 9 (lanes j0..j4): (base ^ ((r & 3) << 5)) + r * 256
+  const uint32_t e1r = ((l ^ ((l >> 4) << 1)) << 3) + (w << 12);
+  // e2 (warp-local, word m = j & 511 at m ^ (((m >> 5) & 7) << 1)): write (l << 3 ^ (r & 7) << 4) + r * 256,
+  // read tb ^ (r3 << 4)
+  uint8_t* Ew = E + (w << 12);
+  const uint32_t e2w = l << 3;
+  const uint32_t e2r = ((l & 1u) << 3) | (((l >> 1) & 7u) << 4) | ((l >> 1) << 8);
+  uint32_t phase = 0;
+
+  for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
+    uint64_t row, blk;
+    item_row(k, row, blk);
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+    const Tw* __restrict__ tw = tw_of<A>(a, limb);
+    const Tw* __restrict__ twq = twq_of<A>(a, limb) + blk * kStrTableWords + t;
+    const uint64_t boff = blk << kB14;
+    const uint64_t xbase = a.n + boff;
+    uint64_t v[32];
+
+    // ---- P1: words from the staging buffer, stage 13, then stages 12..9 per stream ----
+    mbar_wait(bar_full, phase);
+    const LimbConst& c = Cs[phase];
+    grp::p1_read<A, true>(v, St, jt1);
+    __syncwarp();
+    if (l == 0) mbar_arrive_local(bar_rd);
+    stages14<A, true, P1, ILTM0, 0, 1>(v, tw, tw, a.n, xbase + jt1, c);
+    stages14<A, true, P1, ILTM0, 1, 5, 0>(v, tw, tw, a.n, xbase + jt1, c);
+    // e1 of stream A: in place in the lower half of the staging buffer
+    mbar_wait(bar_rd, phase);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + e1w + r * 4096) = v[r];
+    __syncwarp();
+    if (l == 0) mbar_arrive_local(bar_w);
+    stages14<A, true, P1, ILTM0, 1, 5, 1>(v, tw, tw, a.n, xbase + jt1, c);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + 65536 + e1w + r * 4096) = v[16 + r];
+    __syncwarp();
+    if (l == 0) mbar_arrive_local(bar_w + 1);
+
+    // ---- Q2 words of both streams (B's arrive while A computes) ----
+    mbar_wait(bar_w, phase);
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      v[r] = *reinterpret_cast<const uint64_t*>(St + ((e1r ^ ((r & 3) << 5)) + r * 256));
+    mbar_wait(bar_w + 1, phase);
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      v[16 + r] = *reinterpret_cast<const uint64_t*>(St + 65536 + ((e1r ^ ((r & 3) << 5)) + r * 256));
+    // the staging buffer is consumed by this warp; the last of the 16 warps refills it
+    grp::staging_consumed(cnt, l, [&] {
+      if (k + gridDim.x < nitems) {
+        fence_proxy_async();
+        issue(k + gridDim.x, phase ^ 1);
+      }
+    });
+
+    // Q2 twiddles: (N + j) >> (b + 1), b = 5 + i, j = w << 9 | S << 13 (+ r << 5): warp-uniform
+    auto q2tw = [&](uint32_t S) {
+      const uint64_t js = xbase + (static_cast<uint64_t>(w) << 9) + (static_cast<uint64_t>(S) << 13);
+      return [=](int i, int hi) { return ldtw(tw + (js >> (6 + i)) + hi); };
+    };
+    // Q3 / Q4 twiddles: the (stream, entry, thread) table
+    auto q3tw = [&](uint32_t S) {
+      const Tw* p = twq + S * (kStrEntries * 512u);
+      return [=](int i, int hi) { return ldtw(p + ((i == 3 ? 0 : (i == 2 ? 1 : (i == 1 ? 3 : 7))) + hi) * 512); };
+    };
+
+    // ---- stream A: Q2, e2 write; stream B: Q2; A: e2 read ... ----
+    str::pass16<A, 4, false>(v, c, q2tw(0));
+    if (l == 0) bulk_wait_read();  // the previous block's last output store has read this warp's 4 KiB
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256)) = v[r];
+    __syncwarp();
+    str::pass16<A, 4, false>(v + 16, c, q2tw(1));
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(Ew + (e2r ^ (r << 4)));
+    __syncwarp();  // A's words are in registers: the buffer takes B's
+#pragma unroll
+    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256)) = v[16 + r];
+    __syncwarp();
+
+    const int32_t orow16 = static_cast<int32_t>((row * a.n + boff + (static_cast<uint64_t>(w) << 9)) >> 4);
+
+#pragma unroll
+    for (uint32_t S = 0; S < 2; ++S) {
+      uint64_t* x = v + 16 * S;
+      if (S == 0) {
+        // B's Q3 words are read before A's Q3 runs (the loads overlap it), which
+        // also frees the warp's buffer for A's output image
+#pragma unroll
+        for (int r = 0; r < 16; ++r) v[16 + r] = *reinterpret_cast<const uint64_t*>(Ew + (e2r ^ (r << 4)));
+      }
+      str::pass16<A, 4, false>(x, c, q3tw(S));
+      // lane pairs swap: this lane keeps j1 = its bit 0 and gets both j0
+      uint64_t y[16];
+      const bool odd = (l & 1u) != 0;
+#pragma unroll
+      for (int hi = 0; hi < 8; ++hi) {
+        // registers r3 = j1 | hi << 1: own words (j0 = lane bit) with j1 = 0 / 1
+        const uint64_t own0 = x[2 * hi], own1 = x[2 * hi + 1];
+        const uint64_t send = odd ? own0 : own1;
+        const uint64_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
+        y[2 * hi] = odd ? recv : own0;      // j0 = 0, j1 = lane bit
+        y[2 * hi + 1] = odd ? own1 : recv;  // j0 = 1
+      }
+      // Q4: bit 0, twiddle entry 15 + hi
+      const Tw* p4 = twq + S * (kStrEntries * 512u) + 15 * 512;
+#pragma unroll
+      for (int hi = 0; hi < 8; ++hi) {
+        const Tw wv = ldtw(p4 + hi * 512);
+        A::template fwd<false>(y[2 * hi], y[2 * hi + 1], wv, c);
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) y[i] = fwd_out<A>(y[i], c, a.fout);
+      // image: word m = j0 | j1 << 1 | hi << 2 | (l >> 1) << 5 at row m >> 4, chunk ((m >> 1) & 7) ^ (row & 7)
+      if (S == 1) {
+        if (l == 0) bulk_wait_read();  // A's store has read the image
+      }
+      __syncwarp();  // (S == 0: every lane has read B's e2 words)
+#pragma unroll
+      for (int hi = 0; hi < 8; ++hi) {
+        const uint32_t rowi = (hi >> 2) + 2 * (l >> 1);
+        const uint32_t chunk = ((l & 1u) | ((hi & 3) << 1)) ^ (rowi & 7u);
+        *reinterpret_cast<ulonglong2*>(Ew + (rowi << 7) + (chunk << 4)) = make_ulonglong2(y[2 * hi], y[2 * hi + 1]);
+      }
+      fence_proxy_async();
+      __syncwarp();
+      if (l == 0) {
+        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                         reinterpret_cast<uint64_t>(&tout)),
+                     "r"(0), "r"(orow16 + static_cast<int32_t>(S << 9)), "r"(smem_u32(Ew))
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    phase ^= 1;
+  }
+  if (l == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+}  // namespace nk
