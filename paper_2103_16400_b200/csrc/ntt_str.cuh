@@ -103,6 +103,26 @@ __device__ __forceinline__ void pass16(uint64_t* x, const LimbConst& c, F&& twf)
   }
 }
 
+// the same stages on both streams at once (x and x + 16), stage by stage: 16 independent butterflies per stage
+template <class A, int NST, class FA, class FB>
+__device__ __forceinline__ void pass16x2(uint64_t* x, const LimbConst& c, FA&& twa, FB&& twb) {
+#pragma unroll
+  for (int s = 0; s < NST; ++s) {
+    const int i = 3 - s;
+#pragma unroll
+    for (int hi = 0; hi < (16 >> (i + 1)); ++hi) {
+      const typename A::Tw wa = twa(i, hi);
+      const typename A::Tw wb = twb(i, hi);
+#pragma unroll
+      for (int lo = 0; lo < (1 << i); ++lo) {
+        const int r0 = (hi << (i + 1)) | lo, r1 = r0 | (1 << i);
+        A::template fwd<false>(x[r0], x[r1], wa, c);
+        A::template fwd<false>(x[16 + r0], x[16 + r1], wb, c);
+      }
+    }
+  }
+}
+
 }  // namespace str
 
 template <class A, bool ILTM0>
@@ -167,9 +187,12 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t e2r = ((l & 1u) << 3) | (((l >> 1) & 7u) << 4) | ((l >> 1) << 8);
   uint32_t phase = 0;
 
+  uint32_t it_ = 0;
+  (void)it_;
   for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
     uint64_t row, blk;
     item_row(k, row, blk);
+    NK_GTS(0);
     const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
     const Tw* __restrict__ tw = tw_of<A>(a, limb);
     const Tw* __restrict__ twq = twq_of<A>(a, limb) + blk * kStrTableWords + t;
@@ -180,28 +203,62 @@ __global__ void __launch_bounds__(512, 1)
     // ---- P1: words from the staging buffer, stage 13, then stages 12..9 per stream ----
     mbar_wait(bar_full, phase);
     const LimbConst& c = Cs[phase];
+    NK_GTS(1);
     grp::p1_read<A, true>(v, St, jt1);
     __syncwarp();
     if (l == 0) mbar_arrive_local(bar_rd);
+    NK_GTS(2);
     stages14<A, true, P1, ILTM0, 0, 1>(v, tw, tw, a.n, xbase + jt1, c);
     stages14<A, true, P1, ILTM0, 1, 5, 0>(v, tw, tw, a.n, xbase + jt1, c);
+    NK_GTS(3);
     // e1 of stream A: in place in the lower half of the staging buffer
     mbar_wait(bar_rd, phase);
 #pragma unroll
     for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + e1w + r * 4096) = v[r];
     __syncwarp();
     if (l == 0) mbar_arrive_local(bar_w);
+    NK_GTS(4);
     stages14<A, true, P1, ILTM0, 1, 5, 1>(v, tw, tw, a.n, xbase + jt1, c);
 #pragma unroll
     for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + 65536 + e1w + r * 4096) = v[16 + r];
     __syncwarp();
     if (l == 0) mbar_arrive_local(bar_w + 1);
+    NK_GTS(5);
 
-    // ---- Q2 words of both streams (B's arrive while A computes) ----
+    // Twiddles. Q2: (N + j) >> (b + 1), b = 5 + i, j = w << 9 | S << 13 (+ r << 5): warp-uniform loads of
+    // the reference-order table; Q3 / Q4: the (stream, entry, thread) table. The twiddles of a pass's
+    // first two stages (3 values) are loaded ahead of the data movement in front of the pass (`pre`),
+    // so that no pass starts by waiting for L2.
+    auto q2addr = [&](uint32_t S, int i, int hi) {
+      const uint64_t js = xbase + (static_cast<uint64_t>(w) << 9) + (static_cast<uint64_t>(S) << 13);
+      return tw + (js >> (6 + i)) + hi;
+    };
+    auto q3addr = [&](uint32_t S, int i, int hi) {
+#ifdef NK_STR_NOTW  // timing experiment (wrong results): every low-stage twiddle from one address
+      return twq + 0 * (S + i + hi);
+#else
+      return twq + S * (kStrEntries * 512u) + ((i == 3 ? 0 : (i == 2 ? 1 : (i == 1 ? 3 : 7))) + hi) * 512;
+#endif
+    };
+    Tw pa[3], pb[3];
+    pa[0] = ldtw(q2addr(0, 3, 0)), pa[1] = ldtw(q2addr(0, 2, 0)), pa[2] = ldtw(q2addr(0, 2, 1));
+    pb[0] = ldtw(q2addr(1, 3, 0)), pb[1] = ldtw(q2addr(1, 2, 0)), pb[2] = ldtw(q2addr(1, 2, 1));
+    auto q2tw = [&](uint32_t S, const Tw* pre) {
+      return [=](int i, int hi) { return i >= 2 ? pre[i == 3 ? 0 : 1 + hi] : ldtw(q2addr(S, i, hi)); };
+    };
+    auto q3tw = [&](uint32_t S, const Tw* pre) {
+      return [=](int i, int hi) { return i >= 2 ? pre[i == 3 ? 0 : 1 + hi] : ldtw(q3addr(S, i, hi)); };
+    };
+
+    // ---- Q2 of stream A first: the wait for B (every warp through P1) comes after it, when the
+    // slower warps have caught up ----
     mbar_wait(bar_w, phase);
 #pragma unroll
     for (int r = 0; r < 16; ++r)
       v[r] = *reinterpret_cast<const uint64_t*>(St + ((e1r ^ ((r & 3) << 5)) + r * 256));
+    NK_GTS(6);
+    str::pass16<A, 4, false>(v, c, q2tw(0, pa));
+    pa[0] = ldtw(q3addr(0, 3, 0)), pa[1] = ldtw(q3addr(0, 2, 0)), pa[2] = ldtw(q3addr(0, 2, 1));  // A's Q3
     mbar_wait(bar_w + 1, phase);
 #pragma unroll
     for (int r = 0; r < 16; ++r)
@@ -213,26 +270,15 @@ __global__ void __launch_bounds__(512, 1)
         issue(k + gridDim.x, phase ^ 1);
       }
     });
-
-    // Q2 twiddles: (N + j) >> (b + 1), b = 5 + i, j = w << 9 | S << 13 (+ r << 5): warp-uniform
-    auto q2tw = [&](uint32_t S) {
-      const uint64_t js = xbase + (static_cast<uint64_t>(w) << 9) + (static_cast<uint64_t>(S) << 13);
-      return [=](int i, int hi) { return ldtw(tw + (js >> (6 + i)) + hi); };
-    };
-    // Q3 / Q4 twiddles: the (stream, entry, thread) table
-    auto q3tw = [&](uint32_t S) {
-      const Tw* p = twq + S * (kStrEntries * 512u);
-      return [=](int i, int hi) { return ldtw(p + ((i == 3 ? 0 : (i == 2 ? 1 : (i == 1 ? 3 : 7))) + hi) * 512); };
-    };
-
-    // ---- stream A: Q2, e2 write; stream B: Q2; A: e2 read ... ----
-    str::pass16<A, 4, false>(v, c, q2tw(0));
     if (l == 0) bulk_wait_read();  // the previous block's last output store has read this warp's 4 KiB
     __syncwarp();
 #pragma unroll
     for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256)) = v[r];
     __syncwarp();
-    str::pass16<A, 4, false>(v + 16, c, q2tw(1));
+    NK_GTS(7);
+    str::pass16<A, 4, false>(v + 16, c, q2tw(1, pb));
+    pb[0] = ldtw(q3addr(1, 3, 0)), pb[1] = ldtw(q3addr(1, 2, 0)), pb[2] = ldtw(q3addr(1, 2, 1));  // B's Q3
+    NK_GTS(8);
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(Ew + (e2r ^ (r << 4)));
     __syncwarp();  // A's words are in registers: the buffer takes B's
@@ -240,37 +286,38 @@ __global__ void __launch_bounds__(512, 1)
     for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256)) = v[16 + r];
     __syncwarp();
 
+    NK_GTS(9);
     const int32_t orow16 = static_cast<int32_t>((row * a.n + boff + (static_cast<uint64_t>(w) << 9)) >> 4);
-
+    // ---- Q3 of both streams together (B's words read back first), shuffle, Q4 ----
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[16 + r] = *reinterpret_cast<const uint64_t*>(Ew + (e2r ^ (r << 4)));
+    str::pass16x2<A, 4>(v, c, q3tw(0, pa), q3tw(1, pb));
+    const bool odd = (l & 1u) != 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      // lane pairs swap: this lane keeps j1 = its bit 0 and gets both j0
+      // (registers r3 = j1 | hi << 1: own words (j0 = lane bit) with j1 = 0 / 1)
+      const uint64_t own0 = v[2 * q], own1 = v[2 * q + 1];
+      const uint64_t recv = __shfl_xor_sync(0xffffffffu, odd ? own0 : own1, 1);
+      v[2 * q] = odd ? recv : own0;      // j0 = 0, j1 = lane bit
+      v[2 * q + 1] = odd ? own1 : recv;  // j0 = 1
+    }
+    // Q4: bit 0, twiddle entries 15 + hi
+#pragma unroll
+    for (int hi = 0; hi < 8; ++hi) {
+#ifdef NK_STR_NOTW
+      const Tw wa = ldtw(twq), wb = ldtw(twq + 512);
+#else
+      const Tw wa = ldtw(twq + (15 + hi) * 512);
+      const Tw wb = ldtw(twq + (kStrEntries + 15 + hi) * 512);
+#endif
+      A::template fwd<false>(v[2 * hi], v[2 * hi + 1], wa, c);
+      A::template fwd<false>(v[16 + 2 * hi], v[16 + 2 * hi + 1], wb, c);
+    }
+    NK_GTS(10);
 #pragma unroll
     for (uint32_t S = 0; S < 2; ++S) {
-      uint64_t* x = v + 16 * S;
-      if (S == 0) {
-        // B's Q3 words are read before A's Q3 runs (the loads overlap it), which
-        // also frees the warp's buffer for A's output image
-#pragma unroll
-        for (int r = 0; r < 16; ++r) v[16 + r] = *reinterpret_cast<const uint64_t*>(Ew + (e2r ^ (r << 4)));
-      }
-      str::pass16<A, 4, false>(x, c, q3tw(S));
-      // lane pairs swap: this lane keeps j1 = its bit 0 and gets both j0
-      uint64_t y[16];
-      const bool odd = (l & 1u) != 0;
-#pragma unroll
-      for (int hi = 0; hi < 8; ++hi) {
-        // registers r3 = j1 | hi << 1: own words (j0 = lane bit) with j1 = 0 / 1
-        const uint64_t own0 = x[2 * hi], own1 = x[2 * hi + 1];
-        const uint64_t send = odd ? own0 : own1;
-        const uint64_t recv = __shfl_xor_sync(0xffffffffu, send, 1);
-        y[2 * hi] = odd ? recv : own0;      // j0 = 0, j1 = lane bit
-        y[2 * hi + 1] = odd ? own1 : recv;  // j0 = 1
-      }
-      // Q4: bit 0, twiddle entry 15 + hi
-      const Tw* p4 = twq + S * (kStrEntries * 512u) + 15 * 512;
-#pragma unroll
-      for (int hi = 0; hi < 8; ++hi) {
-        const Tw wv = ldtw(p4 + hi * 512);
-        A::template fwd<false>(y[2 * hi], y[2 * hi + 1], wv, c);
-      }
+      uint64_t* y = v + 16 * S;
 #pragma unroll
       for (int i = 0; i < 16; ++i) y[i] = fwd_out<A>(y[i], c, a.fout);
       // image: word m = j0 | j1 << 1 | hi << 2 | (l >> 1) << 5 at row m >> 4, chunk ((m >> 1) & 7) ^ (row & 7)
@@ -294,7 +341,9 @@ __global__ void __launch_bounds__(512, 1)
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     }
+    NK_GTS(11);
     phase ^= 1;
+    ++it_;
   }
   if (l == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
