@@ -148,6 +148,8 @@ struct nk_plan {
   // forward low-stage twiddles of the two-stream kernel (NttArgs::twq), [limb][block][stream][entry][thread]
   ulonglong2* twq_fwd = nullptr;
   uint64_t* twq8_fwd = nullptr;
+  ulonglong2* twq_inv = nullptr;
+  uint64_t* twq8_inv = nullptr;
   nk::LimbConst* lc = nullptr;   // [limb]
   nk::MultConst* mc[3] = {nullptr, nullptr, nullptr};  // fin = 1, 2, 4
 };
@@ -232,8 +234,8 @@ int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64
   a.twl8 = fwd ? p->twl8_fwd : p->twl8_inv;
   a.twg = fwd ? p->twg_fwd : p->twg_inv;
   a.twg8 = fwd ? p->twg8_fwd : p->twg8_inv;
-  a.twq = p->twq_fwd;
-  a.twq8 = p->twq8_fwd;
+  a.twq = fwd ? p->twq_fwd : p->twq_inv;
+  a.twq8 = fwd ? p->twq8_fwd : p->twq8_inv;
   a.lc = p->lc;
   a.n = p->n;
   a.logn = p->logn;
@@ -486,6 +488,8 @@ void nk_plan_destroy(nk_plan* p) {
   cudaFree(p->twg8_inv);
   cudaFree(p->twq_fwd);
   cudaFree(p->twq8_fwd);
+  cudaFree(p->twq_inv);
+  cudaFree(p->twq8_inv);
   cudaFree(p->lc);
   for (auto* m : p->mc) cudaFree(m);
   cudaSetDevice(cur);
@@ -515,7 +519,7 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
   const bool blocks = n >= (uint64_t{1} << 14);
   std::vector<ulonglong2> hgf(blocks ? n * nlimbs : 0), hgi(blocks ? n * nlimbs : 0);
   const uint64_t qper = (n >> 14) * nk::kStrTableWords;  // two-stream table entries per limb
-  std::vector<ulonglong2> hqf(blocks ? qper * nlimbs : 0);
+  std::vector<ulonglong2> hqf(blocks ? qper * nlimbs : 0), hqi(blocks ? qper * nlimbs : 0);
   std::vector<nk::LimbConst> hl(nlimbs);
   std::vector<nk::MultConst> hm[3];
   for (auto& v : hm) v.resize(nlimbs);
@@ -556,9 +560,12 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
       for (uint64_t blk = 0; blk < (n >> 14); ++blk)
         for (uint32_t S = 0; S < 2; ++S)
           for (int e = 0; e < nk::kStrEntries; ++e)
-            for (uint32_t t = 0; t < 512; ++t)
-              hqf[l * qper + blk * nk::kStrTableWords + (S * nk::kStrEntries + e) * 512 + t] =
-                  hf[l * n + nk::str_tw_index(n, blk << 14, S, e, t)];
+            for (uint32_t t = 0; t < 512; ++t) {
+              const uint64_t dst = l * qper + blk * nk::kStrTableWords + (S * nk::kStrEntries + e) * 512 + t;
+              const uint64_t src = l * n + nk::str_tw_index(n, blk << 14, S, e, t);
+              hqf[dst] = hf[src];
+              hqi[dst] = hi[src];
+            }
     }
     // -q modulo 2^64 (the 52-bit negated modulus of ntt.hpp:85-92 agrees modulo 2^52,
     // see modmath.cuh)
@@ -586,7 +593,9 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
                   (e = cudaMalloc(&p->twg_inv, hgi.size() * sizeof(ulonglong2))) ||
                   (e = cudaMalloc(&p->twg8_fwd, hgf.size() * 8)) || (e = cudaMalloc(&p->twg8_inv, hgi.size() * 8)) ||
                   (e = cudaMalloc(&p->twq_fwd, hqf.size() * sizeof(ulonglong2))) ||
-                  (e = cudaMalloc(&p->twq8_fwd, hqf.size() * 8)))) ||
+                  (e = cudaMalloc(&p->twq8_fwd, hqf.size() * 8)) ||
+                  (e = cudaMalloc(&p->twq_inv, hqi.size() * sizeof(ulonglong2))) ||
+                  (e = cudaMalloc(&p->twq8_inv, hqi.size() * 8)))) ||
       (e = cudaMalloc(&p->lc, hl.size() * sizeof(nk::LimbConst))))
     return cleanup(cuda_fail(e, "cudaMalloc(plan tables)"));
   for (int f = 0; f < 3; ++f)
@@ -604,9 +613,9 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
   put(p->tw_fwd, hf.data(), hf.size() * sizeof(ulonglong2));
   put(p->tw_inv, hi.data(), hi.size() * sizeof(ulonglong2));
   // the w halves of the beta = 2^52 entries (double bits; other limbs' words are unused)
-  std::vector<uint64_t> h8[7];
-  const std::vector<ulonglong2>* src8[7] = {&hf, &hi, &hlf, &hli, &hgf, &hgi, &hqf};
-  for (int i = 0; i < 7; ++i) {
+  std::vector<uint64_t> h8[8];
+  const std::vector<ulonglong2>* src8[8] = {&hf, &hi, &hlf, &hli, &hgf, &hgi, &hqf, &hqi};
+  for (int i = 0; i < 8; ++i) {
     h8[i].resize(src8[i]->size());
     for (size_t k = 0; k < h8[i].size(); ++k) h8[i][k] = (*src8[i])[k].x;
   }
@@ -621,6 +630,8 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
     put(p->twg8_inv, h8[5].data(), h8[5].size() * 8);
     put(p->twq_fwd, hqf.data(), hqf.size() * sizeof(ulonglong2));
     put(p->twq8_fwd, h8[6].data(), h8[6].size() * 8);
+    put(p->twq_inv, hqi.data(), hqi.size() * sizeof(ulonglong2));
+    put(p->twq8_inv, h8[7].data(), h8[7].size() * 8);
   }
   put(p->lc, hl.data(), hl.size() * sizeof(nk::LimbConst));
   for (int f = 0; f < 3; ++f) put(p->mc[f], hm[f].data(), nlimbs * sizeof(nk::MultConst));

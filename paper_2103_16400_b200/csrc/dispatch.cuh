@@ -173,6 +173,23 @@ int launch_str_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStre
   return 0;
 }
 
+template <auto KERN>
+int launch_stri_k(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
+  CUtensorMap map;
+  if (int rc = make_map(&map, kRowMap, a.in, buf_words)) return rc;
+  if (int rc = set_smem_once<KERN>(kStrSmemBytes)) return rc;
+  const uint64_t g = nitems < static_cast<uint64_t>(sm_count()) ? nitems : sm_count();
+  KERN<<<static_cast<unsigned>(g), 512, kStrSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));
+  launches++;
+  NK_CUDA(cudaGetLastError());
+  return 0;
+}
+template <class A, bool IL>
+int launch_stri_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
+  if (a.logn > 14) return launch_stri_k<ntt_stri14<A, IL, true>>(a, nitems, buf_words, st);
+  return launch_stri_k<ntt_stri14<A, IL>>(a, nitems, buf_words, st);
+}
+
 // CTA-pair kernel (ntt_pair.cuh): persistent, one cluster of 2 per block in
 // flight, as many clusters as fit (2 CTAs per SM).
 template <auto KERN, bool FWD>
@@ -228,6 +245,9 @@ int launch_tma(const NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm,
   if constexpr (FWD)
     if (!a.mulb && (block_kernel == 2 || block_kernel < 0))  // the default forward: two streams per thread
       return iltm ? launch_str_t<A, true>(a, nitems, buf_words, st) : launch_str_t<A, false>(a, nitems, buf_words, st);
+  if constexpr (!FWD)
+    if (block_kernel == 2)
+      return iltm ? launch_stri_t<A, true>(a, nitems, buf_words, st) : launch_stri_t<A, false>(a, nitems, buf_words, st);
   if (pair)
     return iltm ? launch_pair_t<A, FWD, true>(a, nitems, buf_words, st)
                 : launch_pair_t<A, FWD, false>(a, nitems, buf_words, st);

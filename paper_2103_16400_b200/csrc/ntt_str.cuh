@@ -103,6 +103,23 @@ __device__ __forceinline__ void pass16(uint64_t* x, const LimbConst& c, F&& twf)
   }
 }
 
+// The inverse's stages (bit LO first) on 16 registers; twiddles as in pass16.
+template <class A, class F>
+__device__ __forceinline__ void pass16i(uint64_t* x, const LimbConst& c, F&& twf) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+#pragma unroll
+    for (int hi = 0; hi < (16 >> (i + 1)); ++hi) {
+      const typename A::Tw w = twf(i, hi);
+#pragma unroll
+      for (int lo = 0; lo < (1 << i); ++lo) {
+        const int r0 = (hi << (i + 1)) | lo, r1 = r0 | (1 << i);
+        A::template inv<false>(x[r0], x[r1], w, c);
+      }
+    }
+  }
+}
+
 // the same stages on both streams at once (x and x + 16), stage by stage: 16 independent butterflies per stage
 template <class A, int NST, class FA, class FB>
 __device__ __forceinline__ void pass16x2(uint64_t* x, const LimbConst& c, FA&& twa, FB&& twb) {
@@ -346,6 +363,210 @@ __global__ void __launch_bounds__(512, 1)
     ++it_;
   }
   if (l == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// ntt_stri14: the inverse as two streams per thread, the mirror image of
+// ntt_str14. The inverse's stages 0..12 stay inside the two 8192-word halves;
+// only the last one (bit 13) pairs them, in a thread's own registers.
+//   in   each warp reads the 512 consecutive words of its two streams from the
+//        staging buffer (the TMA's 128B-swizzled lines are the forward's
+//        output image): registers (j0; j2, j3, j4), lane bit 0 = j1
+//   Q4'  bit 0; sh: j0 back to the lane; Q3' bits 1..4; e2' warp-local;
+//   Q2'  bits 5..8; e1' CTA-wide, in place in the stream's staging half (after
+//        every warp has read its input), plain layout: both sides have lanes
+//        j0..j4;  P1' bits 9..12 per stream (lanes j0..j4, warps j5..j8), then
+//        bit 13 on both (n^-1 folded in for canonical outputs), 256-byte
+//        contiguous stores per warp instruction
+// ---------------------------------------------------------------------------
+template <class A, bool ILTM0, bool LONG = false>
+__global__ void __launch_bounds__(512, 1)
+    ntt_stri14(const __grid_constant__ CUtensorMap tin, NttArgs a, uint32_t nitems) {
+  using Tw = typename A::Tw;
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* St = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+  uint8_t* E = St + kStageBytes;
+  const LimbConst* Cs = reinterpret_cast<const LimbConst*>(E + kGrpExBytes);
+  uint64_t* bar_full = reinterpret_cast<uint64_t*>(E + kGrpExBytes + 2 * sizeof(LimbConst));
+  uint64_t* bar_rd = bar_full + 1;  // every warp has read its input words
+  uint64_t* bar_w = bar_full + 2;   // [2] every warp has written its e1' words of stream S
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(bar_full + 4);
+  const uint32_t t = threadIdx.x, l = t & 31u, w = t >> 5;
+  const uint32_t lognb = a.logn - kB14;
+  const uint64_t rowwords16 = a.n >> 4;
+
+  auto item_row = [&](uint32_t k, uint64_t& row, uint64_t& blk) {
+    row = (static_cast<uint64_t>(k) >> lognb) * a.row_mul + a.row_add;
+    blk = static_cast<uint64_t>(k) & ((uint64_t{1} << lognb) - 1);
+  };
+  auto issue = [&](uint32_t k, uint32_t slot) {
+    uint64_t row, blk;
+    item_row(k, row, blk);
+    const int32_t y0 = static_cast<int32_t>(row * rowwords16 + (blk << (kB14 - 4)));
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+    mbar_expect_tx(bar_full, kStageBytes + static_cast<uint32_t>(sizeof(LimbConst)));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tma_load_2d(St + q * 32768, &tin, 0, y0 + q * 256, bar_full);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(Cs + slot)),
+                 "l"(a.lc + limb), "r"(static_cast<uint32_t>(sizeof(LimbConst))), "r"(smem_u32(bar_full))
+                 : "memory");
+  };
+
+  if (t == 0) {
+    mbar_init(bar_full, 1);
+    mbar_init(bar_rd, 16);
+    mbar_init(bar_w, 16);
+    mbar_init(bar_w + 1, 16);
+    *cnt = 0;
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tin)) : "memory");
+  }
+  __syncthreads();
+  if (t == 0 && blockIdx.x < nitems) issue(blockIdx.x, 0);
+
+  // input image (= ntt_str14's output image): pair hi at row (hi >> 2) + 2 (l >> 1),
+  // chunk ((l & 1) | (hi & 3) << 1) ^ (row & 7): base ^ ((hi & 3) << 5) ^ ((hi >> 2) << 4 ...) folded below
+  const uint32_t in0 = w << 12;
+  uint8_t* Ew = E + (w << 12);
+  const uint32_t e2w = l << 3;
+  const uint32_t e2r = ((l & 1u) << 3) | (((l >> 1) & 7u) << 4) | ((l >> 1) << 8);
+  const uint32_t e1w = (l << 3) + (w << 12);  // Q2' map: word l | r << 5 | w << 9
+  const uint32_t e1r = (l << 3) + (w << 8);   // P1' map: word l | w << 5 | r << 9
+  uint32_t phase = 0;
+
+  for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
+    uint64_t row, blk;
+    item_row(k, row, blk);
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+    const Tw* __restrict__ tw = tw_of<A>(a, limb);
+    const Tw* __restrict__ twq = twq_of<A>(a, limb) + blk * kStrTableWords + t;
+    const uint64_t boff = blk << kB14;
+    const uint64_t xbase = a.n + boff;
+    uint64_t* __restrict__ dst = a.out + row * a.n + boff;
+    uint64_t v[32];
+
+    auto q3addr = [&](uint32_t S, int i, int hi) {
+      return twq + S * (kStrEntries * 512u) + ((i == 3 ? 0 : (i == 2 ? 1 : (i == 1 ? 3 : 7))) + hi) * 512;
+    };
+    auto q3tw = [&](uint32_t S) { return [=](int i, int hi) { return ldtw(q3addr(S, i, hi)); }; };
+    auto q2tw = [&](uint32_t S) {
+      const uint64_t js = xbase + (static_cast<uint64_t>(w) << 9) + (static_cast<uint64_t>(S) << 13);
+      return [=](int i, int hi) { return ldtw(tw + (js >> (6 + i)) + hi); };
+    };
+    auto p1tw = [&](uint32_t S) {
+      const uint64_t js = xbase + (static_cast<uint64_t>(S) << 13);
+      return [=](int i, int hi) { return ldtw(tw + (js >> (10 + i)) + hi); };
+    };
+
+    // ---- input: both streams' words, (j0 = 0, 1) pairs ----
+    mbar_wait(bar_full, phase);
+    const LimbConst& c = Cs[phase];
+#pragma unroll
+    for (uint32_t S = 0; S < 2; ++S)
+#pragma unroll
+      for (int hi = 0; hi < 8; ++hi) {
+        const uint32_t rowi = (hi >> 2) + 2 * (l >> 1);
+        const uint32_t chunk = ((l & 1u) | ((hi & 3) << 1)) ^ (rowi & 7u);
+        const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(St + (S << 16) + in0 + (rowi << 7) + (chunk << 4));
+        v[16 * S + 2 * hi] = A::load(p.x);
+        v[16 * S + 2 * hi + 1] = A::load(p.y);
+      }
+    __syncwarp();
+    if (l == 0) mbar_arrive_local(bar_rd);
+
+    const bool odd = (l & 1u) != 0;
+    auto low_passes = [&](uint32_t S) {
+      uint64_t* x = v + 16 * S;
+      // Q4': bit 0
+      const Tw* p4 = twq + S * (kStrEntries * 512u) + 15 * 512;
+#pragma unroll
+      for (int hi = 0; hi < 8; ++hi) {
+        const Tw wv = ldtw(p4 + hi * 512);
+        if (ILTM0) A::template inv<true>(x[2 * hi], x[2 * hi + 1], wv, c);
+        else A::template inv<false>(x[2 * hi], x[2 * hi + 1], wv, c);
+      }
+      // j0 back to the lane: this lane keeps j0 = its bit 0 and gets both j1
+#pragma unroll
+      for (int hi = 0; hi < 8; ++hi) {
+        const uint64_t y0 = x[2 * hi], y1 = x[2 * hi + 1];
+        const uint64_t recv = __shfl_xor_sync(0xffffffffu, odd ? y0 : y1, 1);
+        x[2 * hi] = odd ? recv : y0;      // j1 = 0
+        x[2 * hi + 1] = odd ? y1 : recv;  // j1 = 1
+      }
+      str::pass16i<A>(x, c, q3tw(S));  // Q3': bits 1..4
+    };
+
+    low_passes(0);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + (e2r ^ (r << 4))) = v[r];
+    __syncwarp();
+    low_passes(1);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256));
+    __syncwarp();  // A's words are in registers: the buffer takes B's
+#pragma unroll
+    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + (e2r ^ (r << 4))) = v[16 + r];
+    __syncwarp();
+
+    // ---- Q2' of A; B's words back; e1' of A ----
+    str::pass16i<A>(v, c, q2tw(0));
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      v[16 + r] = *reinterpret_cast<const uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256));
+    mbar_wait(bar_rd, phase);  // every warp has read its input: the staging halves take the streams
+#pragma unroll
+    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + e1w + r * 256) = v[r];
+    __syncwarp();
+    if (l == 0) mbar_arrive_local(bar_w);
+    str::pass16i<A>(v + 16, c, q2tw(1));
+#pragma unroll
+    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + 65536 + e1w + r * 256) = v[16 + r];
+    __syncwarp();
+    if (l == 0) mbar_arrive_local(bar_w + 1);
+
+    // ---- P1': bits 9..12 per stream, then bit 13 ----
+    mbar_wait(bar_w, phase);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(St + e1r + r * 4096);
+    str::pass16i<A>(v, c, p1tw(0));
+    mbar_wait(bar_w + 1, phase);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[16 + r] = *reinterpret_cast<const uint64_t*>(St + 65536 + e1r + r * 4096);
+    grp::staging_consumed(cnt, l, [&] {
+      if (k + gridDim.x < nitems) {
+        fence_proxy_async();
+        issue(k + gridDim.x, phase ^ 1);
+      }
+    });
+    str::pass16i<A>(v + 16, c, p1tw(1));
+
+    constexpr bool kFoldLast = A::kSigned && !LONG;
+    const uint32_t jo = l | (w << 5);
+    if constexpr (kFoldLast) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        A::inv_fold(v[r], v[r + 16], c);
+        dst[jo | (static_cast<uint32_t>(r) << 9)] = v[r];
+        dst[jo | (static_cast<uint32_t>(r + 16) << 9)] = v[r + 16];
+      }
+    } else {
+      const Tw w13 = ldtw(tw + (xbase >> 14));
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        A::template inv<false>(v[r], v[r + 16], w13, c);
+        if constexpr (LONG) {
+          v[r] = A::store(v[r]);  // intermediate of a long row
+          v[r + 16] = A::store(v[r + 16]);
+        } else {
+          v[r] = inv_out<A>(v[r], c, a.fout);
+          v[r + 16] = inv_out<A>(v[r + 16], c, a.fout);
+        }
+        dst[jo | (static_cast<uint32_t>(r) << 9)] = v[r];
+        dst[jo | (static_cast<uint32_t>(r + 16) << 9)] = v[r + 16];
+      }
+    }
+    phase ^= 1;
+  }
 }
 
 }  // namespace nk
