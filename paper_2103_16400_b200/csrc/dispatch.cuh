@@ -246,7 +246,7 @@ int launch_tma(const NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm,
     if (!a.mulb && (block_kernel == 2 || block_kernel < 0))  // the default forward: two streams per thread
       return iltm ? launch_str_t<A, true>(a, nitems, buf_words, st) : launch_str_t<A, false>(a, nitems, buf_words, st);
   if constexpr (!FWD)
-    if (block_kernel == 2)
+    if (block_kernel == 2 || block_kernel < 0)  // the default inverse: two streams per thread
       return iltm ? launch_stri_t<A, true>(a, nitems, buf_words, st) : launch_stri_t<A, false>(a, nitems, buf_words, st);
   if (pair)
     return iltm ? launch_pair_t<A, FWD, true>(a, nitems, buf_words, st)

@@ -433,6 +433,8 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t e1w = (l << 3) + (w << 12);  // Q2' map: word l | r << 5 | w << 9
   const uint32_t e1r = (l << 3) + (w << 8);   // P1' map: word l | w << 5 | r << 9
   uint32_t phase = 0;
+  uint32_t it_ = 0;
+  (void)it_;
 
   for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
     uint64_t row, blk;
@@ -458,9 +460,21 @@ __global__ void __launch_bounds__(512, 1)
       return [=](int i, int hi) { return ldtw(tw + (js >> (10 + i)) + hi); };
     };
 
+    // the first two stages' twiddles of stream A (8 + 8 table entries) are loaded before the wait
+    // for the block, B's while A computes: the block does not start by waiting for L2
+    // (8-byte twiddles; with 16-byte entries the second eight would spill)
+    constexpr bool kPre16 = sizeof(Tw) == 8;
+    Tw ta[kPre16 ? 16 : 8];
+#pragma unroll
+    for (int hi = 0; hi < 8; ++hi) {
+      ta[hi] = ldtw(twq + (15 + hi) * 512);
+      if constexpr (kPre16) ta[8 + hi] = ldtw(q3addr(0, 0, hi));
+    }
+    NK_GTS(0);
     // ---- input: both streams' words, (j0 = 0, 1) pairs ----
     mbar_wait(bar_full, phase);
     const LimbConst& c = Cs[phase];
+    NK_GTS(1);
 #pragma unroll
     for (uint32_t S = 0; S < 2; ++S)
 #pragma unroll
@@ -473,19 +487,18 @@ __global__ void __launch_bounds__(512, 1)
       }
     __syncwarp();
     if (l == 0) mbar_arrive_local(bar_rd);
+    NK_GTS(2);
 
     const bool odd = (l & 1u) != 0;
-    auto low_passes = [&](uint32_t S) {
+    // Q4' (bit 0), j0 back to the lane, Q3' (bits 1..4) of stream S; tq: its first 16 twiddles
+    auto low_passes = [&](uint32_t S, const Tw* tq) {
       uint64_t* x = v + 16 * S;
-      // Q4': bit 0
-      const Tw* p4 = twq + S * (kStrEntries * 512u) + 15 * 512;
 #pragma unroll
       for (int hi = 0; hi < 8; ++hi) {
-        const Tw wv = ldtw(p4 + hi * 512);
-        if (ILTM0) A::template inv<true>(x[2 * hi], x[2 * hi + 1], wv, c);
-        else A::template inv<false>(x[2 * hi], x[2 * hi + 1], wv, c);
+        if (ILTM0) A::template inv<true>(x[2 * hi], x[2 * hi + 1], tq[hi], c);
+        else A::template inv<false>(x[2 * hi], x[2 * hi + 1], tq[hi], c);
       }
-      // j0 back to the lane: this lane keeps j0 = its bit 0 and gets both j1
+      // this lane keeps j0 = its bit 0 and gets both j1
 #pragma unroll
       for (int hi = 0; hi < 8; ++hi) {
         const uint64_t y0 = x[2 * hi], y1 = x[2 * hi + 1];
@@ -493,26 +506,35 @@ __global__ void __launch_bounds__(512, 1)
         x[2 * hi] = odd ? recv : y0;      // j1 = 0
         x[2 * hi + 1] = odd ? y1 : recv;  // j1 = 1
       }
-      str::pass16i<A>(x, c, q3tw(S));  // Q3': bits 1..4
+      str::pass16i<A>(x, c, [=](int i, int hi) { return (kPre16 && i == 0) ? tq[kPre16 ? 8 + hi : 0] : ldtw(q3addr(S, i, hi)); });
     };
 
-    low_passes(0);
+    low_passes(0, ta);
 #pragma unroll
     for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + (e2r ^ (r << 4))) = v[r];
     __syncwarp();
-    low_passes(1);
+    NK_GTS(3);
+#pragma unroll
+    for (int hi = 0; hi < 8; ++hi) {
+      ta[hi] = ldtw(twq + (kStrEntries + 15 + hi) * 512);
+      if constexpr (kPre16) ta[8 + hi] = ldtw(q3addr(1, 0, hi));
+    }
+    low_passes(1, ta);
+    NK_GTS(4);
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256));
     __syncwarp();  // A's words are in registers: the buffer takes B's
 #pragma unroll
     for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + (e2r ^ (r << 4))) = v[16 + r];
     __syncwarp();
+    NK_GTS(5);
 
     // ---- Q2' of A; B's words back; e1' of A ----
     str::pass16i<A>(v, c, q2tw(0));
 #pragma unroll
     for (int r = 0; r < 16; ++r)
       v[16 + r] = *reinterpret_cast<const uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256));
+    NK_GTS(6);
     mbar_wait(bar_rd, phase);  // every warp has read its input: the staging halves take the streams
 #pragma unroll
     for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + e1w + r * 256) = v[r];
@@ -523,12 +545,15 @@ __global__ void __launch_bounds__(512, 1)
     for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + 65536 + e1w + r * 256) = v[16 + r];
     __syncwarp();
     if (l == 0) mbar_arrive_local(bar_w + 1);
+    NK_GTS(7);
 
     // ---- P1': bits 9..12 per stream, then bit 13 ----
     mbar_wait(bar_w, phase);
+    NK_GTS(8);
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(St + e1r + r * 4096);
     str::pass16i<A>(v, c, p1tw(0));
+    NK_GTS(9);
     mbar_wait(bar_w + 1, phase);
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[16 + r] = *reinterpret_cast<const uint64_t*>(St + 65536 + e1r + r * 4096);
@@ -539,6 +564,7 @@ __global__ void __launch_bounds__(512, 1)
       }
     });
     str::pass16i<A>(v + 16, c, p1tw(1));
+    NK_GTS(10);
 
     constexpr bool kFoldLast = A::kSigned && !LONG;
     const uint32_t jo = l | (w << 5);
@@ -565,7 +591,9 @@ __global__ void __launch_bounds__(512, 1)
         dst[jo | (static_cast<uint32_t>(r + 16) << 9)] = v[r + 16];
       }
     }
+    NK_GTS(11);
     phase ^= 1;
+    ++it_;
   }
 }
 
