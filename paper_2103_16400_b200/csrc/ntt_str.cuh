@@ -142,11 +142,265 @@ __device__ __forceinline__ void pass16x2(uint64_t* x, const LimbConst& c, FA&& t
 
 }  // namespace str
 
+namespace str {
+
+// The stamps of an NK_DBG_TIMELINE build (NK_GTS, ntt_grp.cuh) use `a`, `l`, `w`, `it_` of the caller.
+
+// Forward core: from the block in the staging buffer (bar_full waited by the
+// caller) to the Q4 results: v[16 S + 2 hi + j0] of stream S, with lane bit 0 =
+// j1, lane bits 1..4 = j5..j8, warp = j9..j12, before the final reduction.
+// `par`: parity of bar_rd / bar_w for this transform; `before_e2` runs before
+// the warp's 4 KiB buffer is first written (e.g. waits for a store that still
+// reads it); `consumed` once this warp has read its last staging word.
+template <class A, bool ILTM0, class FPRE, class FCONS>
+__device__ __forceinline__ void fwd_core(uint64_t (&v)[32], uint8_t* St, uint8_t* Ew, const LimbConst& c,
+                                         const NttArgs& a, const typename A::Tw* __restrict__ tw,
+                                         const typename A::Tw* __restrict__ twq, uint64_t xbase, uint32_t w,
+                                         uint32_t l, uint64_t* bar_rd, uint64_t* bar_w, uint32_t par, uint32_t it_,
+                                         FPRE&& before_e2, FCONS&& consumed) {
+  using P1 = PassD<9, 5, -1>;
+  using Tw = typename A::Tw;
+  (void)it_;
+  // ---- thread-constant byte offsets ----
+  const uint32_t jt1 = StrMap::jt1(w, l);
+  // e1, write side: stream word j' = jt1 | r << 9 at chunk-swizzled position
+  //   phys(j') = j' ^ (((j' >> 4) & 7) << 1): the half-warp's lanes (j0, j4, j5, j6) hit 16 distinct 8-byte slots
+  const uint32_t e1w = (jt1 ^ (((jt1 >> 4) & 7u) << 1)) << 3;  // + r * 4096 + S * 65536
+  // e1, read side: j' = l | r << 5 | w << 9 (lanes j0..j4): (base ^ ((r & 3) << 5)) + r * 256
+  const uint32_t e1r = ((l ^ ((l >> 4) << 1)) << 3) + (w << 12);
+  // e2 (warp-local, word m = j & 511 at m ^ (((m >> 5) & 7) << 1)): write (l << 3 ^ (r & 7) << 4) + r * 256,
+  // read tb ^ (r3 << 4)
+  const uint32_t e2w = l << 3;
+  const uint32_t e2r = ((l & 1u) << 3) | (((l >> 1) & 7u) << 4) | ((l >> 1) << 8);
+
+  // ---- P1: words from the staging buffer, stage 13, then stages 12..9 per stream ----
+  grp::p1_read<A, true>(v, St, jt1);
+  __syncwarp();
+  if (l == 0) mbar_arrive_local(bar_rd);
+  NK_GTS(2);
+  stages14<A, true, P1, ILTM0, 0, 1>(v, tw, tw, a.n, xbase + jt1, c);
+  stages14<A, true, P1, ILTM0, 1, 5, 0>(v, tw, tw, a.n, xbase + jt1, c);
+  NK_GTS(3);
+  // e1 of stream A: in place in the lower half of the staging buffer
+  mbar_wait(bar_rd, par);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + e1w + r * 4096) = v[r];
+  __syncwarp();
+  if (l == 0) mbar_arrive_local(bar_w);
+  NK_GTS(4);
+  stages14<A, true, P1, ILTM0, 1, 5, 1>(v, tw, tw, a.n, xbase + jt1, c);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + 65536 + e1w + r * 4096) = v[16 + r];
+  __syncwarp();
+  if (l == 0) mbar_arrive_local(bar_w + 1);
+  NK_GTS(5);
+
+  // Twiddles. Q2: (N + j) >> (b + 1), b = 5 + i, j = w << 9 | S << 13 (+ r << 5): warp-uniform loads of
+  // the reference-order table; Q3 / Q4: the (stream, entry, thread) table. The twiddles of a pass's
+  // first two stages (3 values) are loaded ahead of the data movement in front of the pass (`pre`),
+  // so that no pass starts by waiting for L2.
+  auto q2addr = [&](uint32_t S, int i, int hi) {
+    const uint64_t js = xbase + (static_cast<uint64_t>(w) << 9) + (static_cast<uint64_t>(S) << 13);
+    return tw + (js >> (6 + i)) + hi;
+  };
+  auto q3addr = [&](uint32_t S, int i, int hi) {
+#ifdef NK_STR_NOTW  // timing experiment (wrong results): every low-stage twiddle from one address
+    return twq + 0 * (S + i + hi);
+#else
+    return twq + S * (kStrEntries * 512u) + ((i == 3 ? 0 : (i == 2 ? 1 : (i == 1 ? 3 : 7))) + hi) * 512;
+#endif
+  };
+  Tw pa[3], pb[3];
+  pa[0] = ldtw(q2addr(0, 3, 0)), pa[1] = ldtw(q2addr(0, 2, 0)), pa[2] = ldtw(q2addr(0, 2, 1));
+  pb[0] = ldtw(q2addr(1, 3, 0)), pb[1] = ldtw(q2addr(1, 2, 0)), pb[2] = ldtw(q2addr(1, 2, 1));
+  auto q2tw = [&](uint32_t S, const Tw* pre) {
+    return [=](int i, int hi) { return i >= 2 ? pre[i == 3 ? 0 : 1 + hi] : ldtw(q2addr(S, i, hi)); };
+  };
+  auto q3tw = [&](uint32_t S, const Tw* pre) {
+    return [=](int i, int hi) { return i >= 2 ? pre[i == 3 ? 0 : 1 + hi] : ldtw(q3addr(S, i, hi)); };
+  };
+
+  // ---- Q2 of stream A first: the wait for B (every warp through P1) comes after it, when the
+  // slower warps have caught up ----
+  mbar_wait(bar_w, par);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(St + ((e1r ^ ((r & 3) << 5)) + r * 256));
+  NK_GTS(6);
+  pass16<A, 4, false>(v, c, q2tw(0, pa));
+  pa[0] = ldtw(q3addr(0, 3, 0)), pa[1] = ldtw(q3addr(0, 2, 0)), pa[2] = ldtw(q3addr(0, 2, 1));  // A's Q3
+  mbar_wait(bar_w + 1, par);
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+    v[16 + r] = *reinterpret_cast<const uint64_t*>(St + 65536 + ((e1r ^ ((r & 3) << 5)) + r * 256));
+  consumed();  // the staging buffer is consumed by this warp
+  before_e2();
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256)) = v[r];
+  __syncwarp();
+  NK_GTS(7);
+  pass16<A, 4, false>(v + 16, c, q2tw(1, pb));
+  pb[0] = ldtw(q3addr(1, 3, 0)), pb[1] = ldtw(q3addr(1, 2, 0)), pb[2] = ldtw(q3addr(1, 2, 1));  // B's Q3
+  NK_GTS(8);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(Ew + (e2r ^ (r << 4)));
+  __syncwarp();  // A's words are in registers: the buffer takes B's
+#pragma unroll
+  for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256)) = v[16 + r];
+  __syncwarp();
+  NK_GTS(9);
+
+  // ---- Q3 of both streams together (B's words read back first), shuffle, Q4 ----
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[16 + r] = *reinterpret_cast<const uint64_t*>(Ew + (e2r ^ (r << 4)));
+  pass16x2<A, 4>(v, c, q3tw(0, pa), q3tw(1, pb));
+  const bool odd = (l & 1u) != 0;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    // lane pairs swap: this lane keeps j1 = its bit 0 and gets both j0
+    // (registers r3 = j1 | hi << 1: own words (j0 = lane bit) with j1 = 0 / 1)
+    const uint64_t own0 = v[2 * q], own1 = v[2 * q + 1];
+    const uint64_t recv = __shfl_xor_sync(0xffffffffu, odd ? own0 : own1, 1);
+    v[2 * q] = odd ? recv : own0;      // j0 = 0, j1 = lane bit
+    v[2 * q + 1] = odd ? own1 : recv;  // j0 = 1
+  }
+  // Q4: bit 0, twiddle entries 15 + hi
+#pragma unroll
+  for (int hi = 0; hi < 8; ++hi) {
+#ifdef NK_STR_NOTW
+    const Tw wa = ldtw(twq), wb = ldtw(twq + 512);
+#else
+    const Tw wa = ldtw(twq + (15 + hi) * 512);
+    const Tw wb = ldtw(twq + (kStrEntries + 15 + hi) * 512);
+#endif
+    A::template fwd<false>(v[2 * hi], v[2 * hi + 1], wa, c);
+    A::template fwd<false>(v[16 + 2 * hi], v[16 + 2 * hi + 1], wb, c);
+  }
+  __syncwarp();  // every lane has read B's e2 words: the buffer is free
+  NK_GTS(10);
+}
+
+// Inverse core: from v[16 S + 2 hi + j0] (the forward core's output layout,
+// in the policy's representation) through Q4', Q3', Q2' and P1' of both
+// streams; the caller runs the last stage (bit 13) on v[r], v[r + 16], whose
+// word index is l | w << 5 | r << 9. `ta`: stream A's first twiddles (8 Q4'
+// entries, and with 8-byte tables the 8 entries of Q3''s first stage), loaded
+// by the caller ahead of its wait for the block; `inputs_read` runs before the
+// staging halves are first written (waits until every warp has its input);
+// `consumed` once this warp has read its last word of the staging buffer.
+template <class A, bool ILTM0, class FRD, class FCONS>
+__device__ __forceinline__ void inv_core(uint64_t (&v)[32], uint8_t* St, uint8_t* Ew, const LimbConst& c,
+                                         const NttArgs& a, const typename A::Tw* __restrict__ tw,
+                                         const typename A::Tw* __restrict__ twq, uint64_t xbase, uint32_t w,
+                                         uint32_t l, typename A::Tw* ta, uint64_t* bar_w, uint32_t par, uint32_t it_,
+                                         FRD&& inputs_read, FCONS&& consumed) {
+  using Tw = typename A::Tw;
+  (void)it_;
+  constexpr bool kPre16 = sizeof(Tw) == 8;
+  const uint32_t e2w = l << 3;
+  const uint32_t e2r = ((l & 1u) << 3) | (((l >> 1) & 7u) << 4) | ((l >> 1) << 8);
+  const uint32_t e1w = (l << 3) + (w << 12);  // Q2' map: word l | r << 5 | w << 9
+  const uint32_t e1r = (l << 3) + (w << 8);   // P1' map: word l | w << 5 | r << 9
+  auto q3addr = [&](uint32_t S, int i, int hi) {
+    return twq + S * (kStrEntries * 512u) + ((i == 3 ? 0 : (i == 2 ? 1 : (i == 1 ? 3 : 7))) + hi) * 512;
+  };
+  auto q2tw = [&](uint32_t S) {
+    const uint64_t js = xbase + (static_cast<uint64_t>(w) << 9) + (static_cast<uint64_t>(S) << 13);
+    return [=](int i, int hi) { return ldtw(tw + (js >> (6 + i)) + hi); };
+  };
+  auto p1tw = [&](uint32_t S) {
+    const uint64_t js = xbase + (static_cast<uint64_t>(S) << 13);
+    return [=](int i, int hi) { return ldtw(tw + (js >> (10 + i)) + hi); };
+  };
+  const bool odd = (l & 1u) != 0;
+  // Q4' (bit 0), j0 back to the lane, Q3' (bits 1..4) of stream S; tq: its first twiddles
+  auto low_passes = [&](uint32_t S, const Tw* tq) {
+    uint64_t* x = v + 16 * S;
+#pragma unroll
+    for (int hi = 0; hi < 8; ++hi) {
+      if (ILTM0) A::template inv<true>(x[2 * hi], x[2 * hi + 1], tq[hi], c);
+      else A::template inv<false>(x[2 * hi], x[2 * hi + 1], tq[hi], c);
+    }
+    // this lane keeps j0 = its bit 0 and gets both j1
+#pragma unroll
+    for (int hi = 0; hi < 8; ++hi) {
+      const uint64_t y0 = x[2 * hi], y1 = x[2 * hi + 1];
+      const uint64_t recv = __shfl_xor_sync(0xffffffffu, odd ? y0 : y1, 1);
+      x[2 * hi] = odd ? recv : y0;      // j1 = 0
+      x[2 * hi + 1] = odd ? y1 : recv;  // j1 = 1
+    }
+    pass16i<A>(x, c, [=](int i, int hi) { return (kPre16 && i == 0) ? tq[kPre16 ? 8 + hi : 0] : ldtw(q3addr(S, i, hi)); });
+  };
+
+  low_passes(0, ta);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + (e2r ^ (r << 4))) = v[r];
+  __syncwarp();
+  NK_GTS(3);
+#pragma unroll
+  for (int hi = 0; hi < 8; ++hi) {
+    ta[hi] = ldtw(twq + (kStrEntries + 15 + hi) * 512);
+    if constexpr (kPre16) ta[8 + hi] = ldtw(q3addr(1, 0, hi));
+  }
+  low_passes(1, ta);
+  NK_GTS(4);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256));
+  __syncwarp();  // A's words are in registers: the buffer takes B's
+#pragma unroll
+  for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + (e2r ^ (r << 4))) = v[16 + r];
+  __syncwarp();
+  NK_GTS(5);
+
+  // ---- Q2' of A; B's words back; e1' of A ----
+  pass16i<A>(v, c, q2tw(0));
+#pragma unroll
+  for (int r = 0; r < 16; ++r)
+    v[16 + r] = *reinterpret_cast<const uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256));
+  NK_GTS(6);
+  inputs_read();  // every warp has its input: the staging halves take the streams
+#pragma unroll
+  for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + e1w + r * 256) = v[r];
+  __syncwarp();
+  if (l == 0) mbar_arrive_local(bar_w);
+  pass16i<A>(v + 16, c, q2tw(1));
+#pragma unroll
+  for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + 65536 + e1w + r * 256) = v[16 + r];
+  __syncwarp();
+  if (l == 0) mbar_arrive_local(bar_w + 1);
+  NK_GTS(7);
+
+  // ---- P1': bits 9..12 per stream ----
+  mbar_wait(bar_w, par);
+  NK_GTS(8);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(St + e1r + r * 4096);
+  pass16i<A>(v, c, p1tw(0));
+  NK_GTS(9);
+  mbar_wait(bar_w + 1, par);
+#pragma unroll
+  for (int r = 0; r < 16; ++r) v[16 + r] = *reinterpret_cast<const uint64_t*>(St + 65536 + e1r + r * 4096);
+  consumed();
+  pass16i<A>(v + 16, c, p1tw(1));
+  NK_GTS(10);
+}
+
+// stream A's first inverse twiddles (see inv_core)
+template <class A>
+__device__ __forceinline__ void inv_first_twiddles(typename A::Tw* ta, const typename A::Tw* __restrict__ twq) {
+#pragma unroll
+  for (int hi = 0; hi < 8; ++hi) {
+    ta[hi] = ldtw(twq + (15 + hi) * 512);
+    if constexpr (sizeof(typename A::Tw) == 8) ta[8 + hi] = ldtw(twq + (7 + hi) * 512);
+  }
+}
+
+}  // namespace str
+
 template <class A, bool ILTM0>
 __global__ void __launch_bounds__(512, 1)
     ntt_str14(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, NttArgs a,
               uint32_t nitems) {
-  using P1 = PassD<9, 5, -1>;
   using Tw = typename A::Tw;
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* St = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);  // staging (TMA, 128B-swizzled), then e1
@@ -190,20 +444,8 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   if (t == 0 && blockIdx.x < nitems) issue(blockIdx.x, 0);
 
-  // ---- thread-constant byte offsets (derivations: header and section comments) ----
-  const uint32_t jt1 = StrMap::jt1(w, l);
-  // e1, write side: stream word j' = jt1 | r << 9 at chunk-swizzled position
-  //   phys(j') = j' ^ (((j' >> 4) & 7) << 1): the half-warp's lanes (j0, j4, j5, j6) hit 16 distinct 8-byte slots
-  const uint32_t e1w = (jt1 ^ (((jt1 >> 4) & 7u) << 1)) << 3;  // + r * 4096 + S * 65536
-  // e1, read side: j' = l | r << 5 | w << 9 (lanes j0..j4): (base ^ ((r & 3) << 5)) + r * 256
-  const uint32_t e1r = ((l ^ ((l >> 4) << 1)) << 3) + (w << 12);
-  // e2 (warp-local, word m = j & 511 at m ^ (((m >> 5) & 7) << 1)): write (l << 3 ^ (r & 7) << 4) + r * 256,
-  // read tb ^ (r3 << 4)
   uint8_t* Ew = E + (w << 12);
-  const uint32_t e2w = l << 3;
-  const uint32_t e2r = ((l & 1u) << 3) | (((l >> 1) & 7u) << 4) | ((l >> 1) << 8);
   uint32_t phase = 0;
-
   uint32_t it_ = 0;
   (void)it_;
   for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
@@ -214,124 +456,27 @@ __global__ void __launch_bounds__(512, 1)
     const Tw* __restrict__ tw = tw_of<A>(a, limb);
     const Tw* __restrict__ twq = twq_of<A>(a, limb) + blk * kStrTableWords + t;
     const uint64_t boff = blk << kB14;
-    const uint64_t xbase = a.n + boff;
     uint64_t v[32];
 
-    // ---- P1: words from the staging buffer, stage 13, then stages 12..9 per stream ----
     mbar_wait(bar_full, phase);
     const LimbConst& c = Cs[phase];
     NK_GTS(1);
-    grp::p1_read<A, true>(v, St, jt1);
-    __syncwarp();
-    if (l == 0) mbar_arrive_local(bar_rd);
-    NK_GTS(2);
-    stages14<A, true, P1, ILTM0, 0, 1>(v, tw, tw, a.n, xbase + jt1, c);
-    stages14<A, true, P1, ILTM0, 1, 5, 0>(v, tw, tw, a.n, xbase + jt1, c);
-    NK_GTS(3);
-    // e1 of stream A: in place in the lower half of the staging buffer
-    mbar_wait(bar_rd, phase);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + e1w + r * 4096) = v[r];
-    __syncwarp();
-    if (l == 0) mbar_arrive_local(bar_w);
-    NK_GTS(4);
-    stages14<A, true, P1, ILTM0, 1, 5, 1>(v, tw, tw, a.n, xbase + jt1, c);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + 65536 + e1w + r * 4096) = v[16 + r];
-    __syncwarp();
-    if (l == 0) mbar_arrive_local(bar_w + 1);
-    NK_GTS(5);
+    str::fwd_core<A, ILTM0>(
+        v, St, Ew, c, a, tw, twq, a.n + boff, w, l, bar_rd, bar_w, phase, it_,
+        [&] {
+          if (l == 0) bulk_wait_read();  // the previous block's last output store has read this warp's 4 KiB
+        },
+        [&] {
+          grp::staging_consumed(cnt, l, [&] {  // the last of the 16 warps refills the staging buffer
+            if (k + gridDim.x < nitems) {
+              fence_proxy_async();
+              issue(k + gridDim.x, phase ^ 1);
+            }
+          });
+        });
 
-    // Twiddles. Q2: (N + j) >> (b + 1), b = 5 + i, j = w << 9 | S << 13 (+ r << 5): warp-uniform loads of
-    // the reference-order table; Q3 / Q4: the (stream, entry, thread) table. The twiddles of a pass's
-    // first two stages (3 values) are loaded ahead of the data movement in front of the pass (`pre`),
-    // so that no pass starts by waiting for L2.
-    auto q2addr = [&](uint32_t S, int i, int hi) {
-      const uint64_t js = xbase + (static_cast<uint64_t>(w) << 9) + (static_cast<uint64_t>(S) << 13);
-      return tw + (js >> (6 + i)) + hi;
-    };
-    auto q3addr = [&](uint32_t S, int i, int hi) {
-#ifdef NK_STR_NOTW  // timing experiment (wrong results): every low-stage twiddle from one address
-      return twq + 0 * (S + i + hi);
-#else
-      return twq + S * (kStrEntries * 512u) + ((i == 3 ? 0 : (i == 2 ? 1 : (i == 1 ? 3 : 7))) + hi) * 512;
-#endif
-    };
-    Tw pa[3], pb[3];
-    pa[0] = ldtw(q2addr(0, 3, 0)), pa[1] = ldtw(q2addr(0, 2, 0)), pa[2] = ldtw(q2addr(0, 2, 1));
-    pb[0] = ldtw(q2addr(1, 3, 0)), pb[1] = ldtw(q2addr(1, 2, 0)), pb[2] = ldtw(q2addr(1, 2, 1));
-    auto q2tw = [&](uint32_t S, const Tw* pre) {
-      return [=](int i, int hi) { return i >= 2 ? pre[i == 3 ? 0 : 1 + hi] : ldtw(q2addr(S, i, hi)); };
-    };
-    auto q3tw = [&](uint32_t S, const Tw* pre) {
-      return [=](int i, int hi) { return i >= 2 ? pre[i == 3 ? 0 : 1 + hi] : ldtw(q3addr(S, i, hi)); };
-    };
-
-    // ---- Q2 of stream A first: the wait for B (every warp through P1) comes after it, when the
-    // slower warps have caught up ----
-    mbar_wait(bar_w, phase);
-#pragma unroll
-    for (int r = 0; r < 16; ++r)
-      v[r] = *reinterpret_cast<const uint64_t*>(St + ((e1r ^ ((r & 3) << 5)) + r * 256));
-    NK_GTS(6);
-    str::pass16<A, 4, false>(v, c, q2tw(0, pa));
-    pa[0] = ldtw(q3addr(0, 3, 0)), pa[1] = ldtw(q3addr(0, 2, 0)), pa[2] = ldtw(q3addr(0, 2, 1));  // A's Q3
-    mbar_wait(bar_w + 1, phase);
-#pragma unroll
-    for (int r = 0; r < 16; ++r)
-      v[16 + r] = *reinterpret_cast<const uint64_t*>(St + 65536 + ((e1r ^ ((r & 3) << 5)) + r * 256));
-    // the staging buffer is consumed by this warp; the last of the 16 warps refills it
-    grp::staging_consumed(cnt, l, [&] {
-      if (k + gridDim.x < nitems) {
-        fence_proxy_async();
-        issue(k + gridDim.x, phase ^ 1);
-      }
-    });
-    if (l == 0) bulk_wait_read();  // the previous block's last output store has read this warp's 4 KiB
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256)) = v[r];
-    __syncwarp();
-    NK_GTS(7);
-    str::pass16<A, 4, false>(v + 16, c, q2tw(1, pb));
-    pb[0] = ldtw(q3addr(1, 3, 0)), pb[1] = ldtw(q3addr(1, 2, 0)), pb[2] = ldtw(q3addr(1, 2, 1));  // B's Q3
-    NK_GTS(8);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(Ew + (e2r ^ (r << 4)));
-    __syncwarp();  // A's words are in registers: the buffer takes B's
-#pragma unroll
-    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256)) = v[16 + r];
-    __syncwarp();
-
-    NK_GTS(9);
+    // ---- canonical words out: per stream a 4 KiB image and one bulk tensor store ----
     const int32_t orow16 = static_cast<int32_t>((row * a.n + boff + (static_cast<uint64_t>(w) << 9)) >> 4);
-    // ---- Q3 of both streams together (B's words read back first), shuffle, Q4 ----
-#pragma unroll
-    for (int r = 0; r < 16; ++r) v[16 + r] = *reinterpret_cast<const uint64_t*>(Ew + (e2r ^ (r << 4)));
-    str::pass16x2<A, 4>(v, c, q3tw(0, pa), q3tw(1, pb));
-    const bool odd = (l & 1u) != 0;
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      // lane pairs swap: this lane keeps j1 = its bit 0 and gets both j0
-      // (registers r3 = j1 | hi << 1: own words (j0 = lane bit) with j1 = 0 / 1)
-      const uint64_t own0 = v[2 * q], own1 = v[2 * q + 1];
-      const uint64_t recv = __shfl_xor_sync(0xffffffffu, odd ? own0 : own1, 1);
-      v[2 * q] = odd ? recv : own0;      // j0 = 0, j1 = lane bit
-      v[2 * q + 1] = odd ? own1 : recv;  // j0 = 1
-    }
-    // Q4: bit 0, twiddle entries 15 + hi
-#pragma unroll
-    for (int hi = 0; hi < 8; ++hi) {
-#ifdef NK_STR_NOTW
-      const Tw wa = ldtw(twq), wb = ldtw(twq + 512);
-#else
-      const Tw wa = ldtw(twq + (15 + hi) * 512);
-      const Tw wb = ldtw(twq + (kStrEntries + 15 + hi) * 512);
-#endif
-      A::template fwd<false>(v[2 * hi], v[2 * hi + 1], wa, c);
-      A::template fwd<false>(v[16 + 2 * hi], v[16 + 2 * hi + 1], wb, c);
-    }
-    NK_GTS(10);
 #pragma unroll
     for (uint32_t S = 0; S < 2; ++S) {
       uint64_t* y = v + 16 * S;
@@ -340,8 +485,8 @@ __global__ void __launch_bounds__(512, 1)
       // image: word m = j0 | j1 << 1 | hi << 2 | (l >> 1) << 5 at row m >> 4, chunk ((m >> 1) & 7) ^ (row & 7)
       if (S == 1) {
         if (l == 0) bulk_wait_read();  // A's store has read the image
+        __syncwarp();
       }
-      __syncwarp();  // (S == 0: every lane has read B's e2 words)
 #pragma unroll
       for (int hi = 0; hi < 8; ++hi) {
         const uint32_t rowi = (hi >> 2) + 2 * (l >> 1);
@@ -424,14 +569,7 @@ __global__ void __launch_bounds__(512, 1)
   __syncthreads();
   if (t == 0 && blockIdx.x < nitems) issue(blockIdx.x, 0);
 
-  // input image (= ntt_str14's output image): pair hi at row (hi >> 2) + 2 (l >> 1),
-  // chunk ((l & 1) | (hi & 3) << 1) ^ (row & 7): base ^ ((hi & 3) << 5) ^ ((hi >> 2) << 4 ...) folded below
-  const uint32_t in0 = w << 12;
   uint8_t* Ew = E + (w << 12);
-  const uint32_t e2w = l << 3;
-  const uint32_t e2r = ((l & 1u) << 3) | (((l >> 1) & 7u) << 4) | ((l >> 1) << 8);
-  const uint32_t e1w = (l << 3) + (w << 12);  // Q2' map: word l | r << 5 | w << 9
-  const uint32_t e1r = (l << 3) + (w << 8);   // P1' map: word l | w << 5 | r << 9
   uint32_t phase = 0;
   uint32_t it_ = 0;
   (void)it_;
@@ -447,31 +585,12 @@ __global__ void __launch_bounds__(512, 1)
     uint64_t* __restrict__ dst = a.out + row * a.n + boff;
     uint64_t v[32];
 
-    auto q3addr = [&](uint32_t S, int i, int hi) {
-      return twq + S * (kStrEntries * 512u) + ((i == 3 ? 0 : (i == 2 ? 1 : (i == 1 ? 3 : 7))) + hi) * 512;
-    };
-    auto q3tw = [&](uint32_t S) { return [=](int i, int hi) { return ldtw(q3addr(S, i, hi)); }; };
-    auto q2tw = [&](uint32_t S) {
-      const uint64_t js = xbase + (static_cast<uint64_t>(w) << 9) + (static_cast<uint64_t>(S) << 13);
-      return [=](int i, int hi) { return ldtw(tw + (js >> (6 + i)) + hi); };
-    };
-    auto p1tw = [&](uint32_t S) {
-      const uint64_t js = xbase + (static_cast<uint64_t>(S) << 13);
-      return [=](int i, int hi) { return ldtw(tw + (js >> (10 + i)) + hi); };
-    };
-
-    // the first two stages' twiddles of stream A (8 + 8 table entries) are loaded before the wait
-    // for the block, B's while A computes: the block does not start by waiting for L2
-    // (8-byte twiddles; with 16-byte entries the second eight would spill)
-    constexpr bool kPre16 = sizeof(Tw) == 8;
-    Tw ta[kPre16 ? 16 : 8];
-#pragma unroll
-    for (int hi = 0; hi < 8; ++hi) {
-      ta[hi] = ldtw(twq + (15 + hi) * 512);
-      if constexpr (kPre16) ta[8 + hi] = ldtw(q3addr(0, 0, hi));
-    }
+    // the first two stages' twiddles of stream A are loaded before the wait for the block, B's while
+    // A computes: the block does not start by waiting for L2
+    Tw ta[sizeof(Tw) == 8 ? 16 : 8];
+    str::inv_first_twiddles<A>(ta, twq);
     NK_GTS(0);
-    // ---- input: both streams' words, (j0 = 0, 1) pairs ----
+    // ---- input: both streams' words, (j0 = 0, 1) pairs (the forward's output image) ----
     mbar_wait(bar_full, phase);
     const LimbConst& c = Cs[phase];
     NK_GTS(1);
@@ -481,7 +600,8 @@ __global__ void __launch_bounds__(512, 1)
       for (int hi = 0; hi < 8; ++hi) {
         const uint32_t rowi = (hi >> 2) + 2 * (l >> 1);
         const uint32_t chunk = ((l & 1u) | ((hi & 3) << 1)) ^ (rowi & 7u);
-        const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(St + (S << 16) + in0 + (rowi << 7) + (chunk << 4));
+        const ulonglong2 p =
+            *reinterpret_cast<const ulonglong2*>(St + (S << 16) + (w << 12) + (rowi << 7) + (chunk << 4));
         v[16 * S + 2 * hi] = A::load(p.x);
         v[16 * S + 2 * hi + 1] = A::load(p.y);
       }
@@ -489,83 +609,18 @@ __global__ void __launch_bounds__(512, 1)
     if (l == 0) mbar_arrive_local(bar_rd);
     NK_GTS(2);
 
-    const bool odd = (l & 1u) != 0;
-    // Q4' (bit 0), j0 back to the lane, Q3' (bits 1..4) of stream S; tq: its first 16 twiddles
-    auto low_passes = [&](uint32_t S, const Tw* tq) {
-      uint64_t* x = v + 16 * S;
-#pragma unroll
-      for (int hi = 0; hi < 8; ++hi) {
-        if (ILTM0) A::template inv<true>(x[2 * hi], x[2 * hi + 1], tq[hi], c);
-        else A::template inv<false>(x[2 * hi], x[2 * hi + 1], tq[hi], c);
-      }
-      // this lane keeps j0 = its bit 0 and gets both j1
-#pragma unroll
-      for (int hi = 0; hi < 8; ++hi) {
-        const uint64_t y0 = x[2 * hi], y1 = x[2 * hi + 1];
-        const uint64_t recv = __shfl_xor_sync(0xffffffffu, odd ? y0 : y1, 1);
-        x[2 * hi] = odd ? recv : y0;      // j1 = 0
-        x[2 * hi + 1] = odd ? y1 : recv;  // j1 = 1
-      }
-      str::pass16i<A>(x, c, [=](int i, int hi) { return (kPre16 && i == 0) ? tq[kPre16 ? 8 + hi : 0] : ldtw(q3addr(S, i, hi)); });
-    };
+    str::inv_core<A, ILTM0>(
+        v, St, Ew, c, a, tw, twq, xbase, w, l, ta, bar_w, phase, it_, [&] { mbar_wait(bar_rd, phase); },
+        [&] {
+          grp::staging_consumed(cnt, l, [&] {
+            if (k + gridDim.x < nitems) {
+              fence_proxy_async();
+              issue(k + gridDim.x, phase ^ 1);
+            }
+          });
+        });
 
-    low_passes(0, ta);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + (e2r ^ (r << 4))) = v[r];
-    __syncwarp();
-    NK_GTS(3);
-#pragma unroll
-    for (int hi = 0; hi < 8; ++hi) {
-      ta[hi] = ldtw(twq + (kStrEntries + 15 + hi) * 512);
-      if constexpr (kPre16) ta[8 + hi] = ldtw(q3addr(1, 0, hi));
-    }
-    low_passes(1, ta);
-    NK_GTS(4);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256));
-    __syncwarp();  // A's words are in registers: the buffer takes B's
-#pragma unroll
-    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + (e2r ^ (r << 4))) = v[16 + r];
-    __syncwarp();
-    NK_GTS(5);
-
-    // ---- Q2' of A; B's words back; e1' of A ----
-    str::pass16i<A>(v, c, q2tw(0));
-#pragma unroll
-    for (int r = 0; r < 16; ++r)
-      v[16 + r] = *reinterpret_cast<const uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256));
-    NK_GTS(6);
-    mbar_wait(bar_rd, phase);  // every warp has read its input: the staging halves take the streams
-#pragma unroll
-    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + e1w + r * 256) = v[r];
-    __syncwarp();
-    if (l == 0) mbar_arrive_local(bar_w);
-    str::pass16i<A>(v + 16, c, q2tw(1));
-#pragma unroll
-    for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + 65536 + e1w + r * 256) = v[16 + r];
-    __syncwarp();
-    if (l == 0) mbar_arrive_local(bar_w + 1);
-    NK_GTS(7);
-
-    // ---- P1': bits 9..12 per stream, then bit 13 ----
-    mbar_wait(bar_w, phase);
-    NK_GTS(8);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(St + e1r + r * 4096);
-    str::pass16i<A>(v, c, p1tw(0));
-    NK_GTS(9);
-    mbar_wait(bar_w + 1, phase);
-#pragma unroll
-    for (int r = 0; r < 16; ++r) v[16 + r] = *reinterpret_cast<const uint64_t*>(St + 65536 + e1r + r * 4096);
-    grp::staging_consumed(cnt, l, [&] {
-      if (k + gridDim.x < nitems) {
-        fence_proxy_async();
-        issue(k + gridDim.x, phase ^ 1);
-      }
-    });
-    str::pass16i<A>(v + 16, c, p1tw(1));
-    NK_GTS(10);
-
+    // ---- bit 13 (n^-1 folded in for canonical results), stores ----
     constexpr bool kFoldLast = A::kSigned && !LONG;
     const uint32_t jo = l | (w << 5);
     if constexpr (kFoldLast) {
