@@ -425,7 +425,7 @@ int nk_harvey_butterflies(int fwd, uint64_t q, int bit_shift, uint64_t w, uint64
 
 void nk_debug_block_kernel(int which) {
   nk::rt::no_lat = (which == 6);
-  nk::rt::block_kernel = (which == 0 || which == 1 || which == 2) ? which : -1;
+  nk::rt::block_kernel = (which >= 0 && which <= 3) ? which : -1;  // 3: defaults, but poly_mult_mod by poly_mul14
 }
 
 int nk_modulus(uint64_t q, uint32_t* bits, uint64_t* barrett_factor) {
@@ -734,16 +734,18 @@ int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const u
   //    the product applied in the forward's store (CTA-pair kernel), then the
   //    inverse;
   //  * nk_debug_block_kernel(1) or exact_only: the reference's sequence.
-  bool fused = p->logn == kLogBlock && !nk::rt::exact_only && nk::rt::block_kernel <= 0;
+  bool fused = p->logn == kLogBlock && !nk::rt::exact_only && (nk::rt::block_kernel <= 0 || nk::rt::block_kernel == 3);
   for (uint32_t l = 0; l < nlimbs; ++l) fused &= p->bs[limb0 + l] == 52;
   const bool aligned = ((reinterpret_cast<uintptr_t>(f) | reinterpret_cast<uintptr_t>(g)) & 15) == 0 &&
                        (reinterpret_cast<uintptr_t>(res) & 7) == 0;
-  if (fused && nk::rt::block_kernel < 0 && aligned) {
+  if (fused && (nk::rt::block_kernel < 0 || nk::rt::block_kernel == 3) && aligned) {
     nk::PolyArgs pa{};
     pa.a.out = res;
     pa.a.in = f;
     pa.a.tw8 = p->tw8_fwd;
     pa.a.twg8 = p->twg8_fwd;
+    pa.a.twq8 = p->twq8_fwd;
+    pa.itwq8 = p->twq8_inv;
     pa.a.lc = p->lc;
     pa.a.n = p->n;
     pa.a.logn = p->logn;

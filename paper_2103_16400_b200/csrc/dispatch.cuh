@@ -243,10 +243,10 @@ int launch_tma(const NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm,
   // poly_mult_mod's fused product lives in the pair forward only
   const bool pair = a.mulb || block_kernel == 0;
   if constexpr (FWD)
-    if (!a.mulb && (block_kernel == 2 || block_kernel < 0))  // the default forward: two streams per thread
+    if (!a.mulb && (block_kernel == 2 || block_kernel < 0 || block_kernel == 3))  // the default forward: two streams per thread
       return iltm ? launch_str_t<A, true>(a, nitems, buf_words, st) : launch_str_t<A, false>(a, nitems, buf_words, st);
   if constexpr (!FWD)
-    if (block_kernel == 2 || block_kernel < 0)  // the default inverse: two streams per thread
+    if (block_kernel == 2 || block_kernel < 0 || block_kernel == 3)  // the default inverse: two streams per thread
       return iltm ? launch_stri_t<A, true>(a, nitems, buf_words, st) : launch_stri_t<A, false>(a, nitems, buf_words, st);
   if (pair)
     return iltm ? launch_pair_t<A, FWD, true>(a, nitems, buf_words, st)

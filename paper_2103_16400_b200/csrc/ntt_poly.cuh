@@ -32,6 +32,7 @@
 // thread constant there).
 #pragma once
 #include "ntt_grp.cuh"
+#include "ntt_str.cuh"
 
 namespace nk {
 
@@ -39,6 +40,7 @@ struct PolyArgs {
   NttArgs a;             // out, forward tables (tw8 / twg8), lc, n, rows, limbs
   const uint64_t* itw8;  // inverse tables of the plan, same layouts
   const uint64_t* itwg8;
+  const uint64_t* itwq8;  // (two-stream kernel: a.twq8 / itwq8)
 };
 
 // [grp layout][bar_free][TMEM base address]
@@ -249,6 +251,160 @@ __global__ void __launch_bounds__(512, 1)
       uint64_t* __restrict__ dst = a.out + static_cast<uint64_t>(k) * a.n;
 #pragma unroll
       for (int r = 0; r < 32; ++r) dst[ji3 | (static_cast<uint32_t>(r) << 9)] = v[r];
+    }
+    ++it;
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (w == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*tslot), "n"(kPolyTmemCols)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// poly_str14: the same single-kernel poly_mult_mod on the two-stream cores
+// (ntt_str.cuh). The forward core leaves every thread with 16 words of each
+// 8192-word half in exactly the layout the inverse core starts from, so g^
+// goes to Tensor Memory and comes back in the same thread, the product
+// p = f^ g^ is formed in registers, and the inverse starts from them: no
+// product image, and the exchanges of both directions overlap the other
+// stream's arithmetic.
+//   bar_full   g (with the row's limb constants), then f, per row
+//   bar_rd     P1 reads done: once per forward
+//   bar_w[2]   stream written by every warp: g's forward, f's forward, the inverse
+//   bar_free   f's staging words consumed by every warp: the inverse's e1' may use the halves
+// ---------------------------------------------------------------------------
+constexpr size_t kPolyStrSmemBytes = kStrSmemBytes + 16;
+
+template <class A>
+__global__ void __launch_bounds__(512, 1)
+    poly_str14(const __grid_constant__ CUtensorMap tf, const __grid_constant__ CUtensorMap tg, PolyArgs pa,
+               uint32_t nitems) {
+  static_assert(A::kSigned, "poly_str14 runs the signed FP64 policy");
+  using Tw = typename A::Tw;
+  const NttArgs& a = pa.a;
+  extern __shared__ __align__(1024) uint8_t smraw[];
+  uint8_t* St = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+  uint8_t* E = St + kStageBytes;
+  const LimbConst* Cs = reinterpret_cast<const LimbConst*>(E + kGrpExBytes);
+  uint64_t* bar_full = reinterpret_cast<uint64_t*>(E + kGrpExBytes + 2 * sizeof(LimbConst));
+  uint64_t* bar_rd = bar_full + 1;
+  uint64_t* bar_w = bar_full + 2;
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(bar_full + 4);
+  uint64_t* bar_free = bar_full + 5;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bar_full + 6);
+  const uint32_t t = threadIdx.x, l = t & 31u, w = t >> 5;
+
+  // cslot >= 0: also fetch row k's limb constants into that slot
+  auto issue = [&](const CUtensorMap* map, uint32_t k, int cslot) {
+    const int32_t y0 = static_cast<int32_t>(static_cast<uint64_t>(k) * (a.n >> 4));
+    mbar_expect_tx(bar_full, kStageBytes + (cslot >= 0 ? static_cast<uint32_t>(sizeof(LimbConst)) : 0u));
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tma_load_2d(St + q * 32768, map, 0, y0 + q * 256, bar_full);
+    if (cslot >= 0)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(Cs + cslot)),
+                   "l"(a.lc + (a.limb0 + (k % a.nlimbs))), "r"(static_cast<uint32_t>(sizeof(LimbConst))),
+                   "r"(smem_u32(bar_full))
+                   : "memory");
+  };
+
+  if (t == 0) {
+    mbar_init(bar_full, 1);
+    mbar_init(bar_rd, 16);
+    mbar_init(bar_w, 16);
+    mbar_init(bar_w + 1, 16);
+    mbar_init(bar_free, 16);
+    *cnt = 0;
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tf)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tg)) : "memory");
+  }
+  if (w == 0) {  // one warp allocates the TMEM columns (one CTA per SM: never contended by this kernel)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "n"(kPolyTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // this warp's TMEM quarter: lanes 32 (w % 4) .. + 31, columns 64 (w / 4) .. + 63: 32 words per thread
+  const uint32_t taddr = *tslot + ((32u * (w & 3u)) << 16) + 64u * (w >> 2);
+  if (t == 0 && blockIdx.x < nitems) issue(&tg, blockIdx.x, 0);
+
+  uint32_t it = 0;  // rows done by this CTA
+
+  for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
+    uint64_t v[32];
+    const uint32_t limb = a.limb0 + (k % a.nlimbs);
+    const LimbConst& c = Cs[it & 1u];  // valid once g's bar_full phase completes
+
+    // ---- g^ -> TMEM, then f^ (one copy of the forward's code) ----
+#pragma unroll 1
+    for (uint32_t ph = 0; ph < 2; ++ph) {
+      const Tw* __restrict__ tw = a.tw8 + static_cast<uint64_t>(limb) * a.n;
+      const Tw* __restrict__ twq = a.twq8 + static_cast<uint64_t>(limb) * kStrTableWords + tid_opaque();
+      mbar_wait(bar_full, ph);
+      // (thread constants from an opaque thread index: recomputed per transform instead of
+      // staying live across the whole row)
+      const uint32_t to = tid_opaque(), wo = to >> 5, lo = to & 31u;
+      str::fwd_core<A, true>(
+          v, St, E + (wo << 12), c, a, tw, twq, a.n, wo, lo, bar_rd, bar_w, ph, (it + ph) & 1u, 0u, [] {},
+          [&] {
+            if (ph == 0) {
+              grp::staging_consumed(cnt, l, [&] {
+                fence_proxy_async();
+                issue(&tf, k, -1);  // f of the same row
+              });
+            } else {
+              __syncwarp();
+              if (l == 0) mbar_arrive_local(bar_free);  // the staging halves may take the inverse's streams
+            }
+          });
+      if (ph == 0) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = as_u(csubS(as_d(v[i]), c.twoq_d));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tmem_st16(taddr + 16u * q, v + 8 * q);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+    }
+    // ---- p = f^ g^ in registers, the inverse's first twiddles ----
+    const Tw* __restrict__ itw = pa.itw8 + static_cast<uint64_t>(limb) * a.n;
+    const Tw* __restrict__ itwq = pa.itwq8 + static_cast<uint64_t>(limb) * kStrTableWords + tid_opaque();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint64_t gh[8];
+      tmem_ld16(taddr + 16u * q, gh);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[8 * q + i] = as_u(mul_recip(csubS(as_d(v[8 * q + i]), c.twoq_d), as_d(gh[i]), c.qinv, c.q_d));
+    }
+    Tw ta[16];
+    str::inv_first_twiddles<A>(ta, itwq);
+    // ---- inverse (n^-1 folded into the last stage), canonical words out ----
+    const uint32_t to = tid_opaque(), wo = to >> 5, lo = to & 31u;
+    str::inv_core<A, false>(
+        v, St, E + (wo << 12), c, a, itw, itwq, a.n, wo, lo, ta, bar_w, it & 1u, 0u,
+        [&] { mbar_wait(bar_free, it & 1u); },
+        [&] {
+          grp::staging_consumed(cnt, l, [&] {
+            if (k + gridDim.x < nitems) {
+              fence_proxy_async();
+              issue(&tg, k + gridDim.x, static_cast<int>((it + 1u) & 1u));  // g of the next row
+            }
+          });
+        });
+    uint64_t* __restrict__ dst = a.out + static_cast<uint64_t>(k) * a.n;
+    const uint32_t jo = lo | (wo << 5);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      A::inv_fold(v[r], v[r + 16], c);
+      dst[jo | (static_cast<uint32_t>(r) << 9)] = v[r];
+      dst[jo | (static_cast<uint32_t>(r + 16) << 9)] = v[r + 16];
     }
     ++it;
   }

@@ -149,15 +149,15 @@ namespace str {
 // Forward core: from the block in the staging buffer (bar_full waited by the
 // caller) to the Q4 results: v[16 S + 2 hi + j0] of stream S, with lane bit 0 =
 // j1, lane bits 1..4 = j5..j8, warp = j9..j12, before the final reduction.
-// `par`: parity of bar_rd / bar_w for this transform; `before_e2` runs before
+// `par_rd` / `par_w`: parities of bar_rd / bar_w for this transform; `before_e2` runs before
 // the warp's 4 KiB buffer is first written (e.g. waits for a store that still
 // reads it); `consumed` once this warp has read its last staging word.
 template <class A, bool ILTM0, class FPRE, class FCONS>
 __device__ __forceinline__ void fwd_core(uint64_t (&v)[32], uint8_t* St, uint8_t* Ew, const LimbConst& c,
                                          const NttArgs& a, const typename A::Tw* __restrict__ tw,
                                          const typename A::Tw* __restrict__ twq, uint64_t xbase, uint32_t w,
-                                         uint32_t l, uint64_t* bar_rd, uint64_t* bar_w, uint32_t par, uint32_t it_,
-                                         FPRE&& before_e2, FCONS&& consumed) {
+                                         uint32_t l, uint64_t* bar_rd, uint64_t* bar_w, uint32_t par_rd,
+                                         uint32_t par_w, uint32_t it_, FPRE&& before_e2, FCONS&& consumed) {
   using P1 = PassD<9, 5, -1>;
   using Tw = typename A::Tw;
   (void)it_;
@@ -182,7 +182,7 @@ __device__ __forceinline__ void fwd_core(uint64_t (&v)[32], uint8_t* St, uint8_t
   stages14<A, true, P1, ILTM0, 1, 5, 0>(v, tw, tw, a.n, xbase + jt1, c);
   NK_GTS(3);
   // e1 of stream A: in place in the lower half of the staging buffer
-  mbar_wait(bar_rd, par);
+  mbar_wait(bar_rd, par_rd);
 #pragma unroll
   for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(St + e1w + r * 4096) = v[r];
   __syncwarp();
@@ -222,13 +222,13 @@ __device__ __forceinline__ void fwd_core(uint64_t (&v)[32], uint8_t* St, uint8_t
 
   // ---- Q2 of stream A first: the wait for B (every warp through P1) comes after it, when the
   // slower warps have caught up ----
-  mbar_wait(bar_w, par);
+  mbar_wait(bar_w, par_w);
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(St + ((e1r ^ ((r & 3) << 5)) + r * 256));
   NK_GTS(6);
   pass16<A, 4, false>(v, c, q2tw(0, pa));
   pa[0] = ldtw(q3addr(0, 3, 0)), pa[1] = ldtw(q3addr(0, 2, 0)), pa[2] = ldtw(q3addr(0, 2, 1));  // A's Q3
-  mbar_wait(bar_w + 1, par);
+  mbar_wait(bar_w + 1, par_w);
 #pragma unroll
   for (int r = 0; r < 16; ++r)
     v[16 + r] = *reinterpret_cast<const uint64_t*>(St + 65536 + ((e1r ^ ((r & 3) << 5)) + r * 256));
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(512, 1)
     const LimbConst& c = Cs[phase];
     NK_GTS(1);
     str::fwd_core<A, ILTM0>(
-        v, St, Ew, c, a, tw, twq, a.n + boff, w, l, bar_rd, bar_w, phase, it_,
+        v, St, Ew, c, a, tw, twq, a.n + boff, w, l, bar_rd, bar_w, phase, phase, it_,
         [&] {
           if (l == 0) bulk_wait_read();  // the previous block's last output store has read this warp's 4 KiB
         },

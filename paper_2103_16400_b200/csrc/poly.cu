@@ -11,10 +11,16 @@ int run_poly_mul14(const PolyArgs& pa, const uint64_t* f, const uint64_t* g, cud
   CUtensorMap mf, mg;
   if (int rc = make_map(&mf, kRowMap, f, words)) return rc;
   if (int rc = make_map(&mg, kRowMap, g, words)) return rc;
-  if (int rc = set_smem_once<poly_mul14<Arith52S>>(kPolySmemBytes)) return rc;
   const uint64_t grid = pa.a.rows < static_cast<uint64_t>(sm_count()) ? pa.a.rows : sm_count();
-  poly_mul14<Arith52S><<<static_cast<unsigned>(grid), 512, kPolySmemBytes, st>>>(mf, mg, pa,
-                                                                                  static_cast<uint32_t>(pa.a.rows));
+  if (block_kernel == 3) {  // nk_debug_block_kernel(3): the group-exchange version
+    if (int rc = set_smem_once<poly_mul14<Arith52S>>(kPolySmemBytes)) return rc;
+    poly_mul14<Arith52S><<<static_cast<unsigned>(grid), 512, kPolySmemBytes, st>>>(mf, mg, pa,
+                                                                                    static_cast<uint32_t>(pa.a.rows));
+  } else {  // two streams per thread (ntt_str.cuh cores)
+    if (int rc = set_smem_once<poly_str14<Arith52S>>(kPolyStrSmemBytes)) return rc;
+    poly_str14<Arith52S><<<static_cast<unsigned>(grid), 512, kPolyStrSmemBytes, st>>>(
+        mf, mg, pa, static_cast<uint32_t>(pa.a.rows));
+  }
   launches++;
   NK_CUDA(cudaGetLastError());
   return 0;
