@@ -198,8 +198,10 @@ void nk_debug_dump_to(uint64_t* d_buf);
  * result is observable, so the tests can cover both arithmetic paths. Off by
  * default; applies to calls made by the calling thread only. */
 void nk_debug_exact_only(int on);
-/* Testing aid: which kernel transforms 16384-word blocks. -1 (default) = the
- * faster one per direction, 0 = the CTA-pair kernel, 1 = the group-exchange kernel;
+/* Testing aid: which kernel transforms 16384-word blocks. -1 (default) = 2,
+ * 0 = the CTA-pair kernel, 1 = the group-exchange kernel, 2 = two streams per
+ * thread (ntt_str14 / ntt_stri14); 3 = defaults, but the single-kernel
+ * poly_mult_mod by the group-exchange poly_mul14 instead of poly_str14;
  * 6 = defaults, but batches of 2^11..2^13-word rows smaller than the SM count
  * take the plain block kernel instead of the latency kernel (ntt_block_lat).
  * Applies to calls made by the calling thread only. */

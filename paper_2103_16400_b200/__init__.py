@@ -318,8 +318,10 @@ def debug_butterflies(policy, fwd, q, w, x0, x1):
 
 
 def set_block_kernel(which):
-    """Testing aid (nk_debug_block_kernel): -1 = per-direction default,
-    0 = CTA-pair kernel, 1 = group-exchange kernel, for 16384-word blocks;
+    """Testing aid (nk_debug_block_kernel): -1 = default (2), 0 = CTA-pair
+    kernel, 1 = group-exchange kernel, 2 = two streams per thread, for
+    16384-word blocks; 3 = defaults, but poly_mult_mod by the group-exchange
+    single kernel;
     6 = defaults, but small batches of 2^11..2^13-word rows take the plain
     block kernel instead of the latency kernel."""
     lib().nk_debug_block_kernel(int(which))

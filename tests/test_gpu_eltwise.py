@@ -276,10 +276,11 @@ def test_cfg5_sample(nk, oracle):
         assert np.array_equal(got[r], want), r
 
 
-@pytest.mark.parametrize("path", ["single", "pair3", "reference"])
+@pytest.mark.parametrize("path", ["single", "single_grp", "pair3", "reference"])
 def test_poly_16384_paths_and_aliasing(nk, oracle, path):
-    """N = 16384 with 50-bit limbs: the single on-chip kernel (default:
-    forward g to TMEM, forward f, product, inverse), the three-launch sequence
+    """N = 16384 with 50-bit limbs: the single on-chip kernel (default: the
+    two-stream poly_str14; nk_debug_block_kernel(3): the group-exchange
+    poly_mul14; forward g to TMEM, forward f, product, inverse), the three-launch sequence
     (nk_debug_block_kernel(0): forward g, forward f with the dyadic product in
     its store, inverse) and the reference's fwd(1,4)/mult(4)/inv(1,1) sequence
     (exact_only). All must equal the oracle, also when the result aliases f or
@@ -290,7 +291,7 @@ def test_poly_16384_paths_and_aliasing(nk, oracle, path):
     moduli = largest_ntt_primes(50, n, 3)
     plan = nk.RnsNtt(n, moduli)
     nk.set_exact_only(path == "reference")
-    nk.set_block_kernel(0 if path == "pair3" else -1)
+    nk.set_block_kernel({"pair3": 0, "single_grp": 3}.get(path, -1))
     try:
         npolys = 2
         rows = npolys * len(moduli)

@@ -238,11 +238,12 @@ def test_cfg4_full(nk, oracle):
     assert np.array_equal(host(b), x)
 
 
-@pytest.mark.parametrize("kernel", [0, 1], ids=["pair", "grp"])
+@pytest.mark.parametrize("kernel", [0, 1, 2], ids=["pair", "grp", "str"])
 @pytest.mark.parametrize("logn,bits,npolys", [(14, 50, 3), (14, 60, 2), (15, 50, 1), (16, 60, 1)])
 def test_block_kernels_match_oracle(nk, oracle, kernel, logn, bits, npolys, arith):
-    """Both 16384-word block kernels (CTA pair / single CTA), both arithmetic
-    paths, whole rows and the low 14 bits of long rows, odd block counts."""
+    """The three 16384-word block kernel families (CTA pair / group exchange /
+    two streams per thread, the default), both arithmetic paths, whole rows
+    and the low 14 bits of long rows, odd block counts."""
     nk.set_block_kernel(kernel)
     try:
         n = 1 << logn

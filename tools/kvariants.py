@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Device time of the forward / inverse at a config under each 16384-word
-block kernel (nk_debug_block_kernel: 0 CTA pair, 1 group exchange), CUDA
+block kernel (nk_debug_block_kernel: 0 CTA pair, 1 group exchange, 2 two streams per thread), CUDA
 events over back-to-back calls.
 
     python tools/kvariants.py [--n 16384 --limbs 32 --polys 64 --bits 50] [--kernels 0,1]
@@ -38,7 +38,7 @@ def main():
     ap.add_argument("--limbs", type=int, default=32)
     ap.add_argument("--polys", type=int, default=64)
     ap.add_argument("--bits", type=int, default=50)
-    ap.add_argument("--kernels", default="0,1")
+    ap.add_argument("--kernels", default="0,1,2")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--fin", type=int, default=1)
     ap.add_argument("--fout", type=int, default=1)
