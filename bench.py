@@ -48,7 +48,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 METRIC = "fwd/inv NTT Mcoeff/s (N=16384, batched limbs)"
-FWD_KERNEL = "ntt_grp14<Arith52S,fwd>"  # the forward's only launch at cfg3
+FWD_KERNEL = "ntt_str14<Arith52S,fwd>"  # the forward's only launch at cfg3
 # FP64 operations per butterfly of the signed canonical arithmetic
 # (modmath.cuh Arith52S: 6 for the Shoup product, 2 output adds, 1 for the
 # conditional subtraction), the floor the transform kernels are bound by
@@ -656,7 +656,7 @@ def run_configs(rates, hbm, threads):
     out["cfg5"] = {
         "op": "poly_mult_mod, N=16384, 16 x 50-bit limbs x 128 pairs (2048 row pairs)",
         "bound": "fp64 pipe (3 transforms x 9 FP64 ops/butterfly vs the live DFMA rate)",
-        "kernel": "poly_mul14 (both forwards, product, inverse on chip; g^ held in TMEM)",
+        "kernel": "poly_str14 (both forwards, product, inverse on chip, two streams per thread; g^ held in TMEM)",
         "launches_per_call": launches5,
         "us": us5, "Gcoeff_s": N * rows5 / us5 / 1e3, "fp64_floor_us": floor5,
         "roofline_frac": floor5 / us5 if floor5 else None,

@@ -32,7 +32,7 @@ if [ "${SKIP_NCU:-0}" = "0" ]; then
   timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
       --log-file $O/launches_cfg5.csv python tools/prof_ntt.py --n 16384 --limbs 16 --polys 128 --op poly --iters 1 > $O/ncu_cfg5.log 2>&1
   echo "ncu_cfg45=$?" | tee -a $O/status
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:poly_mul14 -s 1 -c 1 \
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:poly_ -s 1 -c 1 \
       -o $O/prof_poly python tools/prof_ntt.py --n 16384 --limbs 16 --polys 128 --op poly --iters 2 > $O/ncu_poly.log 2>&1
   echo "ncu_poly=$?" | tee -a $O/status
 fi

@@ -30,8 +30,11 @@ for r in rows[2:]:
     name = d.get("Kernel Name", "")
     m = re.search(r"(\w+)<(?:nk::)?(\w+), (?:\(bool\))?(\d)", name)
     m1 = re.search(r"(\w+)<(?:nk::)?(\w+)>", name)  # one template argument (poly_mul14<A>)
-    key = (f"{m.group(1)}<{m.group(2)},{'fwd' if m.group(3) == '1' else 'inv'}>" if m
-           else f"{m1.group(1)}<{m1.group(2)}>" if m1 else name[:60])
+    if m and m.group(1) in ("ntt_str14", "ntt_stri14"):  # the direction is in the kernel's name
+        key = f"{m.group(1)}<{m.group(2)},{'fwd' if m.group(1) == 'ntt_str14' else 'inv'}>"
+    else:
+        key = (f"{m.group(1)}<{m.group(2)},{'fwd' if m.group(3) == '1' else 'inv'}>" if m
+               else f"{m1.group(1)}<{m1.group(2)}>" if m1 else name[:60])
     e = {}
     for k, short in keep.items():
         if k in d and d[k]:
