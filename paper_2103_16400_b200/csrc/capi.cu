@@ -86,6 +86,14 @@ uint64_t dbits(double d) {
   std::memcpy(&u, &d, 8);
   return u;
 }
+// a beta = 2^52 table word (the bit pattern of the double w, 0 <= w < q) as the balanced
+// representative of the same residue: w - q when 2w > q (exact: both are integers below 2^52)
+uint64_t balanced8(uint64_t wbits, uint64_t q) {
+  double w;
+  std::memcpy(&w, &wbits, 8);
+  const uint64_t wi = static_cast<uint64_t>(w);
+  return 2 * wi > q ? dbits(w - static_cast<double>(q)) : wbits;
+}
 
 // Makes `dev` current for the duration of one entry-point call and restores
 // the caller's device on return (a call on a plan of another GPU must not
@@ -291,7 +299,7 @@ bool loose_barrett(uint64_t q) { return u128{5} * q < (u128{1} << 63); }
 // testing aid: single butterflies in each arithmetic policy (nk_debug_butterflies)
 // ---------------------------------------------------------------------------
 namespace nk {
-template <class A, bool FWD, bool SIGNED_IO>
+template <class A, bool FWD, bool SIGNED_IO, bool SKIP = false>
 __global__ void bfly_test_kernel(const uint64_t* x0, const uint64_t* x1, uint64_t n, ulonglong2 w,
                                  LimbConstDev c, uint64_t* y0, uint64_t* y1) {
   const uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -307,7 +315,7 @@ __global__ void bfly_test_kernel(const uint64_t* x0, const uint64_t* x1, uint64_
   typename A::Tw wt;
   if constexpr (std::is_same_v<typename A::Tw, uint64_t>) wt = w.x;  // w only (Arith52S)
   else wt = w;
-  if (FWD) A::template fwd<false>(a, b, wt, c);
+  if (FWD) A::template fwd<SKIP>(a, b, wt, c);  // SKIP: a stage without the pre-reduction of x0
   else A::template inv<false>(a, b, wt, c);
   if (SIGNED_IO) {
     y0[i] = static_cast<uint64_t>(static_cast<int64_t>(as_d(a)));
@@ -320,11 +328,11 @@ __global__ void bfly_test_kernel(const uint64_t* x0, const uint64_t* x1, uint64_
 }  // namespace nk
 
 namespace {
-template <class A, bool SIGNED_IO>
+template <class A, bool SIGNED_IO, bool SKIP = false>
 int run_bfly_test(bool fwd, const uint64_t* x0, const uint64_t* x1, uint64_t n, ulonglong2 w,
                   const nk::LimbConstDev& c, uint64_t* y0, uint64_t* y1) {
   const unsigned grid = static_cast<unsigned>((n + 255) / 256);
-  if (fwd) nk::bfly_test_kernel<A, true, SIGNED_IO><<<grid, 256>>>(x0, x1, n, w, c, y0, y1);
+  if (fwd) nk::bfly_test_kernel<A, true, SIGNED_IO, SKIP><<<grid, 256>>>(x0, x1, n, w, c, y0, y1);
   else nk::bfly_test_kernel<A, false, SIGNED_IO><<<grid, 256>>>(x0, x1, n, w, c, y0, y1);
   nk::rt::launches++;
   NK_CUDA(cudaGetLastError());
@@ -347,8 +355,9 @@ int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint
   nk::host::Modulus m;
   if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (w >= q) return fail(NK_ERR_ROOT, "debug_butterflies: twiddle must be < q");
-  const bool b52 = policy == 1 || policy == 2 || policy == 3;
-  if (policy < 0 || policy > 4) return fail(NK_ERR_BIT_SHIFT, "debug_butterflies: policy must be 0..4");
+  const bool b52 = policy == 1 || policy == 2 || policy == 3 || policy == 5;
+  if (policy < 0 || policy > 5) return fail(NK_ERR_BIT_SHIFT, "debug_butterflies: policy must be 0..5");
+  if (policy == 5 && !fwd) return fail(NK_ERR_BIT_SHIFT, "debug_butterflies: policy 5 is a forward stage");
   if (b52 && u128{4} * q >= (u128{1} << 52))
     return fail(NK_ERR_BIT_SHIFT_52, "NttTables: 52-bit accumulator requires 4q < 2^52");
   if (policy == 4 && q >= (uint64_t{1} << 61))
@@ -357,7 +366,7 @@ int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint
   if (!d_x0 || !d_x1 || !d_y0 || !d_y1) return fail(NK_ERR_NULL, "debug_butterflies: NULL buffer");
   const int bs = b52 ? 52 : 64;
   const uint64_t wp = static_cast<uint64_t>((static_cast<u128>(w) << bs) / q);
-  const bool fp = policy == 2 || policy == 3;
+  const bool fp = policy == 2 || policy == 3 || policy == 5;
   auto enc = [fp](uint64_t x) { return fp ? dbits(static_cast<double>(x)) : x; };
   nk::LimbConstDev c{};
   c.q = q;
@@ -370,13 +379,14 @@ int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint
   c.qinv = 1.0 / static_cast<double>(q);
   c.q_bias = static_cast<double>(q) + 4503599627370496.0;
   c.fourq = 4 * q;
-  const ulonglong2 tw = make_ulonglong2(enc(w), enc(wp));
+  const ulonglong2 tw = make_ulonglong2(policy == 3 || policy == 5 ? balanced8(enc(w), q) : enc(w), enc(wp));
   const bool f = fwd != 0;
   switch (policy) {
     case 0: return run_bfly_test<nk::ArithInt<64>, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
     case 1: return run_bfly_test<nk::ArithInt<52>, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
     case 2: return run_bfly_test<nk::Arith52P, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
     case 3: return run_bfly_test<nk::Arith52S, true>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
+    case 5: return run_bfly_test<nk::Arith52S, true, true>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
     default: return run_bfly_test<nk::ArithIntL, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
   }
 }
@@ -617,9 +627,15 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
   // the w halves of the beta = 2^52 entries (double bits; other limbs' words are unused)
   std::vector<uint64_t> h8[8];
   const std::vector<ulonglong2>* src8[8] = {&hf, &hi, &hlf, &hli, &hgf, &hgi, &hqf, &hqi};
+  // ... stored BALANCED, w in (-q/2, q/2] (w - q for 2w > q, the same residue): |w v| < 2q^2 for
+  // |v| < 4q, the range of the signed policy's integer-grid quotient (modmath.cuh, mul_recip_fine)
   for (int i = 0; i < 8; ++i) {
     h8[i].resize(src8[i]->size());
-    for (size_t k = 0; k < h8[i].size(); ++k) h8[i][k] = (*src8[i])[k].x;
+    const size_t per_limb = h8[i].size() / nlimbs;
+    for (size_t k = 0; k < h8[i].size(); ++k) {
+      const uint32_t l = static_cast<uint32_t>(k / per_limb);
+      h8[i][k] = p->bs[l] == 52 ? balanced8((*src8[i])[k].x, p->q[l]) : (*src8[i])[k].x;
+    }
   }
   put(p->tw8_fwd, h8[0].data(), h8[0].size() * 8);
   put(p->tw8_inv, h8[1].data(), h8[1].size() * 8);

@@ -261,23 +261,35 @@ struct Arith52P {
 // beta = 2^52 on the FP64 pipe, SIGNED values (canonical-output transforms
 // only: fout == 1). Requires q < 2^50 (so 4q <= 2^52).
 //
-// Signed product for |v| < 4q from w alone (8-byte twiddles; the quotient
-// comes from the rounded reciprocal qinv = fl(1/q) instead of a Shoup table):
+// Signed product from w alone (8-byte twiddles; the quotient comes from the
+// rounded reciprocal qinv = fl(1/q) instead of a Shoup table):
 //   h1 = fl(w v), l1 = fma(w, v, -h1)            exact TwoProduct: h1 + l1 = w v
-//   k  = fma(h1, qinv, 1.5*2^53) - 1.5*2^53      |h1 qinv| < 4q < 2^52, so the sum
-//        stays in [2^53, 2^54) (ulp 2): k = 2 round(h1 qinv / 2), an even integer
+//   k  = fma(h1, qinv, C) - C                    h1 qinv rounded to the grid of C
 //   e  = fma(-k, q, h1)                          exact: integer, |e| < 2^53
 //   T  = e + l1 = w v - k q                      exact
-// |h1 - wv| <= 2^48 (wv < 2^102), |h1 qinv - h1/q| <= 4q 2^-53 < 1/2 and
-// |h1 qinv - k| <= 1, so |wv/q - k| <= 2^48/q + 1/2 + 1 < 1.75 and |T| < 1.75q.
-// (Measured over random and edge operands: max |T|/q = 1.34.) Six FP64
-// operations, like the Shoup form, but half the twiddle bytes: at N = 16384
-// the tables stream ~N x 16 B per row from L2 otherwise, more than the row.
+// Two grids:
+//  * mul_recip, C = 1.5*2^53 (even integers), for |w v| < 4 q^2 (|h1 qinv| <
+//    2^52 keeps the sum in [2^53, 2^54)): |h1 - wv| <= 2^48, |h1 qinv - h1/q|
+//    < 1/2, |h1 qinv - k| <= 1, so |T| < 1.75q. Used where both factors are
+//    only known below 2q (the dyadic product of two transform outputs).
+//  * mul_recip_fine, C = 1.5*2^52 (integers), for |w v| < 2 q^2 (|h1 qinv| <
+//    2^51 keeps the sum in [2^52, 2^53)): |l1| <= 2^-53 |wv| < q (q / 2^52) <
+//    q/4, |h1 qinv - h1/q| <= 2q 2^-53 (1 + 2^-52) < 1/4, |h1 qinv - k| <= 1/2,
+//    so |T| < q. THE TRANSFORMS' TWIDDLES ARE STORED BALANCED, w in (-q/2, q/2]
+//    (w - q for w > q/2: the same residue, capi.cu balanced8), so every
+//    butterfly product with |v| < 4q is in this case.
 // Signed words drop Harvey's "+2q" (x1' = u - T) and the GS "+2q" (t = x0 - x1):
-//   forward: |x| < 4q in, u = x0 - 2q sgn(x0) [|x0| >= 2q] in (-2q, 2q),
-//            x0' = u + T, x1' = u - T in (-4q, 4q)
+//   forward: |x| < 4q in; a reducing stage takes u = x0 - 2q sgn(x0) [|x0| >=
+//            2q] in (-2q, 2q), x0' = u + T, x1' = u - T in (-3q, 3q); because
+//            |T| < q, the NEXT stage may skip the reduction (u = x0): its
+//            outputs stay below 4q, the bound a reducing stage starts from. The
+//            16384-word kernels reduce on even stages only (fwd_skip below):
+//            6 conditional subtractions (one DADD + four ALU operations each)
+//            in 14 stages instead of 12. At fin = 1 the first stage skips it
+//            too (|x| < q in, < 2q out, < 3q after stage 1).
 //   inverse: |x| < 2q in, s = x0 + x1 in (-4q, 4q) -> (-2q, 2q) by the same
-//            signed conditional subtraction, x1' = T(x0 - x1) in (-2q, 2q)
+//            signed conditional subtraction, x1' = T(x0 - x1) in (-q, q): the
+//            sum doubles at every stage, so every stage reduces.
 // Representatives differ from the reference's lazy ones; canonical results
 // (every value reduced to [0, q) at the end) are identical.
 // The n^-1 products of the folded last inverse stage keep the Shoup form
@@ -326,11 +338,15 @@ __device__ __forceinline__ double csubS(double y, double m) {
 struct Arith52S {
   using Tw = uint64_t;  // w as a double's bit pattern (8-byte tables)
   // Forward stages without the conditional subtraction when the input is
-  // canonical (fin = 1): |x| < q in; after stage 1 |x| < q + q(1 + q/2^52)
-  // < 2.25q; stage 2's multiplicand is then < 2.25q < 4q (valid quotient) and
-  // its outputs are < 2.25q + q(1 + 2.25q/2^52) < 3.82q < 4q, the invariant
-  // the reducing stages start from (every bound uses q < 2^50).
+  // canonical (fin = 1), for the kernels that reduce at every later stage:
+  // |x| < q in, < 2q after stage 1, < 3q after stage 2 (|T| < q), inside the
+  // |x| < 4q a reducing stage starts from.
   static constexpr int kIltmFwd = 2;
+  // The 16384-word kernels' schedule: stage gs (0 = the block's first stage,
+  // index bit 13) skips the reduction when gs is odd -- the stage before it
+  // reduced, so |x| < 3q in and < 4q out -- and at gs = 0 when the input is
+  // canonical (< q in, < 2q out; stage 1: < 3q out; stage 2 reduces).
+  __host__ __device__ static constexpr bool fwd_skip(bool iltm0, int gs) { return (gs & 1) || (iltm0 && gs == 0); }
   static constexpr bool kLoose = false;
   static constexpr bool kFP = true;
   static constexpr bool kSigned = true;
@@ -356,7 +372,7 @@ struct Arith52S {
   template <bool ILTM>
   __device__ static void fwd(uint64_t& x0, uint64_t& x1, uint64_t w, const LimbConstDev& c) {
     const double u = ILTM ? as_d(x0) : csubS(as_d(x0), c.twoq_d);
-    const double t = mul_recip(as_d(x1), as_d(w), c.qinv, c.q_d);
+    const double t = mul_recip_fine(as_d(x1), as_d(w), c.qinv, c.q_d);  // balanced w: |w x1| < 2q^2
     x0 = as_u(__dadd_rn(u, t));
     x1 = as_u(__dsub_rn(u, t));
   }
@@ -367,7 +383,7 @@ struct Arith52S {
     double s = __dadd_rn(a, b);
     if (!ILTM) s = csubS(s, c.twoq_d);
     x0 = as_u(s);
-    x1 = as_u(mul_recip(t, as_d(w), c.qinv, c.q_d));
+    x1 = as_u(mul_recip_fine(t, as_d(w), c.qinv, c.q_d));  // balanced w, |t| < 4q
   }
   __device__ static uint64_t scale_ninv(uint64_t x, const LimbConstDev& c) {
     return as_u(mul_signed(as_d(x), as_d(c.ninv), as_d(c.ninvp), c.qq));

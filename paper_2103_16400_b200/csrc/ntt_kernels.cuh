@@ -460,6 +460,17 @@ struct PassD {
 };
 
 
+// Does forward stage `gs` of a 16384-word block (0 = its first stage, index bit
+// 13; s_local = the stage's position in its pass, iltm0 only on the first pass
+// of a transform with canonical input) skip the pre-reduction of x0? The signed
+// FP64 policy reduces on even stages only (modmath.cuh, Arith52S::fwd_skip);
+// the others skip their first kIltmFwd stages at fin = 1, like the reference.
+template <class A>
+__host__ __device__ constexpr bool fwd_skip14(bool iltm0, int gs, int s_local) {
+  if constexpr (A::kSigned) return A::fwd_skip(iltm0, gs);
+  else return iltm0 && s_local < A::kIltmFwd;
+}
+
 // Stages [S0, S1) (processing order) of the register pass PD, on all 32 words
 // or on one half of them (HALF = 0 / 1: registers 16 HALF .. 16 HALF + 15;
 // only for stages whose butterflies stay inside a half: every stage of a
@@ -502,7 +513,8 @@ __device__ __forceinline__ void stages14(uint64_t (&v)[32], const typename A::Tw
             uint64_t& x0 = v[g * R + r0];
             uint64_t& x1 = v[g * R + r1];
             if (FWD) {
-              if (ILTM0 && s < A::kIltmFwd) A::template fwd<true>(x0, x1, w, c);
+              // kB14 - 1 - b: the stage's number from the block's first stage (index bit 13)
+              if (fwd_skip14<A>(ILTM0, kB14 - 1 - b, s)) A::template fwd<true>(x0, x1, w, c);
               else A::template fwd<false>(x0, x1, w, c);
             } else {
               if (ILTM0 && s == 0) A::template inv<true>(x0, x1, w, c);

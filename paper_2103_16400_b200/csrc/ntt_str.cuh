@@ -86,7 +86,8 @@ namespace str {
 // K stages (forward order: bit LO + K - 1 first) on the 16 registers x[0..15]
 // whose index bits are j_LO .. j_{LO+3}; the twiddle of stage bit b, position
 // hi (the register bits above b) comes from `twf(i, hi)`, i = b - LO.
-template <class A, int NST, bool ILTM, class F>
+// GS0: the first stage's number from the block's first stage (fwd_skip14).
+template <class A, int NST, int GS0, class F>
 __device__ __forceinline__ void pass16(uint64_t* x, const LimbConst& c, F&& twf) {
 #pragma unroll
   for (int s = 0; s < NST; ++s) {
@@ -97,7 +98,8 @@ __device__ __forceinline__ void pass16(uint64_t* x, const LimbConst& c, F&& twf)
 #pragma unroll
       for (int lo = 0; lo < (1 << i); ++lo) {
         const int r0 = (hi << (i + 1)) | lo, r1 = r0 | (1 << i);
-        A::template fwd<false>(x[r0], x[r1], w, c);
+        if (fwd_skip14<A>(false, GS0 + s, 1 << 30)) A::template fwd<true>(x[r0], x[r1], w, c);
+        else A::template fwd<false>(x[r0], x[r1], w, c);
       }
     }
   }
@@ -121,7 +123,7 @@ __device__ __forceinline__ void pass16i(uint64_t* x, const LimbConst& c, F&& twf
 }
 
 // the same stages on both streams at once (x and x + 16), stage by stage: 16 independent butterflies per stage
-template <class A, int NST, class FA, class FB>
+template <class A, int NST, int GS0, class FA, class FB>
 __device__ __forceinline__ void pass16x2(uint64_t* x, const LimbConst& c, FA&& twa, FB&& twb) {
 #pragma unroll
   for (int s = 0; s < NST; ++s) {
@@ -133,8 +135,13 @@ __device__ __forceinline__ void pass16x2(uint64_t* x, const LimbConst& c, FA&& t
 #pragma unroll
       for (int lo = 0; lo < (1 << i); ++lo) {
         const int r0 = (hi << (i + 1)) | lo, r1 = r0 | (1 << i);
-        A::template fwd<false>(x[r0], x[r1], wa, c);
-        A::template fwd<false>(x[16 + r0], x[16 + r1], wb, c);
+        if (fwd_skip14<A>(false, GS0 + s, 1 << 30)) {
+          A::template fwd<true>(x[r0], x[r1], wa, c);
+          A::template fwd<true>(x[16 + r0], x[16 + r1], wb, c);
+        } else {
+          A::template fwd<false>(x[r0], x[r1], wa, c);
+          A::template fwd<false>(x[16 + r0], x[16 + r1], wb, c);
+        }
       }
     }
   }
@@ -226,7 +233,7 @@ __device__ __forceinline__ void fwd_core(uint64_t (&v)[32], uint8_t* St, uint8_t
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[r] = *reinterpret_cast<const uint64_t*>(St + ((e1r ^ ((r & 3) << 5)) + r * 256));
   NK_GTS(6);
-  pass16<A, 4, false>(v, c, q2tw(0, pa));
+  pass16<A, 4, 5>(v, c, q2tw(0, pa));
   pa[0] = ldtw(q3addr(0, 3, 0)), pa[1] = ldtw(q3addr(0, 2, 0)), pa[2] = ldtw(q3addr(0, 2, 1));  // A's Q3
   mbar_wait(bar_w + 1, par_w);
 #pragma unroll
@@ -239,7 +246,7 @@ __device__ __forceinline__ void fwd_core(uint64_t (&v)[32], uint8_t* St, uint8_t
   for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + ((e2w ^ ((r & 7) << 4)) + r * 256)) = v[r];
   __syncwarp();
   NK_GTS(7);
-  pass16<A, 4, false>(v + 16, c, q2tw(1, pb));
+  pass16<A, 4, 5>(v + 16, c, q2tw(1, pb));
   pb[0] = ldtw(q3addr(1, 3, 0)), pb[1] = ldtw(q3addr(1, 2, 0)), pb[2] = ldtw(q3addr(1, 2, 1));  // B's Q3
   NK_GTS(8);
 #pragma unroll
@@ -253,7 +260,7 @@ __device__ __forceinline__ void fwd_core(uint64_t (&v)[32], uint8_t* St, uint8_t
   // ---- Q3 of both streams together (B's words read back first), shuffle, Q4 ----
 #pragma unroll
   for (int r = 0; r < 16; ++r) v[16 + r] = *reinterpret_cast<const uint64_t*>(Ew + (e2r ^ (r << 4)));
-  pass16x2<A, 4>(v, c, q3tw(0, pa), q3tw(1, pb));
+  pass16x2<A, 4, 9>(v, c, q3tw(0, pa), q3tw(1, pb));
   const bool odd = (l & 1u) != 0;
 #pragma unroll
   for (int q = 0; q < 16; ++q) {
@@ -273,8 +280,13 @@ __device__ __forceinline__ void fwd_core(uint64_t (&v)[32], uint8_t* St, uint8_t
     const Tw wa = ldtw(twq + (15 + hi) * 512);
     const Tw wb = ldtw(twq + (kStrEntries + 15 + hi) * 512);
 #endif
-    A::template fwd<false>(v[2 * hi], v[2 * hi + 1], wa, c);
-    A::template fwd<false>(v[16 + 2 * hi], v[16 + 2 * hi + 1], wb, c);
+    if (fwd_skip14<A>(false, 13, 1 << 30)) {
+      A::template fwd<true>(v[2 * hi], v[2 * hi + 1], wa, c);
+      A::template fwd<true>(v[16 + 2 * hi], v[16 + 2 * hi + 1], wb, c);
+    } else {
+      A::template fwd<false>(v[2 * hi], v[2 * hi + 1], wa, c);
+      A::template fwd<false>(v[16 + 2 * hi], v[16 + 2 * hi + 1], wb, c);
+    }
   }
   __syncwarp();  // every lane has read B's e2 words: the buffer is free
   NK_GTS(10);

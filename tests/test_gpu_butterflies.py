@@ -103,9 +103,10 @@ def test_signed_policy_ranges(nk, fwd):
 
 
 def test_signed_policy_product_bound(nk):
-    """Arith52S's rounded-reciprocal product (modmath.cuh mul_recip, w alone,
-    no Shoup table): with x0 = 0 the forward butterfly returns (T, -T), and the
-    documented bound |T| < 1.75q must hold for every multiplicand |v| < 4q."""
+    """Arith52S's rounded-reciprocal product (modmath.cuh mul_recip_fine, w
+    alone, stored balanced, no Shoup table): with x0 = 0 the forward butterfly
+    returns (T, -T), and the documented bound |T| < q must hold for every
+    multiplicand |v| < 4q and every twiddle."""
     rng = np.random.default_rng(11)
     for q in qs(ARITH52S):
         if q == 17:
@@ -114,13 +115,38 @@ def test_signed_policy_product_bound(nk):
             b = np.concatenate([np.array([4 * q - 1, -(4 * q - 1), 2 * q, -2 * q, 0, 1], np.int64),
                                 rng.integers(-4 * q + 1, 4 * q, 8192, dtype=np.int64)])
         a = np.zeros_like(b)
-        for w in twiddles(q, rng) + ([q - 1, q - 2] if q > 17 else []):
+        tws = twiddles(q, rng) + ([q - 1, q - 2, q // 2, q // 2 + 1] if q > 17 else list(range(1, q)))
+        for w in tws:
             y0, y1 = nk.debug_butterflies(ARITH52S, True, q, w, dev(a), dev(b))
             y0, y1 = host(y0), host(y1)
-            assert np.abs(y0).max() * 4 < 7 * q, (q, w, int(np.abs(y0).max()))
+            assert np.abs(y0).max() < q, (q, w, int(np.abs(y0).max()))
             assert np.array_equal(y0, -y1)
             B = b.astype(object)
             assert all(int(u) % q == (w * v) % q for u, v in zip(y0, B)), (q, w)
+
+
+def test_signed_policy_alternating_stages(nk):
+    """The 16384-word kernels' forward schedule (Arith52S::fwd_skip): a reducing
+    stage maps |x| < 4q into |y| < 3q, the non-reducing stage after it |x| < 3q
+    into |y| < 4q (policy 5), both congruent to the butterfly's value."""
+    rng = np.random.default_rng(12)
+    for q in qs(ARITH52S):
+        for policy, rin, rout in ((ARITH52S, 4, 3), (5, 3, 4)):
+            if q == 17:
+                a, b = exhaustive_pairs(-rin * q + 1, rin * q)
+            else:
+                a, b = sample_pairs(q, rng, 4096, -rin + 1e-9, rin)
+                edge = np.array([rin * q - 1, -(rin * q - 1)], np.int64)
+                a = np.concatenate([a, edge, edge, -edge])
+                b = np.concatenate([b, edge, -edge, edge])
+            for w in twiddles(q, rng) + [q // 2, q // 2 + 1, q - 1]:
+                y0, y1 = nk.debug_butterflies(policy, True, q, w, dev(a), dev(b))
+                y0, y1 = host(y0), host(y1)
+                assert np.abs(y0).max() < rout * q and np.abs(y1).max() < rout * q, (policy, q, w)
+                A, B = a.astype(object), b.astype(object)
+                e0, e1 = (A + w * B) % q, (A - w * B) % q
+                assert all(int(u) % q == v for u, v in zip(y0, e0)), (policy, q, w)
+                assert all(int(u) % q == v for u, v in zip(y1, e1)), (policy, q, w)
 
 
 @pytest.mark.parametrize("fwd", [True, False], ids=["fwd", "inv"])

@@ -52,6 +52,33 @@ __global__ void __launch_bounds__(512) kern(uint64_t* out, uint32_t seed) {
         asm volatile("mul.lo.u64 %0, %0, %1;" : "+l"(w[i]) : "l"(w[(i + 3) % CH]));
       } else if (OP == 11) {  // DFMA.RM
         asm volatile("fma.rm.f64 %0, %0, %1, %1;" : "+d"(d[i]) : "d"(e[i]));
+      } else if (OP == 12) {  // FRND.F64 alone
+        asm volatile("cvt.rni.f64.f64 %0, %0;" : "+d"(e[i]));
+      } else if (OP == 13) {  // 8 DFMA (kernel's FP64 : FRND ratio), no FRND
+#pragma unroll
+        for (int r = 0; r < 8; ++r) asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(d[i]) : "d"(e[i]));
+      } else if (OP == 14) {  // 8 DFMA + 1 FRND.F64 on an independent chain
+#pragma unroll
+        for (int r = 0; r < 8; ++r) asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(d[i]) : "d"(e[i]));
+        asm volatile("cvt.rni.f64.f64 %0, %0;" : "+d"(e[(i + 1) % CH]));
+      } else if (OP == 15) {  // 8 DFMA + 2 FRND.F64
+#pragma unroll
+        for (int r = 0; r < 8; ++r) asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(d[i]) : "d"(e[i]));
+        asm volatile("cvt.rni.f64.f64 %0, %0;" : "+d"(e[(i + 1) % CH]));
+        asm volatile("cvt.rni.f64.f64 %0, %0;" : "+d"(e[(i + 2) % CH]));
+      } else if (OP == 16) {  // 8 DFMA + 8 LOP3/IADD (issue-slot sharing)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(d[i]) : "d"(e[i]));
+          asm volatile("xor.b32 %0, %0, %1;" : "+r"(a[i]) : "r"(b[i]));
+        }
+      } else if (OP == 17) {  // 8 DFMA + 1 FRND + 8 LOP3
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          asm volatile("fma.rn.f64 %0, %0, %1, %1;" : "+d"(d[i]) : "d"(e[i]));
+          asm volatile("xor.b32 %0, %0, %1;" : "+r"(a[i]) : "r"(b[i]));
+        }
+        asm volatile("cvt.rni.f64.f64 %0, %0;" : "+d"(e[(i + 1) % CH]));
       }
     }
   }
@@ -98,5 +125,11 @@ int main() {
   run<8>("add.u64", 1);
   run<9>("IMAD+IADD3 (pairs)", 2);
   run<10>("mul.lo.u64", 1);
+  run<12>("FRND.F64", 1);
+  run<13>("8 DFMA", 8);
+  run<14>("8 DFMA + FRND (count 8)", 8);
+  run<15>("8 DFMA + 2 FRND (count 8)", 8);
+  run<16>("8 DFMA + 8 LOP3 (count 8)", 8);
+  run<17>("8 DFMA + 8 LOP3 + FRND (c8)", 8);
   return 0;
 }

@@ -16,6 +16,7 @@ using namespace nk;
 namespace {
 
 constexpr int kChains = 8;
+constexpr int kProbeStages = 4;
 
 __global__ void __launch_bounds__(256) dfma_loop(double* out, int iters) {
   double a[kChains];
@@ -32,8 +33,10 @@ __global__ void __launch_bounds__(256) dfma_loop(double* out, int iters) {
   if (s == 12345.0) out[threadIdx.x] = s;
 }
 
-// butterflies over V register words, three stages per iteration (spans 1, 2,
-// 4), two twiddles: the transforms' inner loop without memory or exchanges
+// butterflies over V register words, four stages per iteration (spans 1, 2,
+// 4, 8), two twiddles: the transforms' inner loop without memory or exchanges.
+// The signed FP64 policy's forward reduces x0 on even stages only, as in the
+// 16384-word kernels (modmath.cuh, Arith52S::fwd_skip).
 template <class Tw>
 __device__ __forceinline__ Tw as_tw(ulonglong2 w) {
   if constexpr (std::is_same_v<Tw, uint64_t>) return w.x;  // w only (Arith52S's 8-byte tables)
@@ -49,12 +52,13 @@ __global__ void __launch_bounds__(512, 1) bfly_loop(uint64_t* out, LimbConstDev 
   const typename A::Tw w[2] = {as_tw<typename A::Tw>(w0), as_tw<typename A::Tw>(w1)};
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
-    for (int s = 0; s < 3; ++s) {
+    for (int s = 0; s < kProbeStages; ++s) {
       const int h = 1 << s;
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         if ((i & h) || h >= V) continue;
         if (INV) A::template inv<false>(v[i], v[i + h], w[(i >> 1) & 1], c);
+        else if (A::kSigned && (s & 1)) A::template fwd<true>(v[i], v[i + h], w[(i >> 1) & 1], c);
         else A::template fwd<false>(v[i], v[i + h], w[(i >> 1) & 1], c);
       }
     }
@@ -104,7 +108,7 @@ int bfly_rate(const LimbConstDev& c, ulonglong2 w0, ulonglong2 w1, double* per_s
   const int rc = time_ms([&] { bfly_loop<A, V, INV><<<nsm, 512>>>(out, c, w0, w1, kIters); }, &ms);
   cudaFree(out);
   if (rc) return rc;
-  *per_s = double(nsm) * 512 * kIters * 3 * (V / 2) / (ms * 1e-3);
+  *per_s = double(nsm) * 512 * kIters * kProbeStages * (V / 2) / (ms * 1e-3);
   return 0;
 }
 
