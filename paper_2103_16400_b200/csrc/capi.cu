@@ -95,6 +95,11 @@ uint64_t balanced8(uint64_t wbits, uint64_t q) {
   return 2 * wi > q ? dbits(w - static_cast<double>(q)) : wbits;
 }
 
+// the balanced representative of w mod q as a double (q < 2^50)
+double bal_d(uint64_t w, uint64_t q) {
+  return 2 * w > q ? -static_cast<double>(q - w) : static_cast<double>(w);
+}
+
 // Makes `dev` current for the duration of one entry-point call and restores
 // the caller's device on return (a call on a plan of another GPU must not
 // move the caller's torch/CUDA current device).
@@ -571,7 +576,8 @@ int nk_plan_create(nk_plan** out, int device, uint64_t n, const uint64_t* moduli
     hl[l] = nk::LimbConst{t.q, 2 * t.q, ~t.q + 1, enc(t.ninv), enc(t.ninvp),
                           std::ldexp(static_cast<double>(t.q), -52), static_cast<double>(2 * t.q),
                           t.bs, 0, static_cast<double>(t.q), 1.0 / static_cast<double>(t.q),
-                          static_cast<double>(t.q) + 4503599627370496.0, enc(nw), enc(nwp), 4 * t.q};
+                          static_cast<double>(t.q) + 4503599627370496.0, enc(nw), enc(nwp), 4 * t.q,
+                          fp ? bal_d(t.ninv, t.q) : 0.0, fp ? bal_d(nw, t.q) : 0.0};
     nk::host::Modulus m;
     nk::host::make_modulus(t.q, &m);
     const int fins[3] = {1, 2, 4};

@@ -160,7 +160,9 @@ struct LimbConstDev {
   // folded last stage of canonical inverses (inv_fold)
   uint64_t nw, nwp;
   uint64_t fourq;  // 4q (ArithIntL)
-  uint64_t pad2[2];  // 128 bytes: one bulk copy into shared memory (ntt_grp14)
+  // Arith52S: n^-1 and n^-1 * w_1 as balanced doubles in (-q/2, q/2] (the folded last stage's
+  // integer-grid products, inv_fold); 128 bytes: one bulk copy into shared memory (ntt_grp14)
+  double ninv_b, nw_b;
 };
 static_assert(sizeof(LimbConstDev) == 128, "LimbConstDev is copied as one 128-byte bulk transfer");
 
@@ -388,16 +390,22 @@ struct Arith52S {
   __device__ static uint64_t scale_ninv(uint64_t x, const LimbConstDev& c) {
     return as_u(mul_signed(as_d(x), as_d(c.ninv), as_d(c.ninvp), c.qq));
   }
-  // see ArithInt::inv_fold; signed doubles |x| < 2q in, canonical words out
+  // see ArithInt::inv_fold; signed doubles |x| < 2q in, canonical words out:
+  // |a +- b| < 4q times the BALANCED constants n^-1, n^-1 w_1 (|w v| < 2q^2:
+  // integer-grid product, |T| < q), then one fix-up to [0, q): 9 FP64
+  // operations per word, no conditional subtraction
   static constexpr bool kFold = true;
-  // (|a +- b| < 4q reduced to < 2q, then the fine product: |T| < 0.875q, one
-  // fix-up to [0, q): 10 FP64 operations per word instead of 12)
   __device__ static void inv_fold(uint64_t& x0, uint64_t& x1, const LimbConstDev& c) {
     const double a = as_d(x0), b = as_d(x1);
-    const double s = csubS(__dadd_rn(a, b), c.twoq_d), t = csubS(__dsub_rn(a, b), c.twoq_d);
-    x0 = canon_small(mul_recip_fine(s, as_d(c.ninv), c.qinv, c.q_d), c);
-    x1 = canon_small(mul_recip_fine(t, as_d(c.nw), c.qinv, c.q_d), c);
+    const double s = __dadd_rn(a, b), t = __dsub_rn(a, b);
+    x0 = canon_small(mul_recip_fine(s, c.ninv_b, c.qinv, c.q_d), c);
+    x1 = canon_small(mul_recip_fine(t, c.nw_b, c.qinv, c.q_d), c);
   }
+  // An inverse stage on the pair (x0, x1) whose two inputs are BOTH products
+  // of the stage before (|x| < q each: T outputs): the sum stays below 2q
+  // without the conditional subtraction. Inside a register pass this is known
+  // per butterfly (the index bit of the previous stage is a register bit).
+  static constexpr bool kInvSkipTT = true;
 };
 
 // ---------------------------------------------------------------------------

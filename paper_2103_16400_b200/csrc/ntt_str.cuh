@@ -116,7 +116,10 @@ __device__ __forceinline__ void pass16i(uint64_t* x, const LimbConst& c, F&& twf
 #pragma unroll
       for (int lo = 0; lo < (1 << i); ++lo) {
         const int r0 = (hi << (i + 1)) | lo, r1 = r0 | (1 << i);
-        A::template inv<false>(x[r0], x[r1], w, c);
+        // signed policy: both inputs are products of stage i - 1 (|x| < q) when that stage's
+        // register bit is set: their sum needs no reduction (Arith52S::kInvSkipTT)
+        if (A::kSigned && i > 0 && ((lo >> (i - 1)) & 1)) A::template inv<true>(x[r0], x[r1], w, c);
+        else A::template inv<false>(x[r0], x[r1], w, c);
       }
     }
   }
