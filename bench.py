@@ -49,10 +49,21 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 METRIC = "fwd/inv NTT Mcoeff/s (N=16384, batched limbs)"
 FWD_KERNEL = "ntt_str14<Arith52S,fwd>"  # the forward's only launch at cfg3
-# FP64 operations per butterfly of the signed canonical arithmetic
-# (modmath.cuh Arith52S: 6 for the Shoup product, 2 output adds, 1 for the
-# conditional subtraction), the floor the transform kernels are bound by
-DP_PER_BFLY = 9
+# FP64 pipe operations per butterfly the signed canonical arithmetic executes
+# by design (modmath.cuh Arith52S: 6 for the rounded-reciprocal product, 2
+# output adds, 1 for a conditional subtraction where a stage has one),
+# averaged over a 16384-word transform:
+#   forward (fin = 1): stages 2, 4, .., 12 reduce, 8 stages do not  -> 8 + 6/14
+#   inverse: stage 0 and the sums of two products do not reduce (120 of the 208
+#            butterflies per thread of stages 1..12 do), the folded last stage
+#            takes 14 per pair without its canonical fix-ups         -> 2008/224
+# Canonicalisation (5 per output word of the forward) is not counted. Round 1
+# and the first half of round 2 counted 9 for both directions (their kernels
+# reduced at every stage); `frac_9op_yardstick` keeps that yardstick.
+DP_PER_BFLY_FWD = 8 + 6 / 14
+DP_PER_BFLY_INV = 2008 / 224
+DP_PER_BFLY_POLY = (2 * DP_PER_BFLY_FWD + DP_PER_BFLY_INV) / 3
+DP_PER_BFLY_OLD = 9
 N = 16384
 NLIMBS = 32
 NPOLYS = 64
@@ -255,7 +266,7 @@ class ClockSampler:
                 pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
                 self.samples.append([str(sm), str(mx), f"{pw:.1f}", hex(r)] +
                                     ["Active" if r & b else "Not Active" for _, b in bits])
-                self._stop.wait(0.02)
+                self._stop.wait(0.002)
 
         def run():
             try:
@@ -307,8 +318,15 @@ class ClockSampler:
                 for k, name in enumerate(names):
                     if s[4 + k].lower().startswith("active"):
                         reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
+        pw = []
+        for s in self.samples:
+            try:
+                pw.append(float(s[2]))
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_min_mhz": min(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "power_w_median": statistics.median(pw) if pw else None, "power_w_max": max(pw) if pw else None,
                 "samples": len(self.samples)}
 
 
@@ -652,10 +670,10 @@ def run_configs(rates, hbm, threads):
     c15, _ = steady_median(lambda: rp5.poly(buf5, f5, g5, sample5, 1), reps=10, warm_seconds=0.2)
     ca5, _ = steady_median(lambda: rp5.poly(buf5, f5, g5, rows5, threads), reps=10, warm_seconds=0.5)
     rp5.close()
-    floor5 = bfly5 * DP_PER_BFLY / fp64 * 1e6 if fp64 else None
+    floor5 = bfly5 * DP_PER_BFLY_POLY / fp64 * 1e6 if fp64 else None
     out["cfg5"] = {
         "op": "poly_mult_mod, N=16384, 16 x 50-bit limbs x 128 pairs (2048 row pairs)",
-        "bound": "fp64 pipe (3 transforms x 9 FP64 ops/butterfly vs the live DFMA rate)",
+        "bound": f"fp64 pipe (2 forwards + 1 inverse, {DP_PER_BFLY_POLY:.2f} FP64 ops/butterfly on average, vs the live DFMA rate)",
         "kernel": "poly_str14 (both forwards, product, inverse on chip, two streams per thread; g^ held in TMEM)",
         "launches_per_call": launches5,
         "us": us5, "Gcoeff_s": N * rows5 / us5 / 1e3, "fp64_floor_us": floor5,
@@ -861,26 +879,31 @@ def run_gpu(args):
         fp64 = rates.get("fp64_ops_per_s") if rates else None
         rows = NPOLYS * nl
         butterflies = (N // 2) * 14 * rows
-        fp64_ops = butterflies * DP_PER_BFLY
+        fp64_ops = butterflies * DP_PER_BFLY_FWD
         achieved_t = fp64_ops / (fwd_ms * 1e-3) / 1e12
         fwd_bytes = 16 * words  # read + write each coefficient once
         roofline = {
             "bound": "fp64", "kernel": FWD_KERNEL, "unit": "TFLOP/s",
             "op_definition": "one FP64 pipe lane-instruction (DADD/DMUL/DFMA) = 1 op; "
-                             f"{DP_PER_BFLY} per butterfly (modmath.cuh Arith52S)",
+                             f"{DP_PER_BFLY_FWD:.3f} per butterfly executed by the forward (8 + a conditional "
+                             "subtraction on 6 of 14 stages), "
+                             f"{DP_PER_BFLY_INV:.3f} by the inverse (modmath.cuh Arith52S)",
             "ops_per_launch": fp64_ops, "butterflies_per_launch": butterflies,
             "achieved": achieved_t,
             "peak": fp64 / 1e12 if fp64 else None,
             "peak_kind": "measured live: DFMA lane-ops/s of independent chains, tools/probe.cu",
             "frac": (achieved_t * 1e12 / fp64) if fp64 else None,
             "t_floor_us": fp64_ops / fp64 * 1e6 if fp64 else None, "t_measured_us": fwd_ms * 1e3,
+            "frac_9op_yardstick": (butterflies * DP_PER_BFLY_OLD / (fwd_ms * 1e-3) / fp64) if fp64 else None,
             "in_register_ceiling": {
                 "bfly_per_s": rates.get("arith52s_fwd_bfly_per_s") if rates else None,
                 "frac": (butterflies / (fwd_ms * 1e-3) / rates["arith52s_fwd_bfly_per_s"])
                 if rates and rates.get("arith52s_fwd_bfly_per_s") else None,
                 "note": "the same Arith52S butterflies looping in registers (no exchanges, no memory)"},
             "inverse": {"t_measured_us": inv_ms * 1e3,
-                        "frac": ((butterflies * DP_PER_BFLY) / (inv_ms * 1e-3) / fp64) if fp64 else None},
+                        "frac": ((butterflies * DP_PER_BFLY_INV) / (inv_ms * 1e-3) / fp64) if fp64 else None,
+                        "frac_9op_yardstick": ((butterflies * DP_PER_BFLY_OLD) / (inv_ms * 1e-3) / fp64)
+                        if fp64 else None},
             "traffic": ncu_traffic(),
             "hbm": {"achieved_gbs": fwd_bytes / (fwd_ms * 1e-3) / 1e9, "peak_gbs": hbm, "peak_kind": peak_kind,
                     "frac": fwd_bytes / (fwd_ms * 1e-3) / 1e9 / hbm, "algorithmic_bytes_per_launch": fwd_bytes},
@@ -942,8 +965,8 @@ def run_gpu(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -209,7 +209,8 @@ void nk_debug_block_kernel(int which);
 /* Testing aid: one butterfly per element pair (x0[i], x1[i]) -> (y0[i], y1[i])
  * in an arithmetic policy of the kernels (0 = ArithInt<64>, 1 = ArithInt<52>,
  * 2 = Arith52P, 3 = Arith52S with int64 words in and out, 4 = ArithIntL,
- * 5 = Arith52S's forward stage without the pre-reduction of x0, int64 words),
+ * 5 / 6 = Arith52S (int64 words) / ArithIntL stage without its conditional
+ * subtraction),
  * twiddle w with its Shoup quotient for the policy's width;
  * fwd != 0: the forward (CT) butterfly, else the inverse (GS). Device buffers. */
 int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint64_t* d_x0,

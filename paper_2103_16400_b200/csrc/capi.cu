@@ -284,7 +284,7 @@ int ntt_dispatch_aligned(const nk_plan* p, bool fwd, uint64_t* res, const uint64
       rc = fwd ? run_ntt<nk::Arith52S, true>(b, words, st) : run_ntt<nk::Arith52S, false>(b, words, st);
     else if (bs == 52)
       rc = fwd ? run_ntt<nk::Arith52P, true>(b, words, st) : run_ntt<nk::Arith52P, false>(b, words, st);
-    else if (b.fout == 1 && !nk::rt::exact_only && max_q(p, limb0 + (uniform ? 0 : l), uniform ? nlimbs : 1) < (uint64_t{1} << 61))
+    else if (b.fout == 1 && !nk::rt::exact_only && max_q(p, limb0 + (uniform ? 0 : l), uniform ? nlimbs : 1) < (uint64_t{1} << 60))
       // beta = 2^64, canonical result only: loose Shoup quotients (nk::ArithIntL)
       rc = fwd ? run_ntt<nk::ArithIntL, true>(b, words, st) : run_ntt<nk::ArithIntL, false>(b, words, st);
     else
@@ -320,8 +320,8 @@ __global__ void bfly_test_kernel(const uint64_t* x0, const uint64_t* x1, uint64_
   typename A::Tw wt;
   if constexpr (std::is_same_v<typename A::Tw, uint64_t>) wt = w.x;  // w only (Arith52S)
   else wt = w;
-  if (FWD) A::template fwd<SKIP>(a, b, wt, c);  // SKIP: a stage without the pre-reduction of x0
-  else A::template inv<false>(a, b, wt, c);
+  if (FWD) A::template fwd<SKIP>(a, b, wt, c);  // SKIP: a stage without its conditional subtraction
+  else A::template inv<SKIP>(a, b, wt, c);
   if (SIGNED_IO) {
     y0[i] = static_cast<uint64_t>(static_cast<int64_t>(as_d(a)));
     y1[i] = static_cast<uint64_t>(static_cast<int64_t>(as_d(b)));
@@ -361,12 +361,11 @@ int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint
   if (!valid_modulus(q, &m)) return fail(NK_ERR_MODULUS, "Modulus: value must be a prime in [3, 2^62)");
   if (w >= q) return fail(NK_ERR_ROOT, "debug_butterflies: twiddle must be < q");
   const bool b52 = policy == 1 || policy == 2 || policy == 3 || policy == 5;
-  if (policy < 0 || policy > 5) return fail(NK_ERR_BIT_SHIFT, "debug_butterflies: policy must be 0..5");
-  if (policy == 5 && !fwd) return fail(NK_ERR_BIT_SHIFT, "debug_butterflies: policy 5 is a forward stage");
+  if (policy < 0 || policy > 6) return fail(NK_ERR_BIT_SHIFT, "debug_butterflies: policy must be 0..6");
   if (b52 && u128{4} * q >= (u128{1} << 52))
     return fail(NK_ERR_BIT_SHIFT_52, "NttTables: 52-bit accumulator requires 4q < 2^52");
-  if (policy == 4 && q >= (uint64_t{1} << 61))
-    return fail(NK_ERR_MODULUS, "debug_butterflies: the loose policy requires q < 2^61");
+  if ((policy == 4 || policy == 6) && q >= (uint64_t{1} << 60))
+    return fail(NK_ERR_MODULUS, "debug_butterflies: the loose policy requires q < 2^60");
   if (n == 0) return 0;
   if (!d_x0 || !d_x1 || !d_y0 || !d_y1) return fail(NK_ERR_NULL, "debug_butterflies: NULL buffer");
   const int bs = b52 ? 52 : 64;
@@ -392,6 +391,7 @@ int nk_debug_butterflies(int policy, int fwd, uint64_t q, uint64_t w, const uint
     case 2: return run_bfly_test<nk::Arith52P, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
     case 3: return run_bfly_test<nk::Arith52S, true>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
     case 5: return run_bfly_test<nk::Arith52S, true, true>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
+    case 6: return run_bfly_test<nk::ArithIntL, false, true>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
     default: return run_bfly_test<nk::ArithIntL, false>(f, d_x0, d_x1, n, tw, c, d_y0, d_y1);
   }
 }

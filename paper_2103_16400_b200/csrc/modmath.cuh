@@ -409,7 +409,7 @@ struct Arith52S {
 };
 
 // ---------------------------------------------------------------------------
-// ArithIntL: beta = 2^64 limbs with q < 2^61, canonical outputs only (fout ==
+// ArithIntL: beta = 2^64 limbs with q < 2^60, canonical outputs only (fout ==
 // 1, like Arith52S for beta = 2^52).
 //
 // The Shoup quotient drops the low x low partial product and the carries of
@@ -419,9 +419,20 @@ struct Arith52S {
 // with d in {0, 1, 2}, and T = w x - qh q (mod 2^64) = T_exact + d q lies in
 // [0, 4q). Cost: one IMAD.WIDE and two IMAD.HI instead of four IMAD.WIDE
 // (IMAD.WIDE issues at half the IMAD rate).
-// Ranges (8q < 2^64): forward words in [0, 8q): u = x0 reduced by 4q once
-// ([0, 4q)), x0' = u + T, x1' = u + 4q - T, both in [0, 8q). Inverse words
-// in [0, 4q): x0' = x0 + x1 reduced by 4q once, x1' = T(x0 + 4q - x1).
+// The bound holds for every 64-bit x (Shoup: w x - floor(w' x / 2^64) q < q (1 +
+// x / 2^64) < 2q), so the multiplicand needs no reduction, and with 16q <= 2^64
+// the words have room to skip reductions:
+//   forward: a reducing stage takes x < 16q: u = x0 reduced by 8q once ([0,
+//            8q)), x0' = u + T, x1' = u + 4q - T, both below 12q; the stage
+//            after it may skip the reduction (u = x0 < 12q): outputs below
+//            16q. The 16384-word kernels reduce on odd stages only (fwd_skip);
+//            inputs are below 4q (fin <= 4) or, after the global passes of a
+//            long row (which reduce at every stage but the first), below 12q.
+//            Final words below 16q: four conditional subtractions to [0, q).
+//   inverse: words in [0, 8q): x0' = x0 + x1 reduced by 8q once, x1' = T(x0 +
+//            8q - x1) < 4q; the sum of two products (both inputs T outputs of
+//            the stage before) stays below 8q without the reduction
+//            (kInvSkipTT: known per butterfly inside a register pass).
 // Representatives differ from the reference's lazy ones; canonical results
 // are identical (they are unique).
 // ---------------------------------------------------------------------------
@@ -442,28 +453,33 @@ struct ArithIntL {
   static constexpr bool kLoose = true;
   __device__ static uint64_t load(uint64_t x) { return x; }
   __device__ static uint64_t store(uint64_t x) { return x; }
-  // inputs below 4q (fin <= 4): the first stage's reduction is a value no-op
+  // ILTM: the stage skips its reduction (inputs below 12q; at fin <= 4 the first stage's
+  // inputs are below 4q)
   template <bool ILTM>
   __device__ static void fwd(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
-    const uint64_t u = ILTM ? x0 : nk::csub(x0, c.fourq);
+    const uint64_t u = ILTM ? x0 : nk::csub(x0, c.fourq << 1);
     const uint64_t t = mul_loose(x1, w.x, w.y, c.negq);
     x0 = u + t;
     x1 = u + c.fourq - t;
   }
+  // the 16384-word kernels' schedule: stage gs (0 = the block's first stage) skips on even gs
+  __host__ __device__ static constexpr bool fwd_skip(bool, int gs) { return (gs & 1) == 0; }
   template <bool ILTM>
   __device__ static void inv(uint64_t& x0, uint64_t& x1, ulonglong2 w, const LimbConstDev& c) {
-    const uint64_t t = x0 + c.fourq - x1;
+    const uint64_t eightq = c.fourq << 1;
+    const uint64_t t = x0 + eightq - x1;
     uint64_t s = x0 + x1;
-    if (!ILTM) s = nk::csub(s, c.fourq);
+    if (!ILTM) s = nk::csub(s, eightq);
     x0 = s;
     x1 = mul_loose(t, w.x, w.y, c.negq);
   }
+  static constexpr bool kInvSkipTT = true;
   __device__ static uint64_t scale_ninv(uint64_t x, const LimbConstDev& c) {
     return mul_loose(x, c.ninv, c.ninvp, c.negq);
   }
-  // [0, 8q) -> [0, q)
-  __device__ static uint64_t red8(uint64_t x, const LimbConstDev& c) {
-    return nk::csub(nk::csub(nk::csub(x, c.fourq), c.twoq), c.q);
+  // [0, 16q) -> [0, q)
+  __device__ static uint64_t red16(uint64_t x, const LimbConstDev& c) {
+    return nk::csub(nk::csub(nk::csub(nk::csub(x, c.fourq << 1), c.fourq), c.twoq), c.q);
   }
   // [0, 4q) -> [0, q)
   __device__ static uint64_t red4(uint64_t x, const LimbConstDev& c) {
@@ -471,7 +487,7 @@ struct ArithIntL {
   }
   static constexpr bool kFold = true;
   __device__ static void inv_fold(uint64_t& x0, uint64_t& x1, const LimbConstDev& c) {
-    const uint64_t s = x0 + x1, t = x0 + c.fourq - x1;  // both below 8q
+    const uint64_t s = x0 + x1, t = x0 + (c.fourq << 1) - x1;  // both below 16q
     x0 = red4(mul_loose(s, c.ninv, c.ninvp, c.negq), c);
     x1 = red4(mul_loose(t, c.nw, c.nwp, c.negq), c);
   }
@@ -512,7 +528,7 @@ __device__ __forceinline__ uint64_t mulmod_signed_canon(uint64_t xbits, uint64_t
 template <class A>
 __device__ __forceinline__ uint64_t fwd_out(uint64_t x, const LimbConstDev& c, int fout) {
   if constexpr (A::kLoose) {
-    return A::red8(x, c);  // canonical-only policy
+    return A::red16(x, c);  // canonical-only policy
   } else if constexpr (A::kSigned) {
     return A::canon(as_d(x), c);
   } else {

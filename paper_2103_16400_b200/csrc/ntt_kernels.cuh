@@ -463,11 +463,12 @@ struct PassD {
 // Does forward stage `gs` of a 16384-word block (0 = its first stage, index bit
 // 13; s_local = the stage's position in its pass, iltm0 only on the first pass
 // of a transform with canonical input) skip the pre-reduction of x0? The signed
-// FP64 policy reduces on even stages only (modmath.cuh, Arith52S::fwd_skip);
-// the others skip their first kIltmFwd stages at fin = 1, like the reference.
+// FP64 policy reduces on even stages only, the loose integer policy on odd
+// ones (modmath.cuh, Arith52S::fwd_skip, ArithIntL::fwd_skip); the exact
+// policies skip their first kIltmFwd stages at fin = 1, like the reference.
 template <class A>
 __host__ __device__ constexpr bool fwd_skip14(bool iltm0, int gs, int s_local) {
-  if constexpr (A::kSigned) return A::fwd_skip(iltm0, gs);
+  if constexpr (A::kSigned || A::kLoose) return A::fwd_skip(iltm0, gs);
   else return iltm0 && s_local < A::kIltmFwd;
 }
 

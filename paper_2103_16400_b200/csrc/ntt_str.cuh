@@ -83,6 +83,12 @@ constexpr size_t kStrSmemBytes = 1024 + kStageBytes + kGrpExBytes + 2 * sizeof(L
 
 namespace str {
 
+template <class A>
+__host__ __device__ constexpr bool inv_skip_tt() {
+  if constexpr (A::kSigned || A::kLoose) return A::kInvSkipTT;
+  else return false;
+}
+
 // K stages (forward order: bit LO + K - 1 first) on the 16 registers x[0..15]
 // whose index bits are j_LO .. j_{LO+3}; the twiddle of stage bit b, position
 // hi (the register bits above b) comes from `twf(i, hi)`, i = b - LO.
@@ -116,9 +122,9 @@ __device__ __forceinline__ void pass16i(uint64_t* x, const LimbConst& c, F&& twf
 #pragma unroll
       for (int lo = 0; lo < (1 << i); ++lo) {
         const int r0 = (hi << (i + 1)) | lo, r1 = r0 | (1 << i);
-        // signed policy: both inputs are products of stage i - 1 (|x| < q) when that stage's
-        // register bit is set: their sum needs no reduction (Arith52S::kInvSkipTT)
-        if (A::kSigned && i > 0 && ((lo >> (i - 1)) & 1)) A::template inv<true>(x[r0], x[r1], w, c);
+        // canonical-only policies: both inputs are products of stage i - 1 when that stage's
+        // register bit is set: their sum needs no reduction (kInvSkipTT, modmath.cuh)
+        if (inv_skip_tt<A>() && i > 0 && ((lo >> (i - 1)) & 1)) A::template inv<true>(x[r0], x[r1], w, c);
         else A::template inv<false>(x[r0], x[r1], w, c);
       }
     }

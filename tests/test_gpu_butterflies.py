@@ -150,21 +150,28 @@ def test_signed_policy_alternating_stages(nk):
 
 
 @pytest.mark.parametrize("fwd", [True, False], ids=["fwd", "inv"])
-def test_loose_policy_ranges(nk, fwd):
-    """ArithIntL: forward words in [0, 8q) stay there, inverse words in
-    [0, 4q) stay there, congruent to the butterfly's value."""
-    rng = np.random.default_rng(9 + fwd)
-    for q in qs(ARITHINTL):
-        r = 8 if fwd else 4
-        if q == 17:
-            a, b = exhaustive_pairs(0, r * q)
+@pytest.mark.parametrize("skip", [False, True], ids=["reducing", "skipping"])
+def test_loose_policy_ranges(nk, fwd, skip):
+    """ArithIntL (q < 2^60, 16q <= 2^64), modmath.cuh: a reducing forward stage
+    maps words in [0, 16q) into [0, 12q), the non-reducing stage after it
+    [0, 12q) into [0, 16q); inverse words stay in [0, 8q), without the
+    reduction when both inputs are products (below 4q). Congruent to the
+    butterfly's value."""
+    rng = np.random.default_rng(9 + fwd + 2 * skip)
+    for q in [17, largest_ntt_primes(60, 1024, 1)[0]]:
+        if fwd:
+            rin, rout = (12, 16) if skip else (16, 12)
         else:
-            a, b = sample_pairs(q, rng, 4096, 0, r)
+            rin, rout = (4, 8) if skip else (8, 8)
+        if q == 17:
+            a, b = exhaustive_pairs(0, rin * q)
+        else:
+            a, b = sample_pairs(q, rng, 4096, 0, rin)
         a, b = a.astype(np.uint64), b.astype(np.uint64)
         for w in twiddles(q, rng):
-            y0, y1 = nk.debug_butterflies(ARITHINTL, fwd, q, w, dev(a), dev(b))
+            y0, y1 = nk.debug_butterflies(6 if skip else ARITHINTL, fwd, q, w, dev(a), dev(b))
             y0, y1 = host(y0).view(np.uint64), host(y1).view(np.uint64)
-            assert int(y0.max()) < r * q and int(y1.max()) < r * q, (q, w)
+            assert int(y0.max()) < rout * q and int(y1.max()) < rout * q, (q, w)
             A, B = a.astype(object), b.astype(object)
             if fwd:
                 e0, e1 = (A + w * B) % q, (A - w * B) % q

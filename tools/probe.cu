@@ -35,8 +35,8 @@ __global__ void __launch_bounds__(256) dfma_loop(double* out, int iters) {
 
 // butterflies over V register words, four stages per iteration (spans 1, 2,
 // 4, 8), two twiddles: the transforms' inner loop without memory or exchanges.
-// The signed FP64 policy's forward reduces x0 on even stages only, as in the
-// 16384-word kernels (modmath.cuh, Arith52S::fwd_skip).
+// The forward reduces x0 on every other stage only, as in the 16384-word
+// kernels (modmath.cuh, Arith52S::fwd_skip / ArithIntL::fwd_skip).
 template <class Tw>
 __device__ __forceinline__ Tw as_tw(ulonglong2 w) {
   if constexpr (std::is_same_v<Tw, uint64_t>) return w.x;  // w only (Arith52S's 8-byte tables)
@@ -58,7 +58,7 @@ __global__ void __launch_bounds__(512, 1) bfly_loop(uint64_t* out, LimbConstDev 
       for (int i = 0; i < V; ++i) {
         if ((i & h) || h >= V) continue;
         if (INV) A::template inv<false>(v[i], v[i + h], w[(i >> 1) & 1], c);
-        else if (A::kSigned && (s & 1)) A::template fwd<true>(v[i], v[i + h], w[(i >> 1) & 1], c);
+        else if (A::fwd_skip(false, s)) A::template fwd<true>(v[i], v[i + h], w[(i >> 1) & 1], c);
         else A::template fwd<false>(v[i], v[i + h], w[(i >> 1) & 1], c);
       }
     }
