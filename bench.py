@@ -817,8 +817,6 @@ def run_gpu(args):
 
     for _ in range(args.warmup):
         step()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sampler = ClockSampler(device)
     barrier()
     torch.cuda.synchronize()
@@ -826,22 +824,35 @@ def run_gpu(args):
     l0 = nk.launch_count()
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
+    # the timed region: K steps between two events (events between the kernels
+    # of a step cost 8 us per step, tools/step_probe.py)
     t_start.record(stream)
     for i in range(args.steps):
-        ev[i][0].record(stream)
         plan.forward(d_f, d_in, 1, 1)
-        ev[i][1].record(stream)
         plan.inverse(d_b, d_f, 1, 1)
-        ev[i][2].record(stream)
     t_end.record(stream)
     torch.cuda.synchronize()
     launches = nk.launch_count() - l0
     barrier()
-    clocks = sampler.stop()
     total_ms = max_over_ranks(t_start.elapsed_time(t_end))
     launches = int(sum_over_ranks(launches))
-    fwd_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in ev)
-    inv_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in ev)
+
+    # per-kernel launch durations for the roofline: K forwards, then K inverses,
+    # back to back between two events each (same buffers, the sampler still running)
+    def kernel_ms(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / args.steps
+
+    fwd_ms = kernel_ms(lambda: plan.forward(d_f, d_in, 1, 1))
+    inv_ms = kernel_ms(lambda: plan.inverse(d_b, d_f, 1, 1))
+    clocks = sampler.stop()
     ms_step = total_ms / args.steps
     coeffs_step = 2 * total_words
     value = coeffs_step / (ms_step * 1e-3) / 1e6
