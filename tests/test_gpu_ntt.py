@@ -429,3 +429,41 @@ def test_host_pipeline_multi_chunk_in_place(nk, oracle, pinned):
     a, b = x[:2_400_000] % np.uint64(q), x[2_400_000:4_800_000] % np.uint64(q)  # two chunks each
     r = nk.eltwise_mult_mod(None, a, b, q, 1)
     assert np.array_equal(r, oracle.eltwise_mult_mod(a, b, q, 1))
+
+
+@pytest.mark.parametrize("pattern", ["max", "alt", "random"])
+def test_signed_policy_bounds_across_moduli(nk, oracle, pattern):
+    """The signed FP64 policy's reduced schedules (balanced twiddles, a
+    reduction on every other forward stage, none for sums of two products in the
+    inverse, modmath.cuh) at the ends of their modulus range: the smallest and
+    the largest 50-bit limb, and 40-, 30- and 20-bit limbs, N = 16384, on
+    worst-case and random operands, canonical outputs of every input factor,
+    and poly_mult_mod of the same operands."""
+    n = 1 << 14
+    moduli = [smallest_ntt_primes(50, n, 1)[0], largest_ntt_primes(50, n, 1)[0], largest_ntt_primes(40, n, 1)[0],
+              largest_ntt_primes(30, n, 1)[0], largest_ntt_primes(20, n, 1)[0]]
+    plan = nk.RnsNtt(n, moduli)
+    q = np.repeat(np.asarray(moduli, dtype=np.uint64), n)
+    base = rows_of(oracle, moduli, n, 1, 77)
+    for fin, fout, fwd in [(1, 1, True), (2, 1, True), (4, 1, True), (1, 1, False), (2, 1, False)]:
+        top = q * np.uint64(fin) - np.uint64(1)
+        if pattern == "max":
+            x = top
+        elif pattern == "alt":
+            x = np.where(np.arange(q.size) % 2 == 0, top, np.uint64(0)).astype(np.uint64)
+        else:
+            x = lifted(oracle, base, moduli, n, fin, 5 + fin)
+        d = dev(x)
+        if fwd:
+            got = host(plan.forward(torch.empty_like(d), d, fin, fout))
+            want = oracle.forward(n, moduli, x, fin, fout)
+        else:
+            got = host(plan.inverse(torch.empty_like(d), d, fin, fout))
+            want = oracle.inverse(n, moduli, x, fin, fout)
+        assert np.array_equal(got, want), f"{'fwd' if fwd else 'inv'} {pattern} fin={fin}"
+    f = (q - np.uint64(1)) if pattern != "random" else base
+    g = f if pattern == "max" else rows_of(oracle, moduli, n, 1, 78)
+    df, dg = dev(f), dev(g)
+    got = host(plan.poly_mult_mod(torch.empty_like(df), df, dg))
+    want = oracle.poly_mult_mod(n, moduli, f, g)
+    assert np.array_equal(got, want), f"poly {pattern}"
