@@ -132,6 +132,25 @@ struct PassOf {
   __host__ __device__ static constexpr int k(int p) { return S::k(td(p)); }
 };
 
+// Does forward stage `gs` of a whole-row or 16384-word-block transform (0 = its
+// first stage; s_local = the stage's position in its pass, iltm0 only on the
+// first pass of a transform with canonical input) skip the pre-reduction of
+// x0? The signed FP64 policy reduces on even stages only, the loose integer
+// policy on odd ones (modmath.cuh, Arith52S::fwd_skip, ArithIntL::fwd_skip);
+// the exact policies skip their first kIltmFwd stages at fin = 1, like the
+// reference.
+template <class A>
+__host__ __device__ constexpr bool fwd_skip_stage(bool iltm0, int gs, int s_local) {
+  if constexpr (A::kSigned || A::kLoose) return A::fwd_skip(iltm0, gs);
+  else return iltm0 && s_local < A::kIltmFwd;
+}
+// Inverse: may the sum of two products of the stage before skip its reduction?
+template <class A>
+__host__ __device__ constexpr bool inv_skip_tt() {
+  if constexpr (A::kSigned || A::kLoose) return A::kInvSkipTT;
+  else return false;
+}
+
 // One register pass: K butterfly bits [LO, LO+K) over G = V / 2^K independent
 // groups held in v[g * 2^K + r]. xt = N + block offset + this thread's index
 // bits (outside the pass). ILTM0: first stage with InputLessThanMod.
@@ -159,10 +178,14 @@ __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const typename
           uint64_t& x0 = v[g * R + r0];
           uint64_t& x1 = v[g * R + r1];
           if (FWD) {
-            if (ILTM0 && s < A::kIltmFwd) A::template fwd<true>(x0, x1, w, c);
+            // LOGB - 1 - b: the stage's number from the row's first stage (whole rows only)
+            if (fwd_skip_stage<A>(ILTM0, LOGB - 1 - b, s)) A::template fwd<true>(x0, x1, w, c);
             else A::template fwd<false>(x0, x1, w, c);
           } else {
-            if (ILTM0 && s == 0) A::template inv<true>(x0, x1, w, c);
+            // canonical-only policies: both inputs are products of the stage before (its bit is a
+            // register bit of this pass): their sum needs no reduction (kInvSkipTT, modmath.cuh)
+            if ((ILTM0 && s == 0) || (inv_skip_tt<A>() && i > 0 && ((l >> (i - 1)) & 1)))
+              A::template inv<true>(x0, x1, w, c);
             else A::template inv<false>(x0, x1, w, c);
           }
         }
@@ -460,16 +483,9 @@ struct PassD {
 };
 
 
-// Does forward stage `gs` of a 16384-word block (0 = its first stage, index bit
-// 13; s_local = the stage's position in its pass, iltm0 only on the first pass
-// of a transform with canonical input) skip the pre-reduction of x0? The signed
-// FP64 policy reduces on even stages only, the loose integer policy on odd
-// ones (modmath.cuh, Arith52S::fwd_skip, ArithIntL::fwd_skip); the exact
-// policies skip their first kIltmFwd stages at fin = 1, like the reference.
 template <class A>
 __host__ __device__ constexpr bool fwd_skip14(bool iltm0, int gs, int s_local) {
-  if constexpr (A::kSigned || A::kLoose) return A::fwd_skip(iltm0, gs);
-  else return iltm0 && s_local < A::kIltmFwd;
+  return fwd_skip_stage<A>(iltm0, gs, s_local);
 }
 
 // Stages [S0, S1) (processing order) of the register pass PD, on all 32 words
@@ -518,7 +534,8 @@ __device__ __forceinline__ void stages14(uint64_t (&v)[32], const typename A::Tw
               if (fwd_skip14<A>(ILTM0, kB14 - 1 - b, s)) A::template fwd<true>(x0, x1, w, c);
               else A::template fwd<false>(x0, x1, w, c);
             } else {
-              if (ILTM0 && s == 0) A::template inv<true>(x0, x1, w, c);
+              if ((ILTM0 && s == 0) || (inv_skip_tt<A>() && i > 0 && ((l >> (i - 1)) & 1)))
+                A::template inv<true>(x0, x1, w, c);
               else A::template inv<false>(x0, x1, w, c);
             }
           }

@@ -83,12 +83,6 @@ constexpr size_t kStrSmemBytes = 1024 + kStageBytes + kGrpExBytes + 2 * sizeof(L
 
 namespace str {
 
-template <class A>
-__host__ __device__ constexpr bool inv_skip_tt() {
-  if constexpr (A::kSigned || A::kLoose) return A::kInvSkipTT;
-  else return false;
-}
-
 // K stages (forward order: bit LO + K - 1 first) on the 16 registers x[0..15]
 // whose index bits are j_LO .. j_{LO+3}; the twiddle of stage bit b, position
 // hi (the register bits above b) comes from `twf(i, hi)`, i = b - LO.
