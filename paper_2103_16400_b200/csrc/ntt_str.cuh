@@ -429,6 +429,8 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t lognb = a.logn - kB14;
   const uint64_t rowwords16 = a.n >> 4;
 
+  // (a 16384-word block's row number fits 32 bits -- 2^32 rows would be 2^49 bytes -- so the
+  // limb of a row is a 32-bit remainder, not a call to the 64-bit division routine)
   auto item_row = [&](uint32_t k, uint64_t& row, uint64_t& blk) {
     row = (static_cast<uint64_t>(k) >> lognb) * a.row_mul + a.row_add;
     blk = static_cast<uint64_t>(k) & ((uint64_t{1} << lognb) - 1);
@@ -437,7 +439,7 @@ __global__ void __launch_bounds__(512, 1)
     uint64_t row, blk;
     item_row(k, row, blk);
     const int32_t y0 = static_cast<int32_t>(row * rowwords16 + (blk << (kB14 - 4)));
-    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row) % a.nlimbs;
     mbar_expect_tx(bar_full, kStageBytes + static_cast<uint32_t>(sizeof(LimbConst)));
 #pragma unroll
     for (int q = 0; q < 4; ++q) tma_load_2d(St + q * 32768, &tin, 0, y0 + q * 256, bar_full);
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(512, 1)
     uint64_t row, blk;
     item_row(k, row, blk);
     NK_GTS(0);
-    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row) % a.nlimbs;
     const Tw* __restrict__ tw = tw_of<A>(a, limb);
     const Tw* __restrict__ twq = twq_of<A>(a, limb) + blk * kStrTableWords + t;
     const uint64_t boff = blk << kB14;
@@ -563,7 +565,7 @@ __global__ void __launch_bounds__(512, 1)
     uint64_t row, blk;
     item_row(k, row, blk);
     const int32_t y0 = static_cast<int32_t>(row * rowwords16 + (blk << (kB14 - 4)));
-    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row) % a.nlimbs;
     mbar_expect_tx(bar_full, kStageBytes + static_cast<uint32_t>(sizeof(LimbConst)));
 #pragma unroll
     for (int q = 0; q < 4; ++q) tma_load_2d(St + q * 32768, &tin, 0, y0 + q * 256, bar_full);
@@ -592,7 +594,7 @@ __global__ void __launch_bounds__(512, 1)
   for (uint32_t k = blockIdx.x; k < nitems; k += gridDim.x) {
     uint64_t row, blk;
     item_row(k, row, blk);
-    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row) % a.nlimbs;
     const Tw* __restrict__ tw = tw_of<A>(a, limb);
     const Tw* __restrict__ twq = twq_of<A>(a, limb) + blk * kStrTableWords + t;
     const uint64_t boff = blk << kB14;
