@@ -40,7 +40,7 @@ int encode_fn(EncodeTiledFn* out) {
   return 0;
 }
 
-enum MapKind { kRowMap = 0, kSuperlineMap = 1, kOutMap = 2, kGrpOutMap = 3, kStrOutMap = 4 };
+enum MapKind { kRowMap = 0, kSuperlineMap = 1, kOutMap = 2, kGrpOutMap = 3, kStrOutMap = 4, kStriOutMap = 5 };
 
 // A tensor map is a pure function of (kind, base, words): the last few are
 // cached per thread, so repeated calls on the same buffers (a serving loop,
@@ -90,6 +90,15 @@ int make_map(CUtensorMap* map, MapKind kind, const uint64_t* base, uint64_t word
     const cuuint32_t estr[2] = {1, 1};
     r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else if (kind == kStriOutMap) {
+    // 2D view [words/512][512] (no swizzle), boxes of 8 rows x 32 words: one warp's words
+    // l | w << 5 | r << 9 for 8 values of r (ntt_stri14's output, str::out_half_tma)
+    const cuuint64_t dims[2] = {512, words / 512};
+    const cuuint64_t strides[1] = {4096};
+    const cuuint32_t box[2] = {32, 8};
+    const cuuint32_t estr[2] = {1, 1};
+    r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   } else if (kind == kGrpOutMap) {
     // 5D view [words/512][4 (j7, j8)][4 (j5, j6)][2 halves][16 words] (128B swizzle),
     // boxes 16 x 1 x 1 x 1 x 8: one half of the runs j5j6 of 8 consecutive
@@ -175,11 +184,12 @@ int launch_str_t(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStre
 
 template <auto KERN>
 int launch_stri_k(const NttArgs& a, uint64_t nitems, uint64_t buf_words, cudaStream_t st) {
-  CUtensorMap map;
+  CUtensorMap map, omap;
   if (int rc = make_map(&map, kRowMap, a.in, buf_words)) return rc;
+  if (int rc = make_map(&omap, kStriOutMap, a.out, buf_words)) return rc;
   if (int rc = set_smem_once<KERN>(kStrSmemBytes)) return rc;
   const uint64_t g = nitems < static_cast<uint64_t>(sm_count()) ? nitems : sm_count();
-  KERN<<<static_cast<unsigned>(g), 512, kStrSmemBytes, st>>>(map, a, static_cast<uint32_t>(nitems));
+  KERN<<<static_cast<unsigned>(g), 512, kStrSmemBytes, st>>>(map, omap, a, static_cast<uint32_t>(nitems));
   launches++;
   NK_CUDA(cudaGetLastError());
   return 0;

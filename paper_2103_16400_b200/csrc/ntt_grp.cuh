@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(512, 1)
     uint64_t row, blk;
     item_row(k, row, blk);
     const int32_t y0 = static_cast<int32_t>(row * rowwords16 + (blk << (kB14 - 4)));
-    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row) % a.nlimbs;
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
     mbar_expect_tx(bar_full, kStageBytes + static_cast<uint32_t>(sizeof(LimbConst)));
 #pragma unroll
     for (int q = 0; q < 4; ++q) tma_load_2d(St + q * 32768, &tin, 0, y0 + q * 256, bar_full);
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(512, 1)
     uint64_t row, blk;
     item_row(k, row, blk);
     NK_GTS(0);
-    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row) % a.nlimbs;
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
     const typename A::Tw* __restrict__ tw = tw_of<A>(a, limb);
     // low pass: the thread-order table (a warp's loads are 32 consecutive entries)
     const typename A::Tw* __restrict__ twl = twg_of<A>(a, limb) + (blk << kB14) + t;

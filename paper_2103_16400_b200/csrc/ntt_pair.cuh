@@ -263,7 +263,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 2)
     uint64_t row, blk;
     item_row(k, row, blk);
     NK_TS(0);
-    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row) % a.nlimbs;
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
     const LimbConst cst = a.lc[limb];
     const typename A::Tw* __restrict__ tw = tw_of<A>(a, limb);
     const typename A::Tw* __restrict__ twl = twl_of<A>(a, limb) + (blk << kB14) + (jt_low >> 5);

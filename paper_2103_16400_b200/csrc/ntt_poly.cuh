@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(512, 1)
     // ---- inverse (n^-1 folded into the last stage), canonical words out ----
     const uint32_t to = tid_opaque(), wo = to >> 5, lo = to & 31u;
     str::inv_core<A, false>(
-        v, St, E + (wo << 12), c, a, itw, itwq, a.n, wo, lo, ta, bar_w, it & 1u, 0u,
+        v, St, E + (wo << 12), c, a, itw, itwq, a.n, wo, lo, ta, bar_w, it & 1u, 0u, [] {},
         [&] { mbar_wait(bar_free, it & 1u); },
         [&] {
           grp::staging_consumed(cnt, l, [&] {

@@ -302,13 +302,14 @@ __device__ __forceinline__ void fwd_core(uint64_t (&v)[32], uint8_t* St, uint8_t
 // entries, and with 8-byte tables the 8 entries of Q3''s first stage), loaded
 // by the caller ahead of its wait for the block; `inputs_read` runs before the
 // staging halves are first written (waits until every warp has its input);
-// `consumed` once this warp has read its last word of the staging buffer.
-template <class A, bool ILTM0, class FRD, class FCONS>
+// `consumed` once this warp has read its last word of the staging buffer;
+// `before_e2` before the warp's 4 KiB of E is first written.
+template <class A, bool ILTM0, class FPRE, class FRD, class FCONS>
 __device__ __forceinline__ void inv_core(uint64_t (&v)[32], uint8_t* St, uint8_t* Ew, const LimbConst& c,
                                          const NttArgs& a, const typename A::Tw* __restrict__ tw,
                                          const typename A::Tw* __restrict__ twq, uint64_t xbase, uint32_t w,
                                          uint32_t l, typename A::Tw* ta, uint64_t* bar_w, uint32_t par, uint32_t it_,
-                                         FRD&& inputs_read, FCONS&& consumed) {
+                                         FPRE&& before_e2, FRD&& inputs_read, FCONS&& consumed) {
   using Tw = typename A::Tw;
   (void)it_;
   constexpr bool kPre16 = sizeof(Tw) == 8;
@@ -348,6 +349,8 @@ __device__ __forceinline__ void inv_core(uint64_t (&v)[32], uint8_t* St, uint8_t
   };
 
   low_passes(0, ta);
+  before_e2();  // e.g. the previous block's output stores have read this warp's 4 KiB
+  __syncwarp();
 #pragma unroll
   for (int r = 0; r < 16; ++r) *reinterpret_cast<uint64_t*>(Ew + (e2r ^ (r << 4))) = v[r];
   __syncwarp();
@@ -410,6 +413,37 @@ __device__ __forceinline__ void inv_first_twiddles(typename A::Tw* ta, const typ
   }
 }
 
+// The inverse's result words out by TMA. Thread (w, l) holds word l | w << 5 | r << 9 in v[r]:
+// for a fixed r the warp's 32 words are 256 contiguous bytes, so 8 values of r are an
+// 8-row x 256-byte box of the output seen as [words / 512][512] (kStriOutMap). Half h
+// (pairs r = 8h .. 8h + 7 of the last stage, i.e. rows 8h.. and 16 + 8h..) goes through the
+// warp's 4 KiB of E as two 2 KiB images and two bulk tensor stores; the caller computes
+// half 1's words while half 0's stores read their images. y0 = the block's first row
+// ((row n + block offset) / 512).
+__device__ __forceinline__ void out_half_tma(const CUtensorMap* tout, uint8_t* Ew, uint32_t w, uint32_t l,
+                                             int32_t y0, const uint64_t (&v)[32], int h) {
+  if (h == 1) {
+    if (l == 0) bulk_wait_read();  // half 0's stores have read the images
+    __syncwarp();
+  }
+#pragma unroll
+  for (int rr = 0; rr < 8; ++rr) {
+    *reinterpret_cast<uint64_t*>(Ew + rr * 256 + l * 8) = v[8 * h + rr];
+    *reinterpret_cast<uint64_t*>(Ew + 2048 + rr * 256 + l * 8) = v[16 + 8 * h + rr];
+  }
+  fence_proxy_async();
+  __syncwarp();
+  if (l == 0) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q)
+      asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                       reinterpret_cast<uint64_t>(tout)),
+                   "r"(static_cast<int32_t>(w << 5)), "r"(y0 + 8 * h + 16 * q), "r"(smem_u32(Ew + 2048 * q))
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+}
+
 }  // namespace str
 
 template <class A, bool ILTM0>
@@ -429,8 +463,6 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t lognb = a.logn - kB14;
   const uint64_t rowwords16 = a.n >> 4;
 
-  // (a 16384-word block's row number fits 32 bits -- 2^32 rows would be 2^49 bytes -- so the
-  // limb of a row is a 32-bit remainder, not a call to the 64-bit division routine)
   auto item_row = [&](uint32_t k, uint64_t& row, uint64_t& blk) {
     row = (static_cast<uint64_t>(k) >> lognb) * a.row_mul + a.row_add;
     blk = static_cast<uint64_t>(k) & ((uint64_t{1} << lognb) - 1);
@@ -439,7 +471,7 @@ __global__ void __launch_bounds__(512, 1)
     uint64_t row, blk;
     item_row(k, row, blk);
     const int32_t y0 = static_cast<int32_t>(row * rowwords16 + (blk << (kB14 - 4)));
-    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row) % a.nlimbs;
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
     mbar_expect_tx(bar_full, kStageBytes + static_cast<uint32_t>(sizeof(LimbConst)));
 #pragma unroll
     for (int q = 0; q < 4; ++q) tma_load_2d(St + q * 32768, &tin, 0, y0 + q * 256, bar_full);
@@ -469,7 +501,7 @@ __global__ void __launch_bounds__(512, 1)
     uint64_t row, blk;
     item_row(k, row, blk);
     NK_GTS(0);
-    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row) % a.nlimbs;
+    const uint32_t limb = a.limb0 + static_cast<uint32_t>(row % a.nlimbs);
     const Tw* __restrict__ tw = tw_of<A>(a, limb);
     const Tw* __restrict__ twq = twq_of<A>(a, limb) + blk * kStrTableWords + t;
     const uint64_t boff = blk << kB14;
@@ -543,7 +575,8 @@ __global__ void __launch_bounds__(512, 1)
 // ---------------------------------------------------------------------------
 template <class A, bool ILTM0, bool LONG = false>
 __global__ void __launch_bounds__(512, 1)
-    ntt_stri14(const __grid_constant__ CUtensorMap tin, NttArgs a, uint32_t nitems) {
+    ntt_stri14(const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout, NttArgs a,
+               uint32_t nitems) {
   using Tw = typename A::Tw;
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* St = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
@@ -557,6 +590,10 @@ __global__ void __launch_bounds__(512, 1)
   const uint32_t lognb = a.logn - kB14;
   const uint64_t rowwords16 = a.n >> 4;
 
+  // (a 16384-word block's row number fits 32 bits -- 2^32 rows would be 2^49 bytes -- so the
+  // limb of a row is a 32-bit remainder here, not a call to the 64-bit division routine;
+  // measured: cfg4 inverse 338 -> 329 us, while the same change cost the forward 6 us and the
+  // CTA-pair kernel 35%, so those keep the call)
   auto item_row = [&](uint32_t k, uint64_t& row, uint64_t& blk) {
     row = (static_cast<uint64_t>(k) >> lognb) * a.row_mul + a.row_add;
     blk = static_cast<uint64_t>(k) & ((uint64_t{1} << lognb) - 1);
@@ -582,6 +619,7 @@ __global__ void __launch_bounds__(512, 1)
     mbar_init(bar_w + 1, 16);
     *cnt = 0;
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tin)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tout)) : "memory");
   }
   __syncthreads();
   if (t == 0 && blockIdx.x < nitems) issue(blockIdx.x, 0);
@@ -599,7 +637,6 @@ __global__ void __launch_bounds__(512, 1)
     const Tw* __restrict__ twq = twq_of<A>(a, limb) + blk * kStrTableWords + t;
     const uint64_t boff = blk << kB14;
     const uint64_t xbase = a.n + boff;
-    uint64_t* __restrict__ dst = a.out + row * a.n + boff;
     uint64_t v[32];
 
     // the first two stages' twiddles of stream A are loaded before the wait for the block, B's while
@@ -627,7 +664,11 @@ __global__ void __launch_bounds__(512, 1)
     NK_GTS(2);
 
     str::inv_core<A, ILTM0>(
-        v, St, Ew, c, a, tw, twq, xbase, w, l, ta, bar_w, phase, it_, [&] { mbar_wait(bar_rd, phase); },
+        v, St, Ew, c, a, tw, twq, xbase, w, l, ta, bar_w, phase, it_,
+        [&] {
+          if (l == 0) bulk_wait_read();  // the previous block's output stores have read this warp's 4 KiB
+        },
+        [&] { mbar_wait(bar_rd, phase); },
         [&] {
           grp::staging_consumed(cnt, l, [&] {
             if (k + gridDim.x < nitems) {
@@ -637,36 +678,37 @@ __global__ void __launch_bounds__(512, 1)
           });
         });
 
-    // ---- bit 13 (n^-1 folded in for canonical results), stores ----
+    // ---- bit 13 (n^-1 folded in for canonical results); result words out by TMA, in two
+    // halves of 8 pairs (plain stores from here cost the inverse 12%: 32 STG.64 per thread
+    // through the LSU against four bulk tensor stores per warp) ----
     constexpr bool kFoldLast = A::kSigned && !LONG;
-    const uint32_t jo = l | (w << 5);
-    if constexpr (kFoldLast) {
+    const int32_t y0 = static_cast<int32_t>((row * a.n + boff) >> 9);
+    Tw w13{};
+    if constexpr (!kFoldLast) w13 = ldtw(tw + (xbase >> 14));
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        A::inv_fold(v[r], v[r + 16], c);
-        dst[jo | (static_cast<uint32_t>(r) << 9)] = v[r];
-        dst[jo | (static_cast<uint32_t>(r + 16) << 9)] = v[r + 16];
-      }
-    } else {
-      const Tw w13 = ldtw(tw + (xbase >> 14));
+    for (int h = 0; h < 2; ++h) {
 #pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        A::template inv<false>(v[r], v[r + 16], w13, c);
-        if constexpr (LONG) {
-          v[r] = A::store(v[r]);  // intermediate of a long row
-          v[r + 16] = A::store(v[r + 16]);
+      for (int r = 8 * h; r < 8 * h + 8; ++r) {
+        if constexpr (kFoldLast) {
+          A::inv_fold(v[r], v[r + 16], c);
         } else {
-          v[r] = inv_out<A>(v[r], c, a.fout);
-          v[r + 16] = inv_out<A>(v[r + 16], c, a.fout);
+          A::template inv<false>(v[r], v[r + 16], w13, c);
+          if constexpr (LONG) {
+            v[r] = A::store(v[r]);  // intermediate of a long row
+            v[r + 16] = A::store(v[r + 16]);
+          } else {
+            v[r] = inv_out<A>(v[r], c, a.fout);
+            v[r + 16] = inv_out<A>(v[r + 16], c, a.fout);
+          }
         }
-        dst[jo | (static_cast<uint32_t>(r) << 9)] = v[r];
-        dst[jo | (static_cast<uint32_t>(r + 16) << 9)] = v[r + 16];
       }
+      str::out_half_tma(&tout, Ew, w, l, y0, v, h);
     }
     NK_GTS(11);
     phase ^= 1;
     ++it_;
   }
+  if (l == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 }  // namespace nk
