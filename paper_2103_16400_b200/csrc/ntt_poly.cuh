@@ -281,8 +281,8 @@ constexpr size_t kPolyStrSmemBytes = kStrSmemBytes + 16;
 
 template <class A>
 __global__ void __launch_bounds__(512, 1)
-    poly_str14(const __grid_constant__ CUtensorMap tf, const __grid_constant__ CUtensorMap tg, PolyArgs pa,
-               uint32_t nitems) {
+    poly_str14(const __grid_constant__ CUtensorMap tf, const __grid_constant__ CUtensorMap tg,
+               const __grid_constant__ CUtensorMap tout, PolyArgs pa, uint32_t nitems) {
   static_assert(A::kSigned, "poly_str14 runs the signed FP64 policy");
   using Tw = typename A::Tw;
   const NttArgs& a = pa.a;
@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(512, 1)
     *cnt = 0;
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tf)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tg)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tout)) : "memory");
   }
   if (w == 0) {  // one warp allocates the TMEM columns (one CTA per SM: never contended by this kernel)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
@@ -352,7 +353,10 @@ __global__ void __launch_bounds__(512, 1)
       // staying live across the whole row)
       const uint32_t to = tid_opaque(), wo = to >> 5, lo = to & 31u;
       str::fwd_core<A, true>(
-          v, St, E + (wo << 12), c, a, tw, twq, a.n, wo, lo, bar_rd, bar_w, ph, (it + ph) & 1u, 0u, [] {},
+          v, St, E + (wo << 12), c, a, tw, twq, a.n, wo, lo, bar_rd, bar_w, ph, (it + ph) & 1u, 0u,
+          [&] {
+            if (lo == 0) bulk_wait_read();  // the previous row's output stores have read this warp's 4 KiB
+          },
           [&] {
             if (ph == 0) {
               grp::staging_consumed(cnt, l, [&] {
@@ -398,16 +402,17 @@ __global__ void __launch_bounds__(512, 1)
             }
           });
         });
-    uint64_t* __restrict__ dst = a.out + static_cast<uint64_t>(k) * a.n;
-    const uint32_t jo = lo | (wo << 5);
+    // (result words out by bulk tensor stores, as in ntt_stri14)
+    const int32_t y0 = static_cast<int32_t>((static_cast<uint64_t>(k) * a.n) >> 9);
 #pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      A::inv_fold(v[r], v[r + 16], c);
-      dst[jo | (static_cast<uint32_t>(r) << 9)] = v[r];
-      dst[jo | (static_cast<uint32_t>(r + 16) << 9)] = v[r + 16];
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+      for (int r = 8 * h; r < 8 * h + 8; ++r) A::inv_fold(v[r], v[r + 16], c);
+      str::out_half_tma(&tout, E + (wo << 12), wo, lo, y0, v, h);
     }
     ++it;
   }
+  if (l == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

@@ -17,9 +17,11 @@ int run_poly_mul14(const PolyArgs& pa, const uint64_t* f, const uint64_t* g, cud
     poly_mul14<Arith52S><<<static_cast<unsigned>(grid), 512, kPolySmemBytes, st>>>(mf, mg, pa,
                                                                                     static_cast<uint32_t>(pa.a.rows));
   } else {  // two streams per thread (ntt_str.cuh cores)
+    CUtensorMap mo;  // the result leaves by bulk tensor stores
+    if (int rc = make_map(&mo, kStriOutMap, pa.a.out, words)) return rc;
     if (int rc = set_smem_once<poly_str14<Arith52S>>(kPolyStrSmemBytes)) return rc;
     poly_str14<Arith52S><<<static_cast<unsigned>(grid), 512, kPolyStrSmemBytes, st>>>(
-        mf, mg, pa, static_cast<uint32_t>(pa.a.rows));
+        mf, mg, mo, pa, static_cast<uint32_t>(pa.a.rows));
   }
   launches++;
   NK_CUDA(cudaGetLastError());
