@@ -570,8 +570,8 @@ __global__ void __launch_bounds__(512, 1)
 //   Q2'  bits 5..8; e1' CTA-wide, in place in the stream's staging half (after
 //        every warp has read its input), plain layout: both sides have lanes
 //        j0..j4;  P1' bits 9..12 per stream (lanes j0..j4, warps j5..j8), then
-//        bit 13 on both (n^-1 folded in for canonical outputs), 256-byte
-//        contiguous stores per warp instruction
+//        bit 13 on both (n^-1 folded in for canonical outputs); the words
+//        leave by bulk tensor stores (str::out_half_tma)
 // ---------------------------------------------------------------------------
 template <class A, bool ILTM0, bool LONG = false>
 __global__ void __launch_bounds__(512, 1)
