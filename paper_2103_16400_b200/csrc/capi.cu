@@ -23,6 +23,7 @@
 #include "eltwise_kernels.cuh"
 #include "host_math.hpp"
 #include "ntt_poly.cuh"
+#include "ntt_polyblk.cuh"
 #include "ntt_str.cuh"
 #include "runtime.hpp"
 
@@ -782,6 +783,40 @@ int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const u
     pa.itw8 = p->tw8_inv;
     pa.itwg8 = p->twg8_inv;
     return nk::rt::run_poly_mul14(pa, f, g, st);
+  }
+  // Whole rows of N = 2^10 .. 2^13 whose limbs share one canonical-only
+  // policy (all beta = 2^52: signed FP64; all beta = 2^64 with q < 2^60: loose
+  // integer): one kernel, one CTA per row pair (ntt_polyblk.cuh), 24 B/coeff.
+  // nk_debug_block_kernel(>= 0) / exact_only keep the reference's sequence.
+  if (p->logn >= 10 && p->logn < kLogBlock && !nk::rt::exact_only && nk::rt::block_kernel < 0) {
+    bool all52 = true, all64 = true;
+    for (uint32_t l = 0; l < nlimbs; ++l) {
+      all52 &= p->bs[limb0 + l] == 52;
+      all64 &= p->bs[limb0 + l] == 64;
+    }
+    if (all52 || (all64 && max_q(p, limb0, nlimbs) < (uint64_t{1} << 60))) {
+      nk::PolyBlkArgs pb{};
+      pb.out = res;
+      pb.f = f;
+      pb.g = g;
+      pb.mc = p->mc[0];
+      for (nk::NttArgs* a : {&pb.fw, &pb.iv}) {
+        a->lc = p->lc;
+        a->n = p->n;
+        a->logn = p->logn;
+        a->limb0 = limb0;
+        a->nlimbs = nlimbs;
+        a->row_mul = 1;
+        a->row_add = 0;
+        a->fin = 1;
+        a->fout = 1;
+      }
+      pb.fw.tw = p->tw_fwd;
+      pb.fw.tw8 = p->tw8_fwd;
+      pb.iv.tw = p->tw_inv;
+      pb.iv.tw8 = p->tw8_inv;
+      return nk::rt::run_poly_block(pb, static_cast<uint64_t>(npolys) * nlimbs, all52, st);
+    }
   }
   uint64_t* gh = nullptr;
   NK_CUDA(cudaMallocAsync(&gh, bytes, st));

@@ -16,6 +16,7 @@ namespace nk {
 struct MultConst;
 struct FmaConst;
 struct PolyArgs;
+struct PolyBlkArgs;
 }  // namespace nk
 
 namespace nk::rt {
@@ -52,6 +53,11 @@ int run_ntt(NttArgs a, uint64_t buf_words, cudaStream_t st);
 // poly_mult_mod of N = 16384 rows in one kernel (poly.cu, ntt_poly.cuh):
 // signed FP64 policy, canonical f and g with 16-byte aligned rows.
 int run_poly_mul14(const PolyArgs& pa, const uint64_t* f, const uint64_t* g, cudaStream_t st);
+
+// poly_mult_mod of whole rows of N = 2^10 .. 2^13 in one kernel (polyblk.cu,
+// ntt_polyblk.cuh): fp64 = the signed FP64 policy (every limb beta = 2^52),
+// else the loose integer policy (every limb beta = 2^64, q < 2^60).
+int run_poly_block(const PolyBlkArgs& pa, uint64_t rows, bool fp64, cudaStream_t st);
 
 // element-wise launchers (eltwise.cu)
 int launch_mult(uint64_t* r, const uint64_t* a, const uint64_t* b, uint64_t total, uint32_t logn,
