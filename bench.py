@@ -252,12 +252,22 @@ class ClockSampler:
         self._t = None
 
     def start(self):
-        def run_nvml():
+        # NVML is initialised here, on the calling thread, before the timed region starts:
+        # a fresh box takes tens of milliseconds for nvmlInit, longer than the region itself
+        nvml = None
+        try:
             import pynvml as nv
 
             nv.nvmlInit()
             h = nv.nvmlDeviceGetHandleByIndex(self.index)
             mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            nvml = (nv, h, mx)
+        except Exception:
+            nvml = None
+
+        def run_nvml():
+            nv, h, mx = nvml
             bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
                     ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4)]
             while not self._stop.is_set():
@@ -269,10 +279,11 @@ class ClockSampler:
                 self._stop.wait(0.002)
 
         def run():
-            try:
-                return run_nvml()
-            except Exception:
-                pass
+            if nvml is not None:
+                try:
+                    return run_nvml()
+                except Exception:
+                    pass
             q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -683,6 +694,40 @@ def run_configs(rates, hbm, threads):
         "cpu_ref_us_1thread": c15 * 1e6 * rows5 / sample5,
         "cpu_ref_1thread_sample": f"{sample5} of {rows5} row pairs, scaled",
         "cpu_ref_us_all_cores": ca5 * 1e6, "speedup_vs_cpu_all_cores": ca5 * 1e6 / us5}
+    del df5, dg5, r5, f5, g5
+
+    # ---- beyond BASELINE's configs: poly_mult_mod of shorter rows (the sizes HE libraries use
+    # below 16384), the same 2^25 coefficients per operand, 16 x 50-bit limbs: one poly_block launch
+    for ns in (4096, 8192):
+        ms_ = largest_ntt_primes(50, ns, 16)
+        Ps = (N * rows5) // (ns * 16)
+        rows_s = Ps * 16
+        fs = make_inputs(ms_, Ps, (6 ^ BASE_SEED) + ns, n=ns)
+        gs = make_inputs(ms_, Ps, (6 ^ BASE_SEED) + ns + 7919, n=ns)
+        ps = nk.RnsNtt(ns, ms_)
+        dfs, dgs = dev(fs), dev(gs)
+        rs = torch.empty_like(dfs)
+        l0 = nk.launch_count()
+        ps.poly_mult_mod(rs, dfs, dgs)
+        launches_s = nk.launch_count() - l0
+        rps = RefPlan(ns, ms_)
+        bufs = np.empty_like(fs)
+        rps.poly(bufs, fs, gs, rows_s, threads)
+        assert np.array_equal(host(rs), bufs), f"poly N={ns} mismatch"
+        us_s = 1e3 * dev_time_ms(lambda: ps.poly_mult_mod(rs, dfs, dgs), 10)
+        cas, _ = steady_median(lambda: rps.poly(bufs, fs, gs, rows_s, threads), reps=5, warm_seconds=0.3)
+        rps.close()
+        logn_s = ns.bit_length() - 1
+        floor_s = 3 * (ns // 2) * logn_s * rows_s * DP_PER_BFLY_POLY / fp64 * 1e6 if fp64 else None
+        out[f"poly_n{ns}"] = {
+            "op": f"poly_mult_mod, N={ns}, 16 x 50-bit limbs x {Ps} pairs ({rows_s} row pairs; not a BASELINE config)",
+            "kernel": "poly_block (one CTA per row pair: g^ parked in shared memory, product in registers)",
+            "bound": "fp64 pipe (cfg5's operation count per butterfly)",
+            "launches_per_call": launches_s, "us": us_s, "Gcoeff_s": ns * rows_s / us_s / 1e3,
+            "fp64_floor_us": floor_s, "roofline_frac": floor_s / us_s if floor_s else None,
+            "hbm_bytes_per_coeff": 24,
+            "cpu_ref_us_all_cores": cas * 1e6, "speedup_vs_cpu_all_cores": cas * 1e6 / us_s}
+        del dfs, dgs, rs, fs, gs, bufs
     return out
 
 

@@ -61,10 +61,15 @@ __device__ __forceinline__ void polyblk_load(uint64_t (&v)[1 << LOGV], const uin
   }
 }
 
-// at most 128 registers per thread (two 256-thread CTAs per SM, like ntt_block's instances)
+// Resident CTAs per SM the register allocation aims at: as many as shared
+// memory allows, but at least 128 registers per thread (tighter caps, 80
+// registers for 16 words per thread, changed nothing measurable).
 template <int LOGB, int LOGV>
 constexpr int polyblk_min_ctas() {
-  return (1 << (LOGB - LOGV)) >= 512 ? 1 : 512 >> (LOGB - LOGV);
+  constexpr int by_smem = static_cast<int>((227 * 1024) / (polyblk_smem_bytes<LOGB, LOGV>() + 1024));
+  constexpr int by_regs = 65536 / ((1 << (LOGB - LOGV)) * 128);
+  constexpr int m = by_smem < by_regs ? by_smem : by_regs;
+  return m < 1 ? 1 : m;
 }
 
 template <int LOGB, int LOGV, class A>
