@@ -265,9 +265,22 @@ int launch_tma(const NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm,
               : launch_grp_t<A, FWD, false>(a, nitems, buf_words, st);
 }
 
-// LOGV = log2(words per thread): 32 words per thread for batches that fill
-// the GPU, 8 for small ones (cfg1: one row), where the row's latency is the
-// metric and 4x more threads per row cut it.
+// LOGV = log2(words per thread): 8 for small batches (cfg1: one row), where
+// the row's latency is the metric and more threads per row cut it; for batches
+// that fill the GPU 16, or 32 where that measured faster (block_logv).
+// 2^25 coefficients, us per call with 32 / 16 / 8 words per thread
+// (tools/prof_ntt.py, 16 limbs):
+//   50-bit, forward: N = 1024 206 / 162 / 165, 2048 186 / 163 / 178, 4096 205 / 200 / 202, 8192 226 / 224 / 335
+//   50-bit, inverse:          222 / 152 / 176,      169 / 156 / 183,      212 / 223 / 255,      256 / 302 / 320
+//   60-bit, forward:          292 / 233 / 243,      287 / 255 / 273,      380 / 288 / 312,      408 / 313 / 422
+//   60-bit, inverse:          338 / 241 / 259,      318 / 258 / 281,      355 / 320 / 323,      398 / 413 / 420
+template <class A, bool FWD>
+constexpr int block_logv(int logb) {
+  if (!FWD && logb == 13) return 5;
+  if (!FWD && A::kFP && logb == 12) return 5;
+  return 4;
+}
+
 template <int LOGB, int LOGV, class A, bool FWD, bool IL>
 int launch_block_t(const NttArgs& a, uint64_t grid, cudaStream_t st) {
   constexpr size_t smem = block_smem_bytes<LOGB, LOGV>();
@@ -318,7 +331,7 @@ int launch_block(uint32_t logb, const NttArgs& a, uint64_t grid, bool iltm, cuda
   return iltm ? launch_block_t<L, V, A, FWD, true>(a, grid, st) : launch_block_t<L, V, A, FWD, false>(a, grid, st)
 #define NK_LB(L) \
   if (small) NK_LB2(L, 3); \
-  NK_LB2(L, 5)
+  NK_LB2(L, (block_logv<A, FWD>(L)))
   switch (logb) {
     case 10: NK_LB(10);
     case 11: NK_LB(11);

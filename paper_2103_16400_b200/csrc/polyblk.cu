@@ -20,9 +20,10 @@ int launch_polyblk_t(const PolyBlkArgs& pa, uint64_t rows, cudaStream_t st) {
 }
 
 // Words per thread (tools/polyblk_bench.py, 2^25 coefficients, us per call for 8 / 16 / 32
-// words per thread): 16 everywhere (50-bit limbs: N = 1024 489 / 395 / 557, 2048 543 / 425 / 458,
-// 4096 660 / 510 / 502; 60-bit limbs: 8192 1189 / 1108 / 1561) except 50-bit limbs at N = 8192
-// (772 / 684 / 663: 32); 8 for batches smaller than the SM count (more threads per row).
+// words per thread):
+//   50-bit limbs: N = 1024 489 / 395 / 557, 2048 543 / 425 / 458, 4096 660 / 510 / 502, 8192 772 / 684 / 663
+//   60-bit limbs:          829 / 900 / 1230,     948 / 973 / 1010,    1105 / 948 / 1168,    1189 / 1108 / 1561
+// 8 for batches smaller than the SM count (more threads per row).
 template <class A>
 int launch_polyblk(const PolyBlkArgs& pa, uint64_t rows, cudaStream_t st) {
   const bool small = rows < static_cast<uint64_t>(sm_count());
@@ -30,8 +31,8 @@ int launch_polyblk(const PolyBlkArgs& pa, uint64_t rows, cudaStream_t st) {
   if (small) return launch_polyblk_t<L, 3, A>(pa, rows, st); \
   return launch_polyblk_t<L, V, A>(pa, rows, st)
   switch (pa.fw.logn) {
-    case 10: NK_PB(10, 4);
-    case 11: NK_PB(11, 4);
+    case 10: NK_PB(10, (A::kSigned ? 4 : 3));
+    case 11: NK_PB(11, (A::kSigned ? 4 : 3));
     case 12: NK_PB(12, 4);
     case 13: NK_PB(13, (A::kSigned ? 5 : 4));
     default: return fail(NK_ERR_CUDA, "internal: poly_block row length");

@@ -254,11 +254,15 @@ def test_block_kernels_match_oracle(nk, oracle, kernel, logn, bits, npolys, arit
 
 
 @pytest.mark.parametrize("logn", [10, 11, 12, 13])
-def test_block_sizes_large_batches(nk, oracle, logn, arith):
-    """Batches of >= #SMs rows take the 32-words-per-thread block kernels (small
-    batches take the 8-words-per-thread ones, test_block_sizes_match_oracle)."""
+@pytest.mark.parametrize("bits", [50, 60])
+def test_block_sizes_large_batches(nk, oracle, logn, bits, arith):
+    """Batches of >= #SMs rows take the block kernels with 16 or 32 words per
+    thread (dispatch.cuh block_logv: chosen per size, policy and direction;
+    small batches take the 8-words-per-thread ones,
+    test_block_sizes_match_oracle). Canonical and lazy factors, so every
+    arithmetic policy runs in both shapes."""
     n = 1 << logn
-    moduli = largest_ntt_primes(50, n, 3)
+    moduli = largest_ntt_primes(bits, n, 3)
     check_dir(nk, oracle, n, moduli, 52, 700 + logn, fwd_factors=[(1, 1), (4, 4), (2, 1)],
               inv_factors=[(1, 1), (2, 2)])
 
