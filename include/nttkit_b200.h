@@ -135,7 +135,9 @@ int nk_ntt_inverse(const nk_plan* plan, uint64_t* d_result, const uint64_t* d_op
 int nk_plan_eltwise_mult_mod(const nk_plan* plan, uint64_t* d_result, const uint64_t* d_a,
                              const uint64_t* d_b, uint32_t limb0, uint32_t nlimbs,
                              uint32_t npolys, uint64_t input_mod_factor, void* stream);
-/* poly_mult_mod over npolys*nlimbs row pairs: fwd(1,4) x2, mult(4), inv(1,1). */
+/* poly_mult_mod over npolys*nlimbs row pairs: the canonical result of fwd(1,4) x2, mult(4),
+ * inv(1,1) (ring.hpp:39-43). One kernel for N = 2^10 .. 2^14 when the limbs share one
+ * accumulator width and q < 2^60 (2^50 at N = 2^14), else that sequence of launches. */
 int nk_poly_mult_mod(const nk_plan* plan, uint64_t* d_result, const uint64_t* d_f,
                      const uint64_t* d_g, uint32_t limb0, uint32_t nlimbs, uint32_t npolys,
                      void* stream);

@@ -12,6 +12,8 @@ tail -3 $O/pytest_gpu.log > $P/gpu_tests_$T.log
 cp $O/launches.csv $P/launches_$T.csv
 cp $O/launches_cfg4.csv $P/launches_cfg4_$T.csv
 cp $O/launches_cfg5.csv $P/launches_cfg5_$T.csv
+cp $O/launches_poly4096.csv $P/launches_poly4096_$T.csv
+cp $O/polyblk.jsonl $P/polyblk_$T.jsonl
 python tools/ncu_summary.py $O/prof_raw.csv > $P/ncu_${T}_cfg3.txt
 python tools/ncu_summary.py $O/prof_poly_raw.csv > $P/ncu_${T}_poly.txt
 python tools/ncu_summary.py $O/prof_elt_raw.csv > $P/ncu_${T}_eltwise_steady.txt

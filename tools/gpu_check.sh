@@ -14,6 +14,7 @@ timeout 900 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench=$?" | t
 timeout 600 python bench.py --impl reference > $O/bench_ref.json 2> $O/bench_ref.err; echo "bench_ref=$?" | tee -a $O/status
 timeout 300 ./tools/api_latency > $O/api_latency.txt 2>&1; echo "api_latency=$?" | tee -a $O/status
 timeout 300 python tools/time_cfgs.py > $O/cfgs.jsonl 2>&1; echo "cfgs=$?" | tee -a $O/status
+timeout 300 python tools/polyblk_bench.py > $O/polyblk.jsonl 2>&1; echo "polyblk=$?" | tee -a $O/status
 if [ "${SKIP_NCU:-0}" = "0" ]; then
   timeout 300 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-configs --no-records > $O/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
@@ -31,6 +32,8 @@ if [ "${SKIP_NCU:-0}" = "0" ]; then
       --log-file $O/launches_cfg4.csv python tools/prof_ntt.py --n 65536 --limbs 24 --polys 16 --bits 60 --fin 4 --iters 1 > $O/ncu_cfg4.log 2>&1
   timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
       --log-file $O/launches_cfg5.csv python tools/prof_ntt.py --n 16384 --limbs 16 --polys 128 --op poly --iters 1 > $O/ncu_cfg5.log 2>&1
+  timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
+      --log-file $O/launches_poly4096.csv python tools/prof_ntt.py --n 4096 --limbs 16 --polys 512 --op poly --iters 1 > $O/ncu_poly4096.log 2>&1
   echo "ncu_cfg45=$?" | tee -a $O/status
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:poly_ -s 1 -c 1 \
       -o $O/prof_poly python tools/prof_ntt.py --n 16384 --limbs 16 --polys 128 --op poly --iters 2 > $O/ncu_poly.log 2>&1
