@@ -72,6 +72,28 @@ struct NttArgs {
 __device__ __forceinline__ ulonglong2 ldtw(const ulonglong2* p) { return __ldg(p); }
 __device__ __forceinline__ uint64_t ldtw(const uint64_t* p) { return __ldg(p); }
 
+// c consecutive table entries in one non-coherent vector load of up to 32
+// bytes (c = 1, 2 or 4 for 8-byte entries, 1 or 2 for 16-byte entries; p
+// aligned to c entries). c is a constant after unrolling.
+__device__ __forceinline__ void ldtw_vec(uint64_t (&w)[4], const uint64_t* p, int c) {
+  if (c == 4) {
+    asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(p));
+  } else if (c == 2) {
+    const ulonglong2 t = __ldg(reinterpret_cast<const ulonglong2*>(p));
+    w[0] = t.x;
+    w[1] = t.y;
+  } else {
+    w[0] = __ldg(p);
+  }
+}
+__device__ __forceinline__ void ldtw_vec(ulonglong2 (&w)[2], const ulonglong2* p, int c) {
+  if (c == 2) {
+    asm("ld.global.nc.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w[0].x), "=l"(w[0].y), "=l"(w[1].x), "=l"(w[1].y) : "l"(p));
+  } else {
+    w[0] = __ldg(p);
+  }
+}
+
 // the twiddle tables of a policy (entries of type A::Tw), offset to limb `limb`
 template <class A>
 __device__ __forceinline__ const typename A::Tw* tw_of(const NttArgs& a, uint32_t limb) {
@@ -168,9 +190,16 @@ __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const typename
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint64_t base = (xt + S::jg(g, LO, K)) >> (b + 1);
+      // the stage's R >> (i + 1) twiddles of this group are consecutive table entries
+      // (aligned to their count): vector loads of up to 32 bytes
+      constexpr int CMAX = 32 / sizeof(typename A::Tw);
+      const int H = R >> (i + 1);
+      const int C = H < CMAX ? H : CMAX;
+      typename A::Tw wv[CMAX];
 #pragma unroll
-      for (int hi = 0; hi < (R >> (i + 1)); ++hi) {
-        const typename A::Tw w = TWS ? tw[base + hi] : ldtw(tw + base + hi);
+      for (int hi = 0; hi < H; ++hi) {
+        if (!TWS && (hi % C) == 0) ldtw_vec(wv, tw + base + hi, C);
+        const typename A::Tw w = TWS ? tw[base + hi] : wv[hi % C];
 #pragma unroll
         for (int l = 0; l < (1 << i); ++l) {
           const int r0 = (hi << (i + 1)) | l;
@@ -226,8 +255,10 @@ __device__ __forceinline__ void run_passes(uint64_t (&v)[1 << LOGV], uint64_t* s
   }
 }
 
+// 512-thread CTAs (N = 8192 at 16 words per thread) are held to 64 registers: two per SM
+// (0 = no occupancy target: an explicit 1 makes ptxas spend 128-168 registers where 72-106 do)
 template <int LOGB, int LOGV, class A, bool FWD, bool ILTM0>
-__global__ void __launch_bounds__(1 << (LOGB - LOGV)) ntt_block(NttArgs a) {
+__global__ void __launch_bounds__(1 << (LOGB - LOGV), (LOGB - LOGV) == 9 ? 2 : 0) ntt_block(NttArgs a) {
   using S = Sched<LOGB, LOGV>;
   using PO = PassOf<LOGB, LOGV, FWD>;
   extern __shared__ uint64_t sm[];

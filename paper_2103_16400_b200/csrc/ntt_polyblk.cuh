@@ -61,19 +61,12 @@ __device__ __forceinline__ void polyblk_load(uint64_t (&v)[1 << LOGV], const uin
   }
 }
 
-// Resident CTAs per SM the register allocation aims at: as many as shared
-// memory allows, but at least 128 registers per thread (tighter caps, 80
-// registers for 16 words per thread, changed nothing measurable).
-template <int LOGB, int LOGV>
-constexpr int polyblk_min_ctas() {
-  constexpr int by_smem = static_cast<int>((227 * 1024) / (polyblk_smem_bytes<LOGB, LOGV>() + 1024));
-  constexpr int by_regs = 65536 / ((1 << (LOGB - LOGV)) * 128);
-  constexpr int m = by_smem < by_regs ? by_smem : by_regs;
-  return m < 1 ? 1 : m;
-}
-
+// Launch bounds: no occupancy target for N <= 4096 (ptxas then uses 48-88 registers; with an
+// explicit target it spends whatever the target allows, 110-128, and fewer CTAs fit). At N =
+// 8192 shared memory leaves one CTA per SM anyway, and the explicit target of one CTA
+// lets the schedule keep more loads in flight (50-bit limbs: 618 us against 766).
 template <int LOGB, int LOGV, class A>
-__global__ void __launch_bounds__(1 << (LOGB - LOGV), polyblk_min_ctas<LOGB, LOGV>()) poly_block(PolyBlkArgs a) {
+__global__ void __launch_bounds__(1 << (LOGB - LOGV), LOGB == 13 ? 1 : 0) poly_block(PolyBlkArgs a) {
   using S = Sched<LOGB, LOGV>;
   using PI = PassOf<LOGB, LOGV, false>;
   extern __shared__ uint64_t sm[];
