@@ -270,13 +270,12 @@ int launch_tma(const NttArgs& a, uint64_t nitems, uint64_t buf_words, bool iltm,
 // that fill the GPU 16, or 32 where that measured faster (block_logv).
 // 2^25 coefficients, us per call with 32 / 16 / 8 words per thread
 // (tools/prof_ntt.py, 16 limbs):
-//   50-bit, forward: N = 1024 206 / 162 / 165, 2048 186 / 163 / 178, 4096 205 / 200 / 202, 8192 226 / 224 / 335
-//   50-bit, inverse:          222 / 152 / 176,      169 / 156 / 183,      212 / 223 / 255,      256 / 302 / 320
-//   60-bit, forward:          292 / 233 / 243,      287 / 255 / 273,      380 / 288 / 312,      408 / 313 / 422
-//   60-bit, inverse:          338 / 241 / 259,      318 / 258 / 281,      355 / 320 / 323,      398 / 413 / 420
+//   50-bit, forward: N = 1024 177 / 150 / 162, 2048 164 / 161 / 168, 4096 199 / 189 / 207, 8192 222 / 215 / 326
+//   50-bit, inverse:          172 / 143 / 173,      164 / 151 / 180,      195 / 206 / 227,      231 / 219 / 309
+//   60-bit, forward:          279 / 231 / 247,      290 / 245 / 274,      327 / 286 / 322,      404 / 331 / 409
+//   60-bit, inverse:          308 / 237 / 254,      345 / 256 / 281,      340 / 321 / 331,      354 / 329 / 411
 template <class A, bool FWD>
 constexpr int block_logv(int logb) {
-  if (!FWD && logb == 13) return 5;
   if (!FWD && A::kFP && logb == 12) return 5;
   return 4;
 }
