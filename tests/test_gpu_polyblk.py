@@ -6,7 +6,7 @@ inverse sequence) and against this library's own multi-launch sequence.
 Covered: both canonical-only policies (50-bit limbs on the FP64 pipe, 60-bit
 limbs on the integer pipes, also small moduli and an explicit 64-bit
 accumulator for a small modulus), both launch shapes (fewer rows than SMs: 8
-words per thread; more: 32 words per thread), limb sub-ranges, aliasing of the
+words per thread; more: 16 or 32 words per thread), limb sub-ranges, aliasing of the
 result with either operand, extreme rows (all q-1, all zero), one launch per
 call, and the fall-back for plans that mix accumulator widths.
 """
@@ -49,7 +49,9 @@ def threads(ref):
 @pytest.mark.parametrize("npolys", [2, 80])
 def test_polyblk_vs_reference(nk, oracle, ref, logn, bits, npolys):
     """3 limbs x npolys row pairs (6 rows: the 8-words-per-thread shape; 240 rows:
-    32 words per thread): one launch, every word equal to the reference's."""
+    16 or 32 words per thread): one launch, every word equal to the reference's,
+    and the same words from 20 repeated launches (the exchange image and the
+    parked spectrum are reused across the three transforms of a row)."""
     n = 1 << logn
     moduli = largest_ntt_primes(bits, n, 3)
     plan = nk.RnsNtt(n, moduli)
@@ -69,6 +71,10 @@ def test_polyblk_vs_reference(nk, oracle, ref, logn, bits, npolys):
     torch.cuda.synchronize()
     assert nk.launch_count() - before == 1
     assert np.array_equal(host(out), want)
+    for _ in range(20):
+        again = torch.empty_like(df)
+        plan.poly_mult_mod(again, df, dg)
+        assert torch.equal(again, out)
     # the library's own multi-launch sequence (the reference's order of operations)
     nk.set_block_kernel(1)
     try:
@@ -164,3 +170,25 @@ def test_polyblk_mixed_widths_fall_back(nk, oracle, ref):
         torch.cuda.synchronize()
         assert nk.launch_count() - before > 1
         assert np.array_equal(host(out), want)
+
+
+@pytest.mark.parametrize("logn,bits,npolys", [(10, 50, 1), (11, 60, 70), (12, 50, 60), (13, 60, 1), (13, 50, 40)])
+def test_polyblk_writes_stay_in_bounds(nk, oracle, ref, logn, bits, npolys):
+    """Guard words around the result stay untouched and the operands are left
+    as they were (the kernel writes its result rows only)."""
+    n = 1 << logn
+    moduli = largest_ntt_primes(bits, n, 3)
+    plan = nk.RnsNtt(n, moduli)
+    rows = npolys * len(moduli)
+    f = rows_uniform(oracle, moduli, n, rows, 2000 + logn)
+    g = rows_uniform(oracle, moduli, n, rows, 3000 + logn)
+    want = ref.poly_mult_mod(n, moduli, f, g, threads=threads(ref))
+    guard = 64
+    sentinel = 0x5A5A5A5A5A5A5A5A
+    buf = torch.full((f.size + 2 * guard,), sentinel, dtype=torch.int64, device="cuda")
+    df, dg = dev(f), dev(g)
+    plan.poly_mult_mod(buf[guard:guard + f.size], df, dg)
+    got = host(buf)
+    assert np.array_equal(got[guard:guard + f.size], want)
+    assert np.all(got[:guard] == np.uint64(sentinel)) and np.all(got[guard + f.size:] == np.uint64(sentinel))
+    assert np.array_equal(host(df), f) and np.array_equal(host(dg), g)
