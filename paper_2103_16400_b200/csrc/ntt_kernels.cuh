@@ -94,6 +94,15 @@ __device__ __forceinline__ void ldtw_vec(ulonglong2 (&w)[2], const ulonglong2* p
   }
 }
 
+// four consecutive row words by one 32-byte access (a thread's contiguous run in the block
+// kernels' first inverse / last forward pass: one full sector per lane instead of two halves)
+__device__ __forceinline__ void ld_words4(uint64_t (&w)[4], const uint64_t* p) {
+  asm volatile("ld.global.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(w[0]), "=l"(w[1]), "=l"(w[2]), "=l"(w[3]) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void st_words4(uint64_t* p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+
 // the twiddle tables of a policy (entries of type A::Tw), offset to limb `limb`
 template <class A>
 __device__ __forceinline__ const typename A::Tw* tw_of(const NttArgs& a, uint32_t limb) {
@@ -282,7 +291,15 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV), (LOGB - LOGV) == 9 ? 2 : 0
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t jg = S::jg(g, LO, K);
-      if constexpr (LO == 0 && R >= 2) {
+      if constexpr (LO == 0 && R >= 4) {
+#pragma unroll
+        for (int r = 0; r < R; r += 4) {
+          uint64_t w4[4];
+          ld_words4(w4, src + jt + jg + r);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[g * R + r + k] = A::load(w4[k]);
+        }
+      } else if constexpr (LO == 0 && R >= 2) {
 #pragma unroll
         for (int r = 0; r < R; r += 2) {
           const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(src + jt + jg + r);
@@ -307,7 +324,11 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV), (LOGB - LOGV) == 9 ? 2 : 0
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const uint32_t jg = S::jg(g, LO, K);
-    if constexpr (LO == 0 && R >= 2) {
+    if constexpr (LO == 0 && R >= 4) {
+#pragma unroll
+      for (int r = 0; r < R; r += 4)
+        st_words4(dst + jt + jg + r, v[g * R + r], v[g * R + r + 1], v[g * R + r + 2], v[g * R + r + 3]);
+    } else if constexpr (LO == 0 && R >= 2) {
 #pragma unroll
       for (int r = 0; r < R; r += 2)
         *reinterpret_cast<ulonglong2*>(dst + jt + jg + r) =
