@@ -188,7 +188,7 @@ __host__ __device__ constexpr bool inv_skip_tt() {
 // TWS: tw points at a copy of the twiddle row in shared memory (ntt_block_lat).
 template <class A, bool FWD, int LOGB, int LOGV, int LO, int K, bool ILTM0, bool TWS = false>
 __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const typename A::Tw* __restrict__ tw,
-                                        uint64_t xt, const LimbConst& c) {
+                                        uint64_t xt, const LimbConst& c, bool fold = false) {
   using S = Sched<LOGB, LOGV>;
   constexpr int R = 1 << K;
   constexpr int G = (1 << LOGV) / R;
@@ -196,6 +196,15 @@ __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const typename
   for (int s = 0; s < K; ++s) {
     const int i = FWD ? (K - 1 - s) : s;  // bit within the pass
     const int b = LO + i;                 // bit of the block index
+    // canonical inverse of a whole row: its last stage (bit LOGB - 1, the single twiddle w_1)
+    // takes the n^-1 factor and leaves canonical words (A::inv_fold; the caller skips inv_out)
+    if (!FWD && s == K - 1 && fold) {
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int r0 = 0; r0 < R / 2; ++r0) A::inv_fold(v[g * R + r0], v[g * R + r0 + R / 2], c);
+      break;
+    }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint64_t base = (xt + S::jg(g, LO, K)) >> (b + 1);
@@ -238,7 +247,7 @@ __device__ __forceinline__ void do_pass(uint64_t (&v)[1 << LOGV], const typename
 template <int LOGB, int LOGV, class A, bool FWD, int P, bool ILTM0, bool TWS = false>
 __device__ __forceinline__ void run_passes(uint64_t (&v)[1 << LOGV], uint64_t* sm,
                                            const typename A::Tw* __restrict__ tw, uint32_t t,
-                                           uint64_t xbase, const LimbConst& c) {
+                                           uint64_t xbase, const LimbConst& c, bool fold = false) {
   using S = Sched<LOGB, LOGV>;
   using PO = PassOf<LOGB, LOGV, FWD>;
   constexpr int LO = PO::lo(P), K = PO::k(P);
@@ -252,7 +261,9 @@ __device__ __forceinline__ void run_passes(uint64_t (&v)[1 << LOGV], uint64_t* s
 #pragma unroll
       for (int r = 0; r < R; ++r) v[g * R + r] = sm[bt + smem_phys(S::jg(g, LO, K) | (r << LO))];
   }
-  do_pass<A, FWD, LOGB, LOGV, LO, K, ILTM0 && P == 0, TWS>(v, tw, xbase + jt, c);
+  // fold: inverse only, in the last pass (its last stage is the row's last: bit LOGB - 1)
+  do_pass<A, FWD, LOGB, LOGV, LO, K, ILTM0 && P == 0, TWS>(v, tw, xbase + jt, c,
+                                                           !FWD && P + 1 == S::NP && fold);
   if constexpr (P + 1 < S::NP) {
     __syncthreads();  // every thread has read the previous image
     const uint32_t bt = smem_phys(jt);
@@ -260,7 +271,7 @@ __device__ __forceinline__ void run_passes(uint64_t (&v)[1 << LOGV], uint64_t* s
     for (int g = 0; g < G; ++g)
 #pragma unroll
       for (int r = 0; r < R; ++r) sm[bt + smem_phys(S::jg(g, LO, K) | (r << LO))] = v[g * R + r];
-    run_passes<LOGB, LOGV, A, FWD, P + 1, ILTM0, TWS>(v, sm, tw, t, xbase, c);
+    run_passes<LOGB, LOGV, A, FWD, P + 1, ILTM0, TWS>(v, sm, tw, t, xbase, c, fold);
   }
 }
 
@@ -312,14 +323,20 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV), (LOGB - LOGV) == 9 ? 2 : 0
       }
     }
   }
-  run_passes<LOGB, LOGV, A, FWD, 0, ILTM0>(v, sm, tw, t, a.n + boff, c);
+  // canonical inverse: n^-1 folded into the last stage (A::inv_fold), no separate n^-1 pass
+  // (not in the 64-register FP64 instances of N = 8192, where the second copy of the last
+  // stage costs more than the saved product: 209 -> 221 us per 2^25 coefficients)
+  const bool fold = !FWD && A::kFold && a.fout == 1 && !(A::kFP && (LOGB - LOGV) == 9);
+  run_passes<LOGB, LOGV, A, FWD, 0, ILTM0>(v, sm, tw, t, a.n + boff, c, fold);
 
   constexpr int PL = S::NP - 1;
   constexpr int LO = PO::lo(PL), K = PO::k(PL);
   constexpr int R = 1 << K, G = S::V / R;
   // ntt_block always transforms whole rows: final words
+  if (!fold) {
 #pragma unroll
-  for (int i = 0; i < S::V; ++i) v[i] = FWD ? fwd_out<A>(v[i], c, a.fout) : inv_out<A>(v[i], c, a.fout);
+    for (int i = 0; i < S::V; ++i) v[i] = FWD ? fwd_out<A>(v[i], c, a.fout) : inv_out<A>(v[i], c, a.fout);
+  }
   const uint32_t jt = S::scatter(t, LO, K);
 #pragma unroll
   for (int g = 0; g < G; ++g) {

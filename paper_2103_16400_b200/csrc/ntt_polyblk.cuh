@@ -111,9 +111,8 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV), LOGB == 13 ? 1 : 0) poly_b
     for (int i = 0; i < S::V; ++i) v[i] = mult_barrett<1, true>(A::red16(v[i], c), park[i * S::T], mc);
   }
   // ---- inverse; canonical factors' product is canonical for the integer policy ----
-  run_passes<LOGB, LOGV, A, false, 0, !A::kSigned>(v, sm, twi, t, a.fw.n, c);
-#pragma unroll
-  for (int i = 0; i < S::V; ++i) v[i] = inv_out<A>(v[i], c, 1);
+  // (n^-1 folded into its last stage: canonical words out, A::inv_fold)
+  run_passes<LOGB, LOGV, A, false, 0, !A::kSigned>(v, sm, twi, t, a.fw.n, c, true);
   constexpr int PL = S::NP - 1;
   constexpr int LO = PI::lo(PL), K = PI::k(PL);
   constexpr int R = 1 << K, G = S::V / R;
