@@ -829,10 +829,14 @@ int nk_poly_mult_mod(const nk_plan* p, uint64_t* res, const uint64_t* f, const u
     if (e != cudaSuccess) return cuda_fail(e, "cudaFreeAsync");
     return 0;
   }
-  // ring.hpp:39-42: g^ = fwd(g,1,4) first so that result may alias g
-  int rc = ntt_dispatch(p, true, gh, g, limb0, nlimbs, npolys, 1, 4, st);
-  if (!rc) rc = ntt_dispatch(p, true, res, f, limb0, nlimbs, npolys, 1, 4, st);
-  if (!rc) rc = nk_plan_eltwise_mult_mod(p, res, res, gh, limb0, nlimbs, npolys, 4, stream);
+  // ring.hpp:39-42: g^ = fwd(g,1,4) first so that result may alias g. Only the canonical
+  // result is observable, so unless exact_only asks for the reference's own sequence the
+  // spectra are canonical too (fwd(1,1), mult(1)): the same words, and limbs below 2^60
+  // then take the faster canonical-only transforms (ArithIntL).
+  const uint64_t lazy = nk::rt::exact_only ? 4 : 1;
+  int rc = ntt_dispatch(p, true, gh, g, limb0, nlimbs, npolys, 1, lazy, st);
+  if (!rc) rc = ntt_dispatch(p, true, res, f, limb0, nlimbs, npolys, 1, lazy, st);
+  if (!rc) rc = nk_plan_eltwise_mult_mod(p, res, res, gh, limb0, nlimbs, npolys, lazy, stream);
   if (!rc) rc = ntt_dispatch(p, false, res, res, limb0, nlimbs, npolys, 1, 1, st);
   cudaError_t e = cudaFreeAsync(gh, st);
   if (rc) return rc;

@@ -192,3 +192,31 @@ def test_polyblk_writes_stay_in_bounds(nk, oracle, ref, logn, bits, npolys):
     assert np.array_equal(got[guard:guard + f.size], want)
     assert np.all(got[:guard] == np.uint64(sentinel)) and np.all(got[guard + f.size:] == np.uint64(sentinel))
     assert np.array_equal(host(df), f) and np.array_equal(host(dg), g)
+
+
+@pytest.mark.parametrize("logn,bits", [(14, 60), (15, 50), (15, 60), (16, 60), (9, 50), (9, 60)])
+def test_poly_multi_launch_sizes_vs_reference(nk, oracle, ref, logn, bits):
+    """Sizes and limb widths without a single-kernel version (N = 16384 with
+    60-bit limbs, N >= 32768, N <= 512): forward / forward / product / inverse
+    launches with canonical spectra; the reference's own lazy sequence under
+    exact_only. Both equal the reference's words."""
+    n = 1 << logn
+    moduli = largest_ntt_primes(bits, n, 2)
+    plan = nk.RnsNtt(n, moduli)
+    rows = 3 * len(moduli)
+    f = rows_uniform(oracle, moduli, n, rows, 9000 + logn)
+    g = rows_uniform(oracle, moduli, n, rows, 9500 + logn)
+    f[:n] = moduli[0] - 1
+    g[:n] = moduli[0] - 1
+    want = ref.poly_mult_mod(n, moduli, f, g, threads=threads(ref))
+    for exact in (False, True):
+        nk.set_exact_only(exact)
+        try:
+            out = torch.empty(f.size, dtype=torch.int64, device="cuda")
+            before = nk.launch_count()
+            plan.poly_mult_mod(out, dev(f), dev(g))
+            torch.cuda.synchronize()
+            assert nk.launch_count() - before > 1
+            assert np.array_equal(host(out), want), exact
+        finally:
+            nk.set_exact_only(False)
