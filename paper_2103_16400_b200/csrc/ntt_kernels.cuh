@@ -461,7 +461,15 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV)) ntt_block_lat(NttArgs a) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const uint32_t jg = S::jg(g, LO, K);
-      if constexpr (LO == 0 && R >= 2) {
+      if constexpr (LO == 0 && R >= 4) {
+#pragma unroll
+        for (int r = 0; r < R; r += 4) {
+          uint64_t w4[4];
+          ld_words4(w4, src + jt + jg + r);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v[g * R + r + k] = A::load(w4[k]);
+        }
+      } else if constexpr (LO == 0 && R >= 2) {
 #pragma unroll
         for (int r = 0; r < R; r += 2) {
           const ulonglong2 p = *reinterpret_cast<const ulonglong2*>(src + jt + jg + r);
@@ -476,18 +484,26 @@ __global__ void __launch_bounds__(1 << (LOGB - LOGV)) ntt_block_lat(NttArgs a) {
   }
   __syncthreads();  // the barrier's initialisation is visible to every thread
   mbar_wait(bar, 0);
-  run_passes<LOGB, LOGV, A, FWD, 0, ILTM0, true>(v, sm, tws, t, a.n, c);
+  // canonical inverse: n^-1 folded into the last stage (A::inv_fold)
+  const bool fold = !FWD && A::kFold && a.fout == 1;
+  run_passes<LOGB, LOGV, A, FWD, 0, ILTM0, true>(v, sm, tws, t, a.n, c, fold);
 
   constexpr int PL = S::NP - 1;
   constexpr int LO = PO::lo(PL), K = PO::k(PL);
   constexpr int R = 1 << K, G = S::V / R;
+  if (!fold) {
 #pragma unroll
-  for (int i = 0; i < S::V; ++i) v[i] = FWD ? fwd_out<A>(v[i], c, a.fout) : inv_out<A>(v[i], c, a.fout);
+    for (int i = 0; i < S::V; ++i) v[i] = FWD ? fwd_out<A>(v[i], c, a.fout) : inv_out<A>(v[i], c, a.fout);
+  }
   const uint32_t jt = S::scatter(t, LO, K);
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const uint32_t jg = S::jg(g, LO, K);
-    if constexpr (LO == 0 && R >= 2) {
+    if constexpr (LO == 0 && R >= 4) {
+#pragma unroll
+      for (int r = 0; r < R; r += 4)
+        st_words4(dst + jt + jg + r, v[g * R + r], v[g * R + r + 1], v[g * R + r + 2], v[g * R + r + 3]);
+    } else if constexpr (LO == 0 && R >= 2) {
 #pragma unroll
       for (int r = 0; r < R; r += 2)
         *reinterpret_cast<ulonglong2*>(dst + jt + jg + r) = make_ulonglong2(v[g * R + r], v[g * R + r + 1]);
